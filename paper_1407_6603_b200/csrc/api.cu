@@ -1,0 +1,1197 @@
+// C-ABI runtime of libwsort_b200: handles, buffer planning, pass scheduling.
+//
+// A handle owns one CUDA stream and grow-only device buffers. A public call
+// stages its small parameter tables in a pinned arena, uploads them with one
+// copy, enqueues its kernels and synchronises once at the end (the ingest
+// path also synchronises once to read the 34-entry length histogram, which
+// sizes the key arena and the pass schedule).
+//
+// Buckets: lengths 1..32 are packed-key buckets grouped by key width into 4
+// lane classes (one segmented launch per class and pass); lengths > 32 are
+// "long groups" sorted by an LSD sequence of stable 1-lane passes over their
+// 8-byte lanes (most significant last), with the text as the byte store.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "wsort.h"
+#include "ws_common.cuh"
+#include "ws_kernels.h"
+
+using namespace ws;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int fail_cuda(cudaError_t e, const char* what, int line) {
+  int code = (e == cudaErrorMemoryAllocation) ? WS_ERR_OOM : WS_ERR_CUDA;
+  cudaGetLastError();
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error at api.cu:%d (%s): %s", line, what, cudaGetErrorString(e));
+  g_err = buf;
+  return code;
+}
+
+#define WS_CUDA(x)                                             \
+  do {                                                         \
+    cudaError_t e_ = (x);                                      \
+    if (e_ != cudaSuccess) return fail_cuda(e_, #x, __LINE__); \
+  } while (0)
+
+#define WS_TRY(x)             \
+  do {                        \
+    int r_ = (x);             \
+    if (r_ != WS_OK) return r_; \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes + bytes / 8, 4096);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap && p) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes + bytes / 4, 1 << 16);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+constexpr int kClasses = 4;  // lane classes 1..4
+
+struct Bucket {
+  uint32_t len = 0;
+  uint64_t count = 0;
+  bool is_long = false;
+  int lanes = 0;             // packed: 1..4
+  uint64_t elem_off = 0;     // packed: element offset inside the lane class region
+  uint64_t idx_off = 0;      // packed: offset in the idx arena (global over buckets)
+  uint64_t long_off = 0;     // long: offset in the grouped long-word list
+  int final_buf = 0;         // packed: which key/idx buffer holds the sorted run
+  int64_t inv = 0, kmax = 0; // stats (valid after ws_sort(h, 1))
+};
+
+struct PhaseRec {
+  std::string name;
+  cudaEvent_t a, b;
+  double bytes;
+  int launches;
+  int kind;
+};
+
+struct SegIn {
+  uint64_t key_off;  // element offset (class-relative for packed buckets)
+  uint64_t idx_off;
+  uint32_t n;
+  uint32_t stat_slot;
+  uint32_t idx_base;
+  int final_buf;  // out
+};
+
+}  // namespace
+
+struct ws_handle {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  // text / word sources
+  DevBuf text;         // corpus bytes (+ padding) or word bytes or rows
+  DevBuf starts, lens; // word-list ingest
+  DevBuf hist, off, totals;
+  DevBuf keys[2], idx[2];
+  DevBuf longlist, longgrp, rank, rank_tmp, lkeys[2], lidx[2];
+  DevBuf tokens;
+  DevBuf stat_inv, stat_k, stat_k_dummy;
+  DevBuf out;
+  DevBuf params;
+  PinBuf pin_params, pin_small;
+  size_t param_used = 0;
+
+  uint64_t n_text = 0;
+  uint32_t nchunks = 0;
+  uint64_t words = 0;
+  uint64_t n_long = 0;
+  bool have_tokens = false;
+  bool ingested = false, sorted = false, have_stats = false;
+  uint64_t class_base[kClasses + 1] = {0};  // u64-word base of each lane class region
+  uint64_t class_elems[kClasses + 1] = {0};
+  uint64_t idx_total = 0;
+  std::vector<Bucket> buckets;
+
+  bool prof = false;
+  std::vector<PhaseRec> phases;
+  std::vector<cudaEvent_t> event_pool;
+  uint64_t launches = 0;
+};
+
+namespace {
+
+// ----------------------------------------------------------------------------
+// helpers
+
+cudaEvent_t get_event(ws_handle* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Phase {
+  ws_handle* h;
+  PhaseRec rec;
+  bool on;
+  Phase(ws_handle* hh, const char* name, double bytes, int kind = 0) : h(hh), on(hh->prof) {
+    if (!on) return;
+    rec.name = name;
+    rec.bytes = bytes;
+    rec.kind = kind;
+    rec.launches = 0;
+    rec.a = get_event(h);
+    rec.b = get_event(h);
+    cudaEventRecord(rec.a, h->st);
+    start_launches = h->launches;
+  }
+  uint64_t start_launches = 0;
+  void end() {
+    if (!on) return;
+    cudaEventRecord(rec.b, h->st);
+    rec.launches = (int)(h->launches - start_launches);
+    if (rec.kind == 1 && rec.launches == 0) rec.launches = 1;
+    h->phases.push_back(rec);
+    on = false;
+  }
+  ~Phase() { end(); }
+};
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail_cuda(e, what, 0);
+  return WS_OK;
+}
+
+// Parameter tables: staged in pinned memory, uploaded with one copy each.
+void params_reset(ws_handle* h) { h->param_used = 0; }
+
+template <class T>
+int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev) {
+  size_t bytes = v.size() * sizeof(T);
+  size_t off = (h->param_used + 255) & ~size_t(255);
+  if (off + bytes > h->pin_params.cap || off + bytes > h->params.cap) {
+    // growing needs the stream idle (the old staging bytes may be in flight)
+    WS_CUDA(cudaStreamSynchronize(h->st));
+    size_t need = std::max<size_t>(2 * (off + bytes), 1 << 20);
+    if (need > h->pin_params.cap) {
+      h->pin_params.release();
+      WS_CUDA(h->pin_params.ensure(need));
+    }
+    if (need > h->params.cap) {
+      h->params.release();
+      WS_CUDA(h->params.ensure(need));
+    }
+    off = 0;
+  }
+  if (bytes) {
+    memcpy(static_cast<uint8_t*>(h->pin_params.p) + off, v.data(), bytes);
+    WS_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(h->params.p) + off,
+                            static_cast<uint8_t*>(h->pin_params.p) + off, bytes,
+                            cudaMemcpyHostToDevice, h->st));
+  }
+  *dev = reinterpret_cast<const T*>(static_cast<uint8_t*>(h->params.p) + off);
+  h->param_used = off + bytes;
+  return WS_OK;
+}
+
+int begin_call(ws_handle* h) {
+  if (!h) return fail(WS_ERR_ARG, "null handle");
+  WS_CUDA(cudaSetDevice(h->device));
+  params_reset(h);
+  g_err.clear();
+  return WS_OK;
+}
+
+// ----------------------------------------------------------------------------
+// segmented sort driver: tile pass + merge levels over `segs`, all of one
+// lane width, data starting in keys0 (+ implicit idx), ping-ponging with
+// keys1/idx1/idx0. Each segment's final buffer parity is written back.
+
+int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* keys0,
+                  uint64_t* keys1, uint32_t* idx0, uint32_t* idx1, bool stats,
+                  unsigned long long* inv, long long* kmax, const char* tag) {
+  std::vector<SegIn*> live;
+  for (auto& s : segs) {
+    s.final_buf = 0;
+    if (s.n > 0) live.push_back(&s);
+  }
+  if (live.empty()) return WS_OK;
+  const uint32_t T = (uint32_t)tile_size(lanes);
+  uint64_t* kb[2] = {keys0, keys1};
+  uint32_t* ib[2] = {idx0, idx1};
+  // pass 0 = tile sort; pass p >= 1 merges runs of T << (p-1)
+  uint32_t max_n = 0;
+  for (auto* s : live) max_n = std::max(max_n, s->n);
+  int passes = 1;
+  while (((uint64_t)T << (passes - 1)) < max_n) ++passes;
+  for (int p = 0; p < passes; ++p) {
+    const uint64_t run = p == 0 ? 0 : ((uint64_t)T << (p - 1));
+    std::vector<SegDesc> d;
+    uint32_t work = 0;
+    double bytes = 0;
+    for (auto* s : live) {
+      if (p > 0 && s->n <= run) continue;
+      SegDesc sd;
+      sd.key_off = s->key_off;
+      sd.idx_off = s->idx_off;
+      sd.n = s->n;
+      sd.tile_begin = work;
+      sd.stat_slot = s->stat_slot;
+      sd.idx_base = s->idx_base;
+      d.push_back(sd);
+      work += (uint32_t)((s->n + T - 1) / T);
+      bytes += 2.0 * s->n * lanes * 8 + (stats ? (p == 0 ? 4.0 : 8.0) * s->n : 0.0);
+      s->final_buf = (p + 1) & 1;
+    }
+    if (d.empty()) break;
+    const SegDesc* dd;
+    WS_TRY(params_upload(h, d, &dd));
+    const int in = p & 1, out = in ^ 1;
+    SortLaunch a;
+    a.keys_in = kb[in];
+    a.keys_out = kb[out];
+    a.idx_in = stats ? ib[in] : nullptr;
+    a.idx_out = stats ? ib[out] : nullptr;
+    a.segs = dd;
+    a.nsegs = (int)d.size();
+    a.work_items = work;
+    a.run = (uint32_t)run;
+    a.inv = inv;
+    a.kmax = kmax;
+    char name[32];
+    snprintf(name, sizeof name, "%s%s_l%d", tag, p == 0 ? "tile" : "merge", lanes);
+    Phase ph(h, name, bytes);
+    if (p == 0) launch_tile_sort(lanes, a, h->st);
+    else launch_merge(lanes, a, h->st);
+    ++h->launches;
+    ph.end();
+    WS_TRY(check_launch(name));
+  }
+  return WS_OK;
+}
+
+// ----------------------------------------------------------------------------
+// planning after the length histogram is known
+
+struct LongGroup {
+  uint32_t len;
+  uint64_t off, count;
+};
+
+// counts[b] for bins 0..31 -> packed buckets; lays out the lane-class regions.
+int plan_packed(ws_handle* h, const uint64_t* counts) {
+  h->buckets.clear();
+  uint64_t elems[kClasses + 1] = {0};
+  uint64_t bin_elem[kMaxPackedLen] = {0};
+  uint64_t idx_run = 0;
+  for (int b = 0; b < kMaxPackedLen; ++b) {
+    if (!counts[b]) continue;
+    int L = b + 1, c = lanes_for_len(L);
+    bin_elem[b] = elems[c];
+    elems[c] += counts[b];
+    Bucket bk;
+    bk.len = L;
+    bk.count = counts[b];
+    bk.lanes = c;
+    bk.elem_off = bin_elem[b];
+    bk.idx_off = idx_run;
+    idx_run += counts[b];
+    h->buckets.push_back(bk);
+  }
+  uint64_t run = 0;
+  for (int c = 1; c <= kClasses; ++c) {
+    h->class_base[c] = run;
+    h->class_elems[c] = elems[c];
+    run += elems[c] * c;
+    run = (run + 1) & ~1ull;  // 16-byte aligned class regions
+  }
+  h->idx_total = idx_run;
+  const size_t key_bytes = run * 8 + 64;
+  WS_CUDA(h->keys[0].ensure(key_bytes));
+  WS_CUDA(h->keys[1].ensure(key_bytes));
+  return WS_OK;
+}
+
+void fill_scatter_params(ws_handle* h, ScatterParams& p) {
+  memset(&p, 0, sizeof p);
+  for (const auto& bk : h->buckets) {
+    if (bk.is_long) continue;
+    p.bin_base[bk.len - 1] = h->class_base[bk.lanes] + bk.elem_off * bk.lanes;
+  }
+  p.keys = h->keys[0].as<uint64_t>();
+  p.longlist = h->longlist.as<uint2>();
+  p.tokens = nullptr;
+}
+
+// Long words (corpus order in h->longlist, m entries) -> stable grouping by
+// length into h->longgrp; appends one bucket per distinct length.
+int group_long_words(ws_handle* h, uint64_t m) {
+  h->n_long = m;
+  if (!m) return WS_OK;
+  WS_CUDA(h->longgrp.ensure(m * sizeof(uint2)));
+  WS_CUDA(h->lkeys[0].ensure(m * 8 + 64));
+  WS_CUDA(h->lkeys[1].ensure(m * 8 + 64));
+  WS_CUDA(h->lidx[0].ensure(m * 4 + 64));
+  WS_CUDA(h->lidx[1].ensure(m * 4 + 64));
+  WS_CUDA(h->stat_k_dummy.ensure(64 * 16));
+  WS_CUDA(h->stat_inv.ensure(64 * 16));
+  launch_len_keys(h->longlist.as<uint2>(), m, h->lkeys[0].as<uint64_t>(), h->st);
+  ++h->launches;
+  std::vector<SegIn> segs(1);
+  segs[0] = SegIn{0, 0, (uint32_t)m, 0, 0, 0};
+  WS_TRY(sort_segments(h, 1, segs, h->lkeys[0].as<uint64_t>(), h->lkeys[1].as<uint64_t>(),
+                       h->lidx[0].as<uint32_t>(), h->lidx[1].as<uint32_t>(), true,
+                       h->stat_inv.as<unsigned long long>(), h->stat_k_dummy.as<long long>(),
+                       "lgroup_"));
+  const int f = segs[0].final_buf;
+  launch_gather_u2(h->longlist.as<uint2>(), h->lidx[f].as<uint32_t>(), m, h->longgrp.as<uint2>(),
+                   h->st);
+  ++h->launches;
+  std::vector<uint64_t> lens(m);
+  WS_CUDA(cudaMemcpyAsync(lens.data(), h->lkeys[f].p, m * 8, cudaMemcpyDeviceToHost, h->st));
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  uint64_t i = 0;
+  while (i < m) {
+    uint64_t j = i;
+    while (j < m && lens[j] == lens[i]) ++j;
+    Bucket bk;
+    bk.len = (uint32_t)lens[i];
+    bk.count = j - i;
+    bk.is_long = true;
+    bk.long_off = i;
+    h->buckets.push_back(bk);
+    i = j;
+  }
+  return WS_OK;
+}
+
+int finish_ingest(ws_handle* h) {
+  h->words = 0;
+  for (auto& b : h->buckets) h->words += b.count;
+  h->ingested = true;
+  h->sorted = false;
+  h->have_stats = false;
+  return WS_OK;
+}
+
+int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags) {
+  if (n >= (1ull << 32) - kTextPad) return fail(WS_ERR_ARG, "text must be shorter than 4 GiB");
+  if (n && !text) return fail(WS_ERR_ARG, "null text");
+  h->ingested = h->sorted = h->have_stats = false;
+  h->have_tokens = false;
+  h->buckets.clear();
+  h->n_text = n;
+  WS_CUDA(h->text.ensure(n + kTextPad));
+  {
+    Phase ph(h, "h2d_text", (double)n, (flags & WS_INGEST_DEVICE_PTR) ? 0 : 1);
+    if (n)
+      WS_CUDA(cudaMemcpyAsync(h->text.p, text, n,
+                              (flags & WS_INGEST_DEVICE_PTR) ? cudaMemcpyDeviceToDevice
+                                                             : cudaMemcpyHostToDevice,
+                              h->st));
+    WS_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(h->text.p) + n, 0, kTextPad, h->st));
+  }
+  const uint32_t nchunks = chunk_count(n);
+  h->nchunks = nchunks;
+  const size_t hist_bytes = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
+  WS_CUDA(h->hist.ensure(hist_bytes));
+  WS_CUDA(h->off.ensure(hist_bytes));
+  WS_CUDA(h->totals.ensure(kHistRows * 4));
+  WS_CUDA(h->pin_small.ensure(1 << 16));
+  const uint8_t* dtext = h->text.as<uint8_t>();
+  uint32_t* tot_host = static_cast<uint32_t*>(h->pin_small.p);
+  if (nchunks) {
+    {
+      Phase ph(h, "count", (double)n);
+      launch_count(dtext, n, h->hist.as<uint32_t>(), nchunks, h->st);
+      ++h->launches;
+    }
+    WS_TRY(check_launch("count_kernel"));
+    {
+      Phase ph(h, "scan", (double)kHistRows * nchunks * 8);
+      launch_scan(h->hist.as<uint32_t>(), h->off.as<uint32_t>(), h->totals.as<uint32_t>(),
+                  nchunks, kHistRows, h->st);
+      ++h->launches;
+    }
+    WS_TRY(check_launch("scan_kernel"));
+    WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+    WS_CUDA(cudaStreamSynchronize(h->st));
+  } else {
+    memset(tot_host, 0, kHistRows * 4);
+  }
+  uint64_t counts[kNumBins];
+  for (int b = 0; b < kNumBins; ++b) counts[b] = tot_host[b];
+  const uint64_t total_words = tot_host[kNumBins];
+  WS_TRY(plan_packed(h, counts));
+  const uint64_t m = counts[kLongBin];
+  WS_CUDA(h->longlist.ensure(std::max<uint64_t>(m, 1) * sizeof(uint2)));
+  ScatterParams p;
+  fill_scatter_params(h, p);
+  if (flags & WS_INGEST_KEEP_TOKENS) {
+    WS_CUDA(h->tokens.ensure(std::max<uint64_t>(total_words, 1) * sizeof(uint2)));
+    p.tokens = h->tokens.as<uint2>();
+    h->have_tokens = true;
+  }
+  if (nchunks) {
+    double kbytes = 0;
+    for (auto& b : h->buckets) kbytes += (double)b.count * b.lanes * 8;
+    Phase ph(h, "scatter", (double)n + kbytes + 8.0 * m);
+    launch_scatter(dtext, n, h->off.as<uint32_t>(), nchunks, p, h->st);
+    ++h->launches;
+  }
+  WS_TRY(check_launch("scatter_kernel"));
+  WS_TRY(group_long_words(h, m));
+  h->words = total_words;
+  return finish_ingest(h);
+}
+
+// ----------------------------------------------------------------------------
+// sort of all buckets
+
+int sort_impl(ws_handle* h, bool stats) {
+  if (!h->ingested) return fail(WS_ERR_STATE, "ws_sort before ingest");
+  const int nb = (int)h->buckets.size();
+  if (stats) {
+    WS_CUDA(h->idx[0].ensure(std::max<uint64_t>(h->idx_total, 1) * 4 + 64));
+    WS_CUDA(h->idx[1].ensure(std::max<uint64_t>(h->idx_total, 1) * 4 + 64));
+    WS_CUDA(h->stat_inv.ensure((size_t)std::max(nb, 1) * 16));
+    WS_CUDA(h->stat_k.ensure((size_t)std::max(nb, 1) * 16));
+    WS_CUDA(h->stat_k_dummy.ensure((size_t)std::max(nb, 1) * 16));
+    WS_CUDA(cudaMemsetAsync(h->stat_inv.p, 0, (size_t)std::max(nb, 1) * 8, h->st));
+    WS_CUDA(cudaMemsetAsync(h->stat_k.p, 0, (size_t)std::max(nb, 1) * 8, h->st));
+  }
+  unsigned long long* inv = stats ? h->stat_inv.as<unsigned long long>() : nullptr;
+  long long* km = stats ? h->stat_k.as<long long>() : nullptr;
+  // packed buckets: one schedule per lane class
+  for (int c = 1; c <= kClasses; ++c) {
+    std::vector<SegIn> segs;
+    std::vector<int> which;
+    for (int i = 0; i < nb; ++i) {
+      const Bucket& b = h->buckets[i];
+      if (b.is_long || b.lanes != c) continue;
+      segs.push_back(SegIn{b.elem_off, b.idx_off, (uint32_t)b.count, (uint32_t)i, 0, 0});
+      which.push_back(i);
+    }
+    if (segs.empty()) continue;
+    uint64_t* k0 = h->keys[0].as<uint64_t>() + h->class_base[c];
+    uint64_t* k1 = h->keys[1].as<uint64_t>() + h->class_base[c];
+    WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(), h->idx[1].as<uint32_t>(),
+                         stats, inv, km, ""));
+    for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
+  }
+  // long groups: LSD over 8-byte lanes, least significant lane first
+  if (h->n_long) {
+    const uint64_t m = h->n_long;
+    WS_CUDA(h->rank.ensure(m * 4 + 64));
+    WS_CUDA(h->rank_tmp.ensure(m * 4 + 64));
+    launch_iota_u32(h->rank.as<uint32_t>(), m, h->st);  // rank[i] = i
+    ++h->launches;
+    int max_lanes = 0;
+    for (auto& b : h->buckets)
+      if (b.is_long) max_lanes = std::max(max_lanes, lanes_for_len(b.len));
+    const uint8_t* ltext = h->text.as<uint8_t>();
+    for (int lane = max_lanes - 1; lane >= 0; --lane) {
+      std::vector<SegIn> segs;
+      std::vector<int> which;
+      for (int i = 0; i < nb; ++i) {
+        const Bucket& b = h->buckets[i];
+        if (!b.is_long || lanes_for_len(b.len) <= lane) continue;
+        segs.push_back(SegIn{b.long_off, b.long_off, (uint32_t)b.count, (uint32_t)i,
+                             (uint32_t)b.long_off, 0});
+        which.push_back(i);
+      }
+      launch_lane_keys(ltext, h->longgrp.as<uint2>(), h->rank.as<uint32_t>(), m, lane,
+                       h->lkeys[0].as<uint64_t>(), h->st);
+      ++h->launches;
+      WS_TRY(sort_segments(h, 1, segs, h->lkeys[0].as<uint64_t>(), h->lkeys[1].as<uint64_t>(),
+                           h->lidx[0].as<uint32_t>(), h->lidx[1].as<uint32_t>(), true,
+                           h->stat_k_dummy.as<unsigned long long>(),
+                           h->stat_k_dummy.as<long long>(), "llsd_"));
+      for (size_t j = 0; j < segs.size(); ++j) {
+        const Bucket& b = h->buckets[which[j]];
+        const uint32_t* perm = h->lidx[segs[j].final_buf].as<uint32_t>() + b.long_off;
+        launch_gather_u32(h->rank.as<uint32_t>(), perm, b.count,
+                          h->rank_tmp.as<uint32_t>() + b.long_off, h->st);
+        ++h->launches;
+        WS_CUDA(cudaMemcpyAsync(h->rank.as<uint32_t>() + b.long_off,
+                                h->rank_tmp.as<uint32_t>() + b.long_off, b.count * 4,
+                                cudaMemcpyDeviceToDevice, h->st));
+      }
+    }
+    if (stats) {
+      // inversions of each group's final rank sequence; K = max(rank[i] - i)
+      launch_iota_keys(h->rank.as<uint32_t>(), m, h->lkeys[0].as<uint64_t>(), h->st);
+      ++h->launches;
+      std::vector<SegIn> segs;
+      for (int i = 0; i < nb; ++i) {
+        const Bucket& b = h->buckets[i];
+        if (!b.is_long) continue;
+        segs.push_back(SegIn{b.long_off, b.long_off, (uint32_t)b.count, (uint32_t)i,
+                             (uint32_t)b.long_off, 0});
+        launch_rank_kmax(h->rank.as<uint32_t>(), b.long_off, b.count, km + i, h->st);
+        ++h->launches;
+      }
+      WS_TRY(sort_segments(h, 1, segs, h->lkeys[0].as<uint64_t>(), h->lkeys[1].as<uint64_t>(),
+                           h->lidx[0].as<uint32_t>(), h->lidx[1].as<uint32_t>(), true, inv,
+                           h->stat_k_dummy.as<long long>(), "linv_"));
+    }
+  }
+  if (stats && nb) {
+    std::vector<int64_t> hinv(nb), hk(nb);
+    WS_CUDA(cudaMemcpyAsync(hinv.data(), h->stat_inv.p, nb * 8, cudaMemcpyDeviceToHost, h->st));
+    WS_CUDA(cudaMemcpyAsync(hk.data(), h->stat_k.p, nb * 8, cudaMemcpyDeviceToHost, h->st));
+    WS_CUDA(cudaStreamSynchronize(h->st));
+    for (int i = 0; i < nb; ++i) {
+      h->buckets[i].inv = hinv[i];
+      h->buckets[i].kmax = hk[i];
+    }
+  }
+  WS_TRY(check_launch("sort"));
+  h->sorted = true;
+  h->have_stats = stats;
+  return WS_OK;
+}
+
+// ----------------------------------------------------------------------------
+// emit
+
+const uint64_t* bucket_keys(ws_handle* h, const Bucket& b, bool sorted) {
+  const int buf = sorted ? b.final_buf : 0;
+  return h->keys[buf].as<uint64_t>() + h->class_base[b.lanes] + b.elem_off * b.lanes;
+}
+
+// Enqueue emission of all buckets into device buffer `dout` (lines or rows).
+int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* offsets) {
+  const int nl = lines ? 1 : 0;
+  std::vector<uint64_t> off(h->buckets.size());
+  uint64_t run = 0;
+  for (size_t i = 0; i < h->buckets.size(); ++i) {
+    off[i] = run;
+    run += h->buckets[i].count * (h->buckets[i].len + nl);
+  }
+  double kb = 0;
+  for (auto& b : h->buckets) kb += b.is_long ? 0.0 : (double)b.count * b.lanes * 8;
+  Phase ph(h, lines ? "emit_lines" : "emit_rows", kb + (double)run);
+  for (int c = 1; c <= kClasses; ++c) {
+    std::vector<EmitSeg> segs;
+    uint32_t blocks = 0;
+    for (size_t i = 0; i < h->buckets.size(); ++i) {
+      const Bucket& b = h->buckets[i];
+      if (b.is_long || b.lanes != c || !b.count) continue;
+      EmitSeg e;
+      e.keys = bucket_keys(h, b, h->sorted);
+      e.out_off = off[i];
+      e.n = (uint32_t)b.count;
+      e.len = b.len;
+      e.block_begin = blocks;
+      e.pad_ = 0;
+      blocks += (uint32_t)((b.count + kEmitWords - 1) / kEmitWords);
+      segs.push_back(e);
+    }
+    if (segs.empty()) continue;
+    const EmitSeg* d;
+    WS_TRY(params_upload(h, segs, &d));
+    launch_emit(c, d, (int)segs.size(), blocks, dout, nl, h->st);
+    ++h->launches;
+  }
+  for (size_t i = 0; i < h->buckets.size(); ++i) {
+    const Bucket& b = h->buckets[i];
+    if (!b.is_long || !b.count) continue;
+    const uint32_t* order = h->sorted ? h->rank.as<uint32_t>() + b.long_off : nullptr;
+    const uint2* words = h->longgrp.as<uint2>() + (h->sorted ? 0 : b.long_off);
+    launch_emit_long(h->text.as<uint8_t>(), words, order, b.count, b.len, dout + off[i], nl, h->st);
+    ++h->launches;
+  }
+  ph.end();
+  WS_TRY(check_launch("emit"));
+  if (offsets) {
+    off.push_back(run);
+    *offsets = off;
+  }
+  return WS_OK;
+}
+
+uint64_t emit_size(ws_handle* h, bool lines) {
+  uint64_t run = 0;
+  for (auto& b : h->buckets) run += b.count * (b.len + (lines ? 1 : 0));
+  return run;
+}
+
+int emit_to_host(ws_handle* h, bool lines, uint8_t* out, uint64_t cap, uint64_t* written) {
+  if (!h->ingested) return fail(WS_ERR_STATE, "emit before ingest");
+  const uint64_t size = emit_size(h, lines);
+  if (written) *written = size;
+  if (!out && cap == 0) return WS_OK;  // size query
+  if (cap < size) return fail(WS_ERR_ARG, "output buffer too small");
+  if (!size) return WS_OK;
+  if (!out) return fail(WS_ERR_ARG, "null output buffer");
+  WS_CUDA(h->out.ensure(size + 64));
+  WS_TRY(emit_device(h, h->out.as<uint8_t>(), lines, nullptr));
+  {
+    Phase ph(h, "d2h_out", (double)size, 1);
+    WS_CUDA(cudaMemcpyAsync(out, h->out.p, size, cudaMemcpyDeviceToHost, h->st));
+  }
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  return WS_OK;
+}
+
+// ----------------------------------------------------------------------------
+// rows / blocks ingest (the _bubble_rows drop-in)
+
+int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows,
+                       const int64_t* counts, const int32_t* widths, bool allow_dup,
+                       std::vector<int>* block_of_bucket) {
+  if (nblocks < 0) return fail(WS_ERR_ARG, "negative block count");
+  h->ingested = h->sorted = h->have_stats = false;
+  h->have_tokens = false;
+  h->buckets.clear();
+  std::vector<int> order(nblocks);
+  for (int i = 0; i < nblocks; ++i) {
+    order[i] = i;
+    if (counts[i] < 0 || widths[i] < 1) return fail(WS_ERR_ARG, "bad block shape");
+    if (counts[i] && !rows[i]) return fail(WS_ERR_ARG, "null rows");
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return widths[a] < widths[b]; });
+  if (!allow_dup)
+    for (int i = 1; i < nblocks; ++i)
+      if (widths[order[i]] == widths[order[i - 1]]) return fail(WS_ERR_ARG, "repeated width");
+  // byte offsets of each block in the device rows buffer (16-byte aligned)
+  std::vector<uint64_t> boff(nblocks);
+  uint64_t total = 0;
+  for (int k = 0; k < nblocks; ++k) {
+    int i = order[k];
+    boff[i] = total;
+    total += (uint64_t)counts[i] * widths[i];
+    total = (total + 15) & ~15ull;
+  }
+  if (total >= (1ull << 32)) return fail(WS_ERR_ARG, "rows must total less than 4 GiB");
+  WS_CUDA(h->text.ensure(total + kTextPad));
+  h->n_text = total;
+  {
+    Phase ph(h, "h2d_rows", (double)total, 1);
+    for (int i = 0; i < nblocks; ++i)
+      if (counts[i])
+        WS_CUDA(cudaMemcpyAsync(h->text.as<uint8_t>() + boff[i], rows[i],
+                                (size_t)counts[i] * widths[i], cudaMemcpyHostToDevice, h->st));
+  }
+  // plan: packed buckets (width <= 32) laid out per lane class, long groups
+  uint64_t elems[kClasses + 1] = {0};
+  uint64_t idx_run = 0, long_run = 0;
+  std::vector<int> bob;
+  for (int k = 0; k < nblocks; ++k) {
+    int i = order[k];
+    if (!counts[i]) continue;
+    Bucket bk;
+    bk.len = (uint32_t)widths[i];
+    bk.count = (uint64_t)counts[i];
+    if (widths[i] <= kMaxPackedLen) {
+      bk.lanes = lanes_for_len(widths[i]);
+      bk.elem_off = elems[bk.lanes];
+      elems[bk.lanes] += bk.count;
+      bk.idx_off = idx_run;
+      idx_run += bk.count;
+    } else {
+      bk.is_long = true;
+      bk.long_off = long_run;
+      long_run += bk.count;
+    }
+    h->buckets.push_back(bk);
+    bob.push_back(i);
+  }
+  uint64_t run = 0;
+  for (int c = 1; c <= kClasses; ++c) {
+    h->class_base[c] = run;
+    h->class_elems[c] = elems[c];
+    run += elems[c] * c;
+    run = (run + 1) & ~1ull;
+  }
+  h->idx_total = idx_run;
+  WS_CUDA(h->keys[0].ensure(run * 8 + 64));
+  WS_CUDA(h->keys[1].ensure(run * 8 + 64));
+  h->n_long = long_run;
+  if (long_run) {
+    WS_CUDA(h->longgrp.ensure(long_run * sizeof(uint2)));
+    WS_CUDA(h->lkeys[0].ensure(long_run * 8 + 64));
+    WS_CUDA(h->lkeys[1].ensure(long_run * 8 + 64));
+    WS_CUDA(h->lidx[0].ensure(long_run * 4 + 64));
+    WS_CUDA(h->lidx[1].ensure(long_run * 4 + 64));
+  }
+  for (size_t k = 0; k < h->buckets.size(); ++k) {
+    const Bucket& b = h->buckets[k];
+    const int i = bob[k];
+    if (!b.is_long) {
+      launch_pack_rows(h->text.as<uint8_t>() + boff[i], b.count, b.len,
+                       h->keys[0].as<uint64_t>() + h->class_base[b.lanes] + b.elem_off * b.lanes,
+                       h->st);
+    } else {
+      launch_rows_longlist(boff[i], b.count, b.len, h->longgrp.as<uint2>() + b.long_off, h->st);
+    }
+    ++h->launches;
+  }
+  WS_TRY(check_launch("pack_rows"));
+  if (block_of_bucket) *block_of_bucket = bob;
+  return finish_ingest(h);
+}
+
+int ingest_words_impl(ws_handle* h, const uint8_t* concat, const uint32_t* lens, uint64_t nwords) {
+  h->ingested = h->sorted = h->have_stats = false;
+  h->have_tokens = false;
+  h->buckets.clear();
+  if (nwords && !lens) return fail(WS_ERR_ARG, "null lens");
+  std::vector<uint64_t> starts(nwords);
+  uint64_t total = 0;
+  for (uint64_t i = 0; i < nwords; ++i) {
+    if (lens[i] == 0) return fail(WS_ERR_ARG, "empty word");
+    starts[i] = total;
+    total += lens[i];
+  }
+  if (total >= (1ull << 32) - kTextPad) return fail(WS_ERR_ARG, "words must total < 4 GiB");
+  if (total && !concat) return fail(WS_ERR_ARG, "null word bytes");
+  WS_CUDA(h->text.ensure(total + kTextPad));
+  WS_CUDA(h->starts.ensure(std::max<uint64_t>(nwords, 1) * 8));
+  WS_CUDA(h->lens.ensure(std::max<uint64_t>(nwords, 1) * 4));
+  h->n_text = total;
+  {
+    Phase ph(h, "h2d_words", (double)total + 12.0 * nwords, 1);
+    if (total) WS_CUDA(cudaMemcpyAsync(h->text.p, concat, total, cudaMemcpyHostToDevice, h->st));
+    if (nwords) {
+      WS_CUDA(cudaMemcpyAsync(h->starts.p, starts.data(), nwords * 8, cudaMemcpyHostToDevice,
+                              h->st));
+      WS_CUDA(cudaMemcpyAsync(h->lens.p, lens, nwords * 4, cudaMemcpyHostToDevice, h->st));
+    }
+  }
+  constexpr uint32_t kWpw = 1024;
+  const uint32_t nwarps = (uint32_t)((nwords + kWpw - 1) / kWpw);
+  const size_t hb = (size_t)kNumBins * std::max<uint32_t>(nwarps, 1) * 4;
+  WS_CUDA(h->hist.ensure(hb));
+  WS_CUDA(h->off.ensure(hb));
+  WS_CUDA(h->totals.ensure(kHistRows * 4));
+  WS_CUDA(h->pin_small.ensure(1 << 16));
+  uint32_t* tot_host = static_cast<uint32_t*>(h->pin_small.p);
+  memset(tot_host, 0, kHistRows * 4);
+  if (nwarps) {
+    WS_CUDA(cudaMemsetAsync(h->hist.p, 0, hb, h->st));
+    launch_words_hist(h->lens.as<uint32_t>(), nwords, kWpw, h->hist.as<uint32_t>(), nwarps, h->st);
+    launch_scan(h->hist.as<uint32_t>(), h->off.as<uint32_t>(), h->totals.as<uint32_t>(), nwarps,
+                kNumBins, h->st);
+    h->launches += 2;
+    WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kNumBins * 4, cudaMemcpyDeviceToHost, h->st));
+    WS_CUDA(cudaStreamSynchronize(h->st));
+  }
+  uint64_t counts[kNumBins];
+  for (int b = 0; b < kNumBins; ++b) counts[b] = tot_host[b];
+  WS_TRY(plan_packed(h, counts));
+  const uint64_t m = counts[kLongBin];
+  WS_CUDA(h->longlist.ensure(std::max<uint64_t>(m, 1) * sizeof(uint2)));
+  ScatterParams p;
+  fill_scatter_params(h, p);
+  launch_words_scatter(h->text.as<uint8_t>(), h->starts.as<uint64_t>(), h->lens.as<uint32_t>(),
+                       nwords, kWpw, h->off.as<uint32_t>(), nwarps, p, h->st);
+  ++h->launches;
+  WS_TRY(check_launch("words_scatter"));
+  WS_TRY(group_long_words(h, m));
+  return finish_ingest(h);
+}
+
+int thread_handle(ws_handle** out);
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+
+extern "C" {
+
+int ws_version(void) { return 10000; }
+
+const char* ws_last_error(void) { return g_err.c_str(); }
+
+int ws_device_count(int32_t* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return WS_OK;
+}
+
+int ws_create(ws_handle** out, int32_t device) {
+  if (!out) return fail(WS_ERR_ARG, "null out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(WS_ERR_CUDA, std::string("no CUDA device available: ") +
+                                 (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+  }
+  if (device < 0 || device >= n) return fail(WS_ERR_ARG, "bad device index");
+  WS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  WS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) {
+    return fail(WS_ERR_CUDA, std::string("libwsort_b200 is built for sm_100a; device is ") +
+                                 prop.name);
+  }
+  static std::mutex mu;
+  static uint64_t attr_done = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!(attr_done & (1ull << device))) {
+      set_sort_attributes();
+      WS_CUDA(cudaGetLastError());
+      attr_done |= 1ull << device;
+    }
+  }
+  ws_handle* h = new ws_handle();
+  h->device = device;
+  e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete h;
+    return fail_cuda(e, "cudaStreamCreate", __LINE__);
+  }
+  *out = h;
+  return WS_OK;
+}
+
+void ws_destroy(ws_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->st);
+  DevBuf* bufs[] = {&h->text, &h->starts, &h->lens, &h->hist, &h->off, &h->totals,
+                    &h->keys[0], &h->keys[1], &h->idx[0], &h->idx[1], &h->longlist,
+                    &h->longgrp, &h->rank, &h->rank_tmp, &h->lkeys[0], &h->lkeys[1],
+                    &h->lidx[0], &h->lidx[1], &h->tokens, &h->stat_inv, &h->stat_k,
+                    &h->stat_k_dummy, &h->out, &h->params};
+  for (DevBuf* b : bufs) b->release();
+  h->pin_params.release();
+  h->pin_small.release();
+  for (auto& p : h->phases) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  cudaStreamDestroy(h->st);
+  delete h;
+}
+
+int ws_ingest_text(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags) {
+  WS_TRY(begin_call(h));
+  return ingest_text_impl(h, text, n, flags);
+}
+
+int ws_ingest_words(ws_handle* h, const uint8_t* concat, const uint32_t* lens, uint64_t nwords) {
+  WS_TRY(begin_call(h));
+  return ingest_words_impl(h, concat, lens, nwords);
+}
+
+int ws_ingest_blocks(ws_handle* h, int32_t nblocks, const uint8_t* const* rows,
+                     const int64_t* counts, const int32_t* widths) {
+  WS_TRY(begin_call(h));
+  if (nblocks && (!rows || !counts || !widths)) return fail(WS_ERR_ARG, "null block arrays");
+  WS_TRY(ingest_blocks_impl(h, nblocks, rows, counts, widths, false, nullptr));
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  return WS_OK;
+}
+
+int ws_buckets(ws_handle* h, int64_t* lengths, int64_t* counts, int32_t cap, int32_t* nbuckets,
+               uint64_t* words) {
+  if (!h) return fail(WS_ERR_ARG, "null handle");
+  if (!h->ingested) return fail(WS_ERR_STATE, "ws_buckets before ingest");
+  const int nb = (int)h->buckets.size();
+  if (nbuckets) *nbuckets = nb;
+  if (words) *words = h->words;
+  for (int i = 0; i < nb && i < cap; ++i) {
+    if (lengths) lengths[i] = h->buckets[i].len;
+    if (counts) counts[i] = (int64_t)h->buckets[i].count;
+  }
+  return WS_OK;
+}
+
+int ws_tokens(ws_handle* h, uint32_t* starts_lens, uint64_t cap_words, uint64_t* nwords) {
+  WS_TRY(begin_call(h));
+  if (!h->have_tokens) return fail(WS_ERR_STATE, "ingest without WS_INGEST_KEEP_TOKENS");
+  if (nwords) *nwords = h->words;
+  if (cap_words < h->words) return fail(WS_ERR_ARG, "token buffer too small");
+  if (h->words) {
+    if (!starts_lens) return fail(WS_ERR_ARG, "null token buffer");
+    WS_CUDA(cudaMemcpyAsync(starts_lens, h->tokens.p, h->words * 8, cudaMemcpyDeviceToHost, h->st));
+  }
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  return WS_OK;
+}
+
+int ws_sort(ws_handle* h, int32_t want_stats) {
+  WS_TRY(begin_call(h));
+  WS_TRY(sort_impl(h, want_stats != 0));
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  return WS_OK;
+}
+
+int ws_stats_closed_form(int64_t n, int64_t inversions, int64_t kmax, int32_t naive,
+                         int64_t stats[3]) {
+  if (!stats) return fail(WS_ERR_ARG, "null stats");
+  stats[0] = stats[1] = stats[2] = 0;
+  if (n < 2) return WS_OK;
+  if (inversions < 0 || kmax < 0 || kmax > n - 1) return fail(WS_ERR_ARG, "bad stats input");
+  if (naive) {
+    stats[0] = n * (n - 1) / 2;
+    stats[1] = inversions;
+    stats[2] = n - 1;
+  } else {
+    const int64_t P = std::min(kmax + 1, n - 1);
+    stats[0] = P * (n - 1) - P * (P - 1) / 2;
+    stats[1] = inversions;
+    stats[2] = P;
+  }
+  return WS_OK;
+}
+
+int ws_bucket_stats(ws_handle* h, int32_t naive, int64_t* stats, int32_t cap) {
+  if (!h) return fail(WS_ERR_ARG, "null handle");
+  if (!h->have_stats) return fail(WS_ERR_STATE, "ws_bucket_stats needs ws_sort(h, 1)");
+  for (int i = 0; i < (int)h->buckets.size() && i < cap; ++i) {
+    const Bucket& b = h->buckets[i];
+    WS_TRY(ws_stats_closed_form((int64_t)b.count, b.inv, b.kmax, naive, stats + 3 * i));
+  }
+  return WS_OK;
+}
+
+int ws_permutation(ws_handle* h, int32_t bucket, uint32_t* perm, uint64_t cap) {
+  WS_TRY(begin_call(h));
+  if (!h->have_stats) return fail(WS_ERR_STATE, "ws_permutation needs ws_sort(h, 1)");
+  if (bucket < 0 || bucket >= (int)h->buckets.size()) return fail(WS_ERR_ARG, "bad bucket");
+  const Bucket& b = h->buckets[bucket];
+  if (cap < b.count) return fail(WS_ERR_ARG, "perm buffer too small");
+  if (!b.count) return WS_OK;
+  if (!b.is_long) {
+    WS_CUDA(cudaMemcpyAsync(perm, h->idx[b.final_buf].as<uint32_t>() + b.idx_off, b.count * 4,
+                            cudaMemcpyDeviceToHost, h->st));
+    WS_CUDA(cudaStreamSynchronize(h->st));
+  } else {
+    WS_CUDA(cudaMemcpyAsync(perm, h->rank.as<uint32_t>() + b.long_off, b.count * 4,
+                            cudaMemcpyDeviceToHost, h->st));
+    WS_CUDA(cudaStreamSynchronize(h->st));
+    for (uint64_t j = 0; j < b.count; ++j) perm[j] -= (uint32_t)b.long_off;
+  }
+  return WS_OK;
+}
+
+int ws_emit_lines(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written) {
+  WS_TRY(begin_call(h));
+  return emit_to_host(h, true, out, cap, written);
+}
+
+int ws_emit_rows(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written) {
+  WS_TRY(begin_call(h));
+  return emit_to_host(h, false, out, cap, written);
+}
+
+int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
+                 uint64_t* written) {
+  WS_TRY(begin_call(h));
+  WS_TRY(ingest_text_impl(h, text, n, 0));
+  params_reset(h);  // the ingest synchronised: staging space is free again
+  WS_TRY(sort_impl(h, false));
+  return emit_to_host(h, true, out, cap, written);
+}
+
+int ws_sort_rows(uint8_t* rows, int64_t n, int32_t width, int32_t naive, int64_t stats[3]) {
+  int64_t counts[1] = {n};
+  int32_t widths[1] = {width};
+  uint8_t* r[1] = {rows};
+  return ws_sort_blocks(1, r, counts, widths, naive, stats, nullptr);
+}
+
+int ws_sort_blocks(int32_t nblocks, uint8_t* const* rows, const int64_t* counts,
+                   const int32_t* widths, int32_t naive, int64_t* stats, uint32_t* const* perms) {
+  g_err.clear();
+  if (nblocks < 0) return fail(WS_ERR_ARG, "negative block count");
+  if (nblocks && (!rows || !counts || !widths || !stats)) return fail(WS_ERR_ARG, "null arrays");
+  // trivial blocks (n < 2 or width 0) need no device work: zero stats, identity perm
+  std::vector<int> work;
+  for (int i = 0; i < nblocks; ++i) {
+    if (counts[i] < 0 || widths[i] < 0) return fail(WS_ERR_ARG, "bad block shape");
+    stats[3 * i] = stats[3 * i + 1] = stats[3 * i + 2] = 0;
+    if (counts[i] >= 2 && widths[i] > 0) {
+      work.push_back(i);
+    } else if (counts[i] >= 2) {
+      // width 0: all rows equal; the reference still runs its full schedule
+      WS_TRY(ws_stats_closed_form(counts[i], 0, 0, naive, stats + 3 * i));
+    }
+    if (perms && perms[i] && !(counts[i] >= 2 && widths[i] > 0))
+      for (int64_t j = 0; j < counts[i]; ++j) perms[i][j] = (uint32_t)j;
+  }
+  if (work.empty()) return WS_OK;
+  ws_handle* h;
+  WS_TRY(thread_handle(&h));
+  WS_TRY(begin_call(h));
+  std::vector<const uint8_t*> r;
+  std::vector<int64_t> c;
+  std::vector<int32_t> w;
+  for (int i : work) {
+    r.push_back(rows[i]);
+    c.push_back(counts[i]);
+    w.push_back(widths[i]);
+  }
+  std::vector<int> bob;
+  WS_TRY(ingest_blocks_impl(h, (int)work.size(), r.data(), c.data(), w.data(), true, &bob));
+  WS_TRY(sort_impl(h, true));
+  // unpack sorted rows back into each block's device region, then to host
+  std::vector<uint64_t> offs;
+  WS_CUDA(h->out.ensure(emit_size(h, false) + 64));
+  WS_TRY(emit_device(h, h->out.as<uint8_t>(), false, &offs));
+  for (size_t k = 0; k < h->buckets.size(); ++k) {
+    const Bucket& b = h->buckets[k];
+    const int i = work[bob[k]];
+    WS_CUDA(cudaMemcpyAsync(rows[i], h->out.as<uint8_t>() + offs[k], b.count * b.len,
+                            cudaMemcpyDeviceToHost, h->st));
+    WS_TRY(ws_stats_closed_form((int64_t)b.count, b.inv, b.kmax, naive, stats + 3 * i));
+  }
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  if (perms) {
+    for (size_t k = 0; k < h->buckets.size(); ++k) {
+      const int i = work[bob[k]];
+      if (perms[i]) WS_TRY(ws_permutation(h, (int)k, perms[i], h->buckets[k].count));
+    }
+  }
+  return WS_OK;
+}
+
+int ws_set_profiling(ws_handle* h, int32_t on) {
+  if (!h) return fail(WS_ERR_ARG, "null handle");
+  h->prof = on != 0;
+  return WS_OK;
+}
+
+int ws_profile(ws_handle* h, ws_phase* out, int32_t cap, int32_t* n) {
+  if (!h) return fail(WS_ERR_ARG, "null handle");
+  WS_CUDA(cudaSetDevice(h->device));
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  if (n) *n = (int32_t)h->phases.size();
+  for (int i = 0; i < (int)h->phases.size() && i < cap; ++i) {
+    const PhaseRec& p = h->phases[i];
+    float ms = 0;
+    WS_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    memset(out[i].name, 0, sizeof out[i].name);
+    strncpy(out[i].name, p.name.c_str(), sizeof out[i].name - 1);
+    out[i].launches = p.launches;
+    out[i].kind = p.kind;
+    out[i].ms = ms;
+    out[i].bytes = p.bytes;
+  }
+  return WS_OK;
+}
+
+int ws_profile_reset(ws_handle* h) {
+  if (!h) return fail(WS_ERR_ARG, "null handle");
+  for (auto& p : h->phases) {
+    h->event_pool.push_back(p.a);
+    h->event_pool.push_back(p.b);
+  }
+  h->phases.clear();
+  return WS_OK;
+}
+
+int ws_launch_count(ws_handle* h, uint64_t* launches) {
+  if (!h || !launches) return fail(WS_ERR_ARG, "null argument");
+  *launches = h->launches;
+  return WS_OK;
+}
+
+int ws_stream(ws_handle* h, void** stream) {
+  if (!h || !stream) return fail(WS_ERR_ARG, "null argument");
+  *stream = (void*)h->st;
+  return WS_OK;
+}
+
+int ws_host_alloc(uint64_t bytes, void** out) {
+  if (!out) return fail(WS_ERR_ARG, "null out");
+  *out = nullptr;
+  WS_CUDA(cudaMallocHost(out, std::max<uint64_t>(bytes, 1)));
+  return WS_OK;
+}
+
+int ws_host_free(void* p) {
+  if (p) WS_CUDA(cudaFreeHost(p));
+  return WS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+struct ThreadHandle {
+  ws_handle* h = nullptr;
+  ~ThreadHandle() {
+    if (h) ws_destroy(h);
+  }
+};
+
+int thread_handle(ws_handle** out) {
+  thread_local ThreadHandle th;
+  if (!th.h) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      dev = 0;
+    }
+    WS_TRY(ws_create(&th.h, dev));
+  }
+  *out = th.h;
+  return WS_OK;
+}
+
+}  // namespace

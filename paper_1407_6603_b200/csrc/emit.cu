@@ -1,0 +1,235 @@
+// Emit: sorted packed keys -> output bytes.
+//
+// Replaces emit_sorted (store.py:105-114: buckets concatenated in ascending
+// length) followed by the CLI payload b"".join(word + b"\n") (cli.py:97), and
+// in rows mode the (count, L) uint8 blocks of FlatBucketMatrix
+// (store.py:46-72). Each CTA unpacks 1024 words into shared memory with the
+// same 16-byte phase as its global destination, then streams the span out
+// with aligned 16-byte stores (byte stores only for the ragged head/tail).
+// Words with L > 32 are copied from the text by (start, len).
+#include <algorithm>
+
+#include "ws_common.cuh"
+#include "ws_kernels.h"
+
+namespace ws {
+
+constexpr int kEmitThreads = 256;
+constexpr int kEmitBuf = kEmitWords * (kMaxPackedLen + 1) + 32;
+
+__device__ __forceinline__ void copy_span_out(const uint8_t* __restrict__ buf, int mis,
+                                              uint64_t o0, uint64_t total, uint8_t* __restrict__ out) {
+  const uint64_t g_end = o0 + total;
+  const uint64_t ab = (o0 + 15) & ~15ull, ae = g_end & ~15ull;
+  if (ab >= ae) {
+    for (uint64_t q = o0 + threadIdx.x; q < g_end; q += kEmitThreads) out[q] = buf[q - o0 + mis];
+    return;
+  }
+  for (uint64_t q = o0 + threadIdx.x; q < ab; q += kEmitThreads) out[q] = buf[q - o0 + mis];
+  for (uint64_t q = ab + 16ull * threadIdx.x; q < ae; q += 16ull * kEmitThreads)
+    *reinterpret_cast<uint4*>(out + q) = *reinterpret_cast<const uint4*>(buf + (q - o0 + mis));
+  for (uint64_t q = ae + threadIdx.x; q < g_end; q += kEmitThreads) out[q] = buf[q - o0 + mis];
+}
+
+template <int LANES>
+__global__ void __launch_bounds__(kEmitThreads)
+emit_kernel(const EmitSeg* __restrict__ segs, int nsegs, uint8_t* __restrict__ out, int nl) {
+  __shared__ __align__(16) uint8_t buf[kEmitBuf];
+  __shared__ int s_seg;
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = nsegs - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (segs[mid].block_begin <= blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    s_seg = lo;
+  }
+  __syncthreads();
+  const EmitSeg sg = segs[s_seg];
+  const uint64_t w0 = (uint64_t)(blockIdx.x - sg.block_begin) * kEmitWords;
+  const int cnt = (int)min((uint64_t)kEmitWords, (uint64_t)sg.n - w0);
+  const int L = (int)sg.len;
+  const int stride = L + nl;
+  const uint64_t o0 = sg.out_off + w0 * stride;
+  const int mis = (int)(o0 & 15);
+  const uint64_t* keys = sg.keys + w0 * LANES;
+  for (int j = threadIdx.x; j < cnt; j += kEmitThreads) {
+    uint64_t k[LANES];
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) k[l] = __ldg(keys + (uint64_t)j * LANES + l);
+    uint8_t* dst = buf + mis + j * stride;
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        int b = 8 * l + q;
+        if (b < L) dst[b] = (uint8_t)(k[l] >> (56 - 8 * q));
+      }
+    }
+    if (nl) dst[L] = '\n';
+  }
+  __syncthreads();
+  copy_span_out(buf, mis, o0, (uint64_t)cnt * stride, out);
+}
+
+void launch_emit(int lanes, const EmitSeg* segs, int nsegs, uint32_t blocks, uint8_t* out,
+                 int with_newline, cudaStream_t st) {
+  if (!blocks) return;
+  switch (lanes) {
+    case 1: emit_kernel<1><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
+    case 2: emit_kernel<2><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
+    case 3: emit_kernel<3><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
+    default: emit_kernel<4><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Long words (L > 32): one warp per word, bytes copied from the text.
+// order[i] (optional) maps output position -> index into words[].
+__global__ void emit_long_kernel(const uint8_t* __restrict__ text, const uint2* __restrict__ words,
+                                 const uint32_t* __restrict__ order, uint64_t n, uint32_t len,
+                                 uint8_t* __restrict__ out, int nl) {
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= n) return;
+  const uint2 w = words[order ? order[gw] : gw];
+  uint8_t* dst = out + gw * (uint64_t)(len + nl);
+  for (uint32_t b = lane; b < len; b += 32) dst[b] = text[(uint64_t)w.x + b];
+  if (nl && lane == 0) dst[len] = '\n';
+}
+
+void launch_emit_long(const uint8_t* text, const uint2* words, const uint32_t* order, uint64_t n,
+                      uint32_t len, uint8_t* out, int with_newline, cudaStream_t st) {
+  if (!n) return;
+  uint64_t threads = n * 32;
+  emit_long_kernel<<<(uint32_t)((threads + 255) / 256), 256, 0, st>>>(text, words, order, n, len,
+                                                                      out, with_newline);
+}
+
+// keys[i] = big-endian lane `lane` of word words[order[i]] (zero past len).
+__global__ void lane_keys_kernel(const uint8_t* __restrict__ text, const uint2* __restrict__ words,
+                                 const uint32_t* __restrict__ order, uint64_t n, uint32_t lane,
+                                 uint64_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint2 w = words[order ? order[i] : i];
+    uint64_t k = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t b = lane * 8 + q;
+      uint64_t byte = b < w.y ? text[(uint64_t)w.x + b] : 0;
+      k |= byte << (56 - 8 * q);
+    }
+    keys[i] = k;
+  }
+}
+
+void launch_lane_keys(const uint8_t* text, const uint2* words, const uint32_t* order, uint64_t n,
+                      uint32_t lane, uint64_t* keys, cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  lane_keys_kernel<<<blocks, 256, 0, st>>>(text, words, order, n, lane, keys);
+}
+
+__global__ void gather_u32_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                                  uint64_t n, uint32_t* __restrict__ dst) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+void launch_gather_u32(const uint32_t* src, const uint32_t* perm, uint64_t n, uint32_t* dst,
+                       cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  gather_u32_kernel<<<blocks, 256, 0, st>>>(src, perm, n, dst);
+}
+
+__global__ void iota_keys_kernel(const uint32_t* __restrict__ vals, uint64_t n,
+                                 uint64_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = vals ? vals[i] : i;
+}
+
+void launch_iota_keys(const uint32_t* vals, uint64_t n, uint64_t* keys, cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  iota_keys_kernel<<<blocks, 256, 0, st>>>(vals, n, keys);
+}
+
+__global__ void len_keys_kernel(const uint2* __restrict__ words, uint64_t n,
+                                uint64_t* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = words[i].y;
+}
+
+// kmax[slot] = max over the group of (rank[i] - i): the early-exit bound K
+// when rank[i] is the original position of the word now at position i.
+__global__ void rank_kmax_kernel(const uint32_t* __restrict__ rank, uint64_t off, uint64_t n,
+                                 long long* __restrict__ kmax) {
+  long long k = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    k = max(k, (long long)rank[off + i] - (long long)(off + i));
+  for (int o = 16; o > 0; o >>= 1) k = max(k, (long long)__shfl_xor_sync(0xffffffffu, k, o));
+  if ((threadIdx.x & 31) == 0 && k > 0) atomicMax(kmax, k);
+}
+
+void launch_rank_kmax(const uint32_t* rank, uint64_t off, uint64_t n, long long* kmax,
+                      cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+  rank_kmax_kernel<<<blocks, 256, 0, st>>>(rank, off, n, kmax);
+}
+
+// (start, len) of row i of an (n, width) block starting at byte `base`.
+__global__ void rows_longlist_kernel(uint64_t base, uint64_t n, uint32_t width,
+                                     uint2* __restrict__ words) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    words[i] = make_uint2((uint32_t)(base + i * width), width);
+}
+
+void launch_rows_longlist(uint64_t base, uint64_t n, uint32_t width, uint2* words,
+                          cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  rows_longlist_kernel<<<blocks, 256, 0, st>>>(base, n, width, words);
+}
+
+// words_out[i] = words_in[perm[i]]
+__global__ void gather_u2_kernel(const uint2* __restrict__ src, const uint32_t* __restrict__ perm,
+                                 uint64_t n, uint2* __restrict__ dst) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+void launch_gather_u2(const uint2* src, const uint32_t* perm, uint64_t n, uint2* dst,
+                      cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  gather_u2_kernel<<<blocks, 256, 0, st>>>(src, perm, n, dst);
+}
+
+__global__ void iota_u32_kernel(uint32_t* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = (uint32_t)i;
+}
+
+void launch_iota_u32(uint32_t* dst, uint64_t n, cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  iota_u32_kernel<<<blocks, 256, 0, st>>>(dst, n);
+}
+
+void launch_len_keys(const uint2* words, uint64_t n, uint64_t* keys, cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  len_keys_kernel<<<blocks, 256, 0, st>>>(words, n, keys);
+}
+
+}  // namespace ws

@@ -1,0 +1,449 @@
+// Ingest: raw text -> per-length buckets of packed keys, in one two-pass
+// stream over the text.
+//
+// Replaces, for the flat layout:
+//   tokenize       = WORD_RE.findall        (ingest.py:15, 26-28)
+//   _group_by_length (stable, corpus order) (store.py:78-82)
+//   build_flat     (count, L) uint8 blocks   (store.py:90-96)
+//
+//   K1 count_kernel   : 4 KiB chunk per CTA, uint4 loads, SWAR byte classes,
+//                       start/end bitmasks, warp-aggregated length histogram
+//                       -> hist[bin][chunk]
+//   K2 scan_kernel    : one CTA per bin row: exclusive scan over chunks
+//   K3 scatter_kernel : re-tokenise the chunk from smem, stable per-bin rank
+//                       (warp word list + __match_any_sync), pack big-endian
+//                       uint64 lanes, write at bucket_base + rank.
+// A word belongs to the chunk that holds its first byte; a word running past
+// its chunk is measured by scanning forward in global memory (the text is
+// zero padded, and zero is a separator).
+#include "ws_common.cuh"
+#include "ws_kernels.h"
+
+namespace ws {
+
+constexpr int kChunk = 4096;
+constexpr int kIngestThreads = 256;  // 16 bytes per thread
+constexpr int kWarps = kIngestThreads / 32;
+constexpr int kMaxWordsPerWarp = 256;  // 512 bytes per warp, <= 1 start per 2 bytes
+
+__device__ __forceinline__ uint32_t bin_of_len(uint32_t len) {
+  return len <= (uint32_t)kMaxPackedLen ? len - 1 : (uint32_t)kLongBin;
+}
+
+// Length of the alnum run starting at text[pos] (pos is known alnum or not).
+__device__ uint32_t run_length_from(const uint8_t* __restrict__ text, uint64_t pos) {
+  uint32_t len = 0;
+  // bring pos to a 16-byte boundary with byte steps
+  while ((pos & 15) != 0) {
+    if (!is_alnum_byte(text[pos])) return len;
+    ++len;
+    ++pos;
+  }
+  while (true) {
+    uint4 v = *reinterpret_cast<const uint4*>(text + pos);
+    uint32_t m = alnum_mask16(v);
+    if (m != 0xFFFFu) return len + __ffs(~m) - 1;
+    len += 16;
+    pos += 16;
+  }
+}
+
+// Starts/ends of the thread's 16-byte segment plus word lengths.
+struct Segment16 {
+  uint32_t starts;  // bit i: byte i starts a word
+  uint32_t ends;    // bit i: byte i ends a word
+  uint64_t base;    // text offset of byte 0
+};
+
+__device__ __forceinline__ Segment16 classify16(const uint8_t* __restrict__ text, uint64_t n,
+                                                 uint64_t base, uint4& v_out) {
+  Segment16 s;
+  s.base = base;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  uint32_t prev = 0, next = 0;
+  if (base < n) {
+    v = *reinterpret_cast<const uint4*>(text + base);
+    prev = base > 0 ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
+    next = (uint32_t)is_alnum_byte(text[base + 16]);
+  }
+  v_out = v;
+  uint32_t m = alnum_mask16(v);
+  s.starts = m & ~((m << 1) | prev) & 0xFFFFu;
+  s.ends = m & ~((m >> 1) | (next << 15)) & 0xFFFFu;
+  return s;
+}
+
+// Length of the word starting at bit i of a segment.
+__device__ __forceinline__ uint32_t word_len(const uint8_t* __restrict__ text, const Segment16& s,
+                                             int i) {
+  uint32_t rest = s.ends >> i;
+  if (rest) return (uint32_t)__ffs(rest);
+  return (uint32_t)(16 - i) + run_length_from(text, s.base + 16);
+}
+
+__global__ void __launch_bounds__(kIngestThreads)
+count_kernel(const uint8_t* __restrict__ text, uint64_t n, uint32_t* __restrict__ hist,
+             uint32_t nchunks) {
+  __shared__ uint32_t shist[kHistRows];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (tid < kHistRows) shist[tid] = 0;
+  __syncthreads();
+  const uint64_t chunk = blockIdx.x;
+  uint4 v;
+  Segment16 seg = classify16(text, n, chunk * kChunk + (uint64_t)tid * 16, v);
+  uint32_t s = seg.starts;
+  // total words of the chunk
+  uint32_t c = __popc(s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0 && c) atomicAdd(&shist[kNumBins], c);
+  // warp-aggregated histogram: one match per word slot, one atomic per distinct bin
+  while (__any_sync(0xffffffffu, s != 0)) {
+    uint32_t key = 0xFFFFFFFFu;
+    if (s) {
+      int i = __ffs(s) - 1;
+      s &= s - 1;
+      key = bin_of_len(word_len(text, seg, i));
+    }
+    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&shist[key], __popc(peers));
+  }
+  __syncthreads();
+  if (tid < kHistRows) hist[(uint64_t)tid * nchunks + chunk] = shist[tid];
+}
+
+// Exclusive scan of one histogram row over chunks; totals[row] = row sum.
+__global__ void __launch_bounds__(1024)
+scan_kernel(const uint32_t* __restrict__ hist, uint32_t* __restrict__ off,
+            uint32_t* __restrict__ totals, uint32_t nchunks) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t row = blockIdx.x;
+  const uint32_t* h = hist + row * nchunks;
+  uint32_t* o = off + row * nchunks;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  constexpr int kItems = 4;
+  for (uint32_t tile = 0; tile < nchunks; tile += 1024 * kItems) {
+    uint32_t vals[kItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      uint32_t j = tile + tid * kItems + k;
+      vals[k] = j < nchunks ? h[j] : 0u;
+      sum += vals[k];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t ws_ = warp_sums[lane];
+      uint32_t wi = ws_;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
+        if (lane >= d) wi += t;
+      }
+      warp_sums[lane] = wi - ws_;  // exclusive
+    }
+    __syncthreads();
+    uint32_t carry = carry_s;
+    uint32_t run = carry + warp_sums[wid] + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      uint32_t j = tile + tid * kItems + k;
+      if (j < nchunks) o[j] = run;
+      run += vals[k];
+    }
+    __syncthreads();
+    if (tid == 1023) carry_s = run;
+    __syncthreads();
+  }
+  if (tid == 0) totals[row] = carry_s;
+}
+
+// Pack up to 32 bytes of a word (from a 4-byte aligned smem chunk) into
+// big-endian uint64 lanes, zero padded past L.
+template <int LANES>
+__device__ __forceinline__ void pack_from_smem(const uint32_t* __restrict__ c32, uint32_t start,
+                                               uint32_t L, uint64_t* __restrict__ dst) {
+#pragma unroll
+  for (int l = 0; l < LANES; ++l) {
+    uint32_t q = start + 8 * l;
+    uint32_t w0 = c32[q >> 2], w1 = c32[(q >> 2) + 1], w2 = c32[(q >> 2) + 2];
+    uint32_t sh = (q & 3) * 8;
+    uint32_t lo = __funnelshift_r(w0, w1, sh);
+    uint32_t hi = __funnelshift_r(w1, w2, sh);
+    uint64_t k = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+    int r = (int)L - 8 * l;
+    if (r < 8) k &= ~0ull << (64 - 8 * r);
+    dst[l] = k;
+  }
+}
+
+__global__ void __launch_bounds__(kIngestThreads)
+scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __restrict__ off,
+               uint32_t nchunks, ScatterParams p) {
+  __shared__ __align__(16) uint32_t chunk32[(kChunk + 64) / 4];
+  __shared__ uint16_t wstart[kWarps][kMaxWordsPerWarp];
+  __shared__ uint32_t wlen[kWarps][kMaxWordsPerWarp];
+  __shared__ uint32_t wpos[kWarps][kMaxWordsPerWarp];
+  __shared__ uint32_t wcnt[kWarps][kHistRows];
+  __shared__ uint32_t wtot[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t chunk = blockIdx.x;
+  const uint64_t cbase = chunk * kChunk;
+  for (int i = tid; i < kWarps * kHistRows; i += kIngestThreads) (&wcnt[0][0])[i] = 0;
+
+  uint4 v;
+  Segment16 seg = classify16(text, n, cbase + (uint64_t)tid * 16, v);
+  reinterpret_cast<uint4*>(chunk32)[tid] = v;
+  if (tid < 4) {
+    uint64_t a = cbase + kChunk + 16 * tid;
+    reinterpret_cast<uint4*>(chunk32)[kChunk / 16 + tid] =
+        a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
+  }
+  // warp-local word list in corpus order (lane-major, then bit order)
+  uint32_t c = __popc(seg.starts);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  uint32_t slot = incl - c;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  {
+    uint32_t s = seg.starts;
+    while (s) {
+      int i = __ffs(s) - 1;
+      s &= s - 1;
+      wstart[wid][slot] = (uint16_t)(tid * 16 + i);
+      wlen[wid][slot] = word_len(text, seg, i);
+      ++slot;
+    }
+  }
+  if (lane == 0) wtot[wid] = total;
+  __syncthreads();  // also publishes chunk32 and zeroed wcnt
+  // pass 1: stable rank inside the warp per bin
+  for (uint32_t b = 0; b < total; b += 32) {
+    uint32_t j = b + lane;
+    uint32_t key = j < total ? bin_of_len(wlen[wid][j]) : 0xFFFFFFFFu;
+    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    if (key != 0xFFFFFFFFu) wpos[wid][j] = wcnt[wid][key] + rank;
+    __syncwarp();
+    if (key != 0xFFFFFFFFu && lane == 31 - __clz(peers)) wcnt[wid][key] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // exclusive scan of per-warp counts over warps, plus the chunk's offsets
+  if (tid < kHistRows) {
+    uint32_t run = (tid == kNumBins) ? off[(uint64_t)kNumBins * nchunks + chunk]
+                                     : off[(uint64_t)tid * nchunks + chunk];
+    for (int w = 0; w < kWarps; ++w) {
+      uint32_t cw = (tid == kNumBins) ? wtot[w] : wcnt[w][tid];
+      wcnt[w][tid] = run;
+      run += cw;
+    }
+  }
+  __syncthreads();
+  const uint8_t* c8 = reinterpret_cast<const uint8_t*>(chunk32);
+  (void)c8;
+  for (uint32_t b = 0; b < total; b += 32) {
+    uint32_t j = b + lane;
+    if (j >= total) break;
+    uint32_t start = wstart[wid][j];
+    uint32_t L = wlen[wid][j];
+    uint32_t bin = bin_of_len(L);
+    if (p.tokens) {
+      uint32_t widx = wcnt[wid][kNumBins] + j;
+      p.tokens[widx] = make_uint2((uint32_t)(cbase + start), L);
+    }
+    if (!p.keys) continue;
+    uint32_t pos = wcnt[wid][bin] + wpos[wid][j];
+    if (bin == (uint32_t)kLongBin) {
+      p.longlist[pos] = make_uint2((uint32_t)(cbase + start), L);
+      continue;
+    }
+    uint64_t* dst = p.keys + p.bin_base[bin] + (uint64_t)pos * lanes_for_len(L);
+    switch (lanes_for_len(L)) {
+      case 1: pack_from_smem<1>(chunk32, start, L, dst); break;
+      case 2: pack_from_smem<2>(chunk32, start, L, dst); break;
+      case 3: pack_from_smem<3>(chunk32, start, L, dst); break;
+      default: pack_from_smem<4>(chunk32, start, L, dst); break;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Word-list ingest (build_flat from a Python list): words are given as one
+// concatenated byte buffer + lengths. starts = exclusive scan of lengths is
+// computed on the host side of the call (cheap) and uploaded with the bytes.
+
+__global__ void words_count_kernel(const uint32_t* __restrict__ lens, uint64_t nwords,
+                                   uint32_t* __restrict__ counts /*[kNumBins]*/) {
+  __shared__ uint32_t sc[kNumBins];
+  if (threadIdx.x < kNumBins) sc[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nwords;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t L = lens[i];
+    if (L) atomicAdd(&sc[bin_of_len(L)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumBins && sc[threadIdx.x]) atomicAdd(&counts[threadIdx.x], sc[threadIdx.x]);
+}
+
+// Stable scatter of a word list: one warp walks a contiguous range of words
+// in order (ranks via __match_any_sync), per-warp per-bin base offsets come
+// from a prior count pass over the same ranges (warp_hist) + scan.
+__global__ void words_warp_hist_kernel(const uint32_t* __restrict__ lens, uint64_t nwords,
+                                       uint32_t words_per_warp, uint32_t* __restrict__ whist,
+                                       uint32_t nwarps_total) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (gw >= nwarps_total) return;
+  uint32_t cnt = 0;  // lane b keeps bin b's count (bins < 32), lane 0 also bin 32
+  uint32_t cnt_long = 0;
+  uint64_t w0 = gw * words_per_warp, w1 = min(nwords, w0 + words_per_warp);
+  for (uint64_t b = w0; b < w1; b += 32) {
+    uint64_t j = b + lane;
+    uint32_t key = j < w1 ? bin_of_len(lens[j]) : 0xFFFFFFFFu;
+    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    // every lane learns the count for bin == lane via ballot
+#pragma unroll 1
+    for (int bin = 0; bin < 32; ++bin) {
+      uint32_t m = __ballot_sync(0xffffffffu, key == (uint32_t)bin);
+      if (lane == bin) cnt += __popc(m);
+    }
+    uint32_t ml = __ballot_sync(0xffffffffu, key == (uint32_t)kLongBin);
+    cnt_long += __popc(ml);
+    (void)peers;
+  }
+  whist[(uint64_t)lane * nwarps_total + gw] = cnt;
+  if (lane == 0) whist[(uint64_t)kLongBin * nwarps_total + gw] = cnt_long;
+}
+
+__global__ void words_scatter_kernel(const uint8_t* __restrict__ bytes,
+                                     const uint64_t* __restrict__ starts,
+                                     const uint32_t* __restrict__ lens, uint64_t nwords,
+                                     uint32_t words_per_warp, const uint32_t* __restrict__ woff,
+                                     uint32_t nwarps_total, ScatterParams p) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  if (gw >= nwarps_total) return;
+  uint32_t base_mine = lane < kNumBins ? woff[(uint64_t)lane * nwarps_total + gw] : 0;
+  uint32_t base_long = woff[(uint64_t)kLongBin * nwarps_total + gw];
+  uint64_t w0 = gw * words_per_warp, w1 = min(nwords, w0 + words_per_warp);
+  for (uint64_t b = w0; b < w1; b += 32) {
+    uint64_t j = b + lane;
+    uint32_t L = j < w1 ? lens[j] : 0;
+    uint32_t key = (j < w1 && L) ? bin_of_len(L) : 0xFFFFFFFFu;
+    uint32_t peers = __match_any_sync(0xffffffffu, key);
+    uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+    // fetch this bin's running base from the lane that owns it
+    uint32_t src = key < 32 ? key : 0;
+    uint32_t bb = __shfl_sync(0xffffffffu, base_mine, src);
+    if (key == (uint32_t)kLongBin) bb = base_long;
+    // advance owners' bases
+    uint32_t add = 0;
+#pragma unroll 1
+    for (int bin = 0; bin < 32; ++bin) {
+      uint32_t m = __ballot_sync(0xffffffffu, key == (uint32_t)bin);
+      if (lane == bin) add = __popc(m);
+    }
+    uint32_t ml = __ballot_sync(0xffffffffu, key == (uint32_t)kLongBin);
+    base_mine += add;
+    uint32_t pos = bb + rank;
+    base_long += __popc(ml);
+    if (key == 0xFFFFFFFFu) continue;
+    uint64_t st = starts[j];
+    if (key == (uint32_t)kLongBin) {
+      p.longlist[pos] = make_uint2((uint32_t)st, L);
+      continue;
+    }
+    int lanes = lanes_for_len(L);
+    uint64_t* dst = p.keys + p.bin_base[key] + (uint64_t)pos * lanes;
+    for (int l = 0; l < lanes; ++l) {
+      uint64_t k = 0;
+      for (int q = 0; q < 8; ++q) {
+        uint32_t bi = 8 * l + q;
+        uint64_t byte = bi < L ? bytes[st + bi] : 0;
+        k |= byte << (56 - 8 * q);
+      }
+      dst[l] = k;
+    }
+  }
+}
+
+// Rows (n x width) -> packed keys of one segment.
+__global__ void pack_rows_kernel(const uint8_t* __restrict__ rows, uint64_t n, uint32_t width,
+                                 uint64_t* __restrict__ keys) {
+  const int lanes = lanes_for_len(width);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t* r = rows + i * width;
+    for (int l = 0; l < lanes; ++l) {
+      uint64_t k = 0;
+      for (int q = 0; q < 8; ++q) {
+        uint32_t bi = 8 * l + q;
+        uint64_t byte = bi < width ? r[bi] : 0;
+        k |= byte << (56 - 8 * q);
+      }
+      keys[i * lanes + l] = k;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+void launch_count(const uint8_t* text, uint64_t n, uint32_t* hist, uint32_t nchunks,
+                  cudaStream_t st) {
+  if (nchunks) count_kernel<<<nchunks, kIngestThreads, 0, st>>>(text, n, hist, nchunks);
+}
+
+void launch_scan(const uint32_t* hist, uint32_t* off, uint32_t* totals, uint32_t nchunks,
+                 int rows, cudaStream_t st) {
+  scan_kernel<<<rows, 1024, 0, st>>>(hist, off, totals, nchunks);
+}
+
+void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32_t nchunks,
+                    const ScatterParams& p, cudaStream_t st) {
+  if (nchunks) scatter_kernel<<<nchunks, kIngestThreads, 0, st>>>(text, n, off, nchunks, p);
+}
+
+uint32_t chunk_count(uint64_t n) { return (uint32_t)((n + kChunk - 1) / kChunk); }
+
+void launch_words_hist(const uint32_t* lens, uint64_t nwords, uint32_t wpw, uint32_t* whist,
+                       uint32_t nwarps, cudaStream_t st) {
+  if (!nwarps) return;
+  uint32_t blocks = (nwarps * 32 + 255) / 256;
+  words_warp_hist_kernel<<<blocks, 256, 0, st>>>(lens, nwords, wpw, whist, nwarps);
+}
+
+void launch_words_scatter(const uint8_t* bytes, const uint64_t* starts, const uint32_t* lens,
+                          uint64_t nwords, uint32_t wpw, const uint32_t* woff, uint32_t nwarps,
+                          const ScatterParams& p, cudaStream_t st) {
+  if (!nwarps) return;
+  uint32_t blocks = (nwarps * 32 + 255) / 256;
+  words_scatter_kernel<<<blocks, 256, 0, st>>>(bytes, starts, lens, nwords, wpw, woff, nwarps, p);
+}
+
+void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t* keys,
+                      cudaStream_t st) {
+  if (!n) return;
+  uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  pack_rows_kernel<<<blocks, 256, 0, st>>>(rows, n, width, keys);
+}
+
+}  // namespace ws

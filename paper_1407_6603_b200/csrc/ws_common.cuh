@@ -1,0 +1,95 @@
+// Shared definitions for libwsort_b200: packed keys, byte classes, segments.
+//
+// Data layout in HBM:
+//   * text       : the corpus bytes, padded with >= 64 zero bytes (zero is a
+//                  separator, so scans past the end always terminate).
+//   * keys       : one region per length bucket L <= 32, 16-byte aligned;
+//                  word i of the bucket is LANES(L) = ceil(L/8) consecutive
+//                  uint64 lanes, bytes packed big-endian and zero-padded, so
+//                  unsigned integer order == the reference's raw byte order
+//                  (compare_words, engine.py:62-69; _bubble_rows byte loop,
+//                  engine.py:101-104).
+//   * idx        : optional uint32 payload = the word's corpus rank inside its
+//                  bucket (stats mode: inversion count, early-exit pass bound).
+//   * long words : L > 32 are kept as (start, len) pairs into the byte buffer
+//                  and sorted by an LSD pass sequence over 8-byte lanes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ws {
+
+constexpr int kMaxPackedLen = 32;           // lengths handled by packed keys
+constexpr int kLongBin = kMaxPackedLen;     // bin index of the L > 32 class
+constexpr int kNumBins = kMaxPackedLen + 1; // bins 0..31 -> L = 1..32, bin 32 = long
+constexpr int kHistRows = kNumBins + 1;     // + one row of per-chunk word totals
+constexpr int kTextPad = 128;               // zero padding after the text
+
+__host__ __device__ constexpr int lanes_for_len(int L) { return (L + 7) >> 3; }
+
+// Byte class of the reference tokenizer WORD_RE = rb"[A-Za-z0-9]+"
+// (ingest.py:15): every other byte, including 0x00 and >= 0x80, separates.
+__device__ __forceinline__ bool is_alnum_byte(uint32_t b) {
+  uint32_t f = b | 0x20u;
+  return (b - 0x30u < 10u) || (f - 0x61u < 26u);
+}
+
+// 4 bytes -> 4-bit mask (bit k = byte k is [A-Za-z0-9]) using SWAR range checks.
+__device__ __forceinline__ uint32_t alnum_mask4(uint32_t v) {
+  const uint32_t hi = v & 0x80808080u;            // bytes >= 0x80 never match
+  const uint32_t x = v & 0x7f7f7f7fu;
+  // digits: 0x30 <= x <= 0x39
+  const uint32_t d = (x + 0x50505050u) & ~(x + 0x46464646u);
+  // letters: 0x61 <= (x | 0x20) <= 0x7a
+  const uint32_t f = x | 0x20202020u;
+  const uint32_t l = (f + 0x1f1f1f1fu) & ~(f + 0x05050505u);
+  uint32_t m = (d | l) & 0x80808080u & ~hi;
+  // gather bit 7 of each byte into bits 0..3
+  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+}
+
+__device__ __forceinline__ uint32_t alnum_mask16(uint4 v) {
+  return alnum_mask4(v.x) | (alnum_mask4(v.y) << 4) | (alnum_mask4(v.z) << 8) |
+         (alnum_mask4(v.w) << 12);
+}
+
+template <int LANES>
+struct Key {
+  uint64_t w[LANES];
+};
+
+template <int LANES>
+__device__ __forceinline__ bool key_lt(const Key<LANES>& a, const Key<LANES>& b) {
+#pragma unroll
+  for (int i = 0; i < LANES; ++i) {
+    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  }
+  return false;
+}
+
+template <int LANES>
+__device__ __forceinline__ bool key_le(const Key<LANES>& a, const Key<LANES>& b) {
+  return !key_lt<LANES>(b, a);
+}
+
+template <int LANES>
+__device__ __forceinline__ Key<LANES> key_max() {
+  Key<LANES> k;
+#pragma unroll
+  for (int i = 0; i < LANES; ++i) k.w[i] = ~0ull;
+  return k;
+}
+
+// One sort segment: a bucket (or a long-word group / LSD pass) whose keys
+// are contiguous. Offsets are in elements of the segment's own key width.
+struct SegDesc {
+  uint64_t key_off;     // element offset of the segment in the key arena (LANES units)
+  uint64_t idx_off;     // element offset in the uint32 idx arena
+  uint32_t n;           // number of words
+  uint32_t tile_begin;  // first work item (tile / output block) of this segment
+  uint32_t stat_slot;   // slot in the per-segment stats arrays
+  uint32_t idx_base;    // value of the idx payload for the segment's first word
+};
+
+}  // namespace ws

@@ -1,0 +1,82 @@
+// Internal launcher declarations shared by the .cu translation units.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ws_common.cuh"
+
+namespace ws {
+
+struct ScatterParams {
+  uint64_t bin_base[kNumBins];  // element offsets (uint64 units) of each bin's key region
+  uint64_t* keys;               // key arena, or nullptr (tokens-only mode)
+  uint2* longlist;              // (start, len) of words with L > 32, corpus order
+  uint2* tokens;                // optional (start, len) per word in corpus order
+};
+
+// ingest.cu
+uint32_t chunk_count(uint64_t n);
+void launch_count(const uint8_t* text, uint64_t n, uint32_t* hist, uint32_t nchunks,
+                  cudaStream_t st);
+void launch_scan(const uint32_t* hist, uint32_t* off, uint32_t* totals, uint32_t nchunks,
+                 int rows, cudaStream_t st);
+void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32_t nchunks,
+                    const ScatterParams& p, cudaStream_t st);
+void launch_words_hist(const uint32_t* lens, uint64_t nwords, uint32_t wpw, uint32_t* whist,
+                       uint32_t nwarps, cudaStream_t st);
+void launch_words_scatter(const uint8_t* bytes, const uint64_t* starts, const uint32_t* lens,
+                          uint64_t nwords, uint32_t wpw, const uint32_t* woff, uint32_t nwarps,
+                          const ScatterParams& p, cudaStream_t st);
+void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t* keys,
+                      cudaStream_t st);
+
+// sort.cu
+struct SortLaunch {
+  const uint64_t* keys_in;
+  uint64_t* keys_out;
+  const uint32_t* idx_in;  // nullptr for the tile pass (idx = position)
+  uint32_t* idx_out;       // nullptr in keys-only mode
+  const SegDesc* segs;     // device array
+  int nsegs;
+  uint32_t work_items;     // grid size
+  uint32_t run;            // merge: run length being merged (>= tile)
+  unsigned long long* inv; // per stat slot
+  long long* kmax;         // per stat slot
+};
+int tile_size(int lanes);
+void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
+void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);
+
+// emit.cu
+struct EmitSeg {
+  const uint64_t* keys;  // sorted keys of the segment
+  uint64_t out_off;      // byte offset of the segment's first word in the output
+  uint32_t n;
+  uint32_t len;
+  uint32_t block_begin;
+  uint32_t pad_;
+};
+constexpr int kEmitWords = 1024;
+void launch_emit(int lanes, const EmitSeg* segs, int nsegs, uint32_t blocks, uint8_t* out,
+                 int with_newline, cudaStream_t st);
+
+// generic (L > 32) helpers
+void launch_emit_long(const uint8_t* text, const uint2* words, const uint32_t* order,
+                      uint64_t n, uint32_t len, uint8_t* out, int with_newline, cudaStream_t st);
+void launch_lane_keys(const uint8_t* text, const uint2* words, const uint32_t* order,
+                      uint64_t n, uint32_t lane, uint64_t* keys, cudaStream_t st);
+void launch_gather_u32(const uint32_t* src, const uint32_t* perm, uint64_t n, uint32_t* dst,
+                       cudaStream_t st);
+void launch_iota_keys(const uint32_t* order, uint64_t n, uint64_t* keys, cudaStream_t st);
+void launch_len_keys(const uint2* words, uint64_t n, uint64_t* keys, cudaStream_t st);
+void launch_rank_kmax(const uint32_t* rank, uint64_t off, uint64_t n, long long* kmax,
+                      cudaStream_t st);
+void launch_rows_longlist(uint64_t base, uint64_t n, uint32_t width, uint2* words,
+                          cudaStream_t st);
+void launch_gather_u2(const uint2* src, const uint32_t* perm, uint64_t n, uint2* dst,
+                      cudaStream_t st);
+void launch_iota_u32(uint32_t* dst, uint64_t n, cudaStream_t st);
+void set_sort_attributes();
+
+}  // namespace ws

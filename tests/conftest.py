@@ -1,0 +1,39 @@
+import json
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLDEN = ROOT / "tests" / "golden"
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu on the GPU box)")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def golden_tokenize():
+    return json.loads((GOLDEN / "tokenize_kat.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def golden_stats():
+    return json.loads((GOLDEN / "stats_kat.json").read_text())
+
+
+@pytest.fixture(scope="session")
+def golden_configs():
+    return json.loads((GOLDEN / "configs.json").read_text())
+
+
+def config_text(rec: dict) -> bytes:
+    from paper_1407_6603_b200 import synth
+
+    text = synth.generate(rec["config"])
+    if rec.get("prefix_words"):
+        text = synth.prefix(text, rec["prefix_words"])
+    return text

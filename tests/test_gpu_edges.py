@@ -1,0 +1,120 @@
+"""GPU edge cases: empty/ragged inputs, chunk/tile boundaries, long words,
+separators, bucket sizes around every tile size and merge level."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_1407_6603_b200 import _native, synth
+from paper_1407_6603_b200.ingest import tokenize
+from paper_1407_6603_b200.pipeline import DeviceCorpus, sort_text
+
+pytestmark = pytest.mark.gpu
+
+
+def check_text(text: bytes, stats: bool = True):
+    want, info = oracle.sort_text(text, mode="fast", max_len=2048)
+    assert sort_text(text) == want
+    assert tokenize(text) == oracle.tokenize(text)
+    if stats:
+        dc = DeviceCorpus()
+        dc.ingest(text)
+        dc.sort(want_stats=True)
+        naive = dc.stats(naive=True)
+        early = dc.stats(naive=False)
+        for L, (n, inv, K, c, s, p) in info.items():
+            assert naive[L] == (c, s, p), L
+            P = min(K + 1, n - 1) if n >= 2 else 0
+            exp = (P * (n - 1) - P * (P - 1) // 2, inv, P) if n >= 2 else (0, 0, 0)
+            assert early[L] == exp, L
+        assert dc.payload() == want
+
+
+@pytest.mark.parametrize("text", [
+    b"", b" ", b"...", b"\x00\x80\xff", b"a", b"a b", b"b a cc", b"pear Apple fig",
+    b"word " * 1000, b"z" * 4096, b"z" * 4097, b"q" * 5000 + b" " + b"r" * 33,
+])
+def test_small_texts(text):
+    check_text(text)
+
+
+def test_separator_bytes():
+    rng = np.random.default_rng(5)
+    seps = np.frombuffer(b" \t\n.,?!'\"-\x00\x80\xff\x7f@[`{/:", dtype=np.uint8)
+    al = np.frombuffer(synth.ALNUM, dtype=np.uint8)
+    for n in (1, 15, 16, 17, 31, 33, 4095, 4096, 4097, 12293, 100_003):
+        t = al[rng.integers(0, 62, n)]
+        m = rng.random(n) < 0.25
+        t[m] = seps[rng.integers(0, len(seps), int(m.sum()))]
+        check_text(t.tobytes())
+
+
+def test_words_crossing_chunk_boundaries():
+    # words straddling the 16-byte, 512-byte (warp) and 4096-byte (CTA) edges
+    parts = []
+    for edge in (16, 512, 4096, 8192):
+        pad = b"x " * ((edge - 7) // 2)
+        parts.append(pad + b" ab" + b"C" * 9 + b"d" * 30 + b" ")
+    check_text(b"".join(parts) * 3)
+
+
+@pytest.mark.parametrize("L", [1, 7, 8, 9, 16, 17, 24, 25, 32, 33, 40, 64, 65, 100, 1000])
+def test_single_length_buckets(L):
+    words = synth.random_words(L, 300, max_len=L, min_len=L)
+    check_text(b" ".join(words))
+
+
+def test_mixed_long_words():
+    rng = np.random.default_rng(11)
+    words = synth.random_words(3, 2000, max_len=90, min_len=1, alphabet=b"abAB01")
+    words += [bytes(rng.choice(list(b"ab"), size=int(L))) for L in rng.integers(33, 300, 200)]
+    rng.shuffle(words)
+    check_text(b"\n".join(words))
+
+
+def test_l1_bucket_all_symbols():
+    al = list(synth.ALNUM)
+    rng = np.random.default_rng(1)
+    check_text(b" ".join(bytes([al[i]]) for i in rng.integers(0, 62, 20000)))
+
+
+@pytest.mark.parametrize("n", [2047, 2048, 2049, 4095, 4096, 4097, 8191, 8193,
+                               16385, 65537, 262145])
+@pytest.mark.parametrize("order", ["random", "descending", "sorted", "dups"])
+def test_bucket_sizes_around_tiles(n, order):
+    for width in (5, 12):  # lanes 1 (T=4096) and 2 (T=2048)
+        rows = synth.bucket_case(n + width, n, width, order)
+        ref = rows.copy()
+        (c, s, p), inv, K = oracle.sort_rows_fast(ref, naive=True)
+        got = rows.copy()
+        stats, perms = _native.sort_blocks([got], True, want_perms=True)
+        assert np.array_equal(got, ref)
+        assert tuple(int(x) for x in stats[0]) == (c, s, p)
+        assert np.array_equal(rows[perms[0].astype(np.int64)], ref)
+        early, _ = _native.sort_blocks([rows.copy()], False)
+        P = min(K + 1, n - 1)
+        assert tuple(int(x) for x in early[0]) == (P * (n - 1) - P * (P - 1) // 2, inv, P)
+
+
+def test_wide_rows_generic_path():
+    for width in (33, 40, 64, 65, 200):
+        for order in ("random", "descending", "dups"):
+            rows = synth.bucket_case(width, 3000, width, order)
+            ref = rows.copy()
+            st = oracle.bubble_rows(ref, naive=False) if width < 64 else oracle.sort_rows_fast(ref, False)[0]
+            stats, _ = _native.sort_blocks([rows], False)
+            assert np.array_equal(rows, ref)
+            assert tuple(int(x) for x in stats[0]) == tuple(st)
+
+
+def test_arbitrary_bytes_rows():
+    # flat blocks may hold any byte values (0x00, 0xff, ...): unsigned order
+    rng = np.random.default_rng(2)
+    for width in (1, 3, 8, 9, 31):
+        rows = rng.integers(0, 256, size=(5000, width), dtype=np.uint8)
+        rows[::7] = 0xFF
+        rows[::11] = 0
+        ref = rows.copy()
+        st = oracle.sort_rows_fast(ref, True)[0]
+        stats, _ = _native.sort_blocks([rows], True)
+        assert np.array_equal(rows, ref) and tuple(int(x) for x in stats[0]) == st
