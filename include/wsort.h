@@ -58,6 +58,7 @@ void ws_destroy(ws_handle* h);
 /* --- ingest ------------------------------------------------------------ */
 #define WS_INGEST_KEEP_TOKENS 1 /* also keep corpus-order (start, len) tokens */
 #define WS_INGEST_DEVICE_PTR 2  /* `text` is a device pointer                 */
+#define WS_INGEST_RESIDENT 4    /* re-use the text the handle already holds   */
 
 /* tokenize (ingest.py:26-28, WORD_RE = rb"[A-Za-z0-9]+" at ingest.py:15) +
  * stable group-by-length (store.py:78-82) + build_flat (store.py:90-96):
@@ -119,6 +120,13 @@ int ws_emit_rows(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written);
  * bytes in, payload bytes out (host buffers; pinned memory is fastest). */
 int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
                  uint64_t* written);
+
+/* Device-resident variant: re-runs ingest + sort + emit on the text the
+ * handle already holds from its last ws_ingest_text (same n), leaving the
+ * payload in device memory (ws_output_device). No host<->device data copy
+ * except the 136-byte length histogram. */
+int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written);
+int ws_output_device(ws_handle* h, void** dptr, uint64_t* size);
 
 /* --- drop-in for the numba kernel ---------------------------------------- */
 /* _bubble_rows(rows, naive) (engine.py:89-114): sorts the C-contiguous uint8

@@ -19,8 +19,10 @@
  * Parity is pinned against the reference run in this container
  * (the JSON fixtures in tests/golden, produced by tests/golden/make_golden.py).
  */
+#define _POSIX_C_SOURCE 200809L
 #include <stdint.h>
 #include <stdlib.h>
+#include <time.h>
 #include <string.h>
 #include <pthread.h>
 
@@ -164,11 +166,15 @@ static void* sort_worker(void* arg) {
     if (!t) return NULL;
     uint32_t L = t;
     int64_t s[3] = {0, 0, 0}, inv = 0, K = 0;
+    struct timespec t0, t1;
+    clock_gettime(CLOCK_MONOTONIC, &t0);
     if (j->mode == 0) or_bubble_rows(j->flat + j->boff[L], (int64_t)j->cnt[L], (int32_t)L, 1, s);
     else or_sort_rows_fast(j->flat + j->boff[L], (int64_t)j->cnt[L], (int32_t)L, 1, s, &inv, &K);
+    clock_gettime(CLOCK_MONOTONIC, &t1);
     if (j->per_len && (int32_t)L <= j->max_len) {
       int64_t* r = j->per_len + (size_t)L * 8;
       r[0] = (int64_t)j->cnt[L]; r[1] = inv; r[2] = K; r[3] = s[0]; r[4] = s[1]; r[5] = s[2];
+      r[6] = (int64_t)(t1.tv_sec - t0.tv_sec) * 1000000000LL + (t1.tv_nsec - t0.tv_nsec);
     }
   }
 }

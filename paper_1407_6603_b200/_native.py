@@ -34,7 +34,7 @@ EXPORTS = (
     "ws_sort", "ws_bucket_stats", "ws_permutation", "ws_emit_lines", "ws_emit_rows",
     "ws_sort_text", "ws_sort_rows", "ws_sort_blocks", "ws_stats_closed_form",
     "ws_set_profiling", "ws_profile", "ws_profile_reset", "ws_launch_count", "ws_stream",
-    "ws_host_alloc", "ws_host_free",
+    "ws_host_alloc", "ws_host_free", "ws_sort_resident", "ws_output_device",
 )
 
 
@@ -89,6 +89,8 @@ def _declare(lib) -> None:
         "ws_stream": (I, [V, ctypes.POINTER(V)]),
         "ws_host_alloc": (I, [ctypes.c_uint64, ctypes.POINTER(V)]),
         "ws_host_free": (I, [V]),
+        "ws_sort_resident": (I, [V, ctypes.c_uint64, c_u64p]),
+        "ws_output_device": (I, [V, ctypes.POINTER(V), c_u64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -287,6 +289,18 @@ class Handle:
                                     c_void_p(ptr(out)), out.nbytes, ctypes.byref(written)),
               "ws_sort_text")
         return int(written.value)
+
+    def sort_resident(self, n: int) -> int:
+        """Ingest + sort + emit of the text already on the device; payload stays in HBM."""
+        written = ctypes.c_uint64(0)
+        check(self.lib.ws_sort_resident(self.h, int(n), ctypes.byref(written)), "ws_sort_resident")
+        return int(written.value)
+
+    def output_device(self) -> tuple[int, int]:
+        p = c_void_p()
+        size = ctypes.c_uint64(0)
+        check(self.lib.ws_output_device(self.h, ctypes.byref(p), ctypes.byref(size)))
+        return int(p.value or 0), int(size.value)
 
     # -- profiling --------------------------------------------------------------
     def set_profiling(self, on: bool) -> None:

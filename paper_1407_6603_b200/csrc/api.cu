@@ -143,12 +143,14 @@ struct ws_handle {
   DevBuf params;
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
+  uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
 
   uint64_t n_text = 0;
   uint32_t nchunks = 0;
   uint64_t words = 0;
   uint64_t n_long = 0;
   bool have_tokens = false;
+  bool text_valid = false;  // h->text holds the last ingested text (reusable, resident)
   bool ingested = false, sorted = false, have_stats = false;
   uint64_t class_base[kClasses + 1] = {0};  // u64-word base of each lane class region
   uint64_t class_elems[kClasses + 1] = {0};
@@ -424,13 +426,20 @@ int finish_ingest(ws_handle* h) {
 
 int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags) {
   if (n >= (1ull << 32) - kTextPad) return fail(WS_ERR_ARG, "text must be shorter than 4 GiB");
-  if (n && !text) return fail(WS_ERR_ARG, "null text");
+  const bool resident = (flags & WS_INGEST_RESIDENT) != 0;
+  if (resident) {
+    if (!h->text_valid || h->n_text != n || h->text.cap < n + kTextPad)
+      return fail(WS_ERR_STATE, "WS_INGEST_RESIDENT without the same text already on the device");
+  } else if (n && !text) {
+    return fail(WS_ERR_ARG, "null text");
+  }
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
   h->buckets.clear();
   h->n_text = n;
-  WS_CUDA(h->text.ensure(n + kTextPad));
-  {
+  h->text_valid = false;
+  if (!resident) WS_CUDA(h->text.ensure(n + kTextPad));
+  if (!resident) {
     Phase ph(h, "h2d_text", (double)n, (flags & WS_INGEST_DEVICE_PTR) ? 0 : 1);
     if (n)
       WS_CUDA(cudaMemcpyAsync(h->text.p, text, n,
@@ -490,6 +499,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   WS_TRY(check_launch("scatter_kernel"));
   WS_TRY(group_long_words(h, m));
   h->words = total_words;
+  h->text_valid = true;
   return finish_ingest(h);
 }
 
@@ -692,6 +702,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
   if (nblocks < 0) return fail(WS_ERR_ARG, "negative block count");
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
+  h->text_valid = false;
   h->buckets.clear();
   std::vector<int> order(nblocks);
   for (int i = 0; i < nblocks; ++i) {
@@ -785,6 +796,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
 int ingest_words_impl(ws_handle* h, const uint8_t* concat, const uint32_t* lens, uint64_t nwords) {
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
+  h->text_valid = false;
   h->buckets.clear();
   if (nwords && !lens) return fail(WS_ERR_ARG, "null lens");
   std::vector<uint64_t> starts(nwords);
@@ -1045,6 +1057,27 @@ int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, ui
   params_reset(h);  // the ingest synchronised: staging space is free again
   WS_TRY(sort_impl(h, false));
   return emit_to_host(h, true, out, cap, written);
+}
+
+int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
+  WS_TRY(begin_call(h));
+  WS_TRY(ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT));
+  params_reset(h);
+  WS_TRY(sort_impl(h, false));
+  const uint64_t size = emit_size(h, true);
+  WS_CUDA(h->out.ensure(size + 64));
+  WS_TRY(emit_device(h, h->out.as<uint8_t>(), true, nullptr));
+  h->out_size = size;
+  if (written) *written = size;
+  WS_CUDA(cudaStreamSynchronize(h->st));
+  return WS_OK;
+}
+
+int ws_output_device(ws_handle* h, void** dptr, uint64_t* size) {
+  if (!h || !dptr) return fail(WS_ERR_ARG, "null argument");
+  *dptr = h->out.p;
+  if (size) *size = h->out_size;
+  return WS_OK;
 }
 
 int ws_sort_rows(uint8_t* rows, int64_t n, int32_t width, int32_t naive, int64_t stats[3]) {

@@ -52,46 +52,84 @@ __device__ uint32_t run_length_from(const uint8_t* __restrict__ text, uint64_t p
 struct Segment16 {
   uint32_t starts;  // bit i: byte i starts a word
   uint32_t ends;    // bit i: byte i ends a word
-  uint64_t base;    // text offset of byte 0
+  uint32_t cont;    // alnum bytes right after the segment (valid when a start is open)
 };
 
-__device__ __forceinline__ Segment16 classify16(const uint8_t* __restrict__ text, uint64_t n,
-                                                 uint64_t base, uint4& v_out) {
-  Segment16 s;
-  s.base = base;
+// Classify the thread's 16 bytes of a 4 KiB chunk. Neighbour bits come from
+// warp shuffles (a global byte only at warp edges). The length of a word that
+// runs past the thread's segment comes from a segmented suffix scan of the
+// per-thread leading-alnum counts (warp shuffles, then a walk over the
+// following warps' chain heads in shared memory); only a word running past
+// the whole chunk scans global memory, and only its starting thread does so.
+__device__ __forceinline__ Segment16 classify_chunk(const uint8_t* __restrict__ text, uint64_t n,
+                                                    uint64_t cbase, uint4& v_out,
+                                                    uint32_t* s_chain /*[kWarps]*/) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t base = cbase + (uint64_t)tid * 16;
   uint4 v = make_uint4(0, 0, 0, 0);
-  uint32_t prev = 0, next = 0;
-  if (base < n) {
-    v = *reinterpret_cast<const uint4*>(text + base);
-    prev = base > 0 ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
-    next = (uint32_t)is_alnum_byte(text[base + 16]);
-  }
+  if (base < n) v = *reinterpret_cast<const uint4*>(text + base);
   v_out = v;
-  uint32_t m = alnum_mask16(v);
+  const uint32_t m = alnum_mask16(v);
+  const uint32_t up = __shfl_up_sync(0xffffffffu, m, 1);
+  const uint32_t dn = __shfl_down_sync(0xffffffffu, m, 1);
+  uint32_t prev = (up >> 15) & 1u, next = dn & 1u;
+  if (lane == 0) prev = (base > 0 && base - 1 < n) ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
+  if (lane == 31) next = (base + 16 < n) ? (uint32_t)is_alnum_byte(text[base + 16]) : 0u;
+  Segment16 s;
   s.starts = m & ~((m << 1) | prev) & 0xFFFFu;
   s.ends = m & ~((m >> 1) | (next << 15)) & 0xFFFFu;
+  // chain (V, F): alnum run from this segment's byte 0 rightwards; F = ended in the warp
+  uint32_t V = (uint32_t)__ffs(~m) - 1;  // leading alnum bytes (16 when m == 0xFFFF)
+  uint32_t F = V < 16;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t V2 = __shfl_down_sync(0xffffffffu, V, d);
+    const uint32_t F2 = __shfl_down_sync(0xffffffffu, F, d);
+    if (lane + d < 32 && !F) {
+      V += V2;
+      F = F2;
+    }
+  }
+  if (lane == 0) s_chain[wid] = V | (F << 31);
+  uint32_t cV = __shfl_down_sync(0xffffffffu, V, 1);
+  uint32_t cF = __shfl_down_sync(0xffffffffu, F, 1);
+  if (lane == 31) cV = cF = 0;
+  __syncthreads();
+  // only a segment whose last word is open needs its continuation
+  const bool open = s.starts && !(s.ends >> (31 - __clz(s.starts)));  // last start has no end
+  if (open && !cF) {
+    for (int w = wid + 1; w < kWarps; ++w) {
+      const uint32_t c = s_chain[w];
+      cV += c & 0x7FFFFFFFu;
+      if (c >> 31) {
+        cF = 1;
+        break;
+      }
+    }
+    if (!cF) cV += run_length_from(text, cbase + kChunk);
+  }
+  s.cont = cV;
   return s;
 }
 
 // Length of the word starting at bit i of a segment.
-__device__ __forceinline__ uint32_t word_len(const uint8_t* __restrict__ text, const Segment16& s,
-                                             int i) {
-  uint32_t rest = s.ends >> i;
+__device__ __forceinline__ uint32_t word_len(const Segment16& s, int i) {
+  const uint32_t rest = s.ends >> i;
   if (rest) return (uint32_t)__ffs(rest);
-  return (uint32_t)(16 - i) + run_length_from(text, s.base + 16);
+  return (uint32_t)(16 - i) + s.cont;
 }
 
 __global__ void __launch_bounds__(kIngestThreads)
 count_kernel(const uint8_t* __restrict__ text, uint64_t n, uint32_t* __restrict__ hist,
              uint32_t nchunks) {
   __shared__ uint32_t shist[kHistRows];
+  __shared__ uint32_t s_chain[kWarps];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   if (tid < kHistRows) shist[tid] = 0;
-  __syncthreads();
   const uint64_t chunk = blockIdx.x;
   uint4 v;
-  Segment16 seg = classify16(text, n, chunk * kChunk + (uint64_t)tid * 16, v);
+  Segment16 seg = classify_chunk(text, n, chunk * kChunk, v, s_chain);  // has a __syncthreads
   uint32_t s = seg.starts;
   // total words of the chunk
   uint32_t c = __popc(s);
@@ -104,7 +142,7 @@ count_kernel(const uint8_t* __restrict__ text, uint64_t n, uint32_t* __restrict_
     if (s) {
       int i = __ffs(s) - 1;
       s &= s - 1;
-      key = bin_of_len(word_len(text, seg, i));
+      key = bin_of_len(word_len(seg, i));
     }
     uint32_t peers = __match_any_sync(0xffffffffu, key);
     if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&shist[key], __popc(peers));
@@ -171,11 +209,13 @@ scan_kernel(const uint32_t* __restrict__ hist, uint32_t* __restrict__ off,
 
 // Pack up to 32 bytes of a word (from a 4-byte aligned smem chunk) into
 // big-endian uint64 lanes, zero padded past L.
-template <int LANES>
+// (one code path for every width: lanes beyond `lanes` are predicated off, so
+// a warp holding words of several lengths does not diverge)
 __device__ __forceinline__ void pack_from_smem(const uint32_t* __restrict__ c32, uint32_t start,
-                                               uint32_t L, uint64_t* __restrict__ dst) {
+                                               uint32_t L, int lanes, uint64_t* __restrict__ dst) {
 #pragma unroll
-  for (int l = 0; l < LANES; ++l) {
+  for (int l = 0; l < 4; ++l) {
+    if (l >= lanes) break;
     uint32_t q = start + 8 * l;
     uint32_t w0 = c32[q >> 2], w1 = c32[(q >> 2) + 1], w2 = c32[(q >> 2) + 2];
     uint32_t sh = (q & 3) * 8;
@@ -197,6 +237,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   __shared__ uint32_t wpos[kWarps][kMaxWordsPerWarp];
   __shared__ uint32_t wcnt[kWarps][kHistRows];
   __shared__ uint32_t wtot[kWarps];
+  __shared__ uint32_t s_chain[kWarps];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t chunk = blockIdx.x;
@@ -204,7 +245,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   for (int i = tid; i < kWarps * kHistRows; i += kIngestThreads) (&wcnt[0][0])[i] = 0;
 
   uint4 v;
-  Segment16 seg = classify16(text, n, cbase + (uint64_t)tid * 16, v);
+  Segment16 seg = classify_chunk(text, n, cbase, v, s_chain);  // has a __syncthreads
   reinterpret_cast<uint4*>(chunk32)[tid] = v;
   if (tid < 4) {
     uint64_t a = cbase + kChunk + 16 * tid;
@@ -227,7 +268,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
       int i = __ffs(s) - 1;
       s &= s - 1;
       wstart[wid][slot] = (uint16_t)(tid * 16 + i);
-      wlen[wid][slot] = word_len(text, seg, i);
+      wlen[wid][slot] = word_len(seg, i);
       ++slot;
     }
   }
@@ -274,13 +315,9 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
       p.longlist[pos] = make_uint2((uint32_t)(cbase + start), L);
       continue;
     }
-    uint64_t* dst = p.keys + p.bin_base[bin] + (uint64_t)pos * lanes_for_len(L);
-    switch (lanes_for_len(L)) {
-      case 1: pack_from_smem<1>(chunk32, start, L, dst); break;
-      case 2: pack_from_smem<2>(chunk32, start, L, dst); break;
-      case 3: pack_from_smem<3>(chunk32, start, L, dst); break;
-      default: pack_from_smem<4>(chunk32, start, L, dst); break;
-    }
+    const int lanes = lanes_for_len(L);
+    uint64_t* dst = p.keys + p.bin_base[bin] + (uint64_t)pos * lanes;
+    pack_from_smem(chunk32, start, L, lanes, dst);
   }
 }
 
