@@ -17,7 +17,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_NAME = "libwsort_b200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+LIB_PATH = Path(os.environ.get("WSORT_LIB") or Path(__file__).resolve().parent / LIB_NAME)
 
 WS_OK = 0
 WS_ERR_ARG = -1

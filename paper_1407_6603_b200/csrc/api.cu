@@ -12,6 +12,7 @@
 // 8-byte lanes (most significant last), with the text as the byte store.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -131,6 +132,8 @@ struct SegIn {
 struct ws_handle {
   int device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t cs[kClasses + 1] = {nullptr};  // one stream per lane class (cs[0] unused)
+  cudaEvent_t ev_fork = nullptr, ev_join[kClasses + 1] = {nullptr};
   // text / word sources
   DevBuf text;         // corpus bytes (+ padding) or word bytes or rows
   DevBuf starts, lens; // word-list ingest
@@ -141,6 +144,7 @@ struct ws_handle {
   DevBuf stat_inv, stat_k, stat_k_dummy;
   DevBuf out;
   DevBuf params;
+  DevBuf splits[kClasses + 2];  // merge-path splits: [0] main stream, [1..4] class streams
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
   uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
@@ -158,6 +162,7 @@ struct ws_handle {
   std::vector<Bucket> buckets;
 
   bool prof = false;
+  bool serial = false;  // WSORT_SERIAL=1: every kernel on the main stream (diagnostics)
   std::vector<PhaseRec> phases;
   std::vector<cudaEvent_t> event_pool;
   uint64_t launches = 0;
@@ -183,7 +188,9 @@ struct Phase {
   ws_handle* h;
   PhaseRec rec;
   bool on;
-  Phase(ws_handle* hh, const char* name, double bytes, int kind = 0) : h(hh), on(hh->prof) {
+  cudaStream_t st;
+  Phase(ws_handle* hh, const char* name, double bytes, int kind = 0, cudaStream_t s = nullptr)
+      : h(hh), on(hh->prof), st(s ? s : hh->st) {
     if (!on) return;
     rec.name = name;
     rec.bytes = bytes;
@@ -191,13 +198,13 @@ struct Phase {
     rec.launches = 0;
     rec.a = get_event(h);
     rec.b = get_event(h);
-    cudaEventRecord(rec.a, h->st);
+    cudaEventRecord(rec.a, st);
     start_launches = h->launches;
   }
   uint64_t start_launches = 0;
   void end() {
     if (!on) return;
-    cudaEventRecord(rec.b, h->st);
+    cudaEventRecord(rec.b, st);
     rec.launches = (int)(h->launches - start_launches);
     if (rec.kind == 1 && rec.launches == 0) rec.launches = 1;
     h->phases.push_back(rec);
@@ -216,12 +223,15 @@ int check_launch(const char* what) {
 void params_reset(ws_handle* h) { h->param_used = 0; }
 
 template <class T>
-int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev) {
+int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev,
+                  cudaStream_t st = nullptr) {
+  if (!st) st = h->st;
   size_t bytes = v.size() * sizeof(T);
   size_t off = (h->param_used + 255) & ~size_t(255);
   if (off + bytes > h->pin_params.cap || off + bytes > h->params.cap) {
-    // growing needs the stream idle (the old staging bytes may be in flight)
+    // growing needs every stream of the handle idle (old staging bytes may be in flight)
     WS_CUDA(cudaStreamSynchronize(h->st));
+    for (int c = 1; c <= kClasses; ++c) WS_CUDA(cudaStreamSynchronize(h->cs[c]));
     size_t need = std::max<size_t>(2 * (off + bytes), 1 << 20);
     if (need > h->pin_params.cap) {
       h->pin_params.release();
@@ -237,7 +247,7 @@ int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev) {
     memcpy(static_cast<uint8_t*>(h->pin_params.p) + off, v.data(), bytes);
     WS_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(h->params.p) + off,
                             static_cast<uint8_t*>(h->pin_params.p) + off, bytes,
-                            cudaMemcpyHostToDevice, h->st));
+                            cudaMemcpyHostToDevice, st));
   }
   *dev = reinterpret_cast<const T*>(static_cast<uint8_t*>(h->params.p) + off);
   h->param_used = off + bytes;
@@ -259,7 +269,9 @@ int begin_call(ws_handle* h) {
 
 int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* keys0,
                   uint64_t* keys1, uint32_t* idx0, uint32_t* idx1, bool stats,
-                  unsigned long long* inv, long long* kmax, const char* tag) {
+                  unsigned long long* inv, long long* kmax, const char* tag,
+                  cudaStream_t st = nullptr) {
+  if (!st) st = h->st;
   std::vector<SegIn*> live;
   for (auto& s : segs) {
     s.final_buf = 0;
@@ -267,6 +279,11 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
   }
   if (live.empty()) return WS_OK;
   const uint32_t T = (uint32_t)tile_size(lanes);
+  const uint32_t TM = (uint32_t)merge_tile_size(lanes);
+  uint64_t total_tiles = 0;  // upper bound of the work items of any pass
+  for (auto* s : live) total_tiles += 2 * ((s->n + std::min(T, TM) - 1) / std::min(T, TM)) + 4;
+  DevBuf& split_buf = h->splits[st == h->st ? 0 : (lanes & 3) + 1];
+  WS_CUDA(split_buf.ensure((total_tiles + 1) * 4));
   uint64_t* kb[2] = {keys0, keys1};
   uint32_t* ib[2] = {idx0, idx1};
   // pass 0 = tile sort; pass p >= 1 merges runs of T << (p-1)
@@ -289,13 +306,18 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
       sd.stat_slot = s->stat_slot;
       sd.idx_base = s->idx_base;
       d.push_back(sd);
-      work += (uint32_t)((s->n + T - 1) / T);
+      if (p == 0) {
+        work += (uint32_t)((s->n + T - 1) / T);
+      } else {  // ceil(2R / TM) tiles for each pair of runs (sort.cu pair_geom)
+        const uint64_t pairs = (s->n + 2 * run - 1) / (2 * run);
+        work += (uint32_t)(pairs * ((2 * run + TM - 1) / TM));
+      }
       bytes += 2.0 * s->n * lanes * 8 + (stats ? (p == 0 ? 4.0 : 8.0) * s->n : 0.0);
       s->final_buf = (p + 1) & 1;
     }
     if (d.empty()) break;
     const SegDesc* dd;
-    WS_TRY(params_upload(h, d, &dd));
+    WS_TRY(params_upload(h, d, &dd, st));
     const int in = p & 1, out = in ^ 1;
     SortLaunch a;
     a.keys_in = kb[in];
@@ -308,12 +330,17 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
     a.run = (uint32_t)run;
     a.inv = inv;
     a.kmax = kmax;
+    a.splits = split_buf.as<uint32_t>();
     char name[32];
     snprintf(name, sizeof name, "%s%s_l%d", tag, p == 0 ? "tile" : "merge", lanes);
-    Phase ph(h, name, bytes);
-    if (p == 0) launch_tile_sort(lanes, a, h->st);
-    else launch_merge(lanes, a, h->st);
-    ++h->launches;
+    Phase ph(h, name, bytes, 0, st);
+    if (p == 0) {
+      launch_tile_sort(lanes, a, st);
+      ++h->launches;
+    } else {
+      launch_merge(lanes, a, st);  // partition + merge kernels
+      h->launches += 2;
+    }
     ph.end();
     WS_TRY(check_launch(name));
   }
@@ -506,8 +533,40 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
 // ----------------------------------------------------------------------------
 // sort of all buckets
 
-int sort_impl(ws_handle* h, bool stats) {
+int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* offsets,
+                int only, cudaStream_t st);
+std::vector<uint64_t> emit_offsets(ws_handle* h, bool lines);
+
+// Optional fused emission: as soon as a lane class is sorted, its stream
+// emits that class's payload bytes (one contiguous range, buckets ascend by
+// length) and starts the D2H copy, overlapping with the classes still sorting.
+struct FusedEmit {
+  uint8_t* dout;  // device payload buffer
+  uint8_t* host;  // host destination
+  std::vector<uint64_t> off;
+};
+
+int fused_class_copy(ws_handle* h, FusedEmit* fe, int cls, cudaStream_t st) {
+  uint64_t lo = UINT64_MAX, hi = 0, sum = 0;
+  for (size_t i = 0; i < h->buckets.size(); ++i) {
+    const Bucket& b = h->buckets[i];
+    if ((b.is_long ? 0 : b.lanes) != cls || !b.count) continue;
+    lo = std::min(lo, fe->off[i]);
+    hi = std::max(hi, fe->off[i + 1]);
+    sum += fe->off[i + 1] - fe->off[i];
+  }
+  if (!sum) return WS_OK;
+  WS_TRY(emit_device(h, fe->dout, true, nullptr, cls, st));
+  if (!fe->host) return WS_OK;  // device-resident output
+  if (hi - lo != sum) return fail(WS_ERR_STATE, "lane class payload is not contiguous");
+  Phase ph(h, "d2h_out", (double)sum, 1, st);
+  WS_CUDA(cudaMemcpyAsync(fe->host + lo, fe->dout + lo, sum, cudaMemcpyDeviceToHost, st));
+  return WS_OK;
+}
+
+int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   if (!h->ingested) return fail(WS_ERR_STATE, "ws_sort before ingest");
+  if (fe) h->sorted = true;  // bucket final buffers are fixed at planning time
   const int nb = (int)h->buckets.size();
   if (stats) {
     WS_CUDA(h->idx[0].ensure(std::max<uint64_t>(h->idx_total, 1) * 4 + 64));
@@ -520,7 +579,9 @@ int sort_impl(ws_handle* h, bool stats) {
   }
   unsigned long long* inv = stats ? h->stat_inv.as<unsigned long long>() : nullptr;
   long long* km = stats ? h->stat_k.as<long long>() : nullptr;
-  // packed buckets: one schedule per lane class
+  // packed buckets: one schedule per lane class, each class on its own stream
+  // (the classes are independent; small classes fill the big one's bubbles)
+  WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
   for (int c = 1; c <= kClasses; ++c) {
     std::vector<SegIn> segs;
     std::vector<int> which;
@@ -531,11 +592,16 @@ int sort_impl(ws_handle* h, bool stats) {
       which.push_back(i);
     }
     if (segs.empty()) continue;
+    cudaStream_t cst = h->serial ? h->st : h->cs[c];
+    WS_CUDA(cudaStreamWaitEvent(cst, h->ev_fork, 0));
     uint64_t* k0 = h->keys[0].as<uint64_t>() + h->class_base[c];
     uint64_t* k1 = h->keys[1].as<uint64_t>() + h->class_base[c];
     WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(), h->idx[1].as<uint32_t>(),
-                         stats, inv, km, ""));
+                         stats, inv, km, "", cst));
     for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
+    if (fe) WS_TRY(fused_class_copy(h, fe, c, cst));
+    WS_CUDA(cudaEventRecord(h->ev_join[c], cst));
+    WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_join[c], 0));
   }
   // long groups: LSD over 8-byte lanes, least significant lane first
   if (h->n_long) {
@@ -594,6 +660,7 @@ int sort_impl(ws_handle* h, bool stats) {
                            h->stat_k_dummy.as<long long>(), "linv_"));
     }
   }
+  if (fe && h->n_long) WS_TRY(fused_class_copy(h, fe, 0, h->st));
   if (stats && nb) {
     std::vector<int64_t> hinv(nb), hk(nb);
     WS_CUDA(cudaMemcpyAsync(hinv.data(), h->stat_inv.p, nb * 8, cudaMemcpyDeviceToHost, h->st));
@@ -619,18 +686,39 @@ const uint64_t* bucket_keys(ws_handle* h, const Bucket& b, bool sorted) {
 }
 
 // Enqueue emission of all buckets into device buffer `dout` (lines or rows).
-int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* offsets) {
-  const int nl = lines ? 1 : 0;
-  std::vector<uint64_t> off(h->buckets.size());
+// Byte offset of every bucket in the payload (ascending bucket order), plus the total.
+std::vector<uint64_t> emit_offsets(ws_handle* h, bool lines) {
+  std::vector<uint64_t> off(h->buckets.size() + 1);
   uint64_t run = 0;
   for (size_t i = 0; i < h->buckets.size(); ++i) {
     off[i] = run;
-    run += h->buckets[i].count * (h->buckets[i].len + nl);
+    run += h->buckets[i].count * (h->buckets[i].len + (lines ? 1 : 0));
   }
-  double kb = 0;
-  for (auto& b : h->buckets) kb += b.is_long ? 0.0 : (double)b.count * b.lanes * 8;
-  Phase ph(h, lines ? "emit_lines" : "emit_rows", kb + (double)run);
+  off.back() = run;
+  return off;
+}
+
+// Enqueue emission into device buffer `dout`: lane class `only` (1..4), the
+// long groups (0), or everything (-1), on stream `st`.
+int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* offsets,
+                int only = -1, cudaStream_t st = nullptr) {
+  if (!st) st = h->st;
+  const int nl = lines ? 1 : 0;
+  std::vector<uint64_t> off = emit_offsets(h, lines);
+  double kb = 0, ob = 0;
+  for (size_t i = 0; i < h->buckets.size(); ++i) {
+    const Bucket& b = h->buckets[i];
+    const int cls = b.is_long ? 0 : b.lanes;
+    if (only >= 0 && cls != only) continue;
+    kb += b.is_long ? 0.0 : (double)b.count * b.lanes * 8;
+    ob += (double)(off[i + 1] - off[i]);
+  }
+  char name[32];
+  snprintf(name, sizeof name, "%s%s", lines ? "emit_lines" : "emit_rows",
+           only < 0 ? "" : (only == 0 ? "_long" : (only == 1 ? "_l1" : only == 2 ? "_l2" : only == 3 ? "_l3" : "_l4")));
+  Phase ph(h, name, kb + ob, 0, st);
   for (int c = 1; c <= kClasses; ++c) {
+    if (only >= 0 && only != c) continue;
     std::vector<EmitSeg> segs;
     uint32_t blocks = 0;
     for (size_t i = 0; i < h->buckets.size(); ++i) {
@@ -648,24 +736,23 @@ int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* 
     }
     if (segs.empty()) continue;
     const EmitSeg* d;
-    WS_TRY(params_upload(h, segs, &d));
-    launch_emit(c, d, (int)segs.size(), blocks, dout, nl, h->st);
+    WS_TRY(params_upload(h, segs, &d, st));
+    launch_emit(c, d, (int)segs.size(), blocks, dout, nl, st);
     ++h->launches;
   }
-  for (size_t i = 0; i < h->buckets.size(); ++i) {
-    const Bucket& b = h->buckets[i];
-    if (!b.is_long || !b.count) continue;
-    const uint32_t* order = h->sorted ? h->rank.as<uint32_t>() + b.long_off : nullptr;
-    const uint2* words = h->longgrp.as<uint2>() + (h->sorted ? 0 : b.long_off);
-    launch_emit_long(h->text.as<uint8_t>(), words, order, b.count, b.len, dout + off[i], nl, h->st);
-    ++h->launches;
+  if (only <= 0) {
+    for (size_t i = 0; i < h->buckets.size(); ++i) {
+      const Bucket& b = h->buckets[i];
+      if (!b.is_long || !b.count) continue;
+      const uint32_t* order = h->sorted ? h->rank.as<uint32_t>() + b.long_off : nullptr;
+      const uint2* words = h->longgrp.as<uint2>() + (h->sorted ? 0 : b.long_off);
+      launch_emit_long(h->text.as<uint8_t>(), words, order, b.count, b.len, dout + off[i], nl, st);
+      ++h->launches;
+    }
   }
   ph.end();
   WS_TRY(check_launch("emit"));
-  if (offsets) {
-    off.push_back(run);
-    *offsets = off;
-  }
+  if (offsets) *offsets = off;
   return WS_OK;
 }
 
@@ -908,9 +995,16 @@ int ws_create(ws_handle** out, int32_t device) {
   }
   ws_handle* h = new ws_handle();
   h->device = device;
+  const char* ser = getenv("WSORT_SERIAL");
+  h->serial = ser && ser[0] == '1';
   e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
+  for (int c = 1; c <= kClasses && e == cudaSuccess; ++c)
+    e = cudaStreamCreateWithFlags(&h->cs[c], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+  for (int c = 1; c <= kClasses && e == cudaSuccess; ++c)
+    e = cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming);
   if (e != cudaSuccess) {
-    delete h;
+    ws_destroy(h);
     return fail_cuda(e, "cudaStreamCreate", __LINE__);
   }
   *out = h;
@@ -920,12 +1014,15 @@ int ws_create(ws_handle** out, int32_t device) {
 void ws_destroy(ws_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
-  cudaStreamSynchronize(h->st);
+  if (h->st) cudaStreamSynchronize(h->st);
+  for (int c = 1; c <= kClasses; ++c)
+    if (h->cs[c]) cudaStreamSynchronize(h->cs[c]);
   DevBuf* bufs[] = {&h->text, &h->starts, &h->lens, &h->hist, &h->off, &h->totals,
                     &h->keys[0], &h->keys[1], &h->idx[0], &h->idx[1], &h->longlist,
                     &h->longgrp, &h->rank, &h->rank_tmp, &h->lkeys[0], &h->lkeys[1],
                     &h->lidx[0], &h->lidx[1], &h->tokens, &h->stat_inv, &h->stat_k,
-                    &h->stat_k_dummy, &h->out, &h->params};
+                    &h->stat_k_dummy, &h->out, &h->params, &h->splits[0], &h->splits[1],
+                    &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5]};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();
@@ -934,7 +1031,12 @@ void ws_destroy(ws_handle* h) {
     cudaEventDestroy(p.b);
   }
   for (auto e : h->event_pool) cudaEventDestroy(e);
-  cudaStreamDestroy(h->st);
+  for (int c = 1; c <= kClasses; ++c) {
+    if (h->cs[c]) cudaStreamDestroy(h->cs[c]);
+    if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
 
@@ -1055,18 +1157,32 @@ int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, ui
   WS_TRY(begin_call(h));
   WS_TRY(ingest_text_impl(h, text, n, 0));
   params_reset(h);  // the ingest synchronised: staging space is free again
-  WS_TRY(sort_impl(h, false));
-  return emit_to_host(h, true, out, cap, written);
+  const uint64_t size = emit_size(h, true);
+  if (written) *written = size;
+  if (cap < size) return fail(WS_ERR_ARG, "output buffer too small");
+  if (!size) return WS_OK;
+  if (!out) return fail(WS_ERR_ARG, "null output buffer");
+  WS_CUDA(h->out.ensure(size + 64));
+  FusedEmit fe;
+  fe.dout = h->out.as<uint8_t>();
+  fe.host = out;
+  fe.off = emit_offsets(h, true);
+  WS_TRY(sort_impl(h, false, &fe));  // sort + per-class emit + D2H, overlapped
+  WS_CUDA(cudaStreamSynchronize(h->st));  // joins every class stream
+  return WS_OK;
 }
 
 int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   WS_TRY(begin_call(h));
   WS_TRY(ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT));
   params_reset(h);
-  WS_TRY(sort_impl(h, false));
   const uint64_t size = emit_size(h, true);
   WS_CUDA(h->out.ensure(size + 64));
-  WS_TRY(emit_device(h, h->out.as<uint8_t>(), true, nullptr));
+  FusedEmit fe;
+  fe.dout = h->out.as<uint8_t>();
+  fe.host = nullptr;
+  fe.off = emit_offsets(h, true);
+  WS_TRY(sort_impl(h, false, &fe));  // each class emits as soon as it is sorted
   h->out_size = size;
   if (written) *written = size;
   WS_CUDA(cudaStreamSynchronize(h->st));

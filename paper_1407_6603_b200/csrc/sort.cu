@@ -34,19 +34,49 @@
 
 namespace ws {
 
-constexpr int kSortThreads = 256;
+#ifndef WS_TILE_E1
+#define WS_TILE_E1 16  // keys per thread in the tile pass, 1-lane keys
+#endif
+#ifndef WS_TILE_NT
+#define WS_TILE_NT 256  // threads per CTA in the tile pass
+#endif
+#ifndef WS_MERGE_E
+#define WS_MERGE_E 9  // outputs per thread in a merge pass (odd: spreads search probes over banks)
+#endif
+#ifndef WS_MERGE_NT
+#define WS_MERGE_NT 256  // threads per CTA in a merge pass
+#endif
+#ifndef WS_MERGE_PERM
+#define WS_MERGE_PERM 1  // thread -> output chunk multiplier (odd; 1 = identity)
+#endif
+
+constexpr int kSortThreads = WS_TILE_NT;
+constexpr int kMergeThreads = WS_MERGE_NT;
 
 __host__ __device__ constexpr int sidx(int i) { return i + (i >> 5); }  // 1 pad / 32 elems
 
+// Tile pass geometry: T = threads * E keys per CTA (E keys per thread in
+// registers); the sorted tile length is also the initial run length.
 template <int LANES>
 struct SortCfg {
-  static constexpr int E = LANES == 1 ? 16 : 8;
-  static constexpr int T = kSortThreads * E;
+  static constexpr int NT = kSortThreads;
+  static constexpr int E = LANES == 1 ? WS_TILE_E1 : 8;
+  static constexpr int T = NT * E;
   static constexpr int S = T + T / 32;  // padded smem stride (elements)
 };
 
+// Merge pass geometry: each CTA emits TM = threads * E outputs.
+template <int LANES>
+struct MergeCfg {
+  static constexpr int NT = kMergeThreads;
+  static constexpr int E = WS_MERGE_E;
+  static constexpr int T = NT * E;
+  static constexpr int S = T + T / 32;
+  static constexpr int MIN_BLOCKS = LANES == 1 ? 2048 / NT : (LANES == 2 ? 1280 / NT : 768 / NT);
+};
+
 template <int LANES, bool STATS>
-constexpr size_t sort_smem_bytes() {
+__host__ __device__ constexpr size_t sort_smem_bytes() {
   return (size_t)SortCfg<LANES>::S * 8 * LANES + (STATS ? (size_t)SortCfg<LANES>::S * 4 : 0);
 }
 
@@ -59,9 +89,8 @@ __device__ __forceinline__ Key<LANES> sld(const uint64_t* __restrict__ sk, int i
   return k;
 }
 
-template <int LANES>
+template <int LANES, int S = SortCfg<LANES>::S>
 __device__ __forceinline__ void sst(uint64_t* __restrict__ sk, int i, const Key<LANES>& k) {
-  constexpr int S = SortCfg<LANES>::S;
 #pragma unroll
   for (int l = 0; l < LANES; ++l) sk[l * S + sidx(i)] = k.w[l];
 }
@@ -169,28 +198,27 @@ __device__ __forceinline__ void flush_stats(uint64_t inv, long long kloc, const 
 }
 
 // Registers (blocked, E per thread) -> padded smem.
-template <int LANES, int E, bool STATS>
+template <int LANES, int E, bool STATS, int S = SortCfg<LANES>::S>
 __device__ __forceinline__ void regs_to_smem(uint64_t* sk, uint32_t* si, const Key<LANES> (&r)[E],
-                                             const uint32_t (&ri)[E]) {
-  const int base = threadIdx.x * E;
+                                             const uint32_t (&ri)[E], int chunk = -1) {
+  const int base = (chunk < 0 ? (int)threadIdx.x : chunk) * E;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
-    sst<LANES>(sk, base + k, r[k]);
+    sst<LANES, S>(sk, base + k, r[k]);
     if (STATS) si[sidx(base + k)] = ri[k];
   }
 }
 
 // smem (padded) -> global, coalesced over the flat uint64 words of cnt keys.
-template <int LANES, bool STATS>
+template <int LANES, bool STATS, int S = SortCfg<LANES>::S, int NT = kSortThreads>
 __device__ __forceinline__ void smem_to_global(const uint64_t* sk, const uint32_t* si, int cnt,
                                                uint64_t* __restrict__ gk, uint32_t* __restrict__ gi) {
-  constexpr int S = SortCfg<LANES>::S;
-  for (int w = threadIdx.x; w < cnt * LANES; w += kSortThreads) {
+  for (int w = threadIdx.x; w < cnt * LANES; w += NT) {
     int j = w / LANES, l = w - j * LANES;
     gk[w] = sk[l * S + sidx(j)];
   }
   if (STATS && gi) {
-    for (int j = threadIdx.x; j < cnt; j += kSortThreads) gi[j] = si[sidx(j)];
+    for (int j = threadIdx.x; j < cnt; j += NT) gi[j] = si[sidx(j)];
   }
 }
 
@@ -293,68 +321,264 @@ __device__ int64_t merge_path_search_global(const uint64_t* __restrict__ A, int6
   return lo;
 }
 
-template <int LANES, bool STATS>
-__global__ void __launch_bounds__(kSortThreads) merge_kernel(SortLaunch a) {
-  constexpr int E = SortCfg<LANES>::E, T = SortCfg<LANES>::T, S = SortCfg<LANES>::S;
-  extern __shared__ __align__(16) uint64_t smem[];
-  uint64_t* sk = smem;
-  uint32_t* si = reinterpret_cast<uint32_t*>(smem + (size_t)LANES * S);
-  __shared__ int64_t s_split[2];
-  const int tid = threadIdx.x, wid = tid >> 5;
-  const SegDesc sd = a.segs[find_segment(a.segs, a.nsegs)];
-  const int64_t n = sd.n, R = a.run;
-  const int64_t out_begin = (int64_t)(blockIdx.x - sd.tile_begin) * T;
-  const int64_t pair_base = (out_begin / (2 * R)) * (2 * R);
-  const int64_t na = min(R, n - pair_base);
-  const int64_t nb = n - pair_base > R ? min(R, n - pair_base - R) : 0;
-  const int64_t d0 = out_begin - pair_base;
-  const int64_t d1 = min(d0 + T, na + nb);
-  const uint64_t* A = a.keys_in + (sd.key_off + pair_base) * LANES;
-  const uint64_t* B = A + R * LANES;
-  if (wid < 2) {
-    int64_t s = merge_path_search_global<LANES>(A, na, B, nb, wid == 0 ? d0 : d1);
-    if ((tid & 31) == 0) s_split[wid] = s;
+// ---- TMA (1-D bulk copy) + mbarrier helpers ---------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
   }
-  __syncthreads();
-  const int64_t a0 = s_split[0], a1 = s_split[1];
-  const int64_t b0 = d0 - a0, b1 = d1 - a1;
-  const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
-  // stage A[a0, a1) then B[b0, b1) into smem
-  for (int w = tid; w < la * LANES; w += kSortThreads) {
-    int j = w / LANES, l = w - j * LANES;
-    sk[l * S + sidx(j)] = __ldg(A + a0 * LANES + w);
+}
+
+// Byte window [src, src + bytes) rounded out to 16-byte boundaries for a bulk
+// copy; returns the offset of src inside the landed window.
+struct Window16 {
+  const uint8_t* g;  // 16-byte aligned global start
+  uint32_t off;      // offset of the first wanted byte in the window
+  uint32_t bytes;    // multiple of 16
+};
+
+__device__ __forceinline__ Window16 window16(const void* src, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  Window16 w;
+  w.g = reinterpret_cast<const uint8_t*>(a & ~uintptr_t(15));
+  w.off = (uint32_t)(a & 15);
+  w.bytes = (w.off + bytes + 15) & ~15u;
+  return w;
+}
+
+// Merge path over two unpadded AoS windows in shared memory.
+template <int LANES, int E, bool STATS>
+__device__ __forceinline__ void merge_path_aos(const uint64_t* __restrict__ A, int na,
+                                               const uint64_t* __restrict__ B, int nb,
+                                               const uint32_t* __restrict__ IA,
+                                               const uint32_t* __restrict__ IB, int diag,
+                                               int64_t a_rem_base, Key<LANES> (&r)[E],
+                                               uint32_t (&ri)[E], uint64_t& inv) {
+  auto ld = [](const uint64_t* p, int i) {
+    Key<LANES> k;
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) k.w[l] = p[i * LANES + l];
+    return k;
+  };
+  int lo = max(0, diag - nb), hi = min(diag, na);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (key_le<LANES>(ld(A, mid), ld(B, diag - 1 - mid))) lo = mid + 1;
+    else hi = mid;
   }
-  for (int w = tid; w < lb * LANES; w += kSortThreads) {
-    int j = w / LANES, l = w - j * LANES;
-    sk[l * S + sidx(la + j)] = __ldg(B + b0 * LANES + w);
-  }
+  int ai = lo, bi = diag - lo;
+  const Key<LANES> kmax = key_max<LANES>();
+  Key<LANES> ka = ai < na ? ld(A, ai) : kmax;
+  Key<LANES> kb = bi < nb ? ld(B, bi) : kmax;
+  uint32_t ia = 0, ib = 0;
   if (STATS) {
-    const uint32_t* IA = a.idx_in + sd.idx_off + pair_base;
-    const uint32_t* IB = IA + R;
-    for (int j = tid; j < la; j += kSortThreads) si[sidx(j)] = __ldg(IA + a0 + j);
-    for (int j = tid; j < lb; j += kSortThreads) si[sidx(la + j)] = __ldg(IB + b0 + j);
+    ia = ai < na ? IA[ai] : 0u;
+    ib = bi < nb ? IB[bi] : 0u;
   }
-  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const bool ta = (bi >= nb) || (ai < na && key_le<LANES>(ka, kb));
+    if (ta) {
+      r[k] = ka;
+      if (STATS) ri[k] = ia;
+      ++ai;
+      if (ai < na) {
+        ka = ld(A, ai);
+        if (STATS) ia = IA[ai];
+      } else {
+        ka = kmax;
+      }
+    } else {
+      r[k] = kb;
+      if (STATS) {
+        ri[k] = ib;
+        inv += (uint64_t)(a_rem_base - ai);
+      }
+      ++bi;
+      if (bi < nb) {
+        kb = ld(B, bi);
+        if (STATS) ib = IB[bi];
+      } else {
+        kb = kmax;
+      }
+    }
+  }
+}
+
+struct PairGeom {
+  int64_t n, pair_base, na, nb, d0, d1;
+  bool empty;  // item past the end of a partial last pair
+};
+
+// Work items of a merge level: every pair of runs gets ceil(2R / T) output
+// tiles, so a tile never straddles two pairs whatever T is.
+__device__ __forceinline__ int64_t tiles_per_pair(int64_t R, int T) { return (2 * R + T - 1) / T; }
+
+__device__ __forceinline__ PairGeom pair_geom(const SegDesc& sd, uint32_t item, int64_t R, int T) {
+  PairGeom g;
+  g.n = sd.n;
+  const int64_t tpp = tiles_per_pair(R, T);
+  const int64_t local = (int64_t)(item - sd.tile_begin);
+  g.pair_base = (local / tpp) * (2 * R);
+  g.na = min(R, g.n - g.pair_base);
+  g.nb = g.n - g.pair_base > R ? min(R, g.n - g.pair_base - R) : 0;
+  g.d0 = (local % tpp) * T;
+  g.empty = g.d0 >= g.na + g.nb;
+  g.d1 = min(g.d0 + T, g.na + g.nb);
+  return g;
+}
+
+// Partition pass: one warp per output tile finds the A/B split of the
+// tile's first output (32-ary merge-path search in global memory). All
+// splits of a level are searched in parallel, so the merge CTAs start their
+// copies immediately.
+template <int LANES>
+__global__ void __launch_bounds__(256) merge_split_kernel(SortLaunch a) {
+  constexpr int T = MergeCfg<LANES>::T;
+  const uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (item >= a.work_items) return;
+  int lo = 0, hi = a.nsegs - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (a.segs[mid].tile_begin <= item) lo = mid; else hi = mid - 1;
+  }
+  const SegDesc sd = a.segs[lo];
+  const PairGeom g = pair_geom(sd, item, a.run, T);
+  if (g.empty) return;
+  const uint64_t* A = a.keys_in + (sd.key_off + g.pair_base) * LANES;
+  const uint64_t* B = A + (int64_t)a.run * LANES;
+  const int64_t s = merge_path_search_global<LANES>(A, g.na, B, g.nb, g.d0);
+  if ((threadIdx.x & 31) == 0) a.splits[item] = (uint32_t)s;
+}
+
+template <int LANES, bool STATS>
+__host__ __device__ constexpr size_t merge_smem_bytes() {
+  // input windows (AoS, 16-byte rounded) and the padded output staging reuse
+  // the same bytes; idx windows / staging follow
+  constexpr size_t keys_in = (size_t)MergeCfg<LANES>::T * 8 * LANES + 64;
+  constexpr size_t keys_out = (size_t)MergeCfg<LANES>::S * 8 * LANES;
+  constexpr size_t kb = keys_in > keys_out ? keys_in : keys_out;
+  constexpr size_t ib = STATS ? (size_t)MergeCfg<LANES>::S * 4 + 64 : 0;
+  return ((kb + 15) & ~size_t(15)) + ib;
+}
+
+template <int LANES, bool STATS>
+__global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
+    merge_kernel(SortLaunch a) {
+  constexpr int E = MergeCfg<LANES>::E, T = MergeCfg<LANES>::T, S = MergeCfg<LANES>::S;
+  constexpr size_t kKeyBytes = (merge_smem_bytes<LANES, false>() + 15) & ~size_t(15);
+  extern __shared__ __align__(16) uint64_t smem[];
+  uint8_t* sbytes = reinterpret_cast<uint8_t*>(smem);
+  uint64_t* sk = smem;                                               // output staging (padded SoA)
+  uint32_t* si = reinterpret_cast<uint32_t*>(sbytes + kKeyBytes);    // idx staging
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const SegDesc sd = a.segs[find_segment(a.segs, a.nsegs)];
+  const int64_t R = a.run;
+  const PairGeom g = pair_geom(sd, blockIdx.x, R, T);
+  if (g.empty) return;  // uniform across the CTA
+  const int64_t a0 = a.splits[blockIdx.x];
+  const int64_t a1 = (g.d1 == g.na + g.nb) ? g.na : (int64_t)a.splits[blockIdx.x + 1];
+  const int64_t b0 = g.d0 - a0, b1 = g.d1 - a1;
+  const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
+  const uint64_t* Ag = a.keys_in + (sd.key_off + g.pair_base + a0) * LANES;
+  const uint64_t* Bg = a.keys_in + (sd.key_off + g.pair_base + R + b0) * LANES;
+  const Window16 wa = window16(Ag, (uint32_t)la * 8 * LANES);
+  const Window16 wb = window16(Bg, (uint32_t)lb * 8 * LANES);
+  const uint32_t b_at = wa.bytes;  // B window lands right after A's
+  Window16 wia{}, wib{};
+  uint32_t ib_at = 0;
+  if (STATS) {
+    const uint32_t* IAg = a.idx_in + sd.idx_off + g.pair_base + a0;
+    const uint32_t* IBg = a.idx_in + sd.idx_off + g.pair_base + R + b0;
+    wia = window16(IAg, (uint32_t)la * 4);
+    wib = window16(IBg, (uint32_t)lb * 4);
+    ib_at = wia.bytes;
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    uint32_t tx = (la ? wa.bytes : 0) + (lb ? wb.bytes : 0);
+    if (STATS) tx += (la ? wia.bytes : 0) + (lb ? wib.bytes : 0);
+    mbar_expect_tx(&bar, tx);
+    if (la) tma_load_1d(sbytes, wa.g, wa.bytes, &bar);
+    if (lb) tma_load_1d(sbytes + b_at, wb.g, wb.bytes, &bar);
+    if (STATS) {
+      uint8_t* ibase = reinterpret_cast<uint8_t*>(si);
+      if (la) tma_load_1d(ibase, wia.g, wia.bytes, &bar);
+      if (lb) tma_load_1d(ibase + ib_at, wib.g, wib.bytes, &bar);
+    }
+  }
+  __syncthreads();  // barrier initialised before anyone waits on it
+  mbar_wait(&bar, 0);
+  const uint64_t* As = reinterpret_cast<const uint64_t*>(sbytes + wa.off);
+  const uint64_t* Bs = reinterpret_cast<const uint64_t*>(sbytes + b_at + wb.off);
+  const uint32_t* IAs = reinterpret_cast<const uint32_t*>(reinterpret_cast<uint8_t*>(si) + wia.off);
+  const uint32_t* IBs =
+      reinterpret_cast<const uint32_t*>(reinterpret_cast<uint8_t*>(si) + ib_at + wib.off);
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
-  merge_path_serial<LANES, E, STATS>(sk, si, 0, la, la, lb, min(tid * E, la + lb), R - a0, r, ri,
-                                     inv);
+  // Lanes of a warp take output chunks far apart (odd multiplier mod NT), so
+  // their binary-search probes do not fall on the same smem banks.
+  const int chunk = (tid * WS_MERGE_PERM) & (kMergeThreads - 1);
+  merge_path_aos<LANES, E, STATS>(As, la, Bs, lb, IAs, IBs, min(chunk * E, la + lb), R - a0, r, ri,
+                                  inv);
   long long kloc = 0;
-  if (STATS && 2 * R >= n) {
+  const int64_t out_begin = g.pair_base + g.d0;
+  if (STATS && 2 * R >= g.n) {
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      int64_t lp = (int64_t)tid * E + k;
+      const int64_t lp = (int64_t)chunk * E + k;
       if (lp < la + lb)
         kloc = max(kloc, (long long)ri[k] - (long long)sd.idx_base - (long long)(out_begin + lp));
     }
   }
-  flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);
+  flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);  // contains __syncthreads
+  __syncthreads();  // every thread is done reading the input windows
+  if (chunk * E < la + lb) regs_to_smem<LANES, E, STATS, S>(sk, si, r, ri, chunk);
   __syncthreads();
-  if (tid * E < la + lb) regs_to_smem<LANES, E, STATS>(sk, si, r, ri);
-  __syncthreads();
-  smem_to_global<LANES, STATS>(sk, si, la + lb, a.keys_out + (sd.key_off + out_begin) * LANES,
-                               STATS ? a.idx_out + sd.idx_off + out_begin : nullptr);
+  smem_to_global<LANES, STATS, S, kMergeThreads>(
+      sk, si, la + lb, a.keys_out + (sd.key_off + out_begin) * LANES,
+      STATS ? a.idx_out + sd.idx_off + out_begin : nullptr);
+}
+
+int merge_tile_size(int lanes) {
+  switch (lanes) {
+    case 1: return MergeCfg<1>::T;
+    case 2: return MergeCfg<2>::T;
+    case 3: return MergeCfg<3>::T;
+    default: return MergeCfg<4>::T;
+  }
 }
 
 int tile_size(int lanes) {
@@ -368,11 +592,10 @@ int tile_size(int lanes) {
 
 template <int LANES, bool STATS>
 static void set_attrs_t() {
-  constexpr int smem = (int)sort_smem_bytes<LANES, STATS>();
   cudaFuncSetAttribute(tile_sort_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       smem);
+                       (int)sort_smem_bytes<LANES, STATS>());
   cudaFuncSetAttribute(merge_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       smem);
+                       (int)merge_smem_bytes<LANES, STATS>());
 }
 
 // Opt every sort instantiation into > 48 KiB of dynamic shared memory on the
@@ -392,7 +615,8 @@ static void launch_tile_t(const SortLaunch& a, cudaStream_t st) {
 
 template <int LANES, bool STATS>
 static void launch_merge_t(const SortLaunch& a, cudaStream_t st) {
-  merge_kernel<LANES, STATS><<<a.work_items, kSortThreads, sort_smem_bytes<LANES, STATS>(), st>>>(a);
+  merge_split_kernel<LANES><<<(a.work_items * 32 + 255) / 256, 256, 0, st>>>(a);
+  merge_kernel<LANES, STATS><<<a.work_items, kMergeThreads, merge_smem_bytes<LANES, STATS>(), st>>>(a);
 }
 
 #define WS_DISPATCH_LANES(fn, lanes, stats, ...)                   \

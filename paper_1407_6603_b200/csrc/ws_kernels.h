@@ -43,8 +43,10 @@ struct SortLaunch {
   uint32_t run;            // merge: run length being merged (>= tile)
   unsigned long long* inv; // per stat slot
   long long* kmax;         // per stat slot
+  uint32_t* splits;        // merge: per work item, A-split of its first output
 };
 int tile_size(int lanes);
+int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);
 
