@@ -154,6 +154,7 @@ struct ws_handle {
   uint64_t words = 0;
   uint64_t n_long = 0;
   bool have_tokens = false;
+  int enc = kEncRaw8;       // key encoding of the current packed buckets
   bool text_valid = false;  // h->text holds the last ingested text (reusable, resident)
   bool ingested = false, sorted = false, have_stats = false;
   uint64_t class_base[kClasses + 1] = {0};  // u64-word base of each lane class region
@@ -283,7 +284,7 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
   uint64_t total_tiles = 0;  // upper bound of the work items of any pass
   for (auto* s : live) total_tiles += 2 * ((s->n + std::min(T, TM) - 1) / std::min(T, TM)) + 4;
   DevBuf& split_buf = h->splits[st == h->st ? 0 : (lanes & 3) + 1];
-  WS_CUDA(split_buf.ensure((total_tiles + 1) * 4));
+  WS_CUDA(split_buf.ensure((2 * total_tiles + 4) * 4));  // (split, segment) per work item
   uint64_t* kb[2] = {keys0, keys1};
   uint32_t* ib[2] = {idx0, idx1};
   // pass 0 = tile sort; pass p >= 1 merges runs of T << (p-1)
@@ -316,15 +317,18 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
       s->final_buf = (p + 1) & 1;
     }
     if (d.empty()) break;
-    const SegDesc* dd;
-    WS_TRY(params_upload(h, d, &dd, st));
     const int in = p & 1, out = in ^ 1;
     SortLaunch a;
+    if (d.size() <= (size_t)kInlineSegs) {
+      std::copy(d.begin(), d.end(), a.inl);
+      a.segs = nullptr;
+    } else {
+      WS_TRY(params_upload(h, d, &a.segs, st));
+    }
     a.keys_in = kb[in];
     a.keys_out = kb[out];
     a.idx_in = stats ? ib[in] : nullptr;
     a.idx_out = stats ? ib[out] : nullptr;
-    a.segs = dd;
     a.nsegs = (int)d.size();
     a.work_items = work;
     a.run = (uint32_t)run;
@@ -363,7 +367,7 @@ int plan_packed(ws_handle* h, const uint64_t* counts) {
   uint64_t idx_run = 0;
   for (int b = 0; b < kMaxPackedLen; ++b) {
     if (!counts[b]) continue;
-    int L = b + 1, c = lanes_for_len(L);
+    int L = b + 1, c = lanes_for_len_enc(L, h->enc);
     bin_elem[b] = elems[c];
     elems[c] += counts[b];
     Bucket bk;
@@ -398,6 +402,7 @@ void fill_scatter_params(ws_handle* h, ScatterParams& p) {
   p.keys = h->keys[0].as<uint64_t>();
   p.longlist = h->longlist.as<uint2>();
   p.tokens = nullptr;
+  p.enc = h->enc;
 }
 
 // Long words (corpus order in h->longlist, m entries) -> stable grouping by
@@ -465,6 +470,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   h->buckets.clear();
   h->n_text = n;
   h->text_valid = false;
+  h->enc = kEncAlnum6;  // tokens are [0-9A-Za-z] only
   if (!resident) WS_CUDA(h->text.ensure(n + kTextPad));
   if (!resident) {
     Phase ph(h, "h2d_text", (double)n, (flags & WS_INGEST_DEVICE_PTR) ? 0 : 1);
@@ -735,9 +741,15 @@ int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* 
       segs.push_back(e);
     }
     if (segs.empty()) continue;
-    const EmitSeg* d;
-    WS_TRY(params_upload(h, segs, &d, st));
-    launch_emit(c, d, (int)segs.size(), blocks, dout, nl, st);
+    EmitTable t;
+    t.nsegs = (int)segs.size();
+    if (segs.size() <= (size_t)kInlineSegs) {
+      std::copy(segs.begin(), segs.end(), t.inl);
+      t.segs = nullptr;
+    } else {
+      WS_TRY(params_upload(h, segs, &t.segs, st));
+    }
+    launch_emit(c, h->enc, t, blocks, dout, nl, st);
     ++h->launches;
   }
   if (only <= 0) {
@@ -790,6 +802,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
   h->text_valid = false;
+  h->enc = kEncRaw8;
   h->buckets.clear();
   std::vector<int> order(nblocks);
   for (int i = 0; i < nblocks; ++i) {
@@ -884,6 +897,7 @@ int ingest_words_impl(ws_handle* h, const uint8_t* concat, const uint32_t* lens,
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
   h->text_valid = false;
+  h->enc = kEncRaw8;  // word lists may hold any byte values
   h->buckets.clear();
   if (nwords && !lens) return fail(WS_ERR_ARG, "null lens");
   std::vector<uint64_t> starts(nwords);

@@ -31,21 +31,43 @@ __device__ __forceinline__ void copy_span_out(const uint8_t* __restrict__ buf, i
   for (uint64_t q = ae + threadIdx.x; q < g_end; q += kEmitThreads) out[q] = buf[q - o0 + mis];
 }
 
+// Unpack one 6-bit alnum key (character k of the big-endian bit string).
 template <int LANES>
+__device__ __forceinline__ void unpack6(const uint64_t (&k)[LANES], int L, uint8_t* dst) {
+  static_assert(LANES <= 3, "6-bit keys use at most 3 lanes");
+#define WS_UNPACK6_CHAR(I)                                                    \
+  if constexpr ((6 * (I) + 5) / 64 < LANES) {                                 \
+    if ((I) < L) dst[I] = (uint8_t)alnum6_byte(code6_at<I>(k));               \
+  }
+  WS_UNPACK6_CHAR(0) WS_UNPACK6_CHAR(1) WS_UNPACK6_CHAR(2) WS_UNPACK6_CHAR(3)
+  WS_UNPACK6_CHAR(4) WS_UNPACK6_CHAR(5) WS_UNPACK6_CHAR(6) WS_UNPACK6_CHAR(7)
+  WS_UNPACK6_CHAR(8) WS_UNPACK6_CHAR(9) WS_UNPACK6_CHAR(10) WS_UNPACK6_CHAR(11)
+  WS_UNPACK6_CHAR(12) WS_UNPACK6_CHAR(13) WS_UNPACK6_CHAR(14) WS_UNPACK6_CHAR(15)
+  WS_UNPACK6_CHAR(16) WS_UNPACK6_CHAR(17) WS_UNPACK6_CHAR(18) WS_UNPACK6_CHAR(19)
+  WS_UNPACK6_CHAR(20) WS_UNPACK6_CHAR(21) WS_UNPACK6_CHAR(22) WS_UNPACK6_CHAR(23)
+  WS_UNPACK6_CHAR(24) WS_UNPACK6_CHAR(25) WS_UNPACK6_CHAR(26) WS_UNPACK6_CHAR(27)
+  WS_UNPACK6_CHAR(28) WS_UNPACK6_CHAR(29) WS_UNPACK6_CHAR(30) WS_UNPACK6_CHAR(31)
+#undef WS_UNPACK6_CHAR
+}
+
+template <int LANES, int ENC>
 __global__ void __launch_bounds__(kEmitThreads)
-emit_kernel(const EmitSeg* __restrict__ segs, int nsegs, uint8_t* __restrict__ out, int nl) {
+emit_kernel(const __grid_constant__ EmitTable t, uint8_t* __restrict__ out, int nl) {
   __shared__ __align__(16) uint8_t buf[kEmitBuf];
   __shared__ int s_seg;
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = nsegs - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (segs[mid].block_begin <= blockIdx.x) lo = mid; else hi = mid - 1;
+  if (threadIdx.x < 32) {  // last segment with block_begin <= blockIdx.x (warp ballot)
+    const int lane = threadIdx.x;
+    int found = 0;
+    for (int base = 0; base < t.nsegs; base += 32) {
+      const int i = base + lane;
+      const bool le = i < t.nsegs && (t.segs ? t.segs[i] : t.inl[i]).block_begin <= blockIdx.x;
+      found += __popc(__ballot_sync(0xffffffffu, le));
+      if (!__shfl_sync(0xffffffffu, (int)le, 31)) break;
     }
-    s_seg = lo;
+    if (lane == 0) s_seg = found - 1;
   }
   __syncthreads();
-  const EmitSeg sg = segs[s_seg];
+  const EmitSeg sg = t.segs ? t.segs[s_seg] : t.inl[s_seg];
   const uint64_t w0 = (uint64_t)(blockIdx.x - sg.block_begin) * kEmitWords;
   const int cnt = (int)min((uint64_t)kEmitWords, (uint64_t)sg.n - w0);
   const int L = (int)sg.len;
@@ -58,12 +80,16 @@ emit_kernel(const EmitSeg* __restrict__ segs, int nsegs, uint8_t* __restrict__ o
 #pragma unroll
     for (int l = 0; l < LANES; ++l) k[l] = __ldg(keys + (uint64_t)j * LANES + l);
     uint8_t* dst = buf + mis + j * stride;
+    if constexpr (ENC == kEncAlnum6) {
+      unpack6<LANES>(k, L, dst);
+    } else {
 #pragma unroll
-    for (int l = 0; l < LANES; ++l) {
+      for (int l = 0; l < LANES; ++l) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        int b = 8 * l + q;
-        if (b < L) dst[b] = (uint8_t)(k[l] >> (56 - 8 * q));
+        for (int q = 0; q < 8; ++q) {
+          int b = 8 * l + q;
+          if (b < L) dst[b] = (uint8_t)(k[l] >> (56 - 8 * q));
+        }
       }
     }
     if (nl) dst[L] = '\n';
@@ -72,14 +98,22 @@ emit_kernel(const EmitSeg* __restrict__ segs, int nsegs, uint8_t* __restrict__ o
   copy_span_out(buf, mis, o0, (uint64_t)cnt * stride, out);
 }
 
-void launch_emit(int lanes, const EmitSeg* segs, int nsegs, uint32_t blocks, uint8_t* out,
+void launch_emit(int lanes, int enc, const EmitTable& t, uint32_t blocks, uint8_t* out,
                  int with_newline, cudaStream_t st) {
   if (!blocks) return;
+  if (enc == kEncAlnum6) {
+    switch (lanes) {
+      case 1: emit_kernel<1, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
+      case 2: emit_kernel<2, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
+      default: emit_kernel<3, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
+    }
+    return;
+  }
   switch (lanes) {
-    case 1: emit_kernel<1><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
-    case 2: emit_kernel<2><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
-    case 3: emit_kernel<3><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
-    default: emit_kernel<4><<<blocks, kEmitThreads, 0, st>>>(segs, nsegs, out, with_newline); break;
+    case 1: emit_kernel<1, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
+    case 2: emit_kernel<2, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
+    case 3: emit_kernel<3, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
+    default: emit_kernel<4, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
   }
 }
 

@@ -228,6 +228,51 @@ __device__ __forceinline__ void pack_from_smem(const uint32_t* __restrict__ c32,
   }
 }
 
+// 6-bit alnum packing (text ingest): characters form one big-endian bit
+// string over up to 3 lanes; the unrolled loop resolves lane/shift at compile
+// time, characters past L are predicated off.
+// 8 big-endian alnum bytes -> their 6-bit codes as one 48-bit big-endian
+// string (SWAR: byte-parallel code arithmetic, then two compaction steps).
+__device__ __forceinline__ uint64_t codes48(uint64_t x) {
+  const uint64_t hi = 0x8080808080808080ull;
+  const uint64_t xh = x | hi;  // every byte >= 0x80: no borrows below
+  const uint64_t ge41 = ((xh - 0x4141414141414141ull) & hi) >> 7;  // 1 per byte >= 'A'
+  const uint64_t ge61 = ((xh - 0x6161616161616161ull) & hi) >> 7;  // 1 per byte >= 'a'
+  const uint64_t off = 0x2F2F2F2F2F2F2F2Full + ge41 * 7 + ge61 * 6;
+  uint64_t c = (xh - off) & 0x3F3F3F3F3F3F3F3Full;  // code per byte
+  c = ((c & 0x3F003F003F003F00ull) >> 2) | (c & 0x003F003F003F003Full);   // 12 bits / 16
+  c = ((c & 0x0FFF00000FFF0000ull) >> 4) | (c & 0x00000FFF00000FFFull);   // 24 bits / 32
+  return ((c >> 32) << 24) | (c & 0xFFFFFFull);                            // 48 bits
+}
+
+__device__ __forceinline__ void pack6_from_smem(const uint32_t* __restrict__ c32, uint32_t start,
+                                                uint32_t L, int lanes, uint64_t* __restrict__ dst) {
+  // raw big-endian 8-byte lanes of the word (as pack_from_smem), then codes
+  uint64_t v[4];
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    v[l] = 0;
+    if (8 * l < (int)L) {
+      const uint32_t q = start + 8 * l;
+      const uint32_t w0 = c32[q >> 2], w1 = c32[(q >> 2) + 1], w2 = c32[(q >> 2) + 2];
+      const uint32_t sh = (q & 3) * 8;
+      const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
+      v[l] = codes48(((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123));
+    }
+  }
+  // concatenate the 48-bit chunks into the 192-bit string, keep 6L bits
+  uint64_t k0 = (v[0] << 16) | (v[1] >> 32);
+  uint64_t k1 = (v[1] << 32) | (v[2] >> 16);
+  uint64_t k2 = (v[2] << 48) | v[3];
+  const int bits = 6 * (int)L;
+  k0 &= bits >= 64 ? ~0ull : ~0ull << (64 - bits);
+  k1 &= bits >= 128 ? ~0ull : (bits <= 64 ? 0ull : ~0ull << (128 - bits));
+  k2 &= bits >= 192 ? ~0ull : (bits <= 128 ? 0ull : ~0ull << (192 - bits));
+  dst[0] = k0;
+  if (lanes > 1) dst[1] = k1;
+  if (lanes > 2) dst[2] = k2;
+}
+
 __global__ void __launch_bounds__(kIngestThreads)
 scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __restrict__ off,
                uint32_t nchunks, ScatterParams p) {
@@ -315,9 +360,12 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
       p.longlist[pos] = make_uint2((uint32_t)(cbase + start), L);
       continue;
     }
-    const int lanes = lanes_for_len(L);
+    const int lanes = lanes_for_len_enc(L, p.enc);
     uint64_t* dst = p.keys + p.bin_base[bin] + (uint64_t)pos * lanes;
-    pack_from_smem(chunk32, start, L, lanes, dst);
+    if (p.enc == kEncAlnum6)
+      pack6_from_smem(chunk32, start, L, lanes, dst);
+    else
+      pack_from_smem(chunk32, start, L, lanes, dst);
   }
 }
 

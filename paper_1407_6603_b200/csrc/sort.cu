@@ -8,15 +8,22 @@
 // corpus order; every pass here is stable too (OETS swaps on strict '>', the
 // merges take A first on ties).
 //
-//   tile pass  : each thread holds E consecutive keys in registers and runs
-//                odd-even transposition sort on them (E phases of
-//                compare-exchange on strict '>': the data-parallel form of
-//                bubble sort), then log2(256) merge-path levels in shared
-//                memory turn 256 runs of E into one sorted tile of T = 256*E.
-//   merge pass : one launch per level; every CTA produces T outputs of one
-//                merged pair; its A/B split points come from a warp-wide
-//                32-ary merge-path search in global memory, then the windows
-//                are staged in shared memory and merged as in the tile pass.
+//   tile pass  : the tile (T = threads * E keys) lands in shared memory by a
+//                1-D TMA bulk copy; each thread takes E consecutive keys into
+//                registers and runs odd-even transposition sort on them (E
+//                phases of compare-exchange on strict '>': the data-parallel
+//                form of bubble sort); log2(threads) merge-path levels in
+//                shared memory then merge the runs into one sorted tile.
+//   merge pass : one partition launch (a warp per output tile finds its
+//                merge-path split in global memory, all in parallel) and one
+//                merge launch per level: each CTA bulk-copies its A and B
+//                windows into shared memory (TMA + mbarrier), merge-path
+//                merges them, and streams the tile out coalesced.
+//
+// E is odd everywhere: with 8-byte keys a warp's blocked accesses (lane l at
+// element E*l + k) then hit 16 distinct bank pairs (conflict-free without
+// padding), and neighbouring lanes' binary-search probes fall on different
+// banks (E = 8 gave 8-way conflicts and a smem-bound merge).
 //
 // Stats mode carries a uint32 payload idx = the word's corpus rank inside its
 // bucket and returns, per bucket:
@@ -35,64 +42,62 @@
 namespace ws {
 
 #ifndef WS_TILE_E1
-#define WS_TILE_E1 16  // keys per thread in the tile pass, 1-lane keys
+#define WS_TILE_E1 15  // keys per thread in the tile pass, 1-lane keys (odd)
+#endif
+#ifndef WS_TILE_EN
+#define WS_TILE_EN 7  // keys per thread in the tile pass, 2..4-lane keys (odd)
 #endif
 #ifndef WS_TILE_NT
 #define WS_TILE_NT 256  // threads per CTA in the tile pass
 #endif
 #ifndef WS_MERGE_E
-#define WS_MERGE_E 9  // outputs per thread in a merge pass (odd: spreads search probes over banks)
+#define WS_MERGE_E 9  // outputs per thread in a merge pass (odd)
 #endif
 #ifndef WS_MERGE_NT
 #define WS_MERGE_NT 256  // threads per CTA in a merge pass
 #endif
-#ifndef WS_MERGE_PERM
-#define WS_MERGE_PERM 1  // thread -> output chunk multiplier (odd; 1 = identity)
-#endif
 
-constexpr int kSortThreads = WS_TILE_NT;
+constexpr int kTileThreads = WS_TILE_NT;
 constexpr int kMergeThreads = WS_MERGE_NT;
 
-__host__ __device__ constexpr int sidx(int i) { return i + (i >> 5); }  // 1 pad / 32 elems
-
-// Tile pass geometry: T = threads * E keys per CTA (E keys per thread in
-// registers); the sorted tile length is also the initial run length.
 template <int LANES>
-struct SortCfg {
-  static constexpr int NT = kSortThreads;
-  static constexpr int E = LANES == 1 ? WS_TILE_E1 : 8;
+struct TileCfg {
+  static constexpr int NT = kTileThreads;
+  static constexpr int E = LANES == 1 ? WS_TILE_E1 : WS_TILE_EN;
   static constexpr int T = NT * E;
-  static constexpr int S = T + T / 32;  // padded smem stride (elements)
 };
 
-// Merge pass geometry: each CTA emits TM = threads * E outputs.
 template <int LANES>
 struct MergeCfg {
   static constexpr int NT = kMergeThreads;
   static constexpr int E = WS_MERGE_E;
   static constexpr int T = NT * E;
-  static constexpr int S = T + T / 32;
-  static constexpr int MIN_BLOCKS = LANES == 1 ? 2048 / NT : (LANES == 2 ? 1280 / NT : 768 / NT);
+  static constexpr int MIN_BLOCKS = LANES == 1 ? 2048 / NT : (LANES == 2 ? 1024 / NT : 512 / NT);
 };
 
-template <int LANES, bool STATS>
-__host__ __device__ constexpr size_t sort_smem_bytes() {
-  return (size_t)SortCfg<LANES>::S * 8 * LANES + (STATS ? (size_t)SortCfg<LANES>::S * 4 : 0);
+// smem bytes: keys (AoS, 16-byte slack on each side for the bulk-copy
+// rounding) followed by the idx payload in stats mode.
+template <int LANES, int T, bool STATS>
+__host__ __device__ constexpr size_t keys_smem_bytes() {
+  return (size_t)T * 8 * LANES + 64;
+}
+template <int LANES, int T, bool STATS>
+__host__ __device__ constexpr size_t pass_smem_bytes() {
+  return keys_smem_bytes<LANES, T, STATS>() + (STATS ? (size_t)T * 4 + 64 : 0);
 }
 
 template <int LANES>
-__device__ __forceinline__ Key<LANES> sld(const uint64_t* __restrict__ sk, int i) {
-  constexpr int S = SortCfg<LANES>::S;
+__device__ __forceinline__ Key<LANES> ldk(const uint64_t* __restrict__ p, int i) {
   Key<LANES> k;
 #pragma unroll
-  for (int l = 0; l < LANES; ++l) k.w[l] = sk[l * S + sidx(i)];
+  for (int l = 0; l < LANES; ++l) k.w[l] = p[i * LANES + l];
   return k;
 }
 
-template <int LANES, int S = SortCfg<LANES>::S>
-__device__ __forceinline__ void sst(uint64_t* __restrict__ sk, int i, const Key<LANES>& k) {
+template <int LANES>
+__device__ __forceinline__ void stk(uint64_t* __restrict__ p, int i, const Key<LANES>& k) {
 #pragma unroll
-  for (int l = 0; l < LANES; ++l) sk[l * S + sidx(i)] = k.w[l];
+  for (int l = 0; l < LANES; ++l) p[i * LANES + l] = k.w[l];
 }
 
 template <int LANES>
@@ -101,224 +106,6 @@ __device__ __forceinline__ Key<LANES> gld(const uint64_t* __restrict__ g, int64_
 #pragma unroll
   for (int l = 0; l < LANES; ++l) k.w[l] = __ldg(g + i * LANES + l);
   return k;
-}
-
-// Merge path inside shared memory: A = [a0, a0+na), B = [b0, b0+nb) of the
-// padded arrays; this thread emits outputs [diag, diag+E). When taking b,
-// the pending A elements are those > b: inv += a_rem_base - ai.
-template <int LANES, int E, bool STATS>
-__device__ __forceinline__ void merge_path_serial(const uint64_t* __restrict__ sk,
-                                                  const uint32_t* __restrict__ si, int a0, int na,
-                                                  int b0, int nb, int diag, int64_t a_rem_base,
-                                                  Key<LANES> (&r)[E], uint32_t (&ri)[E],
-                                                  uint64_t& inv) {
-  int lo = max(0, diag - nb), hi = min(diag, na);
-  while (lo < hi) {
-    int mid = (lo + hi) >> 1;
-    if (key_le<LANES>(sld<LANES>(sk, a0 + mid), sld<LANES>(sk, b0 + diag - 1 - mid)))
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  int ai = lo, bi = diag - lo;
-  const Key<LANES> kmax = key_max<LANES>();
-  Key<LANES> ka = ai < na ? sld<LANES>(sk, a0 + ai) : kmax;
-  Key<LANES> kb = bi < nb ? sld<LANES>(sk, b0 + bi) : kmax;
-  uint32_t ia = 0, ib = 0;
-  if (STATS) {
-    ia = ai < na ? si[sidx(a0 + ai)] : 0xFFFFFFFFu;
-    ib = bi < nb ? si[sidx(b0 + bi)] : 0xFFFFFFFFu;
-  }
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    const bool ta = (bi >= nb) || (ai < na && key_le<LANES>(ka, kb));
-    if (ta) {
-      r[k] = ka;
-      if (STATS) ri[k] = ia;
-      ++ai;
-      if (ai < na) {
-        ka = sld<LANES>(sk, a0 + ai);
-        if (STATS) ia = si[sidx(a0 + ai)];
-      } else {
-        ka = kmax;
-      }
-    } else {
-      r[k] = kb;
-      if (STATS) {
-        ri[k] = ib;
-        inv += (uint64_t)(a_rem_base - ai);
-      }
-      ++bi;
-      if (bi < nb) {
-        kb = sld<LANES>(sk, b0 + bi);
-        if (STATS) ib = si[sidx(b0 + bi)];
-      } else {
-        kb = kmax;
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ int find_segment(const SegDesc* __restrict__ segs, int nsegs) {
-  __shared__ int s_seg;
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = nsegs - 1;  // last seg with tile_begin <= blockIdx.x
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (segs[mid].tile_begin <= blockIdx.x) lo = mid; else hi = mid - 1;
-    }
-    s_seg = lo;
-  }
-  __syncthreads();
-  return s_seg;
-}
-
-template <bool STATS>
-__device__ __forceinline__ void flush_stats(uint64_t inv, long long kloc, const SegDesc& sd,
-                                            unsigned long long* ginv, long long* gk) {
-  if (!STATS) return;
-  __shared__ unsigned long long s_inv;
-  __shared__ long long s_k;
-  if (threadIdx.x == 0) { s_inv = 0; s_k = 0; }
-  __syncthreads();
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    inv += __shfl_xor_sync(0xffffffffu, inv, o);
-    kloc = max(kloc, (long long)__shfl_xor_sync(0xffffffffu, kloc, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (inv) atomicAdd(&s_inv, (unsigned long long)inv);
-    if (kloc > 0) atomicMax(&s_k, kloc);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s_inv) atomicAdd(&ginv[sd.stat_slot], s_inv);
-    if (s_k > 0) atomicMax(&gk[sd.stat_slot], s_k);
-  }
-}
-
-// Registers (blocked, E per thread) -> padded smem.
-template <int LANES, int E, bool STATS, int S = SortCfg<LANES>::S>
-__device__ __forceinline__ void regs_to_smem(uint64_t* sk, uint32_t* si, const Key<LANES> (&r)[E],
-                                             const uint32_t (&ri)[E], int chunk = -1) {
-  const int base = (chunk < 0 ? (int)threadIdx.x : chunk) * E;
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    sst<LANES, S>(sk, base + k, r[k]);
-    if (STATS) si[sidx(base + k)] = ri[k];
-  }
-}
-
-// smem (padded) -> global, coalesced over the flat uint64 words of cnt keys.
-template <int LANES, bool STATS, int S = SortCfg<LANES>::S, int NT = kSortThreads>
-__device__ __forceinline__ void smem_to_global(const uint64_t* sk, const uint32_t* si, int cnt,
-                                               uint64_t* __restrict__ gk, uint32_t* __restrict__ gi) {
-  for (int w = threadIdx.x; w < cnt * LANES; w += NT) {
-    int j = w / LANES, l = w - j * LANES;
-    gk[w] = sk[l * S + sidx(j)];
-  }
-  if (STATS && gi) {
-    for (int j = threadIdx.x; j < cnt; j += NT) gi[j] = si[sidx(j)];
-  }
-}
-
-template <int LANES, bool STATS>
-__global__ void __launch_bounds__(kSortThreads) tile_sort_kernel(SortLaunch a) {
-  constexpr int E = SortCfg<LANES>::E, T = SortCfg<LANES>::T, S = SortCfg<LANES>::S;
-  extern __shared__ __align__(16) uint64_t smem[];
-  uint64_t* sk = smem;
-  uint32_t* si = reinterpret_cast<uint32_t*>(smem + (size_t)LANES * S);
-  const int tid = threadIdx.x;
-  const SegDesc sd = a.segs[find_segment(a.segs, a.nsegs)];
-  const uint64_t start = (uint64_t)(blockIdx.x - sd.tile_begin) * T;
-  const int cnt = (int)min((uint64_t)T, (uint64_t)sd.n - start);
-  const uint64_t* gin = a.keys_in + (sd.key_off + start) * LANES;
-
-  for (int w = tid; w < T * LANES; w += kSortThreads) {
-    int j = w / LANES, l = w - j * LANES;
-    sk[l * S + sidx(j)] = j < cnt ? __ldg(gin + w) : ~0ull;
-  }
-  if (STATS) {
-    for (int j = tid; j < T; j += kSortThreads) si[sidx(j)] = (uint32_t)(sd.idx_base + start + j);
-  }
-  __syncthreads();
-
-  Key<LANES> r[E];
-  uint32_t ri[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    r[k] = sld<LANES>(sk, tid * E + k);
-    ri[k] = STATS ? si[sidx(tid * E + k)] : 0u;
-  }
-  // Odd-even transposition sort of the thread's E keys: E phases, each a
-  // layer of independent compare-exchanges that swap on strictly-greater.
-  uint64_t inv = 0;
-#pragma unroll
-  for (int ph = 0; ph < E; ++ph) {
-#pragma unroll
-    for (int i = ph & 1; i + 1 < E; i += 2) {
-      const bool sw = key_lt<LANES>(r[i + 1], r[i]);
-      if (sw) {
-        Key<LANES> t = r[i]; r[i] = r[i + 1]; r[i + 1] = t;
-        uint32_t u = ri[i]; ri[i] = ri[i + 1]; ri[i + 1] = u;
-      }
-      if (STATS) inv += sw;
-    }
-  }
-  // Merge-path levels inside the tile.
-#pragma unroll 1
-  for (int run = E; run < T; run <<= 1) {
-    __syncthreads();
-    regs_to_smem<LANES, E, STATS>(sk, si, r, ri);
-    __syncthreads();
-    const int gt = (2 * run) / E;
-    const int a0 = (tid / gt) * 2 * run;
-    merge_path_serial<LANES, E, STATS>(sk, si, a0, run, a0 + run, run, (tid % gt) * E, run, r, ri,
-                                       inv);
-  }
-  long long kloc = 0;
-  if (STATS && sd.n <= (uint32_t)T) {
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      int pos = tid * E + k;
-      if (pos < cnt) kloc = max(kloc, (long long)ri[k] - (long long)sd.idx_base - pos);
-    }
-  }
-  flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);
-  __syncthreads();
-  regs_to_smem<LANES, E, STATS>(sk, si, r, ri);
-  __syncthreads();
-  smem_to_global<LANES, STATS>(sk, si, cnt, a.keys_out + (sd.key_off + start) * LANES,
-                               a.idx_out ? a.idx_out + sd.idx_off + start : nullptr);
-}
-
-// Warp-wide 32-ary merge-path search in global memory: the number of A
-// elements among the first d outputs of merge(A, B) (A first on ties).
-template <int LANES>
-__device__ int64_t merge_path_search_global(const uint64_t* __restrict__ A, int64_t na,
-                                            const uint64_t* __restrict__ B, int64_t nb, int64_t d) {
-  const int lane = threadIdx.x & 31;
-  int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
-  while (hi > lo) {
-    const int64_t span = hi - lo;
-    if (span <= 32) {
-      const int64_t x = lo + lane;
-      bool p = false;
-      if (x < hi) p = key_le<LANES>(gld<LANES>(A, x), gld<LANES>(B, d - 1 - x));
-      return lo + __popc(__ballot_sync(0xffffffffu, p));
-    }
-    const int64_t step = (span + 31) / 32;
-    const int64_t x = lo + lane * step;
-    bool p = false;
-    if (x < hi) p = key_le<LANES>(gld<LANES>(A, x), gld<LANES>(B, d - 1 - x));
-    const int c = __popc(__ballot_sync(0xffffffffu, p));
-    const int64_t nlo = c > 0 ? lo + (int64_t)(c - 1) * step + 1 : lo;
-    const int64_t xc = lo + (int64_t)c * step;
-    const int64_t nhi = (c < 32 && xc < hi) ? xc : hi;
-    lo = nlo;
-    hi = nhi;
-  }
-  return lo;
 }
 
 // ---- TMA (1-D bulk copy) + mbarrier helpers ---------------------------------
@@ -360,11 +147,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // Byte window [src, src + bytes) rounded out to 16-byte boundaries for a bulk
-// copy; returns the offset of src inside the landed window.
+// copy; `off` is the offset of src inside the landed window.
 struct Window16 {
-  const uint8_t* g;  // 16-byte aligned global start
-  uint32_t off;      // offset of the first wanted byte in the window
-  uint32_t bytes;    // multiple of 16
+  const uint8_t* g;
+  uint32_t off;
+  uint32_t bytes;
 };
 
 __device__ __forceinline__ Window16 window16(const void* src, uint32_t bytes) {
@@ -376,30 +163,84 @@ __device__ __forceinline__ Window16 window16(const void* src, uint32_t bytes) {
   return w;
 }
 
-// Merge path over two unpadded AoS windows in shared memory.
-template <int LANES, int E, bool STATS>
-__device__ __forceinline__ void merge_path_aos(const uint64_t* __restrict__ A, int na,
-                                               const uint64_t* __restrict__ B, int nb,
-                                               const uint32_t* __restrict__ IA,
-                                               const uint32_t* __restrict__ IB, int diag,
-                                               int64_t a_rem_base, Key<LANES> (&r)[E],
-                                               uint32_t (&ri)[E], uint64_t& inv) {
-  auto ld = [](const uint64_t* p, int i) {
-    Key<LANES> k;
+// ---- shared pieces --------------------------------------------------------------
+
+__device__ __forceinline__ const SegDesc& seg_at(const SortLaunch& a, int i) {
+  return a.segs ? a.segs[i] : a.inl[i];
+}
+
+// Segment of this CTA: the last segment whose first work item <= item. One
+// warp reads up to 32 tile_begin values per step and ballots.
+__device__ __forceinline__ int segment_of(const SortLaunch& a, uint32_t item) {
+  const int lane = threadIdx.x & 31;
+  const int nsegs = a.nsegs;
+  int found = 0;
+  for (int base = 0; base < nsegs; base += 32) {
+    const int i = base + lane;
+    const bool le = i < nsegs && seg_at(a, i).tile_begin <= item;
+    found += __popc(__ballot_sync(0xffffffffu, le));
+    if (!__shfl_sync(0xffffffffu, (int)le, 31)) break;
+  }
+  return found - 1;
+}
+
+__device__ __forceinline__ int find_segment(const SortLaunch& a, uint32_t item) {
+  __shared__ int s_seg;
+  if (threadIdx.x < 32) {
+    const int s = segment_of(a, item);
+    if (threadIdx.x == 0) s_seg = s;
+  }
+  __syncthreads();
+  return s_seg;
+}
+
+template <bool STATS>
+__device__ __forceinline__ void flush_stats(uint64_t inv, long long kloc, const SegDesc& sd,
+                                            unsigned long long* ginv, long long* gk) {
+  if (!STATS) return;
+  __shared__ unsigned long long s_inv;
+  __shared__ long long s_k;
+  if (threadIdx.x == 0) {
+    s_inv = 0;
+    s_k = 0;
+  }
+  __syncthreads();
 #pragma unroll
-    for (int l = 0; l < LANES; ++l) k.w[l] = p[i * LANES + l];
-    return k;
-  };
+  for (int o = 16; o > 0; o >>= 1) {
+    inv += __shfl_xor_sync(0xffffffffu, inv, o);
+    kloc = max(kloc, (long long)__shfl_xor_sync(0xffffffffu, kloc, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (inv) atomicAdd(&s_inv, (unsigned long long)inv);
+    if (kloc > 0) atomicMax(&s_k, kloc);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_inv) atomicAdd(&ginv[sd.stat_slot], s_inv);
+    if (s_k > 0) atomicMax(&gk[sd.stat_slot], s_k);
+  }
+}
+
+// Merge path over two AoS runs in shared memory: this thread emits outputs
+// [diag, diag + E). When taking b, the pending A elements are exactly those
+// > b: inv += a_rem_base - ai.
+template <int LANES, int E, bool STATS>
+__device__ __forceinline__ void merge_path(const uint64_t* __restrict__ A, int na,
+                                           const uint64_t* __restrict__ B, int nb,
+                                           const uint32_t* __restrict__ IA,
+                                           const uint32_t* __restrict__ IB, int diag,
+                                           int64_t a_rem_base, Key<LANES> (&r)[E],
+                                           uint32_t (&ri)[E], uint64_t& inv) {
   int lo = max(0, diag - nb), hi = min(diag, na);
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (key_le<LANES>(ld(A, mid), ld(B, diag - 1 - mid))) lo = mid + 1;
+    if (key_le<LANES>(ldk<LANES>(A, mid), ldk<LANES>(B, diag - 1 - mid))) lo = mid + 1;
     else hi = mid;
   }
   int ai = lo, bi = diag - lo;
   const Key<LANES> kmax = key_max<LANES>();
-  Key<LANES> ka = ai < na ? ld(A, ai) : kmax;
-  Key<LANES> kb = bi < nb ? ld(B, bi) : kmax;
+  Key<LANES> ka = ai < na ? ldk<LANES>(A, ai) : kmax;
+  Key<LANES> kb = bi < nb ? ldk<LANES>(B, bi) : kmax;
   uint32_t ia = 0, ib = 0;
   if (STATS) {
     ia = ai < na ? IA[ai] : 0u;
@@ -413,7 +254,7 @@ __device__ __forceinline__ void merge_path_aos(const uint64_t* __restrict__ A, i
       if (STATS) ri[k] = ia;
       ++ai;
       if (ai < na) {
-        ka = ld(A, ai);
+        ka = ldk<LANES>(A, ai);
         if (STATS) ia = IA[ai];
       } else {
         ka = kmax;
@@ -426,13 +267,154 @@ __device__ __forceinline__ void merge_path_aos(const uint64_t* __restrict__ A, i
       }
       ++bi;
       if (bi < nb) {
-        kb = ld(B, bi);
+        kb = ldk<LANES>(B, bi);
         if (STATS) ib = IB[bi];
       } else {
         kb = kmax;
       }
     }
   }
+}
+
+// Registers (blocked, E per thread starting at element `base`) -> AoS smem.
+template <int LANES, int E, bool STATS>
+__device__ __forceinline__ void regs_to_smem(uint64_t* sk, uint32_t* si, int base,
+                                             const Key<LANES> (&r)[E], const uint32_t (&ri)[E]) {
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    stk<LANES>(sk, base + k, r[k]);
+    if (STATS) si[base + k] = ri[k];
+  }
+}
+
+// AoS smem -> global, coalesced over the flat uint64 words of cnt keys.
+template <int LANES, bool STATS, int NT>
+__device__ __forceinline__ void smem_to_global(const uint64_t* sk, const uint32_t* si, int cnt,
+                                               uint64_t* __restrict__ gk, uint32_t* __restrict__ gi) {
+  const int words = cnt * LANES;
+  int w = threadIdx.x;
+  for (; w + NT < words; w += 2 * NT) {  // two independent stores in flight
+    const uint64_t x = sk[w], y = sk[w + NT];
+    gk[w] = x;
+    gk[w + NT] = y;
+  }
+  if (w < words) gk[w] = sk[w];
+  if (STATS && gi) {
+    for (int j = threadIdx.x; j < cnt; j += NT) gi[j] = si[j];
+  }
+}
+
+// ---- tile pass -------------------------------------------------------------------
+
+template <int LANES, bool STATS>
+__global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_constant__ SortLaunch a) {
+  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
+  constexpr size_t kKeyBytes = keys_smem_bytes<LANES, T, STATS>();
+  extern __shared__ __align__(16) uint64_t smem[];
+  uint8_t* sbytes = reinterpret_cast<uint8_t*>(smem);
+  uint32_t* si = reinterpret_cast<uint32_t*>(sbytes + kKeyBytes);
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const SegDesc sd = seg_at(a, find_segment(a, blockIdx.x));
+  const uint64_t start = (uint64_t)(blockIdx.x - sd.tile_begin) * T;
+  const int cnt = (int)min((uint64_t)T, (uint64_t)sd.n - start);
+  const uint64_t* gin = a.keys_in + (sd.key_off + start) * LANES;
+  const Window16 w = window16(gin, (uint32_t)cnt * 8 * LANES);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, w.bytes);
+    tma_load_1d(sbytes, w.g, w.bytes, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  uint64_t* sk = reinterpret_cast<uint64_t*>(sbytes + w.off);  // element 0 of the tile
+  // all-ones sentinels after the last key: they sort last and, being at the
+  // highest positions, never swap with a real key (ties keep order)
+  for (int j = cnt * LANES + tid; j < T * LANES; j += NT) sk[j] = ~0ull;
+  __syncthreads();
+
+  Key<LANES> r[E];
+  uint32_t ri[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    r[k] = ldk<LANES>(sk, tid * E + k);
+    ri[k] = STATS ? (uint32_t)(sd.idx_base + start + tid * E + k) : 0u;
+  }
+  // Odd-even transposition sort of the thread's E keys: E phases, each a
+  // layer of independent compare-exchanges that swap on strictly-greater.
+  uint64_t inv = 0;
+#pragma unroll
+  for (int ph = 0; ph < E; ++ph) {
+#pragma unroll
+    for (int i = ph & 1; i + 1 < E; i += 2) {
+      const bool sw = key_lt<LANES>(r[i + 1], r[i]);
+      if (sw) {
+        Key<LANES> t = r[i];
+        r[i] = r[i + 1];
+        r[i + 1] = t;
+        uint32_t u = ri[i];
+        ri[i] = ri[i + 1];
+        ri[i + 1] = u;
+      }
+      if (STATS) inv += sw;
+    }
+  }
+  // Merge-path levels inside the tile.
+#pragma unroll 1
+  for (int run = E; run < T; run <<= 1) {
+    __syncthreads();
+    regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
+    __syncthreads();
+    const int gt = (2 * run) / E;  // threads per merged pair
+    const int a0 = (tid / gt) * 2 * run;
+    merge_path<LANES, E, STATS>(sk + (size_t)a0 * LANES, run, sk + (size_t)(a0 + run) * LANES, run,
+                                si + a0, si + a0 + run, (tid % gt) * E, run, r, ri, inv);
+  }
+  long long kloc = 0;
+  if (STATS && sd.n <= (uint32_t)T) {
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int pos = tid * E + k;
+      if (pos < cnt) kloc = max(kloc, (long long)ri[k] - (long long)sd.idx_base - pos);
+    }
+  }
+  flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);
+  __syncthreads();
+  regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
+  __syncthreads();
+  smem_to_global<LANES, STATS, NT>(sk, si, cnt, a.keys_out + (sd.key_off + start) * LANES,
+                                   a.idx_out ? a.idx_out + sd.idx_off + start : nullptr);
+}
+
+// ---- merge pass ------------------------------------------------------------------
+
+// Warp-wide 32-ary merge-path search in global memory: the number of A
+// elements among the first d outputs of merge(A, B) (A first on ties).
+template <int LANES>
+__device__ int64_t merge_path_search_global(const uint64_t* __restrict__ A, int64_t na,
+                                            const uint64_t* __restrict__ B, int64_t nb, int64_t d) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
+  while (hi > lo) {
+    const int64_t span = hi - lo;
+    if (span <= 32) {
+      const int64_t x = lo + lane;
+      bool p = false;
+      if (x < hi) p = key_le<LANES>(gld<LANES>(A, x), gld<LANES>(B, d - 1 - x));
+      return lo + __popc(__ballot_sync(0xffffffffu, p));
+    }
+    const int64_t step = (span + 31) / 32;
+    const int64_t x = lo + lane * step;
+    bool p = false;
+    if (x < hi) p = key_le<LANES>(gld<LANES>(A, x), gld<LANES>(B, d - 1 - x));
+    const int c = __popc(__ballot_sync(0xffffffffu, p));
+    const int64_t nlo = c > 0 ? lo + (int64_t)(c - 1) * step + 1 : lo;
+    const int64_t xc = lo + (int64_t)c * step;
+    const int64_t nhi = (c < 32 && xc < hi) ? xc : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
 }
 
 struct PairGeom {
@@ -442,12 +424,10 @@ struct PairGeom {
 
 // Work items of a merge level: every pair of runs gets ceil(2R / T) output
 // tiles, so a tile never straddles two pairs whatever T is.
-__device__ __forceinline__ int64_t tiles_per_pair(int64_t R, int T) { return (2 * R + T - 1) / T; }
-
 __device__ __forceinline__ PairGeom pair_geom(const SegDesc& sd, uint32_t item, int64_t R, int T) {
   PairGeom g;
   g.n = sd.n;
-  const int64_t tpp = tiles_per_pair(R, T);
+  const int64_t tpp = (2 * R + T - 1) / T;
   const int64_t local = (int64_t)(item - sd.tile_begin);
   g.pair_base = (local / tpp) * (2 * R);
   g.na = min(R, g.n - g.pair_base);
@@ -458,57 +438,46 @@ __device__ __forceinline__ PairGeom pair_geom(const SegDesc& sd, uint32_t item, 
   return g;
 }
 
-// Partition pass: one warp per output tile finds the A/B split of the
-// tile's first output (32-ary merge-path search in global memory). All
-// splits of a level are searched in parallel, so the merge CTAs start their
-// copies immediately.
+// Partition pass: one warp per output tile finds the A/B split of the tile's
+// first output; it also records the tile's segment so the merge CTA skips
+// its own lookup.
 template <int LANES>
-__global__ void __launch_bounds__(256) merge_split_kernel(SortLaunch a) {
+__global__ void __launch_bounds__(256) merge_split_kernel(const __grid_constant__ SortLaunch a) {
   constexpr int T = MergeCfg<LANES>::T;
   const uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (item >= a.work_items) return;
-  int lo = 0, hi = a.nsegs - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.segs[mid].tile_begin <= item) lo = mid; else hi = mid - 1;
-  }
-  const SegDesc sd = a.segs[lo];
+  const int seg = segment_of(a, item);
+  const SegDesc sd = seg_at(a, seg);
   const PairGeom g = pair_geom(sd, item, a.run, T);
-  if (g.empty) return;
-  const uint64_t* A = a.keys_in + (sd.key_off + g.pair_base) * LANES;
-  const uint64_t* B = A + (int64_t)a.run * LANES;
-  const int64_t s = merge_path_search_global<LANES>(A, g.na, B, g.nb, g.d0);
-  if ((threadIdx.x & 31) == 0) a.splits[item] = (uint32_t)s;
-}
-
-template <int LANES, bool STATS>
-__host__ __device__ constexpr size_t merge_smem_bytes() {
-  // input windows (AoS, 16-byte rounded) and the padded output staging reuse
-  // the same bytes; idx windows / staging follow
-  constexpr size_t keys_in = (size_t)MergeCfg<LANES>::T * 8 * LANES + 64;
-  constexpr size_t keys_out = (size_t)MergeCfg<LANES>::S * 8 * LANES;
-  constexpr size_t kb = keys_in > keys_out ? keys_in : keys_out;
-  constexpr size_t ib = STATS ? (size_t)MergeCfg<LANES>::S * 4 + 64 : 0;
-  return ((kb + 15) & ~size_t(15)) + ib;
+  int64_t s = 0;
+  if (!g.empty) {
+    const uint64_t* A = a.keys_in + (sd.key_off + g.pair_base) * LANES;
+    const uint64_t* B = A + (int64_t)a.run * LANES;
+    s = merge_path_search_global<LANES>(A, g.na, B, g.nb, g.d0);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    a.splits[2 * item] = (uint32_t)s;
+    a.splits[2 * item + 1] = (uint32_t)seg;
+  }
 }
 
 template <int LANES, bool STATS>
 __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
-    merge_kernel(SortLaunch a) {
-  constexpr int E = MergeCfg<LANES>::E, T = MergeCfg<LANES>::T, S = MergeCfg<LANES>::S;
-  constexpr size_t kKeyBytes = (merge_smem_bytes<LANES, false>() + 15) & ~size_t(15);
+    merge_kernel(const __grid_constant__ SortLaunch a) {
+  constexpr int E = MergeCfg<LANES>::E, T = MergeCfg<LANES>::T, NT = kMergeThreads;
+  constexpr size_t kKeyBytes = keys_smem_bytes<LANES, T, STATS>();
   extern __shared__ __align__(16) uint64_t smem[];
   uint8_t* sbytes = reinterpret_cast<uint8_t*>(smem);
-  uint64_t* sk = smem;                                               // output staging (padded SoA)
-  uint32_t* si = reinterpret_cast<uint32_t*>(sbytes + kKeyBytes);    // idx staging
+  uint32_t* si = reinterpret_cast<uint32_t*>(sbytes + kKeyBytes);
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
-  const SegDesc sd = a.segs[find_segment(a.segs, a.nsegs)];
   const int64_t R = a.run;
-  const PairGeom g = pair_geom(sd, blockIdx.x, R, T);
+  const uint32_t item = blockIdx.x;
+  const SegDesc sd = seg_at(a, (int)a.splits[2 * item + 1]);  // written by the partition pass
+  const PairGeom g = pair_geom(sd, item, R, T);
   if (g.empty) return;  // uniform across the CTA
-  const int64_t a0 = a.splits[blockIdx.x];
-  const int64_t a1 = (g.d1 == g.na + g.nb) ? g.na : (int64_t)a.splits[blockIdx.x + 1];
+  const int64_t a0 = a.splits[2 * item];
+  const int64_t a1 = (g.d1 == g.na + g.nb) ? g.na : (int64_t)a.splits[2 * item + 2];
   const int64_t b0 = g.d0 - a0, b1 = g.d1 - a1;
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
   const uint64_t* Ag = a.keys_in + (sd.key_off + g.pair_base + a0) * LANES;
@@ -519,10 +488,8 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
   Window16 wia{}, wib{};
   uint32_t ib_at = 0;
   if (STATS) {
-    const uint32_t* IAg = a.idx_in + sd.idx_off + g.pair_base + a0;
-    const uint32_t* IBg = a.idx_in + sd.idx_off + g.pair_base + R + b0;
-    wia = window16(IAg, (uint32_t)la * 4);
-    wib = window16(IBg, (uint32_t)lb * 4);
+    wia = window16(a.idx_in + sd.idx_off + g.pair_base + a0, (uint32_t)la * 4);
+    wib = window16(a.idx_in + sd.idx_off + g.pair_base + R + b0, (uint32_t)lb * 4);
     ib_at = wia.bytes;
   }
   if (tid == 0) {
@@ -548,28 +515,36 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
-  // Lanes of a warp take output chunks far apart (odd multiplier mod NT), so
-  // their binary-search probes do not fall on the same smem banks.
-  const int chunk = (tid * WS_MERGE_PERM) & (kMergeThreads - 1);
-  merge_path_aos<LANES, E, STATS>(As, la, Bs, lb, IAs, IBs, min(chunk * E, la + lb), R - a0, r, ri,
-                                  inv);
+  merge_path<LANES, E, STATS>(As, la, Bs, lb, IAs, IBs, min(tid * E, la + lb), R - a0, r, ri, inv);
   long long kloc = 0;
   const int64_t out_begin = g.pair_base + g.d0;
   if (STATS && 2 * R >= g.n) {
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      const int64_t lp = (int64_t)chunk * E + k;
+      const int64_t lp = (int64_t)tid * E + k;
       if (lp < la + lb)
         kloc = max(kloc, (long long)ri[k] - (long long)sd.idx_base - (long long)(out_begin + lp));
     }
   }
-  flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);  // contains __syncthreads
+  flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);
   __syncthreads();  // every thread is done reading the input windows
-  if (chunk * E < la + lb) regs_to_smem<LANES, E, STATS, S>(sk, si, r, ri, chunk);
+  uint64_t* sk = smem;  // output staging reuses the window bytes (AoS, unpadded)
+  if (tid * E < la + lb) regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
   __syncthreads();
-  smem_to_global<LANES, STATS, S, kMergeThreads>(
-      sk, si, la + lb, a.keys_out + (sd.key_off + out_begin) * LANES,
-      STATS ? a.idx_out + sd.idx_off + out_begin : nullptr);
+  smem_to_global<LANES, STATS, NT>(sk, si, la + lb,
+                                   a.keys_out + (sd.key_off + out_begin) * LANES,
+                                   STATS ? a.idx_out + sd.idx_off + out_begin : nullptr);
+}
+
+// ---- host side ---------------------------------------------------------------------
+
+int tile_size(int lanes) {
+  switch (lanes) {
+    case 1: return TileCfg<1>::T;
+    case 2: return TileCfg<2>::T;
+    case 3: return TileCfg<3>::T;
+    default: return TileCfg<4>::T;
+  }
 }
 
 int merge_tile_size(int lanes) {
@@ -581,21 +556,12 @@ int merge_tile_size(int lanes) {
   }
 }
 
-int tile_size(int lanes) {
-  switch (lanes) {
-    case 1: return SortCfg<1>::T;
-    case 2: return SortCfg<2>::T;
-    case 3: return SortCfg<3>::T;
-    default: return SortCfg<4>::T;
-  }
-}
-
 template <int LANES, bool STATS>
 static void set_attrs_t() {
   cudaFuncSetAttribute(tile_sort_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sort_smem_bytes<LANES, STATS>());
+                       (int)pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>());
   cudaFuncSetAttribute(merge_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)merge_smem_bytes<LANES, STATS>());
+                       (int)pass_smem_bytes<LANES, MergeCfg<LANES>::T, STATS>());
 }
 
 // Opt every sort instantiation into > 48 KiB of dynamic shared memory on the
@@ -609,24 +575,25 @@ void set_sort_attributes() {
 
 template <int LANES, bool STATS>
 static void launch_tile_t(const SortLaunch& a, cudaStream_t st) {
-  tile_sort_kernel<LANES, STATS>
-      <<<a.work_items, kSortThreads, sort_smem_bytes<LANES, STATS>(), st>>>(a);
+  tile_sort_kernel<LANES, STATS><<<a.work_items, kTileThreads,
+                                   pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>(), st>>>(a);
 }
 
 template <int LANES, bool STATS>
 static void launch_merge_t(const SortLaunch& a, cudaStream_t st) {
   merge_split_kernel<LANES><<<(a.work_items * 32 + 255) / 256, 256, 0, st>>>(a);
-  merge_kernel<LANES, STATS><<<a.work_items, kMergeThreads, merge_smem_bytes<LANES, STATS>(), st>>>(a);
+  merge_kernel<LANES, STATS><<<a.work_items, kMergeThreads,
+                               pass_smem_bytes<LANES, MergeCfg<LANES>::T, STATS>(), st>>>(a);
 }
 
-#define WS_DISPATCH_LANES(fn, lanes, stats, ...)                   \
-  do {                                                             \
-    switch (lanes) {                                               \
+#define WS_DISPATCH_LANES(fn, lanes, stats, ...)                                    \
+  do {                                                                              \
+    switch (lanes) {                                                                \
       case 1: stats ? fn<1, true>(__VA_ARGS__) : fn<1, false>(__VA_ARGS__); break; \
       case 2: stats ? fn<2, true>(__VA_ARGS__) : fn<2, false>(__VA_ARGS__); break; \
       case 3: stats ? fn<3, true>(__VA_ARGS__) : fn<3, false>(__VA_ARGS__); break; \
       default: stats ? fn<4, true>(__VA_ARGS__) : fn<4, false>(__VA_ARGS__); break; \
-    }                                                              \
+    }                                                                               \
   } while (0)
 
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st) {

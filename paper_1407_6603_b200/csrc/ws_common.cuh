@@ -28,6 +28,23 @@ constexpr int kTextPad = 128;               // zero padding after the text
 
 __host__ __device__ constexpr int lanes_for_len(int L) { return (L + 7) >> 3; }
 
+// Key encodings. Raw: 8 bits per byte (any byte values; rows / word lists).
+// Alnum6: text ingest only, where every byte is [0-9A-Za-z]: an order-
+// preserving 6-bit code per character ('0'..'9' -> 1..10, 'A'..'Z' -> 11..36,
+// 'a'..'z' -> 37..62) packed as one big-endian bit string over the lanes
+// (character k at bits [6k, 6k+6) from the top), so L <= 10 -> 1 lane,
+// <= 21 -> 2, <= 32 -> 3, and key order == byte order.
+enum KeyEnc : int { kEncRaw8 = 0, kEncAlnum6 = 1 };
+__host__ __device__ constexpr int lanes_for_len_enc(int L, int enc) {
+  return enc == kEncAlnum6 ? (6 * L + 63) >> 6 : (L + 7) >> 3;
+}
+__device__ __forceinline__ uint32_t alnum6_code(uint32_t b) {
+  return b >= 0x61u ? b - 0x3Cu : (b >= 0x41u ? b - 0x36u : b - 0x2Fu);
+}
+__device__ __forceinline__ uint32_t alnum6_byte(uint32_t c) {
+  return c >= 37u ? c + 0x3Cu : (c >= 11u ? c + 0x36u : c + 0x2Fu);
+}
+
 // Byte class of the reference tokenizer WORD_RE = rb"[A-Za-z0-9]+"
 // (ingest.py:15): every other byte, including 0x00 and >= 0x80, separates.
 __device__ __forceinline__ bool is_alnum_byte(uint32_t b) {
@@ -79,6 +96,17 @@ __device__ __forceinline__ Key<LANES> key_max() {
 #pragma unroll
   for (int i = 0; i < LANES; ++i) k.w[i] = ~0ull;
   return k;
+}
+
+// Character k of a 6-bit packed key (k a compile-time constant when unrolled).
+template <int K>
+__device__ __forceinline__ uint32_t code6_at(const uint64_t* key) {
+  constexpr int bit = 6 * K, w = bit >> 6, o = bit & 63;
+  if constexpr (o <= 58) {
+    return (uint32_t)(key[w] >> (58 - o)) & 63u;
+  } else {
+    return (uint32_t)((key[w] << (o - 58)) | (key[w + 1] >> (122 - o))) & 63u;
+  }
 }
 
 // One sort segment: a bucket (or a long-word group / LSD pass) whose keys

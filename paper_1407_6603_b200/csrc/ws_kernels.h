@@ -13,6 +13,7 @@ struct ScatterParams {
   uint64_t* keys;               // key arena, or nullptr (tokens-only mode)
   uint2* longlist;              // (start, len) of words with L > 32, corpus order
   uint2* tokens;                // optional (start, len) per word in corpus order
+  int enc;                      // KeyEnc of the packed keys
 };
 
 // ingest.cu
@@ -32,18 +33,23 @@ void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t*
                       cudaStream_t st);
 
 // sort.cu
+// Segment tables of up to kInlineSegs entries travel in the kernel
+// parameters (constant bank): no host->device copy sits between passes.
+constexpr int kInlineSegs = 40;
+
 struct SortLaunch {
   const uint64_t* keys_in;
   uint64_t* keys_out;
   const uint32_t* idx_in;  // nullptr for the tile pass (idx = position)
   uint32_t* idx_out;       // nullptr in keys-only mode
-  const SegDesc* segs;     // device array
+  const SegDesc* segs;     // device array when nsegs > kInlineSegs, else nullptr
   int nsegs;
   uint32_t work_items;     // grid size
   uint32_t run;            // merge: run length being merged (>= tile)
   unsigned long long* inv; // per stat slot
   long long* kmax;         // per stat slot
   uint32_t* splits;        // merge: per work item, A-split of its first output
+  SegDesc inl[kInlineSegs];  // the segment table when it fits
 };
 int tile_size(int lanes);
 int merge_tile_size(int lanes);
@@ -60,7 +66,12 @@ struct EmitSeg {
   uint32_t pad_;
 };
 constexpr int kEmitWords = 1024;
-void launch_emit(int lanes, const EmitSeg* segs, int nsegs, uint32_t blocks, uint8_t* out,
+struct EmitTable {
+  const EmitSeg* segs;  // device array when nsegs > kInlineSegs, else nullptr
+  int nsegs;
+  EmitSeg inl[kInlineSegs];
+};
+void launch_emit(int lanes, int enc, const EmitTable& t, uint32_t blocks, uint8_t* out,
                  int with_newline, cudaStream_t st);
 
 // generic (L > 32) helpers
