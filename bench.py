@@ -323,6 +323,13 @@ def bench_ours(args) -> None:
             e2e_ms.append(a.elapsed_time(b))
         e2e_launches = ts.handle.launch_count() - e2e_launches0
     clocks = sampler.summary()
+    # one extra (untimed) e2e step with per-phase events, for the timeline
+    ts.handle.profile(reset=True)
+    ts.handle.set_profiling(True)
+    torch.cuda.synchronize(dev)
+    ts.run()
+    ts.handle.set_profiling(False)
+    e2e_phases = ts.handle.profile(reset=True)
 
     t_dev = max_over_ranks(statistics.mean(dev_ms))
     t_e2e = max_over_ranks(statistics.mean(e2e_ms))
@@ -387,9 +394,12 @@ def bench_ours(args) -> None:
             "parity_vs_oracle": parity,
             "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in agg.items()},
         }
+        line["e2e_timeline_ms"] = [[p["name"], round(p["start_ms"], 3), round(p["ms"], 3)]
+                                   for p in e2e_phases]
         if args.profile_json:
             Path(args.profile_json).write_text(json.dumps({"phases": agg, "steps": args.steps,
-                                                           "dev_ms": dev_ms, "e2e_ms": e2e_ms},
+                                                           "dev_ms": dev_ms, "e2e_ms": e2e_ms,
+                                                           "e2e_phases": e2e_phases},
                                                           indent=1))
         print(json.dumps(line), flush=True)
     ts.close()

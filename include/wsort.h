@@ -153,8 +153,9 @@ typedef struct ws_phase {
   char name[32];
   int32_t launches;  /* kernel launches (or copies) in this phase            */
   int32_t kind;      /* 0 = kernel, 1 = host<->device copy                    */
-  double ms;         /* CUDA-event time on the handle's stream                */
+  double ms;         /* CUDA-event time on the stream the phase ran on        */
   double bytes;      /* algorithmic bytes moved (per-pass table)   */
+  double start_ms;   /* start relative to the first recorded phase            */
 } ws_phase;
 
 /* Record CUDA events around every phase while enabled. */

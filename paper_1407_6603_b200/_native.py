@@ -45,6 +45,7 @@ class WsPhase(ctypes.Structure):
         ("kind", ctypes.c_int32),
         ("ms", ctypes.c_double),
         ("bytes", ctypes.c_double),
+        ("start_ms", ctypes.c_double),
     ]
 
 
@@ -312,7 +313,8 @@ class Handle:
         arr = (WsPhase * max(n.value, 1))()
         check(self.lib.ws_profile(self.h, arr, n.value, ctypes.byref(n)))
         res = [dict(name=arr[i].name.decode(), launches=arr[i].launches, kind=arr[i].kind,
-                    ms=arr[i].ms, bytes=arr[i].bytes) for i in range(n.value)]
+                    ms=arr[i].ms, bytes=arr[i].bytes, start_ms=arr[i].start_ms)
+               for i in range(n.value)]
         if reset:
             check(self.lib.ws_profile_reset(self.h))
         return res

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -97,6 +98,11 @@ struct PinBuf {
 };
 
 constexpr int kClasses = 4;  // lane classes 1..4
+// Texts up to this size use the single-pass ingest (capacity-bounded key
+// regions, ~37 bytes per text byte); larger texts the two-pass count + scatter.
+constexpr uint64_t kSinglePassMaxText = 512ull << 20;
+// Host texts at least this large are copied in pieces overlapped with ingest.
+constexpr uint64_t kChunkedH2DMin = 16ull << 20;
 
 struct Bucket {
   uint32_t len = 0;
@@ -108,6 +114,7 @@ struct Bucket {
   uint64_t long_off = 0;     // long: offset in the grouped long-word list
   int final_buf = 0;         // packed: which key/idx buffer holds the sorted run
   int64_t inv = 0, kmax = 0; // stats (valid after ws_sort(h, 1))
+  const uint64_t* in_ptr = nullptr;  // packed: the unsorted keys (ingest output)
 };
 
 struct PhaseRec {
@@ -125,6 +132,7 @@ struct SegIn {
   uint32_t stat_slot;
   uint32_t idx_base;
   int final_buf;  // out
+  const uint64_t* in_ptr = nullptr;  // unsorted keys for the tile pass (default: keys0)
 };
 
 }  // namespace
@@ -133,12 +141,19 @@ struct ws_handle {
   int device = 0;
   cudaStream_t st = nullptr;
   cudaStream_t cs[kClasses + 1] = {nullptr};  // one stream per lane class (cs[0] unused)
+  cudaStream_t es[kClasses + 1] = {nullptr};  // per class: emit of completed buckets
+  cudaStream_t ds[kClasses + 1] = {nullptr};  // per class: D2H of emitted buckets
+  cudaStream_t hs = nullptr;                  // chunked H2D of the text
+  DevBuf overflow;                            // chunked ingest: a word ran past a piece
+  std::vector<cudaEvent_t> sync_events;       // pool of timing-free events
+  size_t sync_used = 0;
   cudaEvent_t ev_fork = nullptr, ev_join[kClasses + 1] = {nullptr};
   // text / word sources
   DevBuf text;         // corpus bytes (+ padding) or word bytes or rows
   DevBuf starts, lens; // word-list ingest
   DevBuf hist, off, totals;
   DevBuf keys[2], idx[2];
+  DevBuf keys_cap, status, ticket;  // single-pass ingest: capacity-bounded regions
   DevBuf longlist, longgrp, rank, rank_tmp, lkeys[2], lidx[2];
   DevBuf tokens;
   DevBuf stat_inv, stat_k, stat_k_dummy;
@@ -214,6 +229,16 @@ struct Phase {
   ~Phase() { end(); }
 };
 
+// Timing-free event from the handle's pool (valid until the next public call).
+cudaEvent_t sync_event(ws_handle* h) {
+  if (h->sync_used == h->sync_events.size()) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    h->sync_events.push_back(e);
+  }
+  return h->sync_events[h->sync_used++];
+}
+
 int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail_cuda(e, what, 0);
@@ -221,7 +246,10 @@ int check_launch(const char* what) {
 }
 
 // Parameter tables: staged in pinned memory, uploaded with one copy each.
-void params_reset(ws_handle* h) { h->param_used = 0; }
+void params_reset(ws_handle* h) {
+  h->param_used = 0;
+  h->sync_used = 0;
+}
 
 template <class T>
 int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev,
@@ -268,10 +296,14 @@ int begin_call(ws_handle* h) {
 // lane width, data starting in keys0 (+ implicit idx), ping-ponging with
 // keys1/idx1/idx0. Each segment's final buffer parity is written back.
 
+// Called after the pass that completes some segments (their final buffer is
+// known): lets the caller emit / copy those segments while later passes run.
+using PassDoneHook = std::function<int(const std::vector<const SegIn*>&, cudaStream_t)>;
+
 int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* keys0,
                   uint64_t* keys1, uint32_t* idx0, uint32_t* idx1, bool stats,
                   unsigned long long* inv, long long* kmax, const char* tag,
-                  cudaStream_t st = nullptr) {
+                  cudaStream_t st = nullptr, const PassDoneHook* on_done = nullptr) {
   if (!st) st = h->st;
   std::vector<SegIn*> live;
   for (auto& s : segs) {
@@ -300,6 +332,7 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
     for (auto* s : live) {
       if (p > 0 && s->n <= run) continue;
       SegDesc sd;
+      sd.in_ptr = p == 0 ? s->in_ptr : nullptr;
       sd.key_off = s->key_off;
       sd.idx_off = s->idx_off;
       sd.n = s->n;
@@ -347,6 +380,13 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
     }
     ph.end();
     WS_TRY(check_launch(name));
+    if (on_done) {
+      std::vector<const SegIn*> done;  // segments whose last pass is p
+      const uint64_t next_run = (uint64_t)T << p;
+      for (auto* s : live)
+        if ((p == 0 || s->n > run) && s->n <= next_run) done.push_back(s);
+      if (!done.empty()) WS_TRY((*on_done)(done, st));
+    }
   }
   return WS_OK;
 }
@@ -390,6 +430,8 @@ int plan_packed(ws_handle* h, const uint64_t* counts) {
   const size_t key_bytes = run * 8 + 64;
   WS_CUDA(h->keys[0].ensure(key_bytes));
   WS_CUDA(h->keys[1].ensure(key_bytes));
+  for (auto& bk : h->buckets)
+    bk.in_ptr = h->keys[0].as<uint64_t>() + h->class_base[bk.lanes] + bk.elem_off * bk.lanes;
   return WS_OK;
 }
 
@@ -472,7 +514,15 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   h->text_valid = false;
   h->enc = kEncAlnum6;  // tokens are [0-9A-Za-z] only
   if (!resident) WS_CUDA(h->text.ensure(n + kTextPad));
-  if (!resident) {
+  // Large host texts are copied in pieces on their own stream and each piece
+  // is ingested as soon as the next one has landed (its last words may run
+  // into it), overlapping the H2D with the single-pass ingest.
+  const char* force2 = getenv("WSORT_TWO_PASS");
+  const bool single = n <= kSinglePassMaxText && !(force2 && force2[0] == '1');
+  const char* nochunk = getenv("WSORT_NO_CHUNKED_H2D");
+  const bool chunked = single && !resident && !(flags & WS_INGEST_DEVICE_PTR) &&
+                       n >= kChunkedH2DMin && !(nochunk && nochunk[0] == '1');
+  if (!resident && !chunked) {
     Phase ph(h, "h2d_text", (double)n, (flags & WS_INGEST_DEVICE_PTR) ? 0 : 1);
     if (n)
       WS_CUDA(cudaMemcpyAsync(h->text.p, text, n,
@@ -483,53 +533,154 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   }
   const uint32_t nchunks = chunk_count(n);
   h->nchunks = nchunks;
-  const size_t hist_bytes = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
-  WS_CUDA(h->hist.ensure(hist_bytes));
-  WS_CUDA(h->off.ensure(hist_bytes));
   WS_CUDA(h->totals.ensure(kHistRows * 4));
   WS_CUDA(h->pin_small.ensure(1 << 16));
   const uint8_t* dtext = h->text.as<uint8_t>();
   uint32_t* tot_host = static_cast<uint32_t*>(h->pin_small.p);
-  if (nchunks) {
-    {
-      Phase ph(h, "count", (double)n);
-      launch_count(dtext, n, h->hist.as<uint32_t>(), nchunks, h->st);
-      ++h->launches;
-    }
-    WS_TRY(check_launch("count_kernel"));
-    {
-      Phase ph(h, "scan", (double)kHistRows * nchunks * 8);
-      launch_scan(h->hist.as<uint32_t>(), h->off.as<uint32_t>(), h->totals.as<uint32_t>(),
-                  nchunks, kHistRows, h->st);
-      ++h->launches;
-    }
-    WS_TRY(check_launch("scan_kernel"));
-    WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
-    WS_CUDA(cudaStreamSynchronize(h->st));
-  } else {
-    memset(tot_host, 0, kHistRows * 4);
-  }
-  uint64_t counts[kNumBins];
-  for (int b = 0; b < kNumBins; ++b) counts[b] = tot_host[b];
-  const uint64_t total_words = tot_host[kNumBins];
-  WS_TRY(plan_packed(h, counts));
-  const uint64_t m = counts[kLongBin];
-  WS_CUDA(h->longlist.ensure(std::max<uint64_t>(m, 1) * sizeof(uint2)));
+  const bool keep_tokens = (flags & WS_INGEST_KEEP_TOKENS) != 0;
   ScatterParams p;
-  fill_scatter_params(h, p);
-  if (flags & WS_INGEST_KEEP_TOKENS) {
-    WS_CUDA(h->tokens.ensure(std::max<uint64_t>(total_words, 1) * sizeof(uint2)));
-    p.tokens = h->tokens.as<uint2>();
-    h->have_tokens = true;
+  memset(&p, 0, sizeof p);
+  p.enc = h->enc;
+  uint64_t region[kNumBins] = {0};
+  uint64_t m = 0, total_words = 0;
+  uint64_t counts[kNumBins];
+  if (single) {
+    // Capacity-bounded per-length regions: at most (n+1)/(L+1) words of length
+    // L fit in n bytes. Bases are multiples of 12 words (16-byte aligned and
+    // divisible by every lane count).
+    uint64_t run = 0;
+    for (int b = 0; b < kMaxPackedLen; ++b) {
+      const int L = b + 1;
+      region[b] = run;
+      run += (n + 1) / (L + 1) * lanes_for_len_enc(L, h->enc);
+      run = (run + 11) / 12 * 12;
+    }
+    WS_CUDA(h->keys_cap.ensure(run * 8 + 256));
+    WS_CUDA(h->longlist.ensure(((n + 1) / (kMaxPackedLen + 2) + 1) * sizeof(uint2)));
+    if (keep_tokens) WS_CUDA(h->tokens.ensure(((n + 1) / 2 + 1) * sizeof(uint2)));
+    WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kHistRows * 8));
+    WS_CUDA(h->ticket.ensure(256));
+    for (int b = 0; b < kMaxPackedLen; ++b) p.bin_base[b] = region[b];
+    p.keys = h->keys_cap.as<uint64_t>();
+    p.longlist = h->longlist.as<uint2>();
+    p.tokens = keep_tokens ? h->tokens.as<uint2>() : nullptr;
+    p.chunk0 = 0;
+    p.nchunks_total = nchunks;
+    p.ticket = h->ticket.as<unsigned int>();
+    p.status = h->status.as<unsigned long long>();
+    p.totals = h->totals.as<uint32_t>();
+    if (nchunks) {
+      WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kHistRows * 8, h->st));
+      WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
+      bool redo = false;
+      if (chunked) {
+        WS_CUDA(h->overflow.ensure(256));
+        WS_CUDA(cudaMemsetAsync(h->overflow.p, 0, 4, h->st));
+        p.overflow = h->overflow.as<unsigned int>();
+        const uint64_t cb = ingest_chunk_bytes();
+        const int P = (int)std::min<uint64_t>(16, std::max<uint64_t>(2, n / (8ull << 20)));
+        const uint64_t piece = (n / P + cb - 1) / cb * cb;
+        std::vector<uint64_t> edge;  // piece boundaries (bytes)
+        for (uint64_t o = 0; o < n; o += piece) edge.push_back(o);
+        edge.push_back(n);
+        const int np = (int)edge.size() - 1;
+        std::vector<cudaEvent_t> landed(np);
+        for (int i = 0; i < np; ++i) {
+          Phase ph(h, "h2d_text", (double)(edge[i + 1] - edge[i]), 1, h->hs);
+          WS_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(h->text.p) + edge[i], text + edge[i],
+                                  edge[i + 1] - edge[i], cudaMemcpyHostToDevice, h->hs));
+          if (i == np - 1)
+            WS_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(h->text.p) + n, 0, kTextPad, h->hs));
+          landed[i] = sync_event(h);
+          WS_CUDA(cudaEventRecord(landed[i], h->hs));
+        }
+        for (int i = 0; i < np; ++i) {
+          const int need = std::min(i + 1, np - 1);
+          WS_CUDA(cudaStreamWaitEvent(h->st, landed[need], 0));
+          ScatterParams pi = p;
+          pi.avail = need == np - 1 ? 0 : edge[need + 1];
+          const uint32_t c0 = (uint32_t)(edge[i] / cb), c1 = (uint32_t)((edge[i + 1] + cb - 1) / cb);
+          Phase ph(h, "ingest", 2.27 * (double)(edge[i + 1] - edge[i]));
+          launch_ingest_lookback(dtext, n, c1 - c0, pi, h->st);
+          ++h->launches;
+        }
+        WS_TRY(check_launch("ingest_kernel"));
+        WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
+                                h->st));
+        WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+        WS_CUDA(cudaStreamSynchronize(h->st));
+        redo = tot_host[kHistRows] != 0;  // a word spanned a whole piece: ingest again
+        if (redo) {
+          p.overflow = nullptr;
+          WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kHistRows * 8, h->st));
+          WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
+        }
+      }
+      if (!chunked || redo) {
+        {
+          // algorithmic bytes: text read + keys written (estimated from the text; exact
+          // counts are only known afterwards)
+          Phase ph(h, "ingest", (double)n + 1.27 * (double)n);
+          launch_ingest_lookback(dtext, n, nchunks, p, h->st);
+          ++h->launches;
+        }
+        WS_TRY(check_launch("ingest_kernel"));
+        WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+        WS_CUDA(cudaStreamSynchronize(h->st));
+      }
+    } else {
+      memset(tot_host, 0, kHistRows * 4);
+    }
+    for (int b = 0; b < kNumBins; ++b) counts[b] = tot_host[b];
+    total_words = tot_host[kNumBins];
+    m = counts[kLongBin];
+    WS_TRY(plan_packed(h, counts));  // compact layout of the sort buffers
+    for (auto& bk : h->buckets)
+      if (!bk.is_long) bk.in_ptr = h->keys_cap.as<uint64_t>() + region[bk.len - 1];
+    if (keep_tokens) h->have_tokens = true;
+  } else {
+    const size_t hist_bytes = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
+    WS_CUDA(h->hist.ensure(hist_bytes));
+    WS_CUDA(h->off.ensure(hist_bytes));
+    if (nchunks) {
+      {
+        Phase ph(h, "count", (double)n);
+        launch_count(dtext, n, h->hist.as<uint32_t>(), nchunks, h->st);
+        ++h->launches;
+      }
+      WS_TRY(check_launch("count_kernel"));
+      {
+        Phase ph(h, "scan", (double)kHistRows * nchunks * 8);
+        launch_scan(h->hist.as<uint32_t>(), h->off.as<uint32_t>(), h->totals.as<uint32_t>(),
+                    nchunks, kHistRows, h->st);
+        ++h->launches;
+      }
+      WS_TRY(check_launch("scan_kernel"));
+      WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+      WS_CUDA(cudaStreamSynchronize(h->st));
+    } else {
+      memset(tot_host, 0, kHistRows * 4);
+    }
+    for (int b = 0; b < kNumBins; ++b) counts[b] = tot_host[b];
+    total_words = tot_host[kNumBins];
+    WS_TRY(plan_packed(h, counts));
+    m = counts[kLongBin];
+    WS_CUDA(h->longlist.ensure(std::max<uint64_t>(m, 1) * sizeof(uint2)));
+    fill_scatter_params(h, p);
+    if (keep_tokens) {
+      WS_CUDA(h->tokens.ensure(std::max<uint64_t>(total_words, 1) * sizeof(uint2)));
+      p.tokens = h->tokens.as<uint2>();
+      h->have_tokens = true;
+    }
+    if (nchunks) {
+      double kbytes = 0;
+      for (auto& b : h->buckets) kbytes += (double)b.count * b.lanes * 8;
+      Phase ph(h, "scatter", (double)n + kbytes + 8.0 * m);
+      launch_scatter(dtext, n, h->off.as<uint32_t>(), nchunks, p, h->st);
+      ++h->launches;
+    }
+    WS_TRY(check_launch("scatter_kernel"));
   }
-  if (nchunks) {
-    double kbytes = 0;
-    for (auto& b : h->buckets) kbytes += (double)b.count * b.lanes * 8;
-    Phase ph(h, "scatter", (double)n + kbytes + 8.0 * m);
-    launch_scatter(dtext, n, h->off.as<uint32_t>(), nchunks, p, h->st);
-    ++h->launches;
-  }
-  WS_TRY(check_launch("scatter_kernel"));
   WS_TRY(group_long_words(h, m));
   h->words = total_words;
   h->text_valid = true;
@@ -540,7 +691,8 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
 // sort of all buckets
 
 int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* offsets,
-                int only, cudaStream_t st);
+                int only = -1, cudaStream_t st = nullptr,
+                const std::vector<int>* subset = nullptr);
 std::vector<uint64_t> emit_offsets(ws_handle* h, bool lines);
 
 // Optional fused emission: as soon as a lane class is sorted, its stream
@@ -588,26 +740,71 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   // packed buckets: one schedule per lane class, each class on its own stream
   // (the classes are independent; small classes fill the big one's bubbles)
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
-  for (int c = 1; c <= kClasses; ++c) {
+  for (int c = kClasses; c >= 1; --c) {  // small (multi-lane) classes are submitted first
     std::vector<SegIn> segs;
     std::vector<int> which;
     for (int i = 0; i < nb; ++i) {
       const Bucket& b = h->buckets[i];
       if (b.is_long || b.lanes != c) continue;
       segs.push_back(SegIn{b.elem_off, b.idx_off, (uint32_t)b.count, (uint32_t)i, 0, 0});
+      segs.back().in_ptr = b.in_ptr;
       which.push_back(i);
     }
     if (segs.empty()) continue;
     cudaStream_t cst = h->serial ? h->st : h->cs[c];
+    cudaStream_t est = h->serial ? h->st : h->es[c];
+    cudaStream_t dst = h->serial ? h->st : h->ds[c];
     WS_CUDA(cudaStreamWaitEvent(cst, h->ev_fork, 0));
     uint64_t* k0 = h->keys[0].as<uint64_t>() + h->class_base[c];
     uint64_t* k1 = h->keys[1].as<uint64_t>() + h->class_base[c];
+    // Fused emission: a bucket is emitted (and copied to the host) right after
+    // the pass that completes it, on side streams, while later passes run.
+    PassDoneHook hook = [&, est, dst](const std::vector<const SegIn*>& done,
+                                      cudaStream_t st) -> int {
+      std::vector<int> bids;
+      for (const SegIn* sg : done) {
+        h->buckets[sg->stat_slot].final_buf = sg->final_buf;
+        bids.push_back((int)sg->stat_slot);
+      }
+      if (est != st) {
+        cudaEvent_t ev = sync_event(h);
+        WS_CUDA(cudaEventRecord(ev, st));
+        WS_CUDA(cudaStreamWaitEvent(est, ev, 0));
+      }
+      WS_TRY(emit_device(h, fe->dout, true, nullptr, -1, est, &bids));
+      if (!fe->host) return WS_OK;
+      if (dst != est) {
+        cudaEvent_t ev2 = sync_event(h);
+        WS_CUDA(cudaEventRecord(ev2, est));
+        WS_CUDA(cudaStreamWaitEvent(dst, ev2, 0));
+      }
+      std::sort(bids.begin(), bids.end());
+      size_t k = 0;
+      while (k < bids.size()) {  // coalesce adjacent output ranges
+        uint64_t lo = fe->off[bids[k]], hi = fe->off[bids[k] + 1];
+        size_t j = k + 1;
+        while (j < bids.size() && fe->off[bids[j]] == hi) hi = fe->off[bids[j++] + 1];
+        if (hi > lo) {
+          Phase ph(h, "d2h_out", (double)(hi - lo), 1, dst);
+          WS_CUDA(cudaMemcpyAsync(fe->host + lo, fe->dout + lo, hi - lo, cudaMemcpyDeviceToHost,
+                                  dst));
+        }
+        k = j;
+      }
+      return WS_OK;
+    };
     WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(), h->idx[1].as<uint32_t>(),
-                         stats, inv, km, "", cst));
+                         stats, inv, km, "", cst, fe ? &hook : nullptr));
     for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
-    if (fe) WS_TRY(fused_class_copy(h, fe, c, cst));
     WS_CUDA(cudaEventRecord(h->ev_join[c], cst));
     WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_join[c], 0));
+    if (fe && est != h->st) {
+      cudaEvent_t e1 = sync_event(h), e2 = sync_event(h);
+      WS_CUDA(cudaEventRecord(e1, est));
+      WS_CUDA(cudaStreamWaitEvent(h->st, e1, 0));
+      WS_CUDA(cudaEventRecord(e2, dst));
+      WS_CUDA(cudaStreamWaitEvent(h->st, e2, 0));
+    }
   }
   // long groups: LSD over 8-byte lanes, least significant lane first
   if (h->n_long) {
@@ -618,14 +815,14 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     ++h->launches;
     int max_lanes = 0;
     for (auto& b : h->buckets)
-      if (b.is_long) max_lanes = std::max(max_lanes, lanes_for_len(b.len));
+      if (b.is_long && b.count > 1) max_lanes = std::max(max_lanes, lanes_for_len(b.len));
     const uint8_t* ltext = h->text.as<uint8_t>();
     for (int lane = max_lanes - 1; lane >= 0; --lane) {
       std::vector<SegIn> segs;
       std::vector<int> which;
       for (int i = 0; i < nb; ++i) {
         const Bucket& b = h->buckets[i];
-        if (!b.is_long || lanes_for_len(b.len) <= lane) continue;
+        if (!b.is_long || b.count < 2 || lanes_for_len(b.len) <= lane) continue;
         segs.push_back(SegIn{b.long_off, b.long_off, (uint32_t)b.count, (uint32_t)i,
                              (uint32_t)b.long_off, 0});
         which.push_back(i);
@@ -687,6 +884,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
 // emit
 
 const uint64_t* bucket_keys(ws_handle* h, const Bucket& b, bool sorted) {
+  if (!sorted && b.in_ptr) return b.in_ptr;
   const int buf = sorted ? b.final_buf : 0;
   return h->keys[buf].as<uint64_t>() + h->class_base[b.lanes] + b.elem_off * b.lanes;
 }
@@ -707,15 +905,18 @@ std::vector<uint64_t> emit_offsets(ws_handle* h, bool lines) {
 // Enqueue emission into device buffer `dout`: lane class `only` (1..4), the
 // long groups (0), or everything (-1), on stream `st`.
 int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* offsets,
-                int only = -1, cudaStream_t st = nullptr) {
+                int only, cudaStream_t st, const std::vector<int>* subset) {
   if (!st) st = h->st;
   const int nl = lines ? 1 : 0;
   std::vector<uint64_t> off = emit_offsets(h, lines);
+  std::vector<char> pick(h->buckets.size(), subset ? 0 : 1);
+  if (subset)
+    for (int i : *subset) pick[i] = 1;
   double kb = 0, ob = 0;
   for (size_t i = 0; i < h->buckets.size(); ++i) {
     const Bucket& b = h->buckets[i];
     const int cls = b.is_long ? 0 : b.lanes;
-    if (only >= 0 && cls != only) continue;
+    if ((only >= 0 && cls != only) || !pick[i]) continue;
     kb += b.is_long ? 0.0 : (double)b.count * b.lanes * 8;
     ob += (double)(off[i + 1] - off[i]);
   }
@@ -729,7 +930,7 @@ int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* 
     uint32_t blocks = 0;
     for (size_t i = 0; i < h->buckets.size(); ++i) {
       const Bucket& b = h->buckets[i];
-      if (b.is_long || b.lanes != c || !b.count) continue;
+      if (b.is_long || b.lanes != c || !b.count || !pick[i]) continue;
       EmitSeg e;
       e.keys = bucket_keys(h, b, h->sorted);
       e.out_off = off[i];
@@ -755,7 +956,7 @@ int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* 
   if (only <= 0) {
     for (size_t i = 0; i < h->buckets.size(); ++i) {
       const Bucket& b = h->buckets[i];
-      if (!b.is_long || !b.count) continue;
+      if (!b.is_long || !b.count || !pick[i]) continue;
       const uint32_t* order = h->sorted ? h->rank.as<uint32_t>() + b.long_off : nullptr;
       const uint2* words = h->longgrp.as<uint2>() + (h->sorted ? 0 : b.long_off);
       launch_emit_long(h->text.as<uint8_t>(), words, order, b.count, b.len, dout + off[i], nl, st);
@@ -1011,9 +1212,20 @@ int ws_create(ws_handle** out, int32_t device) {
   h->device = device;
   const char* ser = getenv("WSORT_SERIAL");
   h->serial = ser && ser[0] == '1';
+  // Priorities: the multi-lane classes are small and their payload can reach
+  // the host while the 1-lane class still sorts, so they (and every emit /
+  // copy stream) outrank the 1-lane class's sort stream.
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
   for (int c = 1; c <= kClasses && e == cudaSuccess; ++c)
-    e = cudaStreamCreateWithFlags(&h->cs[c], cudaStreamNonBlocking);
+    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, c == 1 ? prio_lo : prio_hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->hs, cudaStreamNonBlocking, prio_hi);
+  for (int c = 1; c <= kClasses && e == cudaSuccess; ++c) {
+    e = cudaStreamCreateWithPriority(&h->es[c], cudaStreamNonBlocking, prio_hi);
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&h->ds[c], cudaStreamNonBlocking, prio_hi);
+  }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   for (int c = 1; c <= kClasses && e == cudaSuccess; ++c)
     e = cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming);
@@ -1029,14 +1241,18 @@ void ws_destroy(ws_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
-  for (int c = 1; c <= kClasses; ++c)
+  for (int c = 1; c <= kClasses; ++c) {
     if (h->cs[c]) cudaStreamSynchronize(h->cs[c]);
+    if (h->es[c]) cudaStreamSynchronize(h->es[c]);
+    if (h->ds[c]) cudaStreamSynchronize(h->ds[c]);
+  }
   DevBuf* bufs[] = {&h->text, &h->starts, &h->lens, &h->hist, &h->off, &h->totals,
                     &h->keys[0], &h->keys[1], &h->idx[0], &h->idx[1], &h->longlist,
                     &h->longgrp, &h->rank, &h->rank_tmp, &h->lkeys[0], &h->lkeys[1],
                     &h->lidx[0], &h->lidx[1], &h->tokens, &h->stat_inv, &h->stat_k,
                     &h->stat_k_dummy, &h->out, &h->params, &h->splits[0], &h->splits[1],
-                    &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5]};
+                    &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5],
+                    &h->keys_cap, &h->status, &h->ticket, &h->overflow};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();
@@ -1045,11 +1261,15 @@ void ws_destroy(ws_handle* h) {
     cudaEventDestroy(p.b);
   }
   for (auto e : h->event_pool) cudaEventDestroy(e);
+  for (auto e : h->sync_events) cudaEventDestroy(e);
   for (int c = 1; c <= kClasses; ++c) {
+    if (h->es[c]) cudaStreamDestroy(h->es[c]);
+    if (h->ds[c]) cudaStreamDestroy(h->ds[c]);
     if (h->cs[c]) cudaStreamDestroy(h->cs[c]);
     if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->hs) cudaStreamDestroy(h->hs);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -1293,6 +1513,9 @@ int ws_profile(ws_handle* h, ws_phase* out, int32_t cap, int32_t* n) {
     out[i].kind = p.kind;
     out[i].ms = ms;
     out[i].bytes = p.bytes;
+    float t0 = 0;
+    if (i > 0) WS_CUDA(cudaEventElapsedTime(&t0, h->phases[0].a, p.a));
+    out[i].start_ms = t0;
   }
   return WS_OK;
 }

@@ -31,7 +31,10 @@ __device__ __forceinline__ uint32_t bin_of_len(uint32_t len) {
 }
 
 // Length of the alnum run starting at text[pos] (pos is known alnum or not).
-__device__ uint32_t run_length_from(const uint8_t* __restrict__ text, uint64_t pos) {
+// `avail` bounds the bytes that may be read (chunked H2D: later pieces may not
+// have landed yet); running into it sets *overflow and stops.
+__device__ uint32_t run_length_from(const uint8_t* __restrict__ text, uint64_t pos,
+                                    uint64_t avail = ~0ull, unsigned int* overflow = nullptr) {
   uint32_t len = 0;
   // bring pos to a 16-byte boundary with byte steps
   while ((pos & 15) != 0) {
@@ -40,6 +43,10 @@ __device__ uint32_t run_length_from(const uint8_t* __restrict__ text, uint64_t p
     ++pos;
   }
   while (true) {
+    if (pos + 16 > avail) {
+      if (overflow) atomicOr(overflow, 1u);
+      return len;
+    }
     uint4 v = *reinterpret_cast<const uint4*>(text + pos);
     uint32_t m = alnum_mask16(v);
     if (m != 0xFFFFu) return len + __ffs(~m) - 1;
@@ -63,7 +70,9 @@ struct Segment16 {
 // the whole chunk scans global memory, and only its starting thread does so.
 __device__ __forceinline__ Segment16 classify_chunk(const uint8_t* __restrict__ text, uint64_t n,
                                                     uint64_t cbase, uint4& v_out,
-                                                    uint32_t* s_chain /*[kWarps]*/) {
+                                                    uint32_t* s_chain /*[kWarps]*/,
+                                                    uint64_t avail = ~0ull,
+                                                    unsigned int* overflow = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t base = cbase + (uint64_t)tid * 16;
   uint4 v = make_uint4(0, 0, 0, 0);
@@ -106,7 +115,7 @@ __device__ __forceinline__ Segment16 classify_chunk(const uint8_t* __restrict__ 
         break;
       }
     }
-    if (!cF) cV += run_length_from(text, cbase + kChunk);
+    if (!cF) cV += run_length_from(text, cbase + kChunk, avail, overflow);
   }
   s.cont = cV;
   return s;
@@ -231,24 +240,33 @@ __device__ __forceinline__ void pack_from_smem(const uint32_t* __restrict__ c32,
 // 6-bit alnum packing (text ingest): characters form one big-endian bit
 // string over up to 3 lanes; the unrolled loop resolves lane/shift at compile
 // time, characters past L are predicated off.
-// 8 big-endian alnum bytes -> their 6-bit codes as one 48-bit big-endian
-// string (SWAR: byte-parallel code arithmetic, then two compaction steps).
-__device__ __forceinline__ uint64_t codes48(uint64_t x) {
-  const uint64_t hi = 0x8080808080808080ull;
-  const uint64_t xh = x | hi;  // every byte >= 0x80: no borrows below
-  const uint64_t ge41 = ((xh - 0x4141414141414141ull) & hi) >> 7;  // 1 per byte >= 'A'
-  const uint64_t ge61 = ((xh - 0x6161616161616161ull) & hi) >> 7;  // 1 per byte >= 'a'
-  const uint64_t off = 0x2F2F2F2F2F2F2F2Full + ge41 * 7 + ge61 * 6;
-  uint64_t c = (xh - off) & 0x3F3F3F3F3F3F3F3Full;  // code per byte
-  c = ((c & 0x3F003F003F003F00ull) >> 2) | (c & 0x003F003F003F003Full);   // 12 bits / 16
-  c = ((c & 0x0FFF00000FFF0000ull) >> 4) | (c & 0x00000FFF00000FFFull);   // 24 bits / 32
-  return ((c >> 32) << 24) | (c & 0xFFFFFFull);                            // 48 bits
+// 4 bytes -> their 6-bit alnum codes, byte by byte (SWAR; bytes that are not
+// [0-9A-Za-z] give garbage that the per-word length mask removes later).
+__device__ __forceinline__ uint32_t alnum6_codes4(uint32_t x) {
+  const uint32_t xh = x | 0x80808080u;                        // no borrows below
+  const uint32_t ge41 = ((xh - 0x41414141u) & 0x80808080u) >> 7;  // 1 per byte >= 'A'
+  const uint32_t ge61 = ((xh - 0x61616161u) & 0x80808080u) >> 7;  // 1 per byte >= 'a'
+  return (xh - (0x2F2F2F2Fu + ge41 * 7u + ge61 * 6u)) & 0x3F3F3F3Fu;
 }
 
-__device__ __forceinline__ void pack6_from_smem(const uint32_t* __restrict__ c32, uint32_t start,
-                                                uint32_t L, int lanes, uint64_t* __restrict__ dst) {
-  // raw big-endian 8-byte lanes of the word (as pack_from_smem), then codes
-  uint64_t v[4];
+__device__ __forceinline__ uint4 alnum6_codes16(uint4 v) {
+  return make_uint4(alnum6_codes4(v.x), alnum6_codes4(v.y), alnum6_codes4(v.z),
+                    alnum6_codes4(v.w));
+}
+
+// 4 code bytes (little-endian in a u32, first character lowest) -> 24-bit
+// big-endian code string.
+__device__ __forceinline__ uint32_t codes24(uint32_t le) {
+  uint32_t t = __byte_perm(le, 0, 0x0123);                    // first character on top
+  t = ((t & 0x3F003F00u) >> 2) | (t & 0x003F003Fu);           // 12 bits per half
+  return ((t & 0x0FFF0000u) >> 4) | (t & 0x00000FFFu);        // 24 bits
+}
+
+// 6-bit packing from a chunk whose smem copy already holds codes (text
+// ingest): the word's codes form one big-endian bit string over <= 3 lanes.
+__device__ __forceinline__ void pack6_from_codes(const uint32_t* __restrict__ c32, uint32_t start,
+                                                 uint32_t L, int lanes, uint64_t* __restrict__ dst) {
+  uint64_t v[4];  // 48-bit chunks of 8 characters
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
     v[l] = 0;
@@ -257,10 +275,9 @@ __device__ __forceinline__ void pack6_from_smem(const uint32_t* __restrict__ c32
       const uint32_t w0 = c32[q >> 2], w1 = c32[(q >> 2) + 1], w2 = c32[(q >> 2) + 2];
       const uint32_t sh = (q & 3) * 8;
       const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);
-      v[l] = codes48(((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123));
+      v[l] = ((uint64_t)codes24(lo) << 24) | codes24(hi);
     }
   }
-  // concatenate the 48-bit chunks into the 192-bit string, keep 6L bits
   uint64_t k0 = (v[0] << 16) | (v[1] >> 32);
   uint64_t k1 = (v[1] << 32) | (v[2] >> 16);
   uint64_t k2 = (v[2] << 48) | v[3];
@@ -273,6 +290,40 @@ __device__ __forceinline__ void pack6_from_smem(const uint32_t* __restrict__ c32
   if (lanes > 2) dst[2] = k2;
 }
 
+// Decoupled look-back over chunks, one thread per histogram row: publish the
+// chunk's aggregate, add predecessors' aggregates until an inclusive prefix
+// is found, publish the inclusive prefix. Status word: flag in bits 62-63
+// (1 = aggregate, 2 = inclusive prefix), value in bits 0-31.
+__device__ __forceinline__ uint32_t lookback(unsigned long long* __restrict__ status,
+                                             uint32_t chunk, int row, uint32_t local) {
+  volatile unsigned long long* st = status;
+  const uint64_t me = (uint64_t)chunk * kHistRows + row;
+  if (chunk == 0) {
+    st[me] = (2ull << 62) | local;
+    return 0;
+  }
+  st[me] = (1ull << 62) | local;
+  uint32_t excl = 0;
+  int64_t q = (int64_t)chunk - 1;
+  while (true) {
+    const unsigned long long w = st[(uint64_t)q * kHistRows + row];
+    const uint32_t f = (uint32_t)(w >> 62);
+    if (f == 0) continue;  // predecessor still counting (it is resident: tickets)
+    excl += (uint32_t)w;
+    if (f == 2) break;
+    --q;
+  }
+  st[me] = (2ull << 62) | (excl + local);
+  return excl;
+}
+
+// K3 (two-pass) / single-pass ingest. LOOKBACK = false: chunk offsets come
+// from the scan of K1's histograms and keys land in the compact bucket
+// layout. LOOKBACK = true: CTAs take chunks in ticket order, chain their
+// per-bin offsets through a decoupled look-back and write into
+// capacity-bounded per-length regions (no count pass, no host round trip
+// before the scatter); the last chunk publishes the totals.
+template <bool LOOKBACK>
 __global__ void __launch_bounds__(kIngestThreads)
 scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __restrict__ off,
                uint32_t nchunks, ScatterParams p) {
@@ -283,19 +334,27 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   __shared__ uint32_t wcnt[kWarps][kHistRows];
   __shared__ uint32_t wtot[kWarps];
   __shared__ uint32_t s_chain[kWarps];
+  __shared__ uint32_t s_base[kHistRows];
+  __shared__ uint32_t s_chunk;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint64_t chunk = blockIdx.x;
+  if (LOOKBACK) {
+    if (tid == 0) s_chunk = p.chunk0 + atomicAdd(p.ticket, 1u);
+    __syncthreads();
+  }
+  const uint64_t chunk = LOOKBACK ? s_chunk : p.chunk0 + blockIdx.x;
   const uint64_t cbase = chunk * kChunk;
   for (int i = tid; i < kWarps * kHistRows; i += kIngestThreads) (&wcnt[0][0])[i] = 0;
 
   uint4 v;
-  Segment16 seg = classify_chunk(text, n, cbase, v, s_chain);  // has a __syncthreads
-  reinterpret_cast<uint4*>(chunk32)[tid] = v;
+  Segment16 seg = classify_chunk(text, n, cbase, v, s_chain, p.avail ? p.avail : ~0ull,
+                                 p.overflow);  // has a __syncthreads
+  const bool codes = p.enc == kEncAlnum6;
+  reinterpret_cast<uint4*>(chunk32)[tid] = codes ? alnum6_codes16(v) : v;
   if (tid < 4) {
     uint64_t a = cbase + kChunk + 16 * tid;
-    reinterpret_cast<uint4*>(chunk32)[kChunk / 16 + tid] =
-        a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
+    uint4 la = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(chunk32)[kChunk / 16 + tid] = codes ? alnum6_codes16(la) : la;
   }
   // warp-local word list in corpus order (lane-major, then bit order)
   uint32_t c = __popc(seg.starts);
@@ -331,19 +390,24 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     __syncwarp();
   }
   __syncthreads();
-  // exclusive scan of per-warp counts over warps, plus the chunk's offsets
+  // per-bin: exclusive scan of the warp counts, chunk total, chunk offset
   if (tid < kHistRows) {
-    uint32_t run = (tid == kNumBins) ? off[(uint64_t)kNumBins * nchunks + chunk]
-                                     : off[(uint64_t)tid * nchunks + chunk];
+    uint32_t run = 0;
     for (int w = 0; w < kWarps; ++w) {
-      uint32_t cw = (tid == kNumBins) ? wtot[w] : wcnt[w][tid];
+      const uint32_t cw = (tid == kNumBins) ? wtot[w] : wcnt[w][tid];
       wcnt[w][tid] = run;
       run += cw;
     }
+    uint32_t base;
+    if (LOOKBACK) {
+      base = lookback(p.status, (uint32_t)chunk, tid, run);
+      if (chunk == p.nchunks_total - 1) p.totals[tid] = base + run;
+    } else {
+      base = off[(uint64_t)tid * nchunks + chunk];
+    }
+    s_base[tid] = base;
   }
   __syncthreads();
-  const uint8_t* c8 = reinterpret_cast<const uint8_t*>(chunk32);
-  (void)c8;
   for (uint32_t b = 0; b < total; b += 32) {
     uint32_t j = b + lane;
     if (j >= total) break;
@@ -351,19 +415,19 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     uint32_t L = wlen[wid][j];
     uint32_t bin = bin_of_len(L);
     if (p.tokens) {
-      uint32_t widx = wcnt[wid][kNumBins] + j;
+      uint32_t widx = s_base[kNumBins] + wcnt[wid][kNumBins] + j;
       p.tokens[widx] = make_uint2((uint32_t)(cbase + start), L);
     }
     if (!p.keys) continue;
-    uint32_t pos = wcnt[wid][bin] + wpos[wid][j];
+    uint32_t pos = s_base[bin] + wcnt[wid][bin] + wpos[wid][j];
     if (bin == (uint32_t)kLongBin) {
       p.longlist[pos] = make_uint2((uint32_t)(cbase + start), L);
       continue;
     }
     const int lanes = lanes_for_len_enc(L, p.enc);
     uint64_t* dst = p.keys + p.bin_base[bin] + (uint64_t)pos * lanes;
-    if (p.enc == kEncAlnum6)
-      pack6_from_smem(chunk32, start, L, lanes, dst);
+    if (codes)
+      pack6_from_codes(chunk32, start, L, lanes, dst);
     else
       pack_from_smem(chunk32, start, L, lanes, dst);
   }
@@ -504,8 +568,15 @@ void launch_scan(const uint32_t* hist, uint32_t* off, uint32_t* totals, uint32_t
 
 void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32_t nchunks,
                     const ScatterParams& p, cudaStream_t st) {
-  if (nchunks) scatter_kernel<<<nchunks, kIngestThreads, 0, st>>>(text, n, off, nchunks, p);
+  if (nchunks) scatter_kernel<false><<<nchunks, kIngestThreads, 0, st>>>(text, n, off, nchunks, p);
 }
+
+void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
+                            const ScatterParams& p, cudaStream_t st) {
+  if (nchunks) scatter_kernel<true><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+}
+
+uint32_t ingest_chunk_bytes() { return kChunk; }
 
 uint32_t chunk_count(uint64_t n) { return (uint32_t)((n + kChunk - 1) / kChunk); }
 

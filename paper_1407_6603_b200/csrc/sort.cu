@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
   const SegDesc sd = seg_at(a, find_segment(a, blockIdx.x));
   const uint64_t start = (uint64_t)(blockIdx.x - sd.tile_begin) * T;
   const int cnt = (int)min((uint64_t)T, (uint64_t)sd.n - start);
-  const uint64_t* gin = a.keys_in + (sd.key_off + start) * LANES;
+  const uint64_t* gin = (sd.in_ptr ? sd.in_ptr : a.keys_in + sd.key_off * LANES) + start * LANES;
   const Window16 w = window16(gin, (uint32_t)cnt * 8 * LANES);
   if (tid == 0) {
     mbar_init(&bar, 1);

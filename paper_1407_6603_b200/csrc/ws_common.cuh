@@ -112,6 +112,7 @@ __device__ __forceinline__ uint32_t code6_at(const uint64_t* key) {
 // One sort segment: a bucket (or a long-word group / LSD pass) whose keys
 // are contiguous. Offsets are in elements of the segment's own key width.
 struct SegDesc {
+  const uint64_t* in_ptr;  // tile pass: the segment's unsorted keys (any layout)
   uint64_t key_off;     // element offset of the segment in the key arena (LANES units)
   uint64_t idx_off;     // element offset in the uint32 idx arena
   uint32_t n;           // number of words

@@ -14,6 +14,14 @@ struct ScatterParams {
   uint2* longlist;              // (start, len) of words with L > 32, corpus order
   uint2* tokens;                // optional (start, len) per word in corpus order
   int enc;                      // KeyEnc of the packed keys
+  // single-pass (look-back) mode
+  uint32_t chunk0;              // first chunk of this launch
+  uint32_t nchunks_total;       // chunks of the whole text
+  unsigned int* ticket;         // chunk ticket counter (zeroed before the first launch)
+  unsigned long long* status;   // [nchunks_total][kHistRows] look-back words (zeroed)
+  uint32_t* totals;             // [kHistRows] per-bin totals, written by the last chunk
+  uint64_t avail;               // bytes of text already on the device (0 = all)
+  unsigned int* overflow;       // set when a word runs past `avail`
 };
 
 // ingest.cu
@@ -24,6 +32,9 @@ void launch_scan(const uint32_t* hist, uint32_t* off, uint32_t* totals, uint32_t
                  int rows, cudaStream_t st);
 void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32_t nchunks,
                     const ScatterParams& p, cudaStream_t st);
+void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
+                            const ScatterParams& p, cudaStream_t st);
+uint32_t ingest_chunk_bytes();
 void launch_words_hist(const uint32_t* lens, uint64_t nwords, uint32_t wpw, uint32_t* whist,
                        uint32_t nwarps, cudaStream_t st);
 void launch_words_scatter(const uint8_t* bytes, const uint64_t* starts, const uint32_t* lens,

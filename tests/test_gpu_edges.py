@@ -118,3 +118,21 @@ def test_arbitrary_bytes_rows():
         st = oracle.sort_rows_fast(ref, True)[0]
         stats, _ = _native.sort_blocks([rows], True)
         assert np.array_equal(rows, ref) and tuple(int(x) for x in stats[0]) == st
+
+
+def test_chunked_h2d_long_word_redo():
+    # > 16 MiB host text is copied in pieces overlapped with ingest; a word
+    # longer than a piece forces the non-chunked re-ingest path
+    rng = np.random.default_rng(21)
+    body = b" ".join(synth.random_words(4, 2_000_000, max_len=12))
+    giant = b"Q" * (20 << 20)
+    text = body[: 9 << 20] + b" " + giant + b" " + body[9 << 20:] + b" " + giant + b"R"
+    want, _ = oracle.sort_text(text, mode="fast", max_len=64)
+    assert sort_text(text) == want
+
+
+def test_chunked_h2d_matches_unchunked():
+    text = synth.generate(4, words=4_000_000)
+    assert len(text) > (16 << 20)
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
