@@ -394,8 +394,8 @@ def bench_ours(args) -> None:
             "parity_vs_oracle": parity,
             "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in agg.items()},
         }
-        line["e2e_timeline_ms"] = [[p["name"], round(p["start_ms"], 3), round(p["ms"], 3)]
-                                   for p in e2e_phases]
+        line["e2e_timeline_ms"] = [[p["name"], round(p["start_ms"], 3), round(p["ms"], 3),
+                                    int(p["bytes"])] for p in e2e_phases]
         if args.profile_json:
             Path(args.profile_json).write_text(json.dumps({"phases": agg, "steps": args.steps,
                                                            "dev_ms": dev_ms, "e2e_ms": e2e_ms,

@@ -97,7 +97,8 @@ struct PinBuf {
   }
 };
 
-constexpr int kClasses = 4;  // lane classes 1..4
+constexpr int kClasses = 4;  // lane classes 0..4 (0 = one uint32 key word)
+constexpr int kLongCls = -2;  // emit selector for the L > 32 groups
 // Texts up to this size use the single-pass ingest (capacity-bounded key
 // regions, ~37 bytes per text byte); larger texts the two-pass count + scatter.
 constexpr uint64_t kSinglePassMaxText = 512ull << 20;
@@ -108,7 +109,7 @@ struct Bucket {
   uint32_t len = 0;
   uint64_t count = 0;
   bool is_long = false;
-  int lanes = 0;             // packed: 1..4
+  int lanes = 0;             // packed: 0..4 (lane class, key_bytes(lanes) bytes per key)
   uint64_t elem_off = 0;     // packed: element offset inside the lane class region
   uint64_t idx_off = 0;      // packed: offset in the idx arena (global over buckets)
   uint64_t long_off = 0;     // long: offset in the grouped long-word list
@@ -172,7 +173,7 @@ struct ws_handle {
   int enc = kEncRaw8;       // key encoding of the current packed buckets
   bool text_valid = false;  // h->text holds the last ingested text (reusable, resident)
   bool ingested = false, sorted = false, have_stats = false;
-  uint64_t class_base[kClasses + 1] = {0};  // u64-word base of each lane class region
+  uint64_t class_base[kClasses + 1] = {0};  // byte offset of each lane class region
   uint64_t class_elems[kClasses + 1] = {0};
   uint64_t idx_total = 0;
   std::vector<Bucket> buckets;
@@ -245,6 +246,12 @@ int check_launch(const char* what) {
   return WS_OK;
 }
 
+// Address of element `elem` of lane class `cls` in key buffer `buf` (0/1).
+uint64_t* class_keys(ws_handle* h, int buf, int cls, uint64_t elem) {
+  return reinterpret_cast<uint64_t*>(h->keys[buf].as<uint8_t>() + h->class_base[cls] +
+                                     elem * key_bytes(cls));
+}
+
 // Parameter tables: staged in pinned memory, uploaded with one copy each.
 void params_reset(ws_handle* h) {
   h->param_used = 0;
@@ -260,7 +267,7 @@ int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev,
   if (off + bytes > h->pin_params.cap || off + bytes > h->params.cap) {
     // growing needs every stream of the handle idle (old staging bytes may be in flight)
     WS_CUDA(cudaStreamSynchronize(h->st));
-    for (int c = 1; c <= kClasses; ++c) WS_CUDA(cudaStreamSynchronize(h->cs[c]));
+    for (int c = 0; c <= kClasses; ++c) WS_CUDA(cudaStreamSynchronize(h->cs[c]));
     size_t need = std::max<size_t>(2 * (off + bytes), 1 << 20);
     if (need > h->pin_params.cap) {
       h->pin_params.release();
@@ -315,7 +322,7 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
   const uint32_t TM = (uint32_t)merge_tile_size(lanes);
   uint64_t total_tiles = 0;  // upper bound of the work items of any pass
   for (auto* s : live) total_tiles += 2 * ((s->n + std::min(T, TM) - 1) / std::min(T, TM)) + 4;
-  DevBuf& split_buf = h->splits[st == h->st ? 0 : (lanes & 3) + 1];
+  DevBuf& split_buf = h->splits[st == h->st ? 0 : lanes + 1];
   WS_CUDA(split_buf.ensure((2 * total_tiles + 4) * 4));  // (split, segment) per work item
   uint64_t* kb[2] = {keys0, keys1};
   uint32_t* ib[2] = {idx0, idx1};
@@ -346,7 +353,7 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
         const uint64_t pairs = (s->n + 2 * run - 1) / (2 * run);
         work += (uint32_t)(pairs * ((2 * run + TM - 1) / TM));
       }
-      bytes += 2.0 * s->n * lanes * 8 + (stats ? (p == 0 ? 4.0 : 8.0) * s->n : 0.0);
+      bytes += 2.0 * s->n * key_bytes(lanes) + (stats ? (p == 0 ? 4.0 : 8.0) * s->n : 0.0);
       s->final_buf = (p + 1) & 1;
     }
     if (d.empty()) break;
@@ -419,19 +426,17 @@ int plan_packed(ws_handle* h, const uint64_t* counts) {
     idx_run += counts[b];
     h->buckets.push_back(bk);
   }
-  uint64_t run = 0;
-  for (int c = 1; c <= kClasses; ++c) {
+  uint64_t run = 0;  // bytes
+  for (int c = 0; c <= kClasses; ++c) {
     h->class_base[c] = run;
     h->class_elems[c] = elems[c];
-    run += elems[c] * c;
-    run = (run + 1) & ~1ull;  // 16-byte aligned class regions
+    run += elems[c] * key_bytes(c);
+    run = (run + 15) & ~15ull;  // 16-byte aligned class regions
   }
   h->idx_total = idx_run;
-  const size_t key_bytes = run * 8 + 64;
-  WS_CUDA(h->keys[0].ensure(key_bytes));
-  WS_CUDA(h->keys[1].ensure(key_bytes));
-  for (auto& bk : h->buckets)
-    bk.in_ptr = h->keys[0].as<uint64_t>() + h->class_base[bk.lanes] + bk.elem_off * bk.lanes;
+  WS_CUDA(h->keys[0].ensure(run + 64));
+  WS_CUDA(h->keys[1].ensure(run + 64));
+  for (auto& bk : h->buckets) bk.in_ptr = class_keys(h, 0, bk.lanes, bk.elem_off);
   return WS_OK;
 }
 
@@ -439,7 +444,7 @@ void fill_scatter_params(ws_handle* h, ScatterParams& p) {
   memset(&p, 0, sizeof p);
   for (const auto& bk : h->buckets) {
     if (bk.is_long) continue;
-    p.bin_base[bk.len - 1] = h->class_base[bk.lanes] + bk.elem_off * bk.lanes;
+    p.bin_base[bk.len - 1] = h->class_base[bk.lanes] + bk.elem_off * key_bytes(bk.lanes);
   }
   p.keys = h->keys[0].as<uint64_t>();
   p.longlist = h->longlist.as<uint2>();
@@ -552,13 +557,13 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     for (int b = 0; b < kMaxPackedLen; ++b) {
       const int L = b + 1;
       region[b] = run;
-      run += (n + 1) / (L + 1) * lanes_for_len_enc(L, h->enc);
-      run = (run + 11) / 12 * 12;
+      run += (n + 1) / (L + 1) * key_bytes(lanes_for_len_enc(L, h->enc));
+      run = (run + 95) / 96 * 96;  // 16-byte aligned, a multiple of every key size
     }
-    WS_CUDA(h->keys_cap.ensure(run * 8 + 256));
+    WS_CUDA(h->keys_cap.ensure(run + 256));
     WS_CUDA(h->longlist.ensure(((n + 1) / (kMaxPackedLen + 2) + 1) * sizeof(uint2)));
     if (keep_tokens) WS_CUDA(h->tokens.ensure(((n + 1) / 2 + 1) * sizeof(uint2)));
-    WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kHistRows * 8));
+    WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kLookbackRec * 4));
     WS_CUDA(h->ticket.ensure(256));
     for (int b = 0; b < kMaxPackedLen; ++b) p.bin_base[b] = region[b];
     p.keys = h->keys_cap.as<uint64_t>();
@@ -567,10 +572,10 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     p.chunk0 = 0;
     p.nchunks_total = nchunks;
     p.ticket = h->ticket.as<unsigned int>();
-    p.status = h->status.as<unsigned long long>();
+    p.status = h->status.as<uint32_t>();
     p.totals = h->totals.as<uint32_t>();
     if (nchunks) {
-      WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kHistRows * 8, h->st));
+      WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
       WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
       bool redo = false;
       if (chunked) {
@@ -612,7 +617,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         redo = tot_host[kHistRows] != 0;  // a word spanned a whole piece: ingest again
         if (redo) {
           p.overflow = nullptr;
-          WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kHistRows * 8, h->st));
+          WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
           WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
         }
       }
@@ -636,7 +641,8 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     m = counts[kLongBin];
     WS_TRY(plan_packed(h, counts));  // compact layout of the sort buffers
     for (auto& bk : h->buckets)
-      if (!bk.is_long) bk.in_ptr = h->keys_cap.as<uint64_t>() + region[bk.len - 1];
+      if (!bk.is_long)
+        bk.in_ptr = reinterpret_cast<const uint64_t*>(h->keys_cap.as<uint8_t>() + region[bk.len - 1]);
     if (keep_tokens) h->have_tokens = true;
   } else {
     const size_t hist_bytes = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
@@ -674,7 +680,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     }
     if (nchunks) {
       double kbytes = 0;
-      for (auto& b : h->buckets) kbytes += (double)b.count * b.lanes * 8;
+      for (auto& b : h->buckets) kbytes += (double)b.count * key_bytes(b.lanes);
       Phase ph(h, "scatter", (double)n + kbytes + 8.0 * m);
       launch_scatter(dtext, n, h->off.as<uint32_t>(), nchunks, p, h->st);
       ++h->launches;
@@ -708,7 +714,7 @@ int fused_class_copy(ws_handle* h, FusedEmit* fe, int cls, cudaStream_t st) {
   uint64_t lo = UINT64_MAX, hi = 0, sum = 0;
   for (size_t i = 0; i < h->buckets.size(); ++i) {
     const Bucket& b = h->buckets[i];
-    if ((b.is_long ? 0 : b.lanes) != cls || !b.count) continue;
+    if ((b.is_long ? kLongCls : b.lanes) != cls || !b.count) continue;
     lo = std::min(lo, fe->off[i]);
     hi = std::max(hi, fe->off[i + 1]);
     sum += fe->off[i + 1] - fe->off[i];
@@ -740,7 +746,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   // packed buckets: one schedule per lane class, each class on its own stream
   // (the classes are independent; small classes fill the big one's bubbles)
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
-  for (int c = kClasses; c >= 1; --c) {  // small (multi-lane) classes are submitted first
+  for (int c = kClasses; c >= 0; --c) {  // small (multi-lane) classes are submitted first
     std::vector<SegIn> segs;
     std::vector<int> which;
     for (int i = 0; i < nb; ++i) {
@@ -755,8 +761,8 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     cudaStream_t est = h->serial ? h->st : h->es[c];
     cudaStream_t dst = h->serial ? h->st : h->ds[c];
     WS_CUDA(cudaStreamWaitEvent(cst, h->ev_fork, 0));
-    uint64_t* k0 = h->keys[0].as<uint64_t>() + h->class_base[c];
-    uint64_t* k1 = h->keys[1].as<uint64_t>() + h->class_base[c];
+    uint64_t* k0 = class_keys(h, 0, c, 0);
+    uint64_t* k1 = class_keys(h, 1, c, 0);
     // Fused emission: a bucket is emitted (and copied to the host) right after
     // the pass that completes it, on side streams, while later passes run.
     PassDoneHook hook = [&, est, dst](const std::vector<const SegIn*>& done,
@@ -863,7 +869,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
                            h->stat_k_dummy.as<long long>(), "linv_"));
     }
   }
-  if (fe && h->n_long) WS_TRY(fused_class_copy(h, fe, 0, h->st));
+  if (fe && h->n_long) WS_TRY(fused_class_copy(h, fe, kLongCls, h->st));
   if (stats && nb) {
     std::vector<int64_t> hinv(nb), hk(nb);
     WS_CUDA(cudaMemcpyAsync(hinv.data(), h->stat_inv.p, nb * 8, cudaMemcpyDeviceToHost, h->st));
@@ -886,7 +892,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
 const uint64_t* bucket_keys(ws_handle* h, const Bucket& b, bool sorted) {
   if (!sorted && b.in_ptr) return b.in_ptr;
   const int buf = sorted ? b.final_buf : 0;
-  return h->keys[buf].as<uint64_t>() + h->class_base[b.lanes] + b.elem_off * b.lanes;
+  return class_keys(h, buf, b.lanes, b.elem_off);
 }
 
 // Enqueue emission of all buckets into device buffer `dout` (lines or rows).
@@ -915,17 +921,17 @@ int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* 
   double kb = 0, ob = 0;
   for (size_t i = 0; i < h->buckets.size(); ++i) {
     const Bucket& b = h->buckets[i];
-    const int cls = b.is_long ? 0 : b.lanes;
-    if ((only >= 0 && cls != only) || !pick[i]) continue;
-    kb += b.is_long ? 0.0 : (double)b.count * b.lanes * 8;
+    const int cls = b.is_long ? kLongCls : b.lanes;
+    if ((only != -1 && cls != only) || !pick[i]) continue;
+    kb += b.is_long ? 0.0 : (double)b.count * key_bytes(b.lanes);
     ob += (double)(off[i + 1] - off[i]);
   }
   char name[32];
   snprintf(name, sizeof name, "%s%s", lines ? "emit_lines" : "emit_rows",
-           only < 0 ? "" : (only == 0 ? "_long" : (only == 1 ? "_l1" : only == 2 ? "_l2" : only == 3 ? "_l3" : "_l4")));
+           only == -1 ? "" : (only == kLongCls ? "_long" : (only == 0 ? "_l0" : only == 1 ? "_l1" : only == 2 ? "_l2" : only == 3 ? "_l3" : "_l4")));
   Phase ph(h, name, kb + ob, 0, st);
-  for (int c = 1; c <= kClasses; ++c) {
-    if (only >= 0 && only != c) continue;
+  for (int c = 0; c <= kClasses; ++c) {
+    if (only != -1 && only != c) continue;
     std::vector<EmitSeg> segs;
     uint32_t blocks = 0;
     for (size_t i = 0; i < h->buckets.size(); ++i) {
@@ -953,7 +959,7 @@ int emit_device(ws_handle* h, uint8_t* dout, bool lines, std::vector<uint64_t>* 
     launch_emit(c, h->enc, t, blocks, dout, nl, st);
     ++h->launches;
   }
-  if (only <= 0) {
+  if (only == -1 || only == kLongCls) {
     for (size_t i = 0; i < h->buckets.size(); ++i) {
       const Bucket& b = h->buckets[i];
       if (!b.is_long || !b.count || !pick[i]) continue;
@@ -1046,7 +1052,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
     bk.len = (uint32_t)widths[i];
     bk.count = (uint64_t)counts[i];
     if (widths[i] <= kMaxPackedLen) {
-      bk.lanes = lanes_for_len(widths[i]);
+      bk.lanes = lanes_for_len_enc(widths[i], kEncRaw8);
       bk.elem_off = elems[bk.lanes];
       elems[bk.lanes] += bk.count;
       bk.idx_off = idx_run;
@@ -1059,16 +1065,16 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
     h->buckets.push_back(bk);
     bob.push_back(i);
   }
-  uint64_t run = 0;
-  for (int c = 1; c <= kClasses; ++c) {
+  uint64_t run = 0;  // bytes
+  for (int c = 0; c <= kClasses; ++c) {
     h->class_base[c] = run;
     h->class_elems[c] = elems[c];
-    run += elems[c] * c;
-    run = (run + 1) & ~1ull;
+    run += elems[c] * key_bytes(c);
+    run = (run + 15) & ~15ull;
   }
   h->idx_total = idx_run;
-  WS_CUDA(h->keys[0].ensure(run * 8 + 64));
-  WS_CUDA(h->keys[1].ensure(run * 8 + 64));
+  WS_CUDA(h->keys[0].ensure(run + 64));
+  WS_CUDA(h->keys[1].ensure(run + 64));
   h->n_long = long_run;
   if (long_run) {
     WS_CUDA(h->longgrp.ensure(long_run * sizeof(uint2)));
@@ -1082,8 +1088,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
     const int i = bob[k];
     if (!b.is_long) {
       launch_pack_rows(h->text.as<uint8_t>() + boff[i], b.count, b.len,
-                       h->keys[0].as<uint64_t>() + h->class_base[b.lanes] + b.elem_off * b.lanes,
-                       h->st);
+                       class_keys(h, 0, b.lanes, b.elem_off), h->st);
     } else {
       launch_rows_longlist(boff[i], b.count, b.len, h->longgrp.as<uint2>() + b.long_off, h->st);
     }
@@ -1218,16 +1223,17 @@ int ws_create(ws_handle** out, int32_t device) {
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
-  for (int c = 1; c <= kClasses && e == cudaSuccess; ++c)
-    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, c == 1 ? prio_lo : prio_hi);
+  // the one-word classes (0, 1) hold most keys and sort last
+  for (int c = 0; c <= kClasses && e == cudaSuccess; ++c)
+    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, c <= 1 ? prio_lo : prio_hi);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->hs, cudaStreamNonBlocking, prio_hi);
-  for (int c = 1; c <= kClasses && e == cudaSuccess; ++c) {
+  for (int c = 0; c <= kClasses && e == cudaSuccess; ++c) {
     e = cudaStreamCreateWithPriority(&h->es[c], cudaStreamNonBlocking, prio_hi);
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&h->ds[c], cudaStreamNonBlocking, prio_hi);
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
-  for (int c = 1; c <= kClasses && e == cudaSuccess; ++c)
+  for (int c = 0; c <= kClasses && e == cudaSuccess; ++c)
     e = cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming);
   if (e != cudaSuccess) {
     ws_destroy(h);
@@ -1241,7 +1247,7 @@ void ws_destroy(ws_handle* h) {
   if (!h) return;
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
-  for (int c = 1; c <= kClasses; ++c) {
+  for (int c = 0; c <= kClasses; ++c) {
     if (h->cs[c]) cudaStreamSynchronize(h->cs[c]);
     if (h->es[c]) cudaStreamSynchronize(h->es[c]);
     if (h->ds[c]) cudaStreamSynchronize(h->ds[c]);
@@ -1262,7 +1268,7 @@ void ws_destroy(ws_handle* h) {
   }
   for (auto e : h->event_pool) cudaEventDestroy(e);
   for (auto e : h->sync_events) cudaEventDestroy(e);
-  for (int c = 1; c <= kClasses; ++c) {
+  for (int c = 0; c <= kClasses; ++c) {
     if (h->es[c]) cudaStreamDestroy(h->es[c]);
     if (h->ds[c]) cudaStreamDestroy(h->ds[c]);
     if (h->cs[c]) cudaStreamDestroy(h->cs[c]);

@@ -74,17 +74,21 @@ emit_kernel(const __grid_constant__ EmitTable t, uint8_t* __restrict__ out, int 
   const int stride = L + nl;
   const uint64_t o0 = sg.out_off + w0 * stride;
   const int mis = (int)(o0 & 15);
-  const uint64_t* keys = sg.keys + w0 * LANES;
+  constexpr int NL = LANES < 1 ? 1 : LANES;  // lanes of the unpacked key
   for (int j = threadIdx.x; j < cnt; j += kEmitThreads) {
-    uint64_t k[LANES];
-#pragma unroll
-    for (int l = 0; l < LANES; ++l) k[l] = __ldg(keys + (uint64_t)j * LANES + l);
-    uint8_t* dst = buf + mis + j * stride;
-    if constexpr (ENC == kEncAlnum6) {
-      unpack6<LANES>(k, L, dst);
+    uint64_t k[NL];
+    if constexpr (LANES == 0) {  // one uint32 word: the top half of a lane
+      k[0] = (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(sg.keys) + w0 + j) << 32;
     } else {
 #pragma unroll
-      for (int l = 0; l < LANES; ++l) {
+      for (int l = 0; l < LANES; ++l) k[l] = __ldg(sg.keys + (w0 + j) * LANES + l);
+    }
+    uint8_t* dst = buf + mis + j * stride;
+    if constexpr (ENC == kEncAlnum6) {
+      unpack6<NL>(k, L, dst);
+    } else {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           int b = 8 * l + q;
@@ -103,6 +107,7 @@ void launch_emit(int lanes, int enc, const EmitTable& t, uint32_t blocks, uint8_
   if (!blocks) return;
   if (enc == kEncAlnum6) {
     switch (lanes) {
+      case 0: emit_kernel<0, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
       case 1: emit_kernel<1, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
       case 2: emit_kernel<2, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
       default: emit_kernel<3, kEncAlnum6><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
@@ -110,6 +115,7 @@ void launch_emit(int lanes, int enc, const EmitTable& t, uint32_t blocks, uint8_
     return;
   }
   switch (lanes) {
+    case 0: emit_kernel<0, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
     case 1: emit_kernel<1, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
     case 2: emit_kernel<2, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;
     case 3: emit_kernel<3, kEncRaw8><<<blocks, kEmitThreads, 0, st>>>(t, out, with_newline); break;

@@ -25,6 +25,9 @@ constexpr int kChunk = 4096;
 constexpr int kIngestThreads = 256;  // 16 bytes per thread
 constexpr int kWarps = kIngestThreads / 32;
 constexpr int kMaxWordsPerWarp = 256;  // 512 bytes per warp, <= 1 start per 2 bytes
+// Packed keys of one chunk: at most 2 key bytes per text byte (1-byte words,
+// 4-byte keys, every other byte) plus one 32-byte key running in at the end.
+constexpr int kStageBytes = 2 * kChunk + 64 + 8 * kMaxPackedLen;  // + alignment gaps
 
 __device__ __forceinline__ uint32_t bin_of_len(uint32_t len) {
   return len <= (uint32_t)kMaxPackedLen ? len - 1 : (uint32_t)kLongBin;
@@ -222,9 +225,10 @@ scan_kernel(const uint32_t* __restrict__ hist, uint32_t* __restrict__ off,
 // a warp holding words of several lengths does not diverge)
 __device__ __forceinline__ void pack_from_smem(const uint32_t* __restrict__ c32, uint32_t start,
                                                uint32_t L, int lanes, uint64_t* __restrict__ dst) {
+  const int nl = lanes < 1 ? 1 : lanes;
 #pragma unroll
   for (int l = 0; l < 4; ++l) {
-    if (l >= lanes) break;
+    if (l >= nl) break;
     uint32_t q = start + 8 * l;
     uint32_t w0 = c32[q >> 2], w1 = c32[(q >> 2) + 1], w2 = c32[(q >> 2) + 2];
     uint32_t sh = (q & 3) * 8;
@@ -286,35 +290,89 @@ __device__ __forceinline__ void pack6_from_codes(const uint32_t* __restrict__ c3
   k1 &= bits >= 128 ? ~0ull : (bits <= 64 ? 0ull : ~0ull << (128 - bits));
   k2 &= bits >= 192 ? ~0ull : (bits <= 128 ? 0ull : ~0ull << (192 - bits));
   dst[0] = k0;
-  if (lanes > 1) dst[1] = k1;
-  if (lanes > 2) dst[2] = k2;
+  dst[1] = k1;
+  dst[2] = k2;
 }
 
-// Decoupled look-back over chunks, one thread per histogram row: publish the
-// chunk's aggregate, add predecessors' aggregates until an inclusive prefix
-// is found, publish the inclusive prefix. Status word: flag in bits 62-63
-// (1 = aggregate, 2 = inclusive prefix), value in bits 0-31.
-__device__ __forceinline__ uint32_t lookback(unsigned long long* __restrict__ status,
-                                             uint32_t chunk, int row, uint32_t local) {
-  volatile unsigned long long* st = status;
-  const uint64_t me = (uint64_t)chunk * kHistRows + row;
-  if (chunk == 0) {
-    st[me] = (2ull << 62) | local;
-    return 0;
+// Key store: lane class 0 keeps the top 32 bits of the first lane (6-bit keys
+// of <= 5 characters and raw keys of <= 4 bytes fit), else `lanes` uint64s.
+__device__ __forceinline__ void store_key(uint8_t* dst, int lanes, const uint64_t (&k)[4]) {
+  if (lanes == 0) {
+    *reinterpret_cast<uint32_t*>(dst) = (uint32_t)(k[0] >> 32);
+    return;
   }
-  st[me] = (1ull << 62) | local;
-  uint32_t excl = 0;
+  uint64_t* d = reinterpret_cast<uint64_t*>(dst);
+  d[0] = k[0];
+  if (lanes > 1) d[1] = k[1];
+  if (lanes > 2) d[2] = k[2];
+  if (lanes > 3) d[3] = k[3];
+}
+
+// Decoupled look-back over chunks (record layout: ws_common.cuh kLookbackRec).
+// Values are written before the flag, every writer lane fences, and readers
+// fence after observing the flag.
+static_assert(kRecAgg + kHistRows <= kRecIncl && kRecIncl + kHistRows <= kLookbackRec, "record");
+
+// Warp 0: publish this chunk's per-row values at `where` (kRecAgg / kRecIncl)
+// and raise the flag to `flag` (1 = aggregate, 2 = inclusive prefix).
+__device__ __forceinline__ void publish_record(uint32_t* __restrict__ status, uint32_t chunk,
+                                               const uint32_t* __restrict__ vals, int where,
+                                               uint32_t flag) {
+  const int lane = threadIdx.x & 31;
+  volatile uint32_t* rec = status + (uint64_t)chunk * kLookbackRec;
+  for (int r = lane; r < kHistRows; r += 32) rec[where + r] = vals[r];
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) rec[0] = flag;
+  __syncwarp();
+}
+
+// Warp 0: exclusive prefix of every row over chunks < chunk. Each step reads
+// the flags of 32 predecessors (lane l <-> chunk q - l), waits until all are
+// published, finds the nearest inclusive record (ballot), and every lane up to
+// it fetches its record's rows with independent 16-byte loads (one memory
+// round trip per window); rows are then summed across lanes with redux.sync.
+__device__ __forceinline__ void resolve_prefix_warp(uint32_t* __restrict__ status, uint32_t chunk,
+                                                    uint32_t* __restrict__ excl_out) {
+  constexpr int kVec = (kHistRows + 3) / 4;
+  const int lane = threadIdx.x & 31;
+  volatile uint32_t* st = status;
+  uint32_t acc0 = 0, acc1 = 0;  // rows lane and lane + 32
   int64_t q = (int64_t)chunk - 1;
-  while (true) {
-    const unsigned long long w = st[(uint64_t)q * kHistRows + row];
-    const uint32_t f = (uint32_t)(w >> 62);
-    if (f == 0) continue;  // predecessor still counting (it is resident: tickets)
-    excl += (uint32_t)w;
-    if (f == 2) break;
-    --q;
+  while (q >= 0) {
+    const int64_t mine = q - lane;
+    uint32_t f = 2;  // "before chunk 0" behaves like an inclusive zero
+    if (mine >= 0) {
+      do {
+        f = st[(uint64_t)mine * kLookbackRec];
+      } while (f == 0);
+    }
+    __threadfence();
+    const uint32_t incl = __ballot_sync(0xffffffffu, f == 2);
+    const int stop = incl ? __ffs(incl) - 1 : 31;  // last lane (record) of the window
+    uint4 v[kVec];
+#pragma unroll
+    for (int i = 0; i < kVec; ++i) v[i] = make_uint4(0, 0, 0, 0);
+    if (lane <= stop && mine >= 0) {
+      const int where = (lane == stop && incl) ? kRecIncl : kRecAgg;
+      const uint4* rec = reinterpret_cast<const uint4*>(status + (uint64_t)mine * kLookbackRec + where);
+#pragma unroll
+      for (int i = 0; i < kVec; ++i) v[i] = __ldcg(rec + i);
+    }
+#pragma unroll
+    for (int r = 0; r < kHistRows; ++r) {
+      const uint4 w = v[r >> 2];
+      const uint32_t x = (r & 3) == 0 ? w.x : (r & 3) == 1 ? w.y : (r & 3) == 2 ? w.z : w.w;
+      const uint32_t sum = __reduce_add_sync(0xffffffffu, x);
+      if (lane == (r & 31)) {
+        if (r < 32) acc0 += sum; else acc1 += sum;
+      }
+    }
+    if (incl) break;
+    q -= 32;
   }
-  st[me] = (2ull << 62) | (excl + local);
-  return excl;
+  excl_out[lane] = acc0;
+  if (lane + 32 < kHistRows) excl_out[lane + 32] = acc1;
 }
 
 // K3 (two-pass) / single-pass ingest. LOOKBACK = false: chunk offsets come
@@ -335,6 +393,11 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   __shared__ uint32_t wtot[kWarps];
   __shared__ uint32_t s_chain[kWarps];
   __shared__ uint32_t s_base[kHistRows];
+  __shared__ uint32_t s_run[kHistRows];
+  __shared__ uint32_t s_incl[kHistRows];
+  __shared__ uint32_t s_soff[kMaxPackedLen + 1];
+  __shared__ uint32_t s_send[kMaxPackedLen];
+  __shared__ __align__(16) uint8_t stage[kStageBytes];  // keys of the chunk, grouped by bin
   __shared__ uint32_t s_chunk;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -390,7 +453,8 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     __syncwarp();
   }
   __syncthreads();
-  // per-bin: exclusive scan of the warp counts, chunk total, chunk offset
+  // per-bin: exclusive scan of the warp counts and the chunk total; publish
+  // the chunk's aggregates right away (successors can start resolving)
   if (tid < kHistRows) {
     uint32_t run = 0;
     for (int w = 0; w < kWarps; ++w) {
@@ -398,38 +462,88 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
       wcnt[w][tid] = run;
       run += cw;
     }
-    uint32_t base;
-    if (LOOKBACK) {
-      base = lookback(p.status, (uint32_t)chunk, tid, run);
-      if (chunk == p.nchunks_total - 1) p.totals[tid] = base + run;
-    } else {
-      base = off[(uint64_t)tid * nchunks + chunk];
-    }
-    s_base[tid] = base;
+    s_run[tid] = run;
   }
   __syncthreads();
+  if (LOOKBACK && wid == 0) publish_record(p.status, (uint32_t)chunk, s_run, chunk == 0 ? kRecIncl : kRecAgg,
+                   chunk == 0 ? 2u : 1u);
+  // staging layout: bins back to back in bin order, key_bytes(lanes(bin)) each
+  if (tid == 32) {  // 8-byte aligned bins (uint64 key stores); gaps are skipped below
+    uint32_t o = 0;
+    for (int b = 0; b < kMaxPackedLen; ++b) {
+      o = (o + 7) & ~7u;
+      s_soff[b] = o;
+      o += s_run[b] * (uint32_t)key_bytes(lanes_for_len_enc(b + 1, p.enc));
+      s_send[b] = o;
+    }
+    s_soff[kMaxPackedLen] = o;
+  }
+  __syncthreads();
+  // chunk offsets: warp 0 resolves the decoupled look-back right away (an
+  // early inclusive prefix keeps successors' look-back windows short) while
+  // the other warps already pack their keys
+  if (LOOKBACK && wid == 0) {
+    resolve_prefix_warp(p.status, (uint32_t)chunk, s_base);
+    __syncwarp();
+    if (chunk > 0) {
+      for (int r = lane; r < kHistRows; r += 32) s_incl[r] = s_base[r] + s_run[r];
+      __syncwarp();
+      publish_record(p.status, (uint32_t)chunk, s_incl, kRecIncl, 2u);
+    }
+    if (chunk == p.nchunks_total - 1)
+      for (int r = lane; r < kHistRows; r += 32) p.totals[r] = s_base[r] + s_run[r];
+  }
+  // pack every key into the staging area (no dependence on other chunks)
+  if (p.keys) {
+    for (uint32_t b = 0; b < total; b += 32) {
+      const uint32_t j = b + lane;
+      if (j >= total) break;
+      const uint32_t L = wlen[wid][j];
+      const uint32_t bin = bin_of_len(L);
+      if (bin == (uint32_t)kLongBin) continue;
+      const uint32_t start = wstart[wid][j];
+      const int lanes = lanes_for_len_enc(L, p.enc);
+      const uint32_t lpos = wcnt[wid][bin] + wpos[wid][j];
+      uint64_t k[4];
+      if (codes)
+        pack6_from_codes(chunk32, start, L, lanes, k);
+      else
+        pack_from_smem(chunk32, start, L, lanes, k);
+      store_key(stage + s_soff[bin] + lpos * (uint32_t)key_bytes(lanes), lanes, k);
+    }
+  }
+  if (!LOOKBACK && tid < kHistRows) s_base[tid] = off[(uint64_t)tid * nchunks + chunk];
+  __syncthreads();
+  // stream each bin's run out: consecutive threads write consecutive words
+  if (p.keys) {
+    const uint32_t words4 = s_soff[kMaxPackedLen] >> 2;
+    for (uint32_t i = tid; i < words4; i += kIngestThreads) {
+      const uint32_t byte = i << 2;
+      int lo = 0, hi = kMaxPackedLen - 1;  // bin holding this staging byte
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_soff[mid] <= byte) lo = mid; else hi = mid - 1;
+      }
+      if (byte >= s_send[lo]) continue;  // alignment gap
+      const uint32_t ks = (uint32_t)key_bytes(lanes_for_len_enc(lo + 1, p.enc));
+      uint8_t* dst = reinterpret_cast<uint8_t*>(p.keys) + p.bin_base[lo] +
+                     (uint64_t)s_base[lo] * ks + (byte - s_soff[lo]);
+      *reinterpret_cast<uint32_t*>(dst) = reinterpret_cast<const uint32_t*>(stage)[i];
+    }
+  }
+  // long words and corpus-order tokens go straight out
   for (uint32_t b = 0; b < total; b += 32) {
-    uint32_t j = b + lane;
+    const uint32_t j = b + lane;
     if (j >= total) break;
-    uint32_t start = wstart[wid][j];
-    uint32_t L = wlen[wid][j];
-    uint32_t bin = bin_of_len(L);
+    const uint32_t L = wlen[wid][j];
+    const uint32_t start = wstart[wid][j];
     if (p.tokens) {
-      uint32_t widx = s_base[kNumBins] + wcnt[wid][kNumBins] + j;
+      const uint32_t widx = s_base[kNumBins] + wcnt[wid][kNumBins] + j;
       p.tokens[widx] = make_uint2((uint32_t)(cbase + start), L);
     }
-    if (!p.keys) continue;
-    uint32_t pos = s_base[bin] + wcnt[wid][bin] + wpos[wid][j];
-    if (bin == (uint32_t)kLongBin) {
-      p.longlist[pos] = make_uint2((uint32_t)(cbase + start), L);
-      continue;
-    }
-    const int lanes = lanes_for_len_enc(L, p.enc);
-    uint64_t* dst = p.keys + p.bin_base[bin] + (uint64_t)pos * lanes;
-    if (codes)
-      pack6_from_codes(chunk32, start, L, lanes, dst);
-    else
-      pack_from_smem(chunk32, start, L, lanes, dst);
+    if (p.keys && bin_of_len(L) == (uint32_t)kLongBin)
+      p.longlist[s_base[kLongBin] + wcnt[wid][kLongBin] + wpos[wid][j]] =
+          make_uint2((uint32_t)(cbase + start), L);
   }
 }
 
@@ -520,36 +634,36 @@ __global__ void words_scatter_kernel(const uint8_t* __restrict__ bytes,
       p.longlist[pos] = make_uint2((uint32_t)st, L);
       continue;
     }
-    int lanes = lanes_for_len(L);
-    uint64_t* dst = p.keys + p.bin_base[key] + (uint64_t)pos * lanes;
-    for (int l = 0; l < lanes; ++l) {
-      uint64_t k = 0;
+    const int lanes = lanes_for_len_enc(L, kEncRaw8);
+    uint64_t k[4] = {0, 0, 0, 0};
+    for (int l = 0; l < (lanes < 1 ? 1 : lanes); ++l) {
       for (int q = 0; q < 8; ++q) {
         uint32_t bi = 8 * l + q;
         uint64_t byte = bi < L ? bytes[st + bi] : 0;
-        k |= byte << (56 - 8 * q);
+        k[l] |= byte << (56 - 8 * q);
       }
-      dst[l] = k;
     }
+    store_key(reinterpret_cast<uint8_t*>(p.keys) + p.bin_base[key] + (uint64_t)pos * key_bytes(lanes),
+              lanes, k);
   }
 }
 
 // Rows (n x width) -> packed keys of one segment.
 __global__ void pack_rows_kernel(const uint8_t* __restrict__ rows, uint64_t n, uint32_t width,
                                  uint64_t* __restrict__ keys) {
-  const int lanes = lanes_for_len(width);
+  const int lanes = lanes_for_len_enc(width, kEncRaw8);
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const uint8_t* r = rows + i * width;
-    for (int l = 0; l < lanes; ++l) {
-      uint64_t k = 0;
+    uint64_t k[4] = {0, 0, 0, 0};
+    for (int l = 0; l < (lanes < 1 ? 1 : lanes); ++l) {
       for (int q = 0; q < 8; ++q) {
         uint32_t bi = 8 * l + q;
         uint64_t byte = bi < width ? r[bi] : 0;
-        k |= byte << (56 - 8 * q);
+        k[l] |= byte << (56 - 8 * q);
       }
-      keys[i * lanes + l] = k;
     }
+    store_key(reinterpret_cast<uint8_t*>(keys) + i * key_bytes(lanes), lanes, k);
   }
 }
 

@@ -63,7 +63,7 @@ constexpr int kMergeThreads = WS_MERGE_NT;
 template <int LANES>
 struct TileCfg {
   static constexpr int NT = kTileThreads;
-  static constexpr int E = LANES == 1 ? WS_TILE_E1 : WS_TILE_EN;
+  static constexpr int E = LANES <= 1 ? WS_TILE_E1 : WS_TILE_EN;
   static constexpr int T = NT * E;
 };
 
@@ -72,14 +72,14 @@ struct MergeCfg {
   static constexpr int NT = kMergeThreads;
   static constexpr int E = WS_MERGE_E;
   static constexpr int T = NT * E;
-  static constexpr int MIN_BLOCKS = LANES == 1 ? 2048 / NT : (LANES == 2 ? 1024 / NT : 512 / NT);
+  static constexpr int MIN_BLOCKS = LANES <= 1 ? 2048 / NT : (LANES == 2 ? 1024 / NT : 512 / NT);
 };
 
 // smem bytes: keys (AoS, 16-byte slack on each side for the bulk-copy
 // rounding) followed by the idx payload in stats mode.
 template <int LANES, int T, bool STATS>
 __host__ __device__ constexpr size_t keys_smem_bytes() {
-  return (size_t)T * 8 * LANES + 64;
+  return (size_t)T * key_bytes(LANES) + 64;
 }
 template <int LANES, int T, bool STATS>
 __host__ __device__ constexpr size_t pass_smem_bytes() {
@@ -87,25 +87,41 @@ __host__ __device__ constexpr size_t pass_smem_bytes() {
 }
 
 template <int LANES>
-__device__ __forceinline__ Key<LANES> ldk(const uint64_t* __restrict__ p, int i) {
+using KW = typename KeyTraits<LANES>::W;
+
+template <int LANES>
+__device__ __forceinline__ Key<LANES> ldk(const KW<LANES>* __restrict__ p, int i) {
+  constexpr int NW = KeyTraits<LANES>::NW;
   Key<LANES> k;
 #pragma unroll
-  for (int l = 0; l < LANES; ++l) k.w[l] = p[i * LANES + l];
+  for (int l = 0; l < NW; ++l) k.w[l] = p[i * NW + l];
   return k;
 }
 
 template <int LANES>
-__device__ __forceinline__ void stk(uint64_t* __restrict__ p, int i, const Key<LANES>& k) {
+__device__ __forceinline__ void stk(KW<LANES>* __restrict__ p, int i, const Key<LANES>& k) {
+  constexpr int NW = KeyTraits<LANES>::NW;
 #pragma unroll
-  for (int l = 0; l < LANES; ++l) p[i * LANES + l] = k.w[l];
+  for (int l = 0; l < NW; ++l) p[i * NW + l] = k.w[l];
 }
 
 template <int LANES>
-__device__ __forceinline__ Key<LANES> gld(const uint64_t* __restrict__ g, int64_t i) {
+__device__ __forceinline__ Key<LANES> gld(const KW<LANES>* __restrict__ g, int64_t i) {
+  constexpr int NW = KeyTraits<LANES>::NW;
   Key<LANES> k;
 #pragma unroll
-  for (int l = 0; l < LANES; ++l) k.w[l] = __ldg(g + i * LANES + l);
+  for (int l = 0; l < NW; ++l) k.w[l] = __ldg(g + i * NW + l);
   return k;
+}
+
+// Key arrays are passed around as uint64_t*; kernels view them in words of W.
+template <int LANES>
+__device__ __forceinline__ const KW<LANES>* kv(const uint64_t* p) {
+  return reinterpret_cast<const KW<LANES>*>(p);
+}
+template <int LANES>
+__device__ __forceinline__ KW<LANES>* kv(uint64_t* p) {
+  return reinterpret_cast<KW<LANES>*>(p);
 }
 
 // ---- TMA (1-D bulk copy) + mbarrier helpers ---------------------------------
@@ -225,8 +241,8 @@ __device__ __forceinline__ void flush_stats(uint64_t inv, long long kloc, const 
 // [diag, diag + E). When taking b, the pending A elements are exactly those
 // > b: inv += a_rem_base - ai.
 template <int LANES, int E, bool STATS>
-__device__ __forceinline__ void merge_path(const uint64_t* __restrict__ A, int na,
-                                           const uint64_t* __restrict__ B, int nb,
+__device__ __forceinline__ void merge_path(const KW<LANES>* __restrict__ A, int na,
+                                           const KW<LANES>* __restrict__ B, int nb,
                                            const uint32_t* __restrict__ IA,
                                            const uint32_t* __restrict__ IB, int diag,
                                            int64_t a_rem_base, Key<LANES> (&r)[E],
@@ -278,7 +294,7 @@ __device__ __forceinline__ void merge_path(const uint64_t* __restrict__ A, int n
 
 // Registers (blocked, E per thread starting at element `base`) -> AoS smem.
 template <int LANES, int E, bool STATS>
-__device__ __forceinline__ void regs_to_smem(uint64_t* sk, uint32_t* si, int base,
+__device__ __forceinline__ void regs_to_smem(KW<LANES>* sk, uint32_t* si, int base,
                                              const Key<LANES> (&r)[E], const uint32_t (&ri)[E]) {
 #pragma unroll
   for (int k = 0; k < E; ++k) {
@@ -289,12 +305,12 @@ __device__ __forceinline__ void regs_to_smem(uint64_t* sk, uint32_t* si, int bas
 
 // AoS smem -> global, coalesced over the flat uint64 words of cnt keys.
 template <int LANES, bool STATS, int NT>
-__device__ __forceinline__ void smem_to_global(const uint64_t* sk, const uint32_t* si, int cnt,
-                                               uint64_t* __restrict__ gk, uint32_t* __restrict__ gi) {
-  const int words = cnt * LANES;
+__device__ __forceinline__ void smem_to_global(const KW<LANES>* sk, const uint32_t* si, int cnt,
+                                               KW<LANES>* __restrict__ gk, uint32_t* __restrict__ gi) {
+  const int words = cnt * KeyTraits<LANES>::NW;
   int w = threadIdx.x;
   for (; w + NT < words; w += 2 * NT) {  // two independent stores in flight
-    const uint64_t x = sk[w], y = sk[w + NT];
+    const KW<LANES> x = sk[w], y = sk[w + NT];
     gk[w] = x;
     gk[w + NT] = y;
   }
@@ -309,6 +325,8 @@ __device__ __forceinline__ void smem_to_global(const uint64_t* sk, const uint32_
 template <int LANES, bool STATS>
 __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_constant__ SortLaunch a) {
   constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
+  constexpr int NW = KeyTraits<LANES>::NW, KB = key_bytes(LANES);
+  using W = KW<LANES>;
   constexpr size_t kKeyBytes = keys_smem_bytes<LANES, T, STATS>();
   extern __shared__ __align__(16) uint64_t smem[];
   uint8_t* sbytes = reinterpret_cast<uint8_t*>(smem);
@@ -318,8 +336,9 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
   const SegDesc sd = seg_at(a, find_segment(a, blockIdx.x));
   const uint64_t start = (uint64_t)(blockIdx.x - sd.tile_begin) * T;
   const int cnt = (int)min((uint64_t)T, (uint64_t)sd.n - start);
-  const uint64_t* gin = (sd.in_ptr ? sd.in_ptr : a.keys_in + sd.key_off * LANES) + start * LANES;
-  const Window16 w = window16(gin, (uint32_t)cnt * 8 * LANES);
+  const W* gin = (sd.in_ptr ? kv<LANES>(sd.in_ptr) : kv<LANES>(a.keys_in) + sd.key_off * NW) +
+                 start * NW;
+  const Window16 w = window16(gin, (uint32_t)cnt * KB);
   if (tid == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, w.bytes);
@@ -327,10 +346,10 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  uint64_t* sk = reinterpret_cast<uint64_t*>(sbytes + w.off);  // element 0 of the tile
+  W* sk = reinterpret_cast<W*>(sbytes + w.off);  // element 0 of the tile
   // all-ones sentinels after the last key: they sort last and, being at the
   // highest positions, never swap with a real key (ties keep order)
-  for (int j = cnt * LANES + tid; j < T * LANES; j += NT) sk[j] = ~0ull;
+  for (int j = cnt * NW + tid; j < T * NW; j += NT) sk[j] = ~W(0);
   __syncthreads();
 
   Key<LANES> r[E];
@@ -367,7 +386,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
     __syncthreads();
     const int gt = (2 * run) / E;  // threads per merged pair
     const int a0 = (tid / gt) * 2 * run;
-    merge_path<LANES, E, STATS>(sk + (size_t)a0 * LANES, run, sk + (size_t)(a0 + run) * LANES, run,
+    merge_path<LANES, E, STATS>(sk + (size_t)a0 * NW, run, sk + (size_t)(a0 + run) * NW, run,
                                 si + a0, si + a0 + run, (tid % gt) * E, run, r, ri, inv);
   }
   long long kloc = 0;
@@ -382,7 +401,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
   __syncthreads();
   regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
   __syncthreads();
-  smem_to_global<LANES, STATS, NT>(sk, si, cnt, a.keys_out + (sd.key_off + start) * LANES,
+  smem_to_global<LANES, STATS, NT>(sk, si, cnt, kv<LANES>(a.keys_out) + (sd.key_off + start) * NW,
                                    a.idx_out ? a.idx_out + sd.idx_off + start : nullptr);
 }
 
@@ -391,8 +410,8 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
 // Warp-wide 32-ary merge-path search in global memory: the number of A
 // elements among the first d outputs of merge(A, B) (A first on ties).
 template <int LANES>
-__device__ int64_t merge_path_search_global(const uint64_t* __restrict__ A, int64_t na,
-                                            const uint64_t* __restrict__ B, int64_t nb, int64_t d) {
+__device__ int64_t merge_path_search_global(const KW<LANES>* __restrict__ A, int64_t na,
+                                            const KW<LANES>* __restrict__ B, int64_t nb, int64_t d) {
   const int lane = threadIdx.x & 31;
   int64_t lo = max((int64_t)0, d - nb), hi = min(d, na);
   while (hi > lo) {
@@ -451,8 +470,9 @@ __global__ void __launch_bounds__(256) merge_split_kernel(const __grid_constant_
   const PairGeom g = pair_geom(sd, item, a.run, T);
   int64_t s = 0;
   if (!g.empty) {
-    const uint64_t* A = a.keys_in + (sd.key_off + g.pair_base) * LANES;
-    const uint64_t* B = A + (int64_t)a.run * LANES;
+    constexpr int NW = KeyTraits<LANES>::NW;
+    const KW<LANES>* A = kv<LANES>(a.keys_in) + (sd.key_off + g.pair_base) * NW;
+    const KW<LANES>* B = A + (int64_t)a.run * NW;
     s = merge_path_search_global<LANES>(A, g.na, B, g.nb, g.d0);
   }
   if ((threadIdx.x & 31) == 0) {
@@ -465,6 +485,8 @@ template <int LANES, bool STATS>
 __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
     merge_kernel(const __grid_constant__ SortLaunch a) {
   constexpr int E = MergeCfg<LANES>::E, T = MergeCfg<LANES>::T, NT = kMergeThreads;
+  constexpr int NW = KeyTraits<LANES>::NW, KB = key_bytes(LANES);
+  using W = KW<LANES>;
   constexpr size_t kKeyBytes = keys_smem_bytes<LANES, T, STATS>();
   extern __shared__ __align__(16) uint64_t smem[];
   uint8_t* sbytes = reinterpret_cast<uint8_t*>(smem);
@@ -480,10 +502,10 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
   const int64_t a1 = (g.d1 == g.na + g.nb) ? g.na : (int64_t)a.splits[2 * item + 2];
   const int64_t b0 = g.d0 - a0, b1 = g.d1 - a1;
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
-  const uint64_t* Ag = a.keys_in + (sd.key_off + g.pair_base + a0) * LANES;
-  const uint64_t* Bg = a.keys_in + (sd.key_off + g.pair_base + R + b0) * LANES;
-  const Window16 wa = window16(Ag, (uint32_t)la * 8 * LANES);
-  const Window16 wb = window16(Bg, (uint32_t)lb * 8 * LANES);
+  const W* Ag = kv<LANES>(a.keys_in) + (sd.key_off + g.pair_base + a0) * NW;
+  const W* Bg = kv<LANES>(a.keys_in) + (sd.key_off + g.pair_base + R + b0) * NW;
+  const Window16 wa = window16(Ag, (uint32_t)la * KB);
+  const Window16 wb = window16(Bg, (uint32_t)lb * KB);
   const uint32_t b_at = wa.bytes;  // B window lands right after A's
   Window16 wia{}, wib{};
   uint32_t ib_at = 0;
@@ -507,8 +529,8 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
   }
   __syncthreads();  // barrier initialised before anyone waits on it
   mbar_wait(&bar, 0);
-  const uint64_t* As = reinterpret_cast<const uint64_t*>(sbytes + wa.off);
-  const uint64_t* Bs = reinterpret_cast<const uint64_t*>(sbytes + b_at + wb.off);
+  const W* As = reinterpret_cast<const W*>(sbytes + wa.off);
+  const W* Bs = reinterpret_cast<const W*>(sbytes + b_at + wb.off);
   const uint32_t* IAs = reinterpret_cast<const uint32_t*>(reinterpret_cast<uint8_t*>(si) + wia.off);
   const uint32_t* IBs =
       reinterpret_cast<const uint32_t*>(reinterpret_cast<uint8_t*>(si) + ib_at + wib.off);
@@ -528,11 +550,11 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
   }
   flush_stats<STATS>(inv, kloc, sd, a.inv, a.kmax);
   __syncthreads();  // every thread is done reading the input windows
-  uint64_t* sk = smem;  // output staging reuses the window bytes (AoS, unpadded)
+  W* sk = reinterpret_cast<W*>(smem);  // output staging reuses the window bytes (AoS)
   if (tid * E < la + lb) regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
   __syncthreads();
   smem_to_global<LANES, STATS, NT>(sk, si, la + lb,
-                                   a.keys_out + (sd.key_off + out_begin) * LANES,
+                                   kv<LANES>(a.keys_out) + (sd.key_off + out_begin) * NW,
                                    STATS ? a.idx_out + sd.idx_off + out_begin : nullptr);
 }
 
@@ -540,6 +562,7 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
 
 int tile_size(int lanes) {
   switch (lanes) {
+    case 0: return TileCfg<0>::T;
     case 1: return TileCfg<1>::T;
     case 2: return TileCfg<2>::T;
     case 3: return TileCfg<3>::T;
@@ -549,6 +572,7 @@ int tile_size(int lanes) {
 
 int merge_tile_size(int lanes) {
   switch (lanes) {
+    case 0: return MergeCfg<0>::T;
     case 1: return MergeCfg<1>::T;
     case 2: return MergeCfg<2>::T;
     case 3: return MergeCfg<3>::T;
@@ -567,6 +591,7 @@ static void set_attrs_t() {
 // Opt every sort instantiation into > 48 KiB of dynamic shared memory on the
 // current device (called once per device by the handle).
 void set_sort_attributes() {
+  set_attrs_t<0, false>(); set_attrs_t<0, true>();
   set_attrs_t<1, false>(); set_attrs_t<1, true>();
   set_attrs_t<2, false>(); set_attrs_t<2, true>();
   set_attrs_t<3, false>(); set_attrs_t<3, true>();
@@ -589,6 +614,7 @@ static void launch_merge_t(const SortLaunch& a, cudaStream_t st) {
 #define WS_DISPATCH_LANES(fn, lanes, stats, ...)                                    \
   do {                                                                              \
     switch (lanes) {                                                                \
+      case 0: stats ? fn<0, true>(__VA_ARGS__) : fn<0, false>(__VA_ARGS__); break; \
       case 1: stats ? fn<1, true>(__VA_ARGS__) : fn<1, false>(__VA_ARGS__); break; \
       case 2: stats ? fn<2, true>(__VA_ARGS__) : fn<2, false>(__VA_ARGS__); break; \
       case 3: stats ? fn<3, true>(__VA_ARGS__) : fn<3, false>(__VA_ARGS__); break; \

@@ -25,6 +25,13 @@ constexpr int kLongBin = kMaxPackedLen;     // bin index of the L > 32 class
 constexpr int kNumBins = kMaxPackedLen + 1; // bins 0..31 -> L = 1..32, bin 32 = long
 constexpr int kHistRows = kNumBins + 1;     // + one row of per-chunk word totals
 constexpr int kTextPad = 128;               // zero padding after the text
+// Single-pass ingest look-back record per chunk (uint32 words): [0] flag,
+// [kRecAgg + r] the chunk's own count of row r, [kRecIncl + r] the inclusive
+// prefix of row r. Aggregates and prefixes live apart so a reader that saw
+// flag 1 never reads values being overwritten by the later prefix.
+constexpr int kRecAgg = 4;        // 16-byte aligned: readers fetch rows as uint4
+constexpr int kRecIncl = 40;
+constexpr int kLookbackRec = 80;
 
 __host__ __device__ constexpr int lanes_for_len(int L) { return (L + 7) >> 3; }
 
@@ -35,8 +42,10 @@ __host__ __device__ constexpr int lanes_for_len(int L) { return (L + 7) >> 3; }
 // (character k at bits [6k, 6k+6) from the top), so L <= 10 -> 1 lane,
 // <= 21 -> 2, <= 32 -> 3, and key order == byte order.
 enum KeyEnc : int { kEncRaw8 = 0, kEncAlnum6 = 1 };
+// Lane class of a word of length L: 0 = one uint32 key word (6-bit text keys
+// of <= 5 characters, raw keys of <= 4 bytes), else the number of uint64 lanes.
 __host__ __device__ constexpr int lanes_for_len_enc(int L, int enc) {
-  return enc == kEncAlnum6 ? (6 * L + 63) >> 6 : (L + 7) >> 3;
+  return enc == kEncAlnum6 ? (L <= 5 ? 0 : (6 * L + 63) >> 6) : (L <= 4 ? 0 : (L + 7) >> 3);
 }
 __device__ __forceinline__ uint32_t alnum6_code(uint32_t b) {
   return b >= 0x61u ? b - 0x3Cu : (b >= 0x41u ? b - 0x36u : b - 0x2Fu);
@@ -71,15 +80,30 @@ __device__ __forceinline__ uint32_t alnum_mask16(uint4 v) {
          (alnum_mask4(v.w) << 12);
 }
 
+// Key word type per lane class: LANES >= 1 -> LANES big-endian uint64 lanes;
+// LANES == 0 -> one uint32 (6-bit text keys of <= 5 characters, raw keys of
+// <= 4 bytes), which halves the bytes the shortest (most common) words move.
+template <int LANES>
+struct KeyTraits {
+  using W = uint64_t;
+  static constexpr int NW = LANES;
+};
+template <>
+struct KeyTraits<0> {
+  using W = uint32_t;
+  static constexpr int NW = 1;
+};
+__host__ __device__ constexpr int key_bytes(int lanes) { return lanes == 0 ? 4 : 8 * lanes; }
+
 template <int LANES>
 struct Key {
-  uint64_t w[LANES];
+  typename KeyTraits<LANES>::W w[KeyTraits<LANES>::NW];
 };
 
 template <int LANES>
 __device__ __forceinline__ bool key_lt(const Key<LANES>& a, const Key<LANES>& b) {
 #pragma unroll
-  for (int i = 0; i < LANES; ++i) {
+  for (int i = 0; i < KeyTraits<LANES>::NW; ++i) {
     if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
   }
   return false;
@@ -94,7 +118,7 @@ template <int LANES>
 __device__ __forceinline__ Key<LANES> key_max() {
   Key<LANES> k;
 #pragma unroll
-  for (int i = 0; i < LANES; ++i) k.w[i] = ~0ull;
+  for (int i = 0; i < KeyTraits<LANES>::NW; ++i) k.w[i] = ~typename KeyTraits<LANES>::W(0);
   return k;
 }
 

@@ -9,7 +9,7 @@
 namespace ws {
 
 struct ScatterParams {
-  uint64_t bin_base[kNumBins];  // element offsets (uint64 units) of each bin's key region
+  uint64_t bin_base[kNumBins];  // byte offset of each bin's key region in `keys`
   uint64_t* keys;               // key arena, or nullptr (tokens-only mode)
   uint2* longlist;              // (start, len) of words with L > 32, corpus order
   uint2* tokens;                // optional (start, len) per word in corpus order
@@ -18,7 +18,7 @@ struct ScatterParams {
   uint32_t chunk0;              // first chunk of this launch
   uint32_t nchunks_total;       // chunks of the whole text
   unsigned int* ticket;         // chunk ticket counter (zeroed before the first launch)
-  unsigned long long* status;   // [nchunks_total][kHistRows] look-back words (zeroed)
+  uint32_t* status;             // [nchunks_total][kLookbackRec] look-back records (zeroed)
   uint32_t* totals;             // [kHistRows] per-bin totals, written by the last chunk
   uint64_t avail;               // bytes of text already on the device (0 = all)
   unsigned int* overflow;       // set when a word runs past `avail`
