@@ -59,6 +59,11 @@ void ws_destroy(ws_handle* h);
 #define WS_INGEST_KEEP_TOKENS 1 /* also keep corpus-order (start, len) tokens */
 #define WS_INGEST_DEVICE_PTR 2  /* `text` is a device pointer                 */
 #define WS_INGEST_RESIDENT 4    /* re-use the text the handle already holds   */
+#define WS_INGEST_UNORDERED 8   /* payload-only: words of one length may sit in
+                                   any order inside their bucket before the sort
+                                   (the sorted output is the same); ws_sort(h, 1)
+                                   and ws_permutation then fail with
+                                   WS_ERR_STATE. Ignored with KEEP_TOKENS. */
 
 /* tokenize (ingest.py:26-28, WORD_RE = rb"[A-Za-z0-9]+" at ingest.py:15) +
  * stable group-by-length (store.py:78-82) + build_flat (store.py:90-96):

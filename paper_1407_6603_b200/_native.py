@@ -26,6 +26,8 @@ WS_ERR_OOM = -3
 WS_ERR_STATE = -4
 WS_INGEST_KEEP_TOKENS = 1
 WS_INGEST_DEVICE_PTR = 2
+WS_INGEST_RESIDENT = 4
+WS_INGEST_UNORDERED = 8
 
 # Every symbol include/wsort.h declares (checked by tests/test_abi.py).
 EXPORTS = (
@@ -210,8 +212,11 @@ class Handle:
 
     # -- ingest -----------------------------------------------------------
     def ingest_text(self, text, keep_tokens: bool = False, device_ptr: int | None = None,
-                    n: int | None = None) -> None:
-        flags = WS_INGEST_KEEP_TOKENS if keep_tokens else 0
+                    n: int | None = None, unordered: bool = False) -> None:
+        """`unordered`: payload-only ingest (WS_INGEST_UNORDERED) - words of
+        one length may sit in any order before the sort; sort(stats=True)
+        and permutation() then raise."""
+        flags = (WS_INGEST_KEEP_TOKENS if keep_tokens else 0) | (WS_INGEST_UNORDERED if unordered else 0)
         if device_ptr is not None:
             check(self.lib.ws_ingest_text(self.h, c_void_p(device_ptr), int(n),
                                           flags | WS_INGEST_DEVICE_PTR), "ws_ingest_text")

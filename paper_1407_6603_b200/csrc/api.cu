@@ -155,6 +155,7 @@ struct ws_handle {
   DevBuf hist, off, totals;
   DevBuf keys[2], idx[2];
   DevBuf keys_cap, status, ticket;  // single-pass ingest: capacity-bounded regions
+  DevBuf fill;                      // reserve-mode counters (WS_INGEST_UNORDERED)
   DevBuf longlist, longgrp, rank, rank_tmp, lkeys[2], lidx[2];
   DevBuf tokens;
   DevBuf stat_inv, stat_k, stat_k_dummy;
@@ -170,6 +171,7 @@ struct ws_handle {
   uint64_t words = 0;
   uint64_t n_long = 0;
   bool have_tokens = false;
+  bool unordered = false;  // last ingest placed bucket runs in completion order
   int enc = kEncRaw8;       // key encoding of the current packed buckets
   bool text_valid = false;  // h->text holds the last ingested text (reusable, resident)
   bool ingested = false, sorted = false, have_stats = false;
@@ -514,6 +516,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   }
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
+  h->unordered = false;
   h->buckets.clear();
   h->n_text = n;
   h->text_valid = false;
@@ -563,8 +566,10 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     WS_CUDA(h->keys_cap.ensure(run + 256));
     WS_CUDA(h->longlist.ensure(((n + 1) / (kMaxPackedLen + 2) + 1) * sizeof(uint2)));
     if (keep_tokens) WS_CUDA(h->tokens.ensure(((n + 1) / 2 + 1) * sizeof(uint2)));
-    WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kLookbackRec * 4));
+    const bool reserve = (flags & WS_INGEST_UNORDERED) && !keep_tokens;
+    if (!reserve) WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kLookbackRec * 4));
     WS_CUDA(h->ticket.ensure(256));
+    WS_CUDA(h->fill.ensure(kHistRows * 4));
     for (int b = 0; b < kMaxPackedLen; ++b) p.bin_base[b] = region[b];
     p.keys = h->keys_cap.as<uint64_t>();
     p.longlist = h->longlist.as<uint2>();
@@ -574,9 +579,19 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     p.ticket = h->ticket.as<unsigned int>();
     p.status = h->status.as<uint32_t>();
     p.totals = h->totals.as<uint32_t>();
+    p.fill = reserve ? h->fill.as<uint32_t>() : nullptr;
+    const void* totals_src = reserve ? h->fill.p : h->totals.p;
+    auto reset_chain = [&]() -> int {
+      if (reserve) {
+        WS_CUDA(cudaMemsetAsync(h->fill.p, 0, kHistRows * 4, h->st));
+      } else {
+        WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
+        WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
+      }
+      return WS_OK;
+    };
     if (nchunks) {
-      WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
-      WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
+      WS_TRY(reset_chain());
       bool redo = false;
       if (chunked) {
         WS_CUDA(h->overflow.ensure(256));
@@ -605,6 +620,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ScatterParams pi = p;
           pi.avail = need == np - 1 ? 0 : edge[need + 1];
           const uint32_t c0 = (uint32_t)(edge[i] / cb), c1 = (uint32_t)((edge[i + 1] + cb - 1) / cb);
+          pi.chunk0 = reserve ? c0 : 0;  // look-back numbers chunks by its global ticket
           Phase ph(h, "ingest", 2.27 * (double)(edge[i + 1] - edge[i]));
           launch_ingest_lookback(dtext, n, c1 - c0, pi, h->st);
           ++h->launches;
@@ -612,13 +628,12 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         WS_TRY(check_launch("ingest_kernel"));
         WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
                                 h->st));
-        WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+        WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
         redo = tot_host[kHistRows] != 0;  // a word spanned a whole piece: ingest again
         if (redo) {
           p.overflow = nullptr;
-          WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
-          WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
+          WS_TRY(reset_chain());
         }
       }
       if (!chunked || redo) {
@@ -630,7 +645,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ++h->launches;
         }
         WS_TRY(check_launch("ingest_kernel"));
-        WS_CUDA(cudaMemcpyAsync(tot_host, h->totals.p, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+        WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
       }
     } else {
@@ -644,6 +659,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
       if (!bk.is_long)
         bk.in_ptr = reinterpret_cast<const uint64_t*>(h->keys_cap.as<uint8_t>() + region[bk.len - 1]);
     if (keep_tokens) h->have_tokens = true;
+    h->unordered = reserve;
   } else {
     const size_t hist_bytes = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
     WS_CUDA(h->hist.ensure(hist_bytes));
@@ -730,6 +746,8 @@ int fused_class_copy(ws_handle* h, FusedEmit* fe, int cls, cudaStream_t st) {
 
 int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   if (!h->ingested) return fail(WS_ERR_STATE, "ws_sort before ingest");
+  if (stats && h->unordered)
+    return fail(WS_ERR_STATE, "stats need corpus order: ingest without WS_INGEST_UNORDERED");
   if (fe) h->sorted = true;  // bucket final buffers are fixed at planning time
   const int nb = (int)h->buckets.size();
   if (stats) {
@@ -1008,6 +1026,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
   if (nblocks < 0) return fail(WS_ERR_ARG, "negative block count");
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
+  h->unordered = false;
   h->text_valid = false;
   h->enc = kEncRaw8;
   h->buckets.clear();
@@ -1102,6 +1121,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
 int ingest_words_impl(ws_handle* h, const uint8_t* concat, const uint32_t* lens, uint64_t nwords) {
   h->ingested = h->sorted = h->have_stats = false;
   h->have_tokens = false;
+  h->unordered = false;
   h->text_valid = false;
   h->enc = kEncRaw8;  // word lists may hold any byte values
   h->buckets.clear();
@@ -1395,7 +1415,7 @@ int ws_emit_rows(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written) {
 int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
                  uint64_t* written) {
   WS_TRY(begin_call(h));
-  WS_TRY(ingest_text_impl(h, text, n, 0));
+  WS_TRY(ingest_text_impl(h, text, n, WS_INGEST_UNORDERED));
   params_reset(h);  // the ingest synchronised: staging space is free again
   const uint64_t size = emit_size(h, true);
   if (written) *written = size;
@@ -1414,7 +1434,7 @@ int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, ui
 
 int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   WS_TRY(begin_call(h));
-  WS_TRY(ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT));
+  WS_TRY(ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT | WS_INGEST_UNORDERED));
   params_reset(h);
   const uint64_t size = emit_size(h, true);
   WS_CUDA(h->out.ensure(size + 64));

@@ -375,13 +375,16 @@ __device__ __forceinline__ void resolve_prefix_warp(uint32_t* __restrict__ statu
   if (lane + 32 < kHistRows) excl_out[lane + 32] = acc1;
 }
 
-// K3 (two-pass) / single-pass ingest. LOOKBACK = false: chunk offsets come
+// K3 (two-pass) / single-pass ingest. MODE kByScan: chunk offsets come
 // from the scan of K1's histograms and keys land in the compact bucket
-// layout. LOOKBACK = true: CTAs take chunks in ticket order, chain their
+// layout. kByLookback: CTAs take chunks in ticket order, chain their
 // per-bin offsets through a decoupled look-back and write into
 // capacity-bounded per-length regions (no count pass, no host round trip
-// before the scatter); the last chunk publishes the totals.
-template <bool LOOKBACK>
+// before the scatter); the last chunk publishes the totals. kByReserve: like
+// kByLookback, but every chunk reserves its runs with one atomicAdd per bin
+// (no dependence between chunks; bucket order = chunk completion order).
+enum ScatterMode : int { kByScan = 0, kByLookback = 1, kByReserve = 2 };
+template <int MODE>
 __global__ void __launch_bounds__(kIngestThreads)
 scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __restrict__ off,
                uint32_t nchunks, ScatterParams p) {
@@ -400,6 +403,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   __shared__ __align__(16) uint8_t stage[kStageBytes];  // keys of the chunk, grouped by bin
   __shared__ uint32_t s_chunk;
 
+  constexpr bool LOOKBACK = MODE == kByLookback;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (LOOKBACK) {
     if (tid == 0) s_chunk = p.chunk0 + atomicAdd(p.ticket, 1u);
@@ -465,6 +469,8 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     s_run[tid] = run;
   }
   __syncthreads();
+  if (MODE == kByReserve && tid < kHistRows && s_run[tid])  // result needed only after packing
+    s_base[tid] = atomicAdd(p.fill + tid, s_run[tid]);
   if (LOOKBACK && wid == 0) publish_record(p.status, (uint32_t)chunk, s_run, chunk == 0 ? kRecIncl : kRecAgg,
                    chunk == 0 ? 2u : 1u);
   // staging layout: bins back to back in bin order, key_bytes(lanes(bin)) each
@@ -512,7 +518,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
       store_key(stage + s_soff[bin] + lpos * (uint32_t)key_bytes(lanes), lanes, k);
     }
   }
-  if (!LOOKBACK && tid < kHistRows) s_base[tid] = off[(uint64_t)tid * nchunks + chunk];
+  if (MODE == kByScan && tid < kHistRows) s_base[tid] = off[(uint64_t)tid * nchunks + chunk];
   __syncthreads();
   // stream each bin's run out: consecutive threads write consecutive words
   if (p.keys) {
@@ -682,12 +688,16 @@ void launch_scan(const uint32_t* hist, uint32_t* off, uint32_t* totals, uint32_t
 
 void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32_t nchunks,
                     const ScatterParams& p, cudaStream_t st) {
-  if (nchunks) scatter_kernel<false><<<nchunks, kIngestThreads, 0, st>>>(text, n, off, nchunks, p);
+  if (nchunks) scatter_kernel<kByScan><<<nchunks, kIngestThreads, 0, st>>>(text, n, off, nchunks, p);
 }
 
 void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st) {
-  if (nchunks) scatter_kernel<true><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+  if (!nchunks) return;
+  if (p.fill)
+    scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+  else
+    scatter_kernel<kByLookback><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }

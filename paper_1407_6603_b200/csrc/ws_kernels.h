@@ -22,6 +22,11 @@ struct ScatterParams {
   uint32_t* totals;             // [kHistRows] per-bin totals, written by the last chunk
   uint64_t avail;               // bytes of text already on the device (0 = all)
   unsigned int* overflow;       // set when a word runs past `avail`
+  // reserve mode (payload-only sorts): when set, each chunk reserves its run
+  // of every bin with one atomicAdd on fill[row] instead of the look-back;
+  // runs then land in completion order, so bucket order is not corpus order
+  // (stats / permutations / tokens need the look-back). fill[] ends as totals.
+  uint32_t* fill;               // [kHistRows] zeroed reservation counters, or nullptr
 };
 
 // ingest.cu

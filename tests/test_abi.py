@@ -23,6 +23,17 @@ def test_header_declares_the_binding_table():
     assert header_symbols() == sorted(_native.EXPORTS)
 
 
+def test_header_constants_match_binding():
+    text = HEADER.read_text()
+    consts = dict((k, int(v)) for k, v in re.findall(r"#define\s+(WS_\w+)\s+(-?\d+)", text))
+    for name, value in consts.items():
+        if hasattr(_native, name):
+            assert getattr(_native, name) == value, name
+    for name in ("WS_INGEST_KEEP_TOKENS", "WS_INGEST_DEVICE_PTR", "WS_INGEST_RESIDENT",
+                 "WS_INGEST_UNORDERED"):
+        assert consts[name] == getattr(_native, name)
+
+
 def test_library_exports_every_header_symbol():
     lib = ctypes.CDLL(str(_native.LIB_PATH))
     for name in header_symbols():

@@ -136,3 +136,22 @@ def test_chunked_h2d_matches_unchunked():
     assert len(text) > (16 << 20)
     want, _ = oracle.sort_text(text, mode="fast")
     assert sort_text(text) == want
+
+
+def test_unordered_ingest_payload_and_state_errors():
+    # WS_INGEST_UNORDERED (the payload-only path of ws_sort_text /
+    # ws_sort_resident) reserves bucket runs per chunk with atomics: same
+    # sorted payload, but stats / permutations must be refused
+    for text in (synth.generate(0, seed=3), synth.generate(4, words=300_000, seed=4),
+                 b"q" * 5000 + b" " + b"r" * 33 + b" a" * 7000):
+        want, _ = oracle.sort_text(text, mode="fast", max_len=8192)
+        h = _native.Handle(0)
+        h.ingest_text(text, unordered=True)
+        h.sort(False)
+        assert h.emit_lines().tobytes() == want
+        with pytest.raises(RuntimeError, match="corpus order"):
+            h.sort(True)
+        h.ingest_text(text)  # a later ordered ingest restores stats
+        h.sort(True)
+        assert h.emit_lines().tobytes() == want
+        h.close()
