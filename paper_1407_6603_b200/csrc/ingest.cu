@@ -25,9 +25,6 @@ constexpr int kChunk = 4096;
 constexpr int kIngestThreads = 256;  // 16 bytes per thread
 constexpr int kWarps = kIngestThreads / 32;
 constexpr int kMaxWordsPerWarp = 256;  // 512 bytes per warp, <= 1 start per 2 bytes
-// Packed keys of one chunk: at most 2 key bytes per text byte (1-byte words,
-// 4-byte keys, every other byte) plus one 32-byte key running in at the end.
-constexpr int kStageBytes = 2 * kChunk + 64 + 8 * kMaxPackedLen;  // + alignment gaps
 
 __device__ __forceinline__ uint32_t bin_of_len(uint32_t len) {
   return len <= (uint32_t)kMaxPackedLen ? len - 1 : (uint32_t)kLongBin;
@@ -392,15 +389,15 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   __shared__ uint16_t wstart[kWarps][kMaxWordsPerWarp];
   __shared__ uint32_t wlen[kWarps][kMaxWordsPerWarp];
   __shared__ uint32_t wpos[kWarps][kMaxWordsPerWarp];
+  __shared__ uint32_t ord[kChunk / 2];  // packed words in bin-major order: start | L << 16
   __shared__ uint32_t wcnt[kWarps][kHistRows];
   __shared__ uint32_t wtot[kWarps];
   __shared__ uint32_t s_chain[kWarps];
   __shared__ uint32_t s_base[kHistRows];
   __shared__ uint32_t s_run[kHistRows];
   __shared__ uint32_t s_incl[kHistRows];
-  __shared__ uint32_t s_soff[kMaxPackedLen + 1];
-  __shared__ uint32_t s_send[kMaxPackedLen];
-  __shared__ __align__(16) uint8_t stage[kStageBytes];  // keys of the chunk, grouped by bin
+  __shared__ uint32_t s_boff[kMaxPackedLen + 1];  // bin-major word offset of each bin
+  __shared__ uint64_t s_dst[kMaxPackedLen];       // key byte address of ord slot 0, per bin
   __shared__ uint32_t s_chunk;
 
   constexpr bool LOOKBACK = MODE == kByLookback;
@@ -412,6 +409,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
   const uint64_t chunk = LOOKBACK ? s_chunk : p.chunk0 + blockIdx.x;
   const uint64_t cbase = chunk * kChunk;
   for (int i = tid; i < kWarps * kHistRows; i += kIngestThreads) (&wcnt[0][0])[i] = 0;
+  if (MODE == kByScan && tid < kHistRows) s_base[tid] = off[(uint64_t)tid * nchunks + chunk];
 
   uint4 v;
   Segment16 seg = classify_chunk(text, n, cbase, v, s_chain, p.avail ? p.avail : ~0ull,
@@ -457,8 +455,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     __syncwarp();
   }
   __syncthreads();
-  // per-bin: exclusive scan of the warp counts and the chunk total; publish
-  // the chunk's aggregates right away (successors can start resolving)
+  // per-bin: exclusive scan of the warp counts and the chunk total
   if (tid < kHistRows) {
     uint32_t run = 0;
     for (int w = 0; w < kWarps; ++w) {
@@ -469,26 +466,14 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     s_run[tid] = run;
   }
   __syncthreads();
-  if (MODE == kByReserve && tid < kHistRows && s_run[tid])  // result needed only after packing
+  // chunk offsets: one atomic per bin (reserve), or the decoupled look-back
+  // (warp 0, publishing the aggregate first); the other warps meanwhile
+  // scan the bins and build the bin-major word order
+  if (MODE == kByReserve && tid < kHistRows && s_run[tid])
     s_base[tid] = atomicAdd(p.fill + tid, s_run[tid]);
-  if (LOOKBACK && wid == 0) publish_record(p.status, (uint32_t)chunk, s_run, chunk == 0 ? kRecIncl : kRecAgg,
-                   chunk == 0 ? 2u : 1u);
-  // staging layout: bins back to back in bin order, key_bytes(lanes(bin)) each
-  if (tid == 32) {  // 8-byte aligned bins (uint64 key stores); gaps are skipped below
-    uint32_t o = 0;
-    for (int b = 0; b < kMaxPackedLen; ++b) {
-      o = (o + 7) & ~7u;
-      s_soff[b] = o;
-      o += s_run[b] * (uint32_t)key_bytes(lanes_for_len_enc(b + 1, p.enc));
-      s_send[b] = o;
-    }
-    s_soff[kMaxPackedLen] = o;
-  }
-  __syncthreads();
-  // chunk offsets: warp 0 resolves the decoupled look-back right away (an
-  // early inclusive prefix keeps successors' look-back windows short) while
-  // the other warps already pack their keys
   if (LOOKBACK && wid == 0) {
+    publish_record(p.status, (uint32_t)chunk, s_run, chunk == 0 ? kRecIncl : kRecAgg,
+                   chunk == 0 ? 2u : 1u);
     resolve_prefix_warp(p.status, (uint32_t)chunk, s_base);
     __syncwarp();
     if (chunk > 0) {
@@ -499,57 +484,57 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     if (chunk == p.nchunks_total - 1)
       for (int r = lane; r < kHistRows; r += 32) p.totals[r] = s_base[r] + s_run[r];
   }
-  // pack every key into the staging area (no dependence on other chunks)
-  if (p.keys) {
-    for (uint32_t b = 0; b < total; b += 32) {
-      const uint32_t j = b + lane;
-      if (j >= total) break;
-      const uint32_t L = wlen[wid][j];
-      const uint32_t bin = bin_of_len(L);
-      if (bin == (uint32_t)kLongBin) continue;
-      const uint32_t start = wstart[wid][j];
-      const int lanes = lanes_for_len_enc(L, p.enc);
-      const uint32_t lpos = wcnt[wid][bin] + wpos[wid][j];
-      uint64_t k[4];
-      if (codes)
-        pack6_from_codes(chunk32, start, L, lanes, k);
-      else
-        pack_from_smem(chunk32, start, L, lanes, k);
-      store_key(stage + s_soff[bin] + lpos * (uint32_t)key_bytes(lanes), lanes, k);
+  if (wid == 1) {  // exclusive scan of the packed bins' counts (lane = bin)
+    const uint32_t cnt = s_run[lane];
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += t;
     }
+    s_boff[lane] = inc - cnt;
+    if (lane == 31) s_boff[kMaxPackedLen] = inc;
   }
-  if (MODE == kByScan && tid < kHistRows) s_base[tid] = off[(uint64_t)tid * nchunks + chunk];
   __syncthreads();
-  // stream each bin's run out: consecutive threads write consecutive words
-  if (p.keys) {
-    const uint32_t words4 = s_soff[kMaxPackedLen] >> 2;
-    for (uint32_t i = tid; i < words4; i += kIngestThreads) {
-      const uint32_t byte = i << 2;
-      int lo = 0, hi = kMaxPackedLen - 1;  // bin holding this staging byte
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_soff[mid] <= byte) lo = mid; else hi = mid - 1;
-      }
-      if (byte >= s_send[lo]) continue;  // alignment gap
-      const uint32_t ks = (uint32_t)key_bytes(lanes_for_len_enc(lo + 1, p.enc));
-      uint8_t* dst = reinterpret_cast<uint8_t*>(p.keys) + p.bin_base[lo] +
-                     (uint64_t)s_base[lo] * ks + (byte - s_soff[lo]);
-      *reinterpret_cast<uint32_t*>(dst) = reinterpret_cast<const uint32_t*>(stage)[i];
-    }
-  }
-  // long words and corpus-order tokens go straight out
+  // bin-major word order of the packed words (long words / tokens go out here)
   for (uint32_t b = 0; b < total; b += 32) {
     const uint32_t j = b + lane;
     if (j >= total) break;
     const uint32_t L = wlen[wid][j];
     const uint32_t start = wstart[wid][j];
+    const uint32_t bin = bin_of_len(L);
+    if (bin != (uint32_t)kLongBin) {
+      ord[s_boff[bin] + wcnt[wid][bin] + wpos[wid][j]] = start | (L << 16);
+    } else if (p.keys) {
+      p.longlist[s_base[kLongBin] + wcnt[wid][kLongBin] + wpos[wid][j]] =
+          make_uint2((uint32_t)(cbase + start), L);
+    }
     if (p.tokens) {
       const uint32_t widx = s_base[kNumBins] + wcnt[wid][kNumBins] + j;
       p.tokens[widx] = make_uint2((uint32_t)(cbase + start), L);
     }
-    if (p.keys && bin_of_len(L) == (uint32_t)kLongBin)
-      p.longlist[s_base[kLongBin] + wcnt[wid][kLongBin] + wpos[wid][j]] =
-          make_uint2((uint32_t)(cbase + start), L);
+  }
+  if (tid < kMaxPackedLen) {  // global key address of bin-major slot 0 of each bin
+    const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc(tid + 1, p.enc));
+    s_dst[tid] = p.bin_base[tid] + ((uint64_t)s_base[tid] - s_boff[tid]) * ks;
+  }
+  __syncthreads();
+  // pack: consecutive threads take consecutive words of one bin (same length,
+  // no divergence) and store their keys to consecutive global addresses
+  if (p.keys) {
+    const uint32_t npacked = s_boff[kMaxPackedLen];
+    uint8_t* keys = reinterpret_cast<uint8_t*>(p.keys);
+    for (uint32_t k = tid; k < npacked; k += kIngestThreads) {
+      const uint32_t e = ord[k];
+      const uint32_t start = e & 0xFFFFu, L = e >> 16;
+      const int lanes = lanes_for_len_enc(L, p.enc);
+      uint64_t key[4];
+      if (codes)
+        pack6_from_codes(chunk32, start, L, lanes, key);
+      else
+        pack_from_smem(chunk32, start, L, lanes, key);
+      store_key(keys + s_dst[L - 1] + (uint64_t)k * key_bytes(lanes), lanes, key);
+    }
   }
 }
 
