@@ -126,6 +126,17 @@ int ws_emit_rows(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written);
 int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
                  uint64_t* written);
 
+/* Batch of independent corpora (a serving loop): the same result as calling
+ * ws_sort_text(h, texts[i], sizes[i], outs[i], caps[i], &written[i]) for
+ * each i, with up to `inflight` corpora in flight (<= 0: 3; at most 4) on
+ * internal slot handles owned by h. Uploads are staggered so one corpus
+ * crosses PCIe host->device while earlier ones sort and come back
+ * device->host. outs[i] may repeat with period `inflight` (a slot finishes
+ * corpus i before starting i + inflight). Returns the first failure. */
+int ws_sort_texts(ws_handle* h, int32_t count, const uint8_t* const* texts, const uint64_t* sizes,
+                  uint8_t* const* outs, const uint64_t* caps, uint64_t* written,
+                  int32_t inflight);
+
 /* Device-resident variant: re-runs ingest + sort + emit on the text the
  * handle already holds from its last ws_ingest_text (same n), leaving the
  * payload in device memory (ws_output_device). No host<->device data copy

@@ -36,7 +36,7 @@ EXPORTS = (
     "ws_sort", "ws_bucket_stats", "ws_permutation", "ws_emit_lines", "ws_emit_rows",
     "ws_sort_text", "ws_sort_rows", "ws_sort_blocks", "ws_stats_closed_form",
     "ws_set_profiling", "ws_profile", "ws_profile_reset", "ws_launch_count", "ws_stream",
-    "ws_host_alloc", "ws_host_free", "ws_sort_resident", "ws_output_device",
+    "ws_host_alloc", "ws_host_free", "ws_sort_resident", "ws_output_device", "ws_sort_texts",
 )
 
 
@@ -81,6 +81,7 @@ def _declare(lib) -> None:
         "ws_emit_lines": (I, [V, V, ctypes.c_uint64, c_u64p]),
         "ws_emit_rows": (I, [V, V, ctypes.c_uint64, c_u64p]),
         "ws_sort_text": (I, [V, V, ctypes.c_uint64, V, ctypes.c_uint64, c_u64p]),
+        "ws_sort_texts": (I, [V, ctypes.c_int32, V, V, V, V, V, ctypes.c_int32]),
         "ws_sort_rows": (I, [V, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, V]),
         "ws_sort_blocks": (I, [ctypes.c_int32, V, V, V, ctypes.c_int32, V, V]),
         "ws_stats_closed_form": (I, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
@@ -295,6 +296,23 @@ class Handle:
                                     c_void_p(ptr(out)), out.nbytes, ctypes.byref(written)),
               "ws_sort_text")
         return int(written.value)
+
+    def sort_texts(self, texts: list, outs: list, inflight: int = 0) -> list[int]:
+        """Batch of corpora, up to `inflight` in flight (ws_sort_texts): texts[i]
+        and outs[i] are uint8 numpy arrays (pinned for full PCIe speed);
+        returns the payload sizes."""
+        k = len(texts)
+        if len(outs) != k:
+            raise ValueError("texts and outs differ in length")
+        tp = (ctypes.c_void_p * max(k, 1))(*[ptr(t) for t in texts])
+        op = (ctypes.c_void_p * max(k, 1))(*[ptr(o) for o in outs])
+        sz = np.array([t.nbytes for t in texts] or [0], dtype=np.uint64)
+        cp = np.array([o.nbytes for o in outs] or [0], dtype=np.uint64)
+        wr = np.zeros(max(k, 1), dtype=np.uint64)
+        check(self.lib.ws_sort_texts(self.h, k, ctypes.cast(tp, c_void_p), c_void_p(ptr(sz)),
+                                     ctypes.cast(op, c_void_p), c_void_p(ptr(cp)),
+                                     c_void_p(ptr(wr)), int(inflight)), "ws_sort_texts")
+        return [int(x) for x in wr[:k]]
 
     def sort_resident(self, n: int) -> int:
         """Ingest + sort + emit of the text already on the device; payload stays in HBM."""

@@ -11,12 +11,14 @@
 // "long groups" sorted by an LSD sequence of stable 1-lane passes over their
 // 8-byte lanes (most significant last), with the text as the byte store.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "wsort.h"
@@ -41,6 +43,12 @@ int fail_cuda(cudaError_t e, const char* what, int line) {
   snprintf(buf, sizeof buf, "CUDA error at api.cu:%d (%s): %s", line, what, cudaGetErrorString(e));
   g_err = buf;
   return code;
+}
+
+// WSORT_TRACE=1: host timestamps of the batch pipeline's stages (stderr)
+double trace_ms() {
+  static const auto t0 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 #define WS_CUDA(x)                                             \
@@ -162,6 +170,7 @@ struct ws_handle {
   DevBuf out;
   DevBuf params;
   DevBuf splits[kClasses + 2];  // merge-path splits: [0] main stream, [1..4] class streams
+  DevBuf rcounts[2], rtotals[2];  // radix passes of lane classes 0 and 1
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
   uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
@@ -185,6 +194,7 @@ struct ws_handle {
   std::vector<PhaseRec> phases;
   std::vector<cudaEvent_t> event_pool;
   uint64_t launches = 0;
+  std::vector<ws_handle*> peers;  // extra in-flight slots of ws_sort_texts
 };
 
 namespace {
@@ -400,6 +410,91 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
   return WS_OK;
 }
 
+// Payload-only sort of one-word keys (lane classes 0 and 1): stable LSD radix
+// passes over 8-bit digits of the bits each bucket uses (radix.cu). Pass p
+// reads buffer p & 1 (pass 0: the segment's in_ptr) and writes (p + 1) & 1;
+// a bucket is done after ceil(bits / 8) passes.
+int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* keys0,
+                        uint64_t* keys1, cudaStream_t st, const PassDoneHook* on_done) {
+  const int kb_bytes = key_bytes(lanes);
+  const int keybits = 8 * kb_bytes;
+  const int cbits = h->enc == kEncAlnum6 ? 6 : 8;  // bits per character
+  const uint32_t T = (uint32_t)radix_tile_size(lanes);
+  struct Plan {
+    SegIn* s;
+    int passes;
+    uint32_t shift0, ntiles;
+  };
+  std::vector<Plan> plan;
+  int max_passes = 0;
+  uint64_t count_words = 0;
+  for (auto& s : segs) {
+    s.final_buf = 0;
+    if (!s.n) continue;
+    const int bits = std::min(keybits, cbits * (int)h->buckets[s.stat_slot].len);
+    const int passes = std::max(1, (bits + 7) / 8);
+    plan.push_back(Plan{&s, passes, (uint32_t)(keybits - bits), (s.n + T - 1) / T});
+    max_passes = std::max(max_passes, passes);
+    count_words += 256ull * plan.back().ntiles;
+    s.final_buf = passes & 1;
+  }
+  if (plan.empty()) return WS_OK;
+  DevBuf& cb = h->rcounts[lanes];
+  DevBuf& tb = h->rtotals[lanes];
+  WS_CUDA(cb.ensure(count_words * 4 + 64));
+  const size_t tot_bytes = (size_t)max_passes * plan.size() * 256 * 4;
+  WS_CUDA(tb.ensure(tot_bytes));
+  WS_CUDA(cudaMemsetAsync(tb.p, 0, tot_bytes, st));
+  uint8_t* kb[2] = {reinterpret_cast<uint8_t*>(keys0), reinterpret_cast<uint8_t*>(keys1)};
+  for (int p = 0; p < max_passes; ++p) {
+    std::vector<RadixSeg> d;
+    uint32_t work = 0;
+    uint64_t coff = 0;
+    double bytes = 0;
+    for (auto& pl : plan) {
+      if (pl.passes <= p) continue;
+      RadixSeg r;
+      const uint64_t off = pl.s->key_off * kb_bytes;
+      r.in = p == 0 ? static_cast<const void*>(pl.s->in_ptr) : kb[p & 1] + off;
+      r.out = kb[(p + 1) & 1] + off;
+      r.coff = coff;
+      r.n = pl.s->n;
+      r.tile_begin = work;
+      r.ntiles = pl.ntiles;
+      r.shift = pl.shift0 + 8 * p;
+      d.push_back(r);
+      work += pl.ntiles;
+      coff += 256ull * pl.ntiles;
+      bytes += 3.0 * pl.s->n * kb_bytes;  // upsweep read + downsweep read and write
+    }
+    RadixLaunch a;
+    if (d.size() <= (size_t)kInlineSegs) {
+      std::copy(d.begin(), d.end(), a.inl);
+      a.segs = nullptr;
+    } else {
+      WS_TRY(params_upload(h, d, &a.segs, st));
+    }
+    a.nsegs = (int)d.size();
+    a.work_items = work;
+    a.counts = cb.as<uint32_t>();
+    a.totals = tb.as<uint32_t>() + (size_t)p * plan.size() * 256;
+    char name[32];
+    snprintf(name, sizeof name, "radix_l%d", lanes);
+    Phase ph(h, name, bytes, 0, st);
+    launch_radix_pass(lanes, a, st);
+    h->launches += 3;
+    ph.end();
+    WS_TRY(check_launch(name));
+    if (on_done) {
+      std::vector<const SegIn*> done;
+      for (auto& pl : plan)
+        if (pl.passes == p + 1) done.push_back(pl.s);
+      if (!done.empty()) WS_TRY((*on_done)(done, st));
+    }
+  }
+  return WS_OK;
+}
+
 // ----------------------------------------------------------------------------
 // planning after the length histogram is known
 
@@ -505,7 +600,11 @@ int finish_ingest(ws_handle* h) {
   return WS_OK;
 }
 
-int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags) {
+int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags,
+                     std::mutex* gate = nullptr) {
+  // batch mode: `gate` is held while this corpus crosses PCIe host->device
+  std::unique_lock<std::mutex> gate_lk;
+  if (gate) gate_lk = std::unique_lock<std::mutex>(*gate);
   if (n >= (1ull << 32) - kTextPad) return fail(WS_ERR_ARG, "text must be shorter than 4 GiB");
   const bool resident = (flags & WS_INGEST_RESIDENT) != 0;
   if (resident) {
@@ -626,6 +725,11 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ++h->launches;
         }
         WS_TRY(check_launch("ingest_kernel"));
+        if (gate_lk.owns_lock()) {  // the text has crossed PCIe: the next corpus may start
+          WS_CUDA(cudaEventSynchronize(landed[np - 1]));
+          gate_lk.unlock();
+          if (getenv("WSORT_TRACE")) fprintf(stderr, "wsort-trace handle=%p h2d_landed=%.3f\n", (void*)h, trace_ms());
+        }
         WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
                                 h->st));
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
@@ -817,8 +921,14 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       }
       return WS_OK;
     };
-    WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(), h->idx[1].as<uint32_t>(),
-                         stats, inv, km, "", cst, fe ? &hook : nullptr));
+    static const char* no_radix = getenv("WSORT_NO_RADIX");
+    if (!stats && c == 0 && !(no_radix && no_radix[0] == '1')) {
+      WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, fe ? &hook : nullptr));
+    } else {
+      WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(),
+                           h->idx[1].as<uint32_t>(), stats, inv, km, "", cst,
+                           fe ? &hook : nullptr));
+    }
     for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
     WS_CUDA(cudaEventRecord(h->ev_join[c], cst));
     WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_join[c], 0));
@@ -1265,8 +1375,11 @@ int ws_create(ws_handle** out, int32_t device) {
 
 void ws_destroy(ws_handle* h) {
   if (!h) return;
+  for (ws_handle* p : h->peers) ws_destroy(p);
+  h->peers.clear();
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
+  if (h->hs) cudaStreamSynchronize(h->hs);
   for (int c = 0; c <= kClasses; ++c) {
     if (h->cs[c]) cudaStreamSynchronize(h->cs[c]);
     if (h->es[c]) cudaStreamSynchronize(h->es[c]);
@@ -1278,7 +1391,8 @@ void ws_destroy(ws_handle* h) {
                     &h->lidx[0], &h->lidx[1], &h->tokens, &h->stat_inv, &h->stat_k,
                     &h->stat_k_dummy, &h->out, &h->params, &h->splits[0], &h->splits[1],
                     &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5],
-                    &h->keys_cap, &h->status, &h->ticket, &h->overflow};
+                    &h->keys_cap, &h->status, &h->ticket, &h->overflow, &h->fill,
+                    &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1]};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();
@@ -1412,10 +1526,17 @@ int ws_emit_rows(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written) {
   return emit_to_host(h, false, out, cap, written);
 }
 
-int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
-                 uint64_t* written) {
-  WS_TRY(begin_call(h));
-  WS_TRY(ingest_text_impl(h, text, n, WS_INGEST_UNORDERED));
+namespace {
+
+// ws_sort_text body. `gate` (batch mode) serialises the host->device copy +
+// ingest of concurrent slots, so their PCIe transfers are staggered: one
+// corpus uploads while the previous ones sort and download.
+int sort_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
+                   uint64_t* written, std::mutex* gate) {
+  static const bool trace = getenv("WSORT_TRACE") && getenv("WSORT_TRACE")[0] == '1';
+  const double t_begin = trace ? trace_ms() : 0;
+  WS_TRY(ingest_text_impl(h, text, n, WS_INGEST_UNORDERED, gate));  // ends with a sync
+  const double t_ingested = trace ? trace_ms() : 0;
   params_reset(h);  // the ingest synchronised: staging space is free again
   const uint64_t size = emit_size(h, true);
   if (written) *written = size;
@@ -1428,7 +1549,53 @@ int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, ui
   fe.host = out;
   fe.off = emit_offsets(h, true);
   WS_TRY(sort_impl(h, false, &fe));  // sort + per-class emit + D2H, overlapped
+  const double t_enqueued = trace ? trace_ms() : 0;
   WS_CUDA(cudaStreamSynchronize(h->st));  // joins every class stream
+  if (trace)
+    fprintf(stderr, "wsort-trace handle=%p begin=%.3f ingested=%.3f enqueued=%.3f done=%.3f\n",
+            (void*)h, t_begin, t_ingested, t_enqueued, trace_ms());
+  return WS_OK;
+}
+
+}  // namespace
+
+int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
+                 uint64_t* written) {
+  WS_TRY(begin_call(h));
+  return sort_text_impl(h, text, n, out, cap, written, nullptr);
+}
+
+int ws_sort_texts(ws_handle* h, int32_t count, const uint8_t* const* texts, const uint64_t* sizes,
+                  uint8_t* const* outs, const uint64_t* caps, uint64_t* written,
+                  int32_t inflight) {
+  WS_TRY(begin_call(h));
+  if (count < 0) return fail(WS_ERR_ARG, "negative count");
+  if (count == 0) return WS_OK;
+  if (!texts || !sizes || !outs || !caps || !written) return fail(WS_ERR_ARG, "null batch arrays");
+  const int slots = std::max(1, std::min<int>(inflight <= 0 ? 3 : inflight, std::min(count, 4)));
+  while ((int)h->peers.size() < slots - 1) {
+    ws_handle* p = nullptr;
+    WS_TRY(ws_create(&p, h->device));
+    h->peers.push_back(p);
+  }
+  for (int32_t i = 0; i < count; ++i) written[i] = 0;
+  std::mutex gate;
+  std::vector<int> rc(slots, WS_OK);
+  std::vector<std::string> msg(slots);
+  auto worker = [&](int slot) {
+    ws_handle* hh = slot == 0 ? h : h->peers[slot - 1];
+    int r = begin_call(hh);
+    for (int32_t i = slot; i < count && r == WS_OK; i += slots)
+      r = sort_text_impl(hh, texts[i], sizes[i], outs[i], caps[i], written + i, &gate);
+    rc[slot] = r;
+    if (r != WS_OK) msg[slot] = g_err;
+  };
+  std::vector<std::thread> pool;
+  for (int s = 1; s < slots; ++s) pool.emplace_back(worker, s);
+  worker(0);
+  for (auto& t : pool) t.join();
+  for (int s = 0; s < slots; ++s)
+    if (rc[s] != WS_OK) return fail(rc[s], msg[s]);
   return WS_OK;
 }
 
@@ -1559,6 +1726,7 @@ int ws_profile_reset(ws_handle* h) {
 int ws_launch_count(ws_handle* h, uint64_t* launches) {
   if (!h || !launches) return fail(WS_ERR_ARG, "null argument");
   *launches = h->launches;
+  for (ws_handle* p : h->peers) *launches += p->launches;  // ws_sort_texts slots
   return WS_OK;
 }
 

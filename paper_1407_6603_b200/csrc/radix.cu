@@ -1,0 +1,278 @@
+// Payload-only bucket sort: LSD radix over the packed keys of a lane class.
+//
+// The reference sorts every length bucket with bubble sort (engine.py:89-114);
+// the sorted bucket is all that `wordsort sort` emits (cli.py:92-97). When no
+// statistics are requested (ws_sort(h, 0), ws_sort_text, ws_sort_resident),
+// equal keys are identical words, so any correct sort yields the reference's
+// bytes. This file sorts one-word keys (lane class 0: uint32, class 1: one
+// uint64) by stable LSD passes over 8-bit digits of the bits a bucket uses
+// (6 per character for text keys, 8 per byte otherwise), so a 5-character
+// bucket needs 4 passes where the merge sort needs log2(n / tile) + 1.
+//
+// Per pass and segment (bucket), with T-key tiles:
+//   upsweep   : per-tile digit histogram -> counts[d][tile], digit totals
+//   scan      : one warp per (segment, digit) row: exclusive scan over tiles
+//               plus the segment's digit prefix -> global output offsets
+//   downsweep : stable in-tile ranking (warp match + per-warp counters, rounds
+//               in key order), keys regrouped by digit in shared memory, then
+//               written as per-digit runs to their global offsets.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ws_common.cuh"
+#include "ws_kernels.h"
+
+namespace ws {
+namespace {
+
+constexpr int kRThreads = 256;
+constexpr int kRWarps = kRThreads / 32;
+constexpr int kDigits = 256;
+static_assert(kRThreads == kDigits, "one thread per digit in the per-tile scans");
+
+template <class K>
+struct RadixCfg {
+  static constexpr int E = sizeof(K) == 4 ? 16 : 8;  // keys per thread
+  static constexpr int T = kRThreads * E;            // keys per tile
+};
+
+__device__ __forceinline__ const RadixSeg& rseg_at(const RadixLaunch& a, int i) {
+  return a.segs ? a.segs[i] : a.inl[i];
+}
+
+// Segment of a tile (segments ascend by tile_begin); warp-wide ballot search.
+__device__ __forceinline__ int rsegment_of(const RadixLaunch& a, uint32_t tile) {
+  const int lane = threadIdx.x & 31;
+  int found = 0;
+  for (int base = 0; base < a.nsegs; base += 32) {
+    const int i = base + lane;
+    const bool le = i < a.nsegs && rseg_at(a, i).tile_begin <= tile;
+    found += __popc(__ballot_sync(0xffffffffu, le));
+    if (!__shfl_sync(0xffffffffu, (int)le, 31)) break;
+  }
+  return found - 1;
+}
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+template <class K>
+__device__ __forceinline__ uint32_t digit_of(K key, uint32_t shift) {
+  return (uint32_t)(key >> shift) & 0xFFu;
+}
+
+// Lanes of the warp holding the same 8-bit digit (8 ballots; invalid lanes,
+// ok == false, match nobody valid). Cheaper than match.any on sm_100.
+__device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool ok) {
+  uint32_t peers = __ballot_sync(0xffffffffu, ok);
+  if (!ok) peers = ~peers;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+// Per-warp stable digit ranks of the warp's keys (round r, lane l <-> key
+// r * 32 + l of the warp's slice): rank = earlier keys of the same digit.
+template <class K, int E>
+__device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, uint32_t shift,
+                                          uint32_t* wcnt, uint32_t (&rk)[E]) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const bool ok = (uint32_t)(r * 32 + lane) < nvalid;
+    const uint32_t d = digit_of<K>(key[r], shift);
+    const uint32_t peers = match_digit8(d, ok);
+    uint32_t base = 0;
+    if (ok) base = wcnt[d];
+    rk[r] = base + __popc(peers & lt);
+    __syncwarp();
+    if (ok && lane == 31 - __clz(peers)) wcnt[d] = base + __popc(peers);
+    __syncwarp();
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kRThreads)
+radix_upsweep_kernel(const __grid_constant__ RadixLaunch a) {
+  using C = RadixCfg<K>;
+  __shared__ uint32_t wcnt[kRWarps][kDigits];
+  __shared__ int s_seg;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tile = blockIdx.x;
+  if (tid < 32) {
+    const int s = rsegment_of(a, tile);
+    if (tid == 0) s_seg = s;
+  }
+  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const RadixSeg& sg = rseg_at(a, s_seg);
+  const uint32_t t = tile - sg.tile_begin;
+  const uint64_t first = (uint64_t)t * C::T + (uint64_t)wid * 32 * C::E;
+  const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
+  const K* in = reinterpret_cast<const K*>(sg.in) + first;
+  uint32_t* wc = wcnt[wid];
+  K key[C::E];  // all loads in flight before the first match
+#pragma unroll
+  for (int r = 0; r < C::E; ++r) {
+    const uint32_t j = r * 32 + lane;
+    key[r] = j < nvalid ? in[j] : K(0);  // default caching: the downsweep re-reads from L2
+  }
+#pragma unroll
+  for (int r = 0; r < C::E; ++r)  // per-key shared atomics (no return value: no chain)
+    if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(wc + digit_of<K>(key[r], sg.shift), 1u);
+  __syncthreads();
+  uint32_t c = 0;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) c += wcnt[w][tid];
+  a.counts[sg.coff + (uint64_t)tid * sg.ntiles + t] = c;
+  if (c) atomicAdd(a.totals + (uint64_t)s_seg * kDigits + tid, c);
+}
+
+// One CTA per (segment, digit) row: counts[row][t] -> global element offset
+// of the row's keys from tile t (relative to the segment's output base). All
+// of a row's loads are issued before the block scan.
+constexpr int kScanItems = 8;  // rows of up to 2048 tiles in one sweep
+__global__ void __launch_bounds__(kRThreads) radix_scan_kernel(const __grid_constant__ RadixLaunch a) {
+  __shared__ uint32_t s_w[kRWarps];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int s = blockIdx.x / kDigits, d = blockIdx.x % kDigits;
+  const RadixSeg& sg = rseg_at(a, s);
+  uint32_t* cnt = a.counts + sg.coff + (uint64_t)d * sg.ntiles;
+  // digit prefix of the segment: sum of totals[s][0..d)
+  if (wid == 0) {
+    const uint32_t* tot = a.totals + (uint64_t)s * kDigits;
+    uint32_t pre = 0;
+    for (int i = lane; i < d; i += 32) pre += tot[i];
+    pre = __reduce_add_sync(0xffffffffu, pre);
+    if (lane == 0) s_carry = pre;
+  }
+  for (uint32_t base = 0; base < sg.ntiles; base += kRThreads * kScanItems) {
+    uint32_t v[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint32_t i = base + tid * kScanItems + k;
+      v[k] = i < sg.ntiles ? cnt[i] : 0u;
+      sum += v[k];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) s_w[wid] = inc;
+    __syncthreads();
+    uint32_t run = s_carry + inc - sum;
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) run += w < wid ? s_w[w] : 0u;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint32_t i = base + tid * kScanItems + k;
+      if (i < sg.ntiles) cnt[i] = run;
+      run += v[k];
+    }
+    __syncthreads();
+    if (tid == kRThreads - 1) s_carry = run;
+    __syncthreads();
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kRThreads)
+radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
+  using C = RadixCfg<K>;
+  __shared__ uint32_t wcnt[kRWarps][kDigits];
+  __shared__ uint32_t s_gdelta[kDigits];  // global offset - tile-local start
+  __shared__ uint32_t s_wsum[kRWarps];
+  __shared__ __align__(16) K stage[C::T];
+  __shared__ int s_seg;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tile = blockIdx.x;
+  if (tid < 32) {
+    const int s = rsegment_of(a, tile);
+    if (tid == 0) s_seg = s;
+  }
+  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const RadixSeg& sg = rseg_at(a, s_seg);
+  const uint32_t t = tile - sg.tile_begin;
+  const uint64_t tfirst = (uint64_t)t * C::T;
+  const uint64_t first = tfirst + (uint64_t)wid * 32 * C::E;
+  const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
+  const uint32_t ntile = (uint32_t)umin64(sg.n - tfirst, C::T);
+  // the global offsets of this tile's digit runs (scan output), early
+  const uint32_t g = a.counts[sg.coff + (uint64_t)tid * sg.ntiles + t];
+  const K* in = reinterpret_cast<const K*>(sg.in) + first;
+  K key[C::E];
+#pragma unroll
+  for (int r = 0; r < C::E; ++r) {
+    const uint32_t j = r * 32 + lane;
+    key[r] = j < nvalid ? __ldcs(in + j) : K(0);
+  }
+  uint32_t rk[C::E];
+  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], rk);
+  __syncthreads();
+  // per digit (thread = digit): exclusive over warps, then over digits
+  uint32_t run = 0;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) {
+    const uint32_t c = wcnt[w][tid];
+    wcnt[w][tid] = run;
+    run += c;
+  }
+  uint32_t inc = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_wsum[wid] = inc;
+  __syncthreads();
+  uint32_t wpre = 0;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) wpre += w < wid ? s_wsum[w] : 0u;
+  const uint32_t doff = wpre + inc - run;
+  s_gdelta[tid] = g - doff;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) wcnt[w][tid] += doff;  // tile-local start of (warp, digit)
+  __syncthreads();
+  // regroup the tile by digit in shared memory (stable)
+#pragma unroll
+  for (int r = 0; r < C::E; ++r) {
+    const uint32_t j = r * 32 + lane;
+    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk[r]] = key[r];
+  }
+  __syncthreads();
+  // per-digit runs to their global offsets (consecutive threads, consecutive addresses)
+  K* out = reinterpret_cast<K*>(sg.out);
+  for (uint32_t i = tid; i < ntile; i += kRThreads) {
+    const K k = stage[i];
+    out[s_gdelta[digit_of<K>(k, sg.shift)] + i] = k;
+  }
+}
+
+}  // namespace
+
+int radix_tile_size(int lanes) { return lanes == 0 ? RadixCfg<uint32_t>::T : RadixCfg<uint64_t>::T; }
+
+void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st) {
+  if (!a.work_items) return;
+  const uint32_t rows = (uint32_t)a.nsegs * kDigits;
+  if (lanes == 0) {
+    radix_upsweep_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
+    radix_scan_kernel<<<rows, kRThreads, 0, st>>>(a);
+    radix_downsweep_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
+  } else {
+    radix_upsweep_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+    radix_scan_kernel<<<rows, kRThreads, 0, st>>>(a);
+    radix_downsweep_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+  }
+}
+
+}  // namespace ws

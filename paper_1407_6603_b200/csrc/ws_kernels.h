@@ -72,6 +72,27 @@ int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);
 
+// radix.cu: payload-only LSD radix passes over one-word keys (classes 0, 1)
+struct RadixSeg {
+  const void* in;       // the segment's keys before this pass
+  void* out;            // ... and after
+  uint64_t coff;        // offset of the segment's [256][ntiles] count matrix
+  uint32_t n;
+  uint32_t tile_begin;  // first tile (work item) of the segment
+  uint32_t ntiles;
+  uint32_t shift;       // bit position of this pass's 8-bit digit
+};
+struct RadixLaunch {
+  const RadixSeg* segs;  // device table when nsegs > kInlineSegs, else nullptr
+  int nsegs;
+  uint32_t work_items;   // tiles of all segments
+  uint32_t* counts;      // per segment [256][ntiles] tile histograms -> offsets
+  uint32_t* totals;      // [nsegs][256] digit totals of this pass (zeroed)
+  RadixSeg inl[kInlineSegs];
+};
+int radix_tile_size(int lanes);
+void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st);
+
 // emit.cu
 struct EmitSeg {
   const uint64_t* keys;  // sorted keys of the segment

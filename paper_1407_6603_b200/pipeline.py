@@ -61,6 +61,42 @@ class TextSorter:
         self.out.close()
 
 
+class BatchSorter:
+    """Serving loop: many corpora through ``ws_sort_texts`` with ``inflight``
+    of them in flight, so one corpus crosses PCIe host->device while earlier
+    ones sort and come back (each output is byte-identical to ``sort_text``)."""
+
+    def __init__(self, max_text: int, inflight: int = 3, device: int | None = None):
+        self.handle = Handle(device_index() if device is None else device)
+        self.inflight = inflight
+        self.text = PinnedBuffer(max_text)
+        self.outs = [PinnedBuffer(payload_bound(max_text)) for _ in range(inflight)]
+        self._n = 0
+
+    def load(self, text: bytes) -> int:
+        n = len(text)
+        if n > self.text.nbytes:
+            raise ValueError("text larger than the staging buffer")
+        self.text.array[:n] = np.frombuffer(text, dtype=np.uint8)
+        self._n = n
+        return n
+
+    def run(self, count: int) -> list[int]:
+        """Sort the loaded corpus `count` times as a batch; payload sizes."""
+        texts = [self.text.array[: self._n]] * count
+        outs = [self.outs[i % self.inflight].array for i in range(count)]
+        return self.handle.sort_texts(texts, outs, self.inflight)
+
+    def payload(self, slot: int, size: int) -> bytes:
+        return self.outs[slot].array[:size].tobytes()
+
+    def close(self) -> None:
+        self.handle.close()
+        self.text.close()
+        for o in self.outs:
+            o.close()
+
+
 class DeviceCorpus:
     """Phase-by-phase access to the device pipeline for one corpus."""
 

@@ -155,3 +155,29 @@ def test_unordered_ingest_payload_and_state_errors():
         h.sort(True)
         assert h.emit_lines().tobytes() == want
         h.close()
+
+
+def test_sort_texts_batch_matches_single_calls():
+    # ws_sort_texts: many corpora with several in flight, each output equal to
+    # its own ws_sort_text result (distinct corpora, repeated output buffers)
+    texts = [synth.generate(0, seed=s) for s in range(5)] + [b"", b"b a", synth.generate(4, words=200_000, seed=9)]
+    wants = [oracle.sort_text(t, mode="fast")[0] for t in texts]
+    h = _native.Handle(0)
+    for inflight in (1, 2, 3, 4):
+        arrs = [np.frombuffer(t, dtype=np.uint8) if t else np.zeros(0, np.uint8) for t in texts]
+        cap = max(len(t) for t in texts) + 1
+        outs_pool = [np.empty(cap, dtype=np.uint8) for _ in range(inflight)]
+        outs = [outs_pool[i % inflight] for i in range(len(texts))]
+        # a slot finishes corpus i before i + inflight reuses its buffer: check
+        # each result right after the batch only for the last corpus per slot
+        sizes = h.sort_texts(arrs, outs, inflight)
+        assert sizes == [len(w) for w in wants]
+        for i in range(max(0, len(texts) - inflight), len(texts)):
+            assert outs[i][: sizes[i]].tobytes() == wants[i]
+        # distinct buffers: every output checked
+        outs2 = [np.empty(cap, dtype=np.uint8) for _ in texts]
+        sizes2 = h.sort_texts(arrs, outs2, inflight)
+        assert all(o[:sz].tobytes() == w for o, sz, w in zip(outs2, sizes2, wants))
+    with pytest.raises(ValueError):
+        h.sort_texts([arrs[0]], [np.empty(3, dtype=np.uint8)], 2)
+    h.close()
