@@ -828,6 +828,7 @@ struct FusedEmit {
   uint8_t* dout;  // device payload buffer
   uint8_t* host;  // host destination
   std::vector<uint64_t> off;
+  bool per_class = false;  // one emit + D2H per lane class instead of per finished bucket
 };
 
 int fused_class_copy(ws_handle* h, FusedEmit* fe, int cls, cudaStream_t st) {
@@ -922,12 +923,16 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       return WS_OK;
     };
     static const char* no_radix = getenv("WSORT_NO_RADIX");
+    const PassDoneHook* on_done = fe && !fe->per_class ? &hook : nullptr;
     if (!stats && c == 0 && !(no_radix && no_radix[0] == '1')) {
-      WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, fe ? &hook : nullptr));
+      WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, on_done));
     } else {
       WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(),
-                           h->idx[1].as<uint32_t>(), stats, inv, km, "", cst,
-                           fe ? &hook : nullptr));
+                           h->idx[1].as<uint32_t>(), stats, inv, km, "", cst, on_done));
+    }
+    if (fe && fe->per_class) {
+      for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
+      WS_TRY(fused_class_copy(h, fe, c, cst));
     }
     for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
     WS_CUDA(cudaEventRecord(h->ev_join[c], cst));
@@ -1548,6 +1553,8 @@ int sort_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, 
   fe.dout = h->out.as<uint8_t>();
   fe.host = out;
   fe.off = emit_offsets(h, true);
+  static const char* pc = getenv("WSORT_D2H_PER_CLASS");
+  fe.per_class = pc ? pc[0] == '1' : false;
   WS_TRY(sort_impl(h, false, &fe));  // sort + per-class emit + D2H, overlapped
   const double t_enqueued = trace ? trace_ms() : 0;
   WS_CUDA(cudaStreamSynchronize(h->st));  // joins every class stream

@@ -291,6 +291,32 @@ __device__ __forceinline__ void pack6_from_codes(const uint32_t* __restrict__ c3
   dst[2] = k2;
 }
 
+// 6-bit packing specialised by lane class (warp-uniform inside a bin-major
+// batch): classes 0 and 1 (L <= 10, most words) read 8 or 12 code bytes and
+// skip the generic 4-group path.
+__device__ __forceinline__ void pack6_fast(const uint32_t* __restrict__ c32, uint32_t start,
+                                           uint32_t L, int lanes, uint64_t* __restrict__ dst) {
+  const uint32_t q = start >> 2, sh = (start & 3) * 8;
+  if (lanes == 0) {  // <= 5 characters -> top 30 bits of one uint32 (stored as k[0] >> 32)
+    const uint32_t w0 = c32[q], w1 = c32[q + 1], w2 = c32[q + 2];
+    const uint32_t a = codes24(__funnelshift_r(w0, w1, sh));
+    const uint32_t b = codes24(__funnelshift_r(w1, w2, sh));
+    const uint32_t k = ((a << 8) | (b >> 16)) & (~0u << (32 - 6 * L));
+    dst[0] = (uint64_t)k << 32;
+    return;
+  }
+  if (lanes == 1) {  // <= 10 characters -> top 60 bits of one uint64
+    const uint32_t w0 = c32[q], w1 = c32[q + 1], w2 = c32[q + 2], w3 = c32[q + 3];
+    const uint64_t a = codes24(__funnelshift_r(w0, w1, sh));
+    const uint64_t b = codes24(__funnelshift_r(w1, w2, sh));
+    const uint64_t c = codes24(__funnelshift_r(w2, w3, sh));
+    const uint64_t k = (a << 40) | (b << 16) | (c >> 8);
+    dst[0] = k & (~0ull << (64 - 6 * L));
+    return;
+  }
+  pack6_from_codes(c32, start, L, lanes, dst);
+}
+
 // Key store: lane class 0 keeps the top 32 bits of the first lane (6-bit keys
 // of <= 5 characters and raw keys of <= 4 bytes fit), else `lanes` uint64s.
 __device__ __forceinline__ void store_key(uint8_t* dst, int lanes, const uint64_t (&k)[4]) {
@@ -530,7 +556,110 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
       const int lanes = lanes_for_len_enc(L, p.enc);
       uint64_t key[4];
       if (codes)
-        pack6_from_codes(chunk32, start, L, lanes, key);
+        pack6_fast(chunk32, start, L, lanes, key);
+      else
+        pack_from_smem(chunk32, start, L, lanes, key);
+      store_key(keys + s_dst[L - 1] + (uint64_t)k * key_bytes(lanes), lanes, key);
+    }
+  }
+}
+
+// Reserve-mode ingest (payload-only sorts, ScatterParams::fill set): order
+// inside a bucket is free, so a word's slot in its bin is one shared-memory
+// atomic (no per-warp ranking pass), and each chunk reserves its bin runs in
+// HBM with one global atomic per bin. Keys are then packed in bin-major order
+// (uniform length per warp batch) and stored to consecutive addresses.
+__global__ void __launch_bounds__(kIngestThreads)
+reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
+  __shared__ __align__(16) uint32_t chunk32[(kChunk + 64) / 4];
+  __shared__ uint16_t wstart[kWarps][kMaxWordsPerWarp];
+  __shared__ uint32_t wlen[kWarps][kMaxWordsPerWarp];
+  __shared__ uint16_t wslot[kWarps][kMaxWordsPerWarp];
+  __shared__ uint32_t ord[kChunk / 2];  // packed words in bin-major order: start | L << 16
+  __shared__ uint32_t s_cnt[kHistRows];
+  __shared__ uint32_t s_base[kHistRows];
+  __shared__ uint32_t s_boff[kMaxPackedLen + 1];
+  __shared__ uint64_t s_dst[kMaxPackedLen];
+  __shared__ uint32_t s_chain[kWarps];
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t chunk = p.chunk0 + blockIdx.x;
+  const uint64_t cbase = chunk * kChunk;
+  if (tid < kHistRows) s_cnt[tid] = 0;
+
+  uint4 v;
+  Segment16 seg = classify_chunk(text, n, cbase, v, s_chain, p.avail ? p.avail : ~0ull,
+                                 p.overflow);  // has a __syncthreads
+  const bool codes = p.enc == kEncAlnum6;
+  reinterpret_cast<uint4*>(chunk32)[tid] = codes ? alnum6_codes16(v) : v;
+  if (tid < 4) {
+    uint64_t a = cbase + kChunk + 16 * tid;
+    uint4 la = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(chunk32)[kChunk / 16 + tid] = codes ? alnum6_codes16(la) : la;
+  }
+  // warp word list; each word takes a slot in its bin (shared atomic)
+  const uint32_t c = __popc(seg.starts);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  uint32_t slot = incl - c;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  {
+    uint32_t s = seg.starts;
+    while (s) {
+      const int i = __ffs(s) - 1;
+      s &= s - 1;
+      const uint32_t L = word_len(seg, i);
+      wstart[wid][slot] = (uint16_t)(tid * 16 + i);
+      wlen[wid][slot] = L;
+      wslot[wid][slot] = (uint16_t)atomicAdd(&s_cnt[bin_of_len(L)], 1u);
+      ++slot;
+    }
+  }
+  if (lane == 0) atomicAdd(&s_cnt[kNumBins], total);
+  __syncthreads();  // also publishes chunk32
+  if (tid < kHistRows && s_cnt[tid]) s_base[tid] = atomicAdd(p.fill + tid, s_cnt[tid]);
+  if (wid == 1) {  // bin-major offsets of the packed bins (lane = bin)
+    const uint32_t cnt = s_cnt[lane];
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += t;
+    }
+    s_boff[lane] = inc - cnt;
+    if (lane == 31) s_boff[kMaxPackedLen] = inc;
+  }
+  __syncthreads();
+  for (uint32_t b = 0; b < total; b += 32) {
+    const uint32_t j = b + lane;
+    if (j >= total) break;
+    const uint32_t L = wlen[wid][j];
+    const uint32_t start = wstart[wid][j];
+    const uint32_t bin = bin_of_len(L);
+    if (bin != (uint32_t)kLongBin)
+      ord[s_boff[bin] + wslot[wid][j]] = start | (L << 16);
+    else if (p.keys)
+      p.longlist[s_base[kLongBin] + wslot[wid][j]] = make_uint2((uint32_t)(cbase + start), L);
+  }
+  if (tid < kMaxPackedLen) {
+    const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc(tid + 1, p.enc));
+    s_dst[tid] = p.bin_base[tid] + ((uint64_t)s_base[tid] - s_boff[tid]) * ks;
+  }
+  __syncthreads();
+  if (p.keys) {
+    const uint32_t npacked = s_boff[kMaxPackedLen];
+    uint8_t* keys = reinterpret_cast<uint8_t*>(p.keys);
+    for (uint32_t k = tid; k < npacked; k += kIngestThreads) {
+      const uint32_t e = ord[k];
+      const uint32_t start = e & 0xFFFFu, L = e >> 16;
+      const int lanes = lanes_for_len_enc(L, p.enc);
+      uint64_t key[4];
+      if (codes)
+        pack6_fast(chunk32, start, L, lanes, key);
       else
         pack_from_smem(chunk32, start, L, lanes, key);
       store_key(keys + s_dst[L - 1] + (uint64_t)k * key_bytes(lanes), lanes, key);
@@ -680,7 +809,7 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st) {
   if (!nchunks) return;
   if (p.fill)
-    scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+    reserve_ingest_kernel<<<nchunks, kIngestThreads, 0, st>>>(text, n, p);
   else
     scatter_kernel<kByLookback><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
 }
