@@ -247,11 +247,15 @@ __device__ __forceinline__ void merge_path(const KW<LANES>* __restrict__ A, int 
                                            const uint32_t* __restrict__ IB, int diag,
                                            int64_t a_rem_base, Key<LANES> (&r)[E],
                                            uint32_t (&ri)[E], uint64_t& inv) {
-  int lo = max(0, diag - nb), hi = min(diag, na);
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (key_le<LANES>(ldk<LANES>(A, mid), ldk<LANES>(B, diag - 1 - mid))) lo = mid + 1;
-    else hi = mid;
+  // lower bound of the diagonal: the range halves the same way whichever side
+  // wins, so lanes stay converged; the body is predicated selects
+  int lo = max(0, diag - nb);
+  int len = min(diag, na) - lo;
+  while (len > 0) {
+    const int half = len >> 1, mid = lo + half;
+    const bool p = key_le<LANES>(ldk<LANES>(A, mid), ldk<LANES>(B, diag - 1 - mid));
+    lo = p ? mid + 1 : lo;
+    len = p ? len - half - 1 : half;
   }
   int ai = lo, bi = diag - lo;
   const Key<LANES> kmax = key_max<LANES>();
@@ -262,32 +266,31 @@ __device__ __forceinline__ void merge_path(const KW<LANES>* __restrict__ A, int 
     ia = ai < na ? IA[ai] : 0u;
     ib = bi < nb ? IB[bi] : 0u;
   }
+  // branch-free merge: take one side, advance it, reload only that side
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const bool ta = (bi >= nb) || (ai < na && key_le<LANES>(ka, kb));
-    if (ta) {
-      r[k] = ka;
-      if (STATS) ri[k] = ia;
-      ++ai;
-      if (ai < na) {
-        ka = ldk<LANES>(A, ai);
-        if (STATS) ia = IA[ai];
-      } else {
-        ka = kmax;
-      }
-    } else {
-      r[k] = kb;
-      if (STATS) {
-        ri[k] = ib;
-        inv += (uint64_t)(a_rem_base - ai);
-      }
-      ++bi;
-      if (bi < nb) {
-        kb = ldk<LANES>(B, bi);
-        if (STATS) ib = IB[bi];
-      } else {
-        kb = kmax;
-      }
+#pragma unroll
+    for (int l = 0; l < KeyTraits<LANES>::NW; ++l) r[k].w[l] = ta ? ka.w[l] : kb.w[l];
+    if (STATS) {
+      ri[k] = ta ? ia : ib;
+      inv += ta ? 0ull : (uint64_t)(a_rem_base - ai);
+    }
+    ai += ta ? 1 : 0;
+    bi += ta ? 0 : 1;
+    const int nx = ta ? ai : bi;
+    const bool ok = ta ? ai < na : bi < nb;
+    const KW<LANES>* src = ta ? A : B;
+    const Key<LANES> nk = ok ? ldk<LANES>(src, nx) : kmax;
+#pragma unroll
+    for (int l = 0; l < KeyTraits<LANES>::NW; ++l) {
+      ka.w[l] = ta ? nk.w[l] : ka.w[l];
+      kb.w[l] = ta ? kb.w[l] : nk.w[l];
+    }
+    if (STATS) {
+      const uint32_t ni = ok ? (ta ? IA : IB)[nx] : 0u;
+      ia = ta ? ni : ia;
+      ib = ta ? ib : ni;
     }
   }
 }

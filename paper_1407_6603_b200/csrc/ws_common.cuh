@@ -100,13 +100,17 @@ struct Key {
   typename KeyTraits<LANES>::W w[KeyTraits<LANES>::NW];
 };
 
+// Branch-free lexicographic compares over the key words (no divergence when
+// lanes of a warp decide at different words).
 template <int LANES>
 __device__ __forceinline__ bool key_lt(const Key<LANES>& a, const Key<LANES>& b) {
+  bool lt = a.w[0] < b.w[0], eq = a.w[0] == b.w[0];
 #pragma unroll
-  for (int i = 0; i < KeyTraits<LANES>::NW; ++i) {
-    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i];
+  for (int i = 1; i < KeyTraits<LANES>::NW; ++i) {
+    lt = lt | (eq & (a.w[i] < b.w[i]));
+    eq = eq & (a.w[i] == b.w[i]);
   }
-  return false;
+  return lt;
 }
 
 template <int LANES>

@@ -3,9 +3,9 @@ report (needs -lineinfo): python tools/ncu_lines.py REP KERNEL_REGEX [TOP]."""
 import csv, subprocess, sys, collections
 
 
-def main(rep, kernel, top=40):
+def main(rep, kernel, top=40, skip=0):
     out = subprocess.run(['ncu', '-i', rep, '--page', 'source', '--csv', '--print-source', 'cuda,sass',
-                          '--kernel-name', 'regex:' + kernel, '--launch-count', '1'],
+                          '--kernel-name', 'regex:' + kernel, '--launch-skip', str(skip), '--launch-count', '1'],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     agg = collections.defaultdict(lambda: [0, 0])
