@@ -73,6 +73,7 @@ __device__ __forceinline__ Segment16 classify_chunk(const uint8_t* __restrict__ 
                                                     uint32_t* s_chain /*[kWarps]*/,
                                                     uint64_t avail = ~0ull,
                                                     unsigned int* overflow = nullptr) {
+  __shared__ uint32_t s_edge[2 * kWarps];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t base = cbase + (uint64_t)tid * 16;
   uint4 v = make_uint4(0, 0, 0, 0);
@@ -81,12 +82,13 @@ __device__ __forceinline__ Segment16 classify_chunk(const uint8_t* __restrict__ 
   const uint32_t m = alnum_mask16(v);
   const uint32_t up = __shfl_up_sync(0xffffffffu, m, 1);
   const uint32_t dn = __shfl_down_sync(0xffffffffu, m, 1);
-  uint32_t prev = (up >> 15) & 1u, next = dn & 1u;
-  if (lane == 0) prev = (base > 0 && base - 1 < n) ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
-  if (lane == 31) next = (base + 16 < n) ? (uint32_t)is_alnum_byte(text[base + 16]) : 0u;
-  Segment16 s;
-  s.starts = m & ~((m << 1) | prev) & 0xFFFFu;
-  s.ends = m & ~((m >> 1) | (next << 15)) & 0xFFFFu;
+  // warp-edge neighbours come from the adjacent warps' masks (shared memory,
+  // after the barrier below); only the chunk's two outer edges read a byte
+  uint32_t edge = 0;
+  if (wid == 0 && lane == 0)
+    edge = (base > 0 && base - 1 < n) ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
+  if (wid == kWarps - 1 && lane == 31)
+    edge = (base + 16 < n) ? (uint32_t)is_alnum_byte(text[base + 16]) : 0u;
   // chain (V, F): alnum run from this segment's byte 0 rightwards; F = ended in the warp
   uint32_t V = (uint32_t)__ffs(~m) - 1;  // leading alnum bytes (16 when m == 0xFFFF)
   uint32_t F = V < 16;
@@ -100,10 +102,18 @@ __device__ __forceinline__ Segment16 classify_chunk(const uint8_t* __restrict__ 
     }
   }
   if (lane == 0) s_chain[wid] = V | (F << 31);
+  if (lane == 0) s_edge[2 * wid] = m & 1u;                 // first byte of the warp
+  if (lane == 31) s_edge[2 * wid + 1] = (m >> 15) & 1u;    // last byte of the warp
   uint32_t cV = __shfl_down_sync(0xffffffffu, V, 1);
   uint32_t cF = __shfl_down_sync(0xffffffffu, F, 1);
   if (lane == 31) cV = cF = 0;
   __syncthreads();
+  uint32_t prev = (up >> 15) & 1u, next = dn & 1u;
+  if (lane == 0) prev = wid == 0 ? edge : s_edge[2 * wid - 1];
+  if (lane == 31) next = wid == kWarps - 1 ? edge : s_edge[2 * wid + 2];
+  Segment16 s;
+  s.starts = m & ~((m << 1) | prev) & 0xFFFFu;
+  s.ends = m & ~((m >> 1) | (next << 15)) & 0xFFFFu;
   // only a segment whose last word is open needs its continuation
   const bool open = s.starts && !(s.ends >> (31 - __clz(s.starts)));  // last start has no end
   if (open && !cF) {
@@ -572,11 +582,9 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
 __global__ void __launch_bounds__(kIngestThreads)
 reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
   __shared__ __align__(16) uint32_t chunk32[(kChunk + 64) / 4];
-  __shared__ uint16_t wstart[kWarps][kMaxWordsPerWarp];
-  __shared__ uint32_t wlen[kWarps][kMaxWordsPerWarp];
-  __shared__ uint16_t wslot[kWarps][kMaxWordsPerWarp];
   __shared__ uint32_t ord[kChunk / 2];  // packed words in bin-major order: start | L << 16
   __shared__ uint32_t s_cnt[kHistRows];
+  __shared__ uint32_t s_cur[kNumBins];  // per-bin cursors into ord (long bin: into its run)
   __shared__ uint32_t s_base[kHistRows];
   __shared__ uint32_t s_boff[kMaxPackedLen + 1];
   __shared__ uint64_t s_dst[kMaxPackedLen];
@@ -597,32 +605,14 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
     uint4 la = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4*>(chunk32)[kChunk / 16 + tid] = codes ? alnum6_codes16(la) : la;
   }
-  // warp word list; each word takes a slot in its bin (shared atomic)
-  const uint32_t c = __popc(seg.starts);
-  uint32_t incl = c;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += t;
-  }
-  uint32_t slot = incl - c;
-  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  {
-    uint32_t s = seg.starts;
-    while (s) {
-      const int i = __ffs(s) - 1;
-      s &= s - 1;
-      const uint32_t L = word_len(seg, i);
-      wstart[wid][slot] = (uint16_t)(tid * 16 + i);
-      wlen[wid][slot] = L;
-      wslot[wid][slot] = (uint16_t)atomicAdd(&s_cnt[bin_of_len(L)], 1u);
-      ++slot;
-    }
-  }
-  if (lane == 0) atomicAdd(&s_cnt[kNumBins], total);
+  // count the chunk's words per bin (no return value, nothing kept)
+  for (uint32_t s = seg.starts; s; s &= s - 1)
+    atomicAdd(&s_cnt[bin_of_len(word_len(seg, __ffs(s) - 1))], 1u);
+  const uint32_t words = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(seg.starts));
+  if (lane == 0 && words) atomicAdd(&s_cnt[kNumBins], words);
   __syncthreads();  // also publishes chunk32
   if (tid < kHistRows && s_cnt[tid]) s_base[tid] = atomicAdd(p.fill + tid, s_cnt[tid]);
-  if (wid == 1) {  // bin-major offsets of the packed bins (lane = bin)
+  if (wid == 1) {  // bin-major offsets of the packed bins (lane = bin) = their cursors
     const uint32_t cnt = s_cnt[lane];
     uint32_t inc = cnt;
 #pragma unroll
@@ -631,19 +621,23 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
       if (lane >= d) inc += t;
     }
     s_boff[lane] = inc - cnt;
-    if (lane == 31) s_boff[kMaxPackedLen] = inc;
+    s_cur[lane] = inc - cnt;
+    if (lane == 31) {
+      s_boff[kMaxPackedLen] = inc;
+      s_cur[kLongBin] = 0;
+    }
   }
   __syncthreads();
-  for (uint32_t b = 0; b < total; b += 32) {
-    const uint32_t j = b + lane;
-    if (j >= total) break;
-    const uint32_t L = wlen[wid][j];
-    const uint32_t start = wstart[wid][j];
-    const uint32_t bin = bin_of_len(L);
+  // place every word: packed ones into ord (bin-major), long ones into their run
+  for (uint32_t s = seg.starts; s; s &= s - 1) {
+    const int i = __ffs(s) - 1;
+    const uint32_t L = word_len(seg, i), bin = bin_of_len(L);
+    const uint32_t at = atomicAdd(&s_cur[bin], 1u);
+    const uint32_t start = (uint32_t)(tid * 16 + i);
     if (bin != (uint32_t)kLongBin)
-      ord[s_boff[bin] + wslot[wid][j]] = start | (L << 16);
+      ord[at] = start | (L << 16);
     else if (p.keys)
-      p.longlist[s_base[kLongBin] + wslot[wid][j]] = make_uint2((uint32_t)(cbase + start), L);
+      p.longlist[s_base[kLongBin] + at] = make_uint2((uint32_t)(cbase + start), L);
   }
   if (tid < kMaxPackedLen) {
     const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc(tid + 1, p.enc));
