@@ -697,7 +697,10 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         WS_CUDA(cudaMemsetAsync(h->overflow.p, 0, 4, h->st));
         p.overflow = h->overflow.as<unsigned int>();
         const uint64_t cb = ingest_chunk_bytes();
-        const int P = (int)std::min<uint64_t>(16, std::max<uint64_t>(2, n / (8ull << 20)));
+        // pieces of >= 8 MB let the ingest start before the whole text has
+        // landed; in batch mode (gate) other corpora fill that gap, and one
+        // copy keeps PCIe faster while the device->host direction is busy
+        const int P = gate ? 1 : (int)std::min<uint64_t>(16, std::max<uint64_t>(2, n / (8ull << 20)));
         const uint64_t piece = (n / P + cb - 1) / cb * cb;
         std::vector<uint64_t> edge;  // piece boundaries (bytes)
         for (uint64_t o = 0; o < n; o += piece) edge.push_back(o);
