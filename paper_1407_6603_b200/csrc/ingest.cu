@@ -413,10 +413,9 @@ __device__ __forceinline__ void resolve_prefix_warp(uint32_t* __restrict__ statu
 // layout. kByLookback: CTAs take chunks in ticket order, chain their
 // per-bin offsets through a decoupled look-back and write into
 // capacity-bounded per-length regions (no count pass, no host round trip
-// before the scatter); the last chunk publishes the totals. kByReserve: like
-// kByLookback, but every chunk reserves its runs with one atomicAdd per bin
-// (no dependence between chunks; bucket order = chunk completion order).
-enum ScatterMode : int { kByScan = 0, kByLookback = 1, kByReserve = 2 };
+// before the scatter); the last chunk publishes the totals. (Payload-only
+// ingests use reserve_ingest_kernel below instead.)
+enum ScatterMode : int { kByScan = 0, kByLookback = 1 };
 template <int MODE>
 __global__ void __launch_bounds__(kIngestThreads)
 scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __restrict__ off,
@@ -502,11 +501,9 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     s_run[tid] = run;
   }
   __syncthreads();
-  // chunk offsets: one atomic per bin (reserve), or the decoupled look-back
-  // (warp 0, publishing the aggregate first); the other warps meanwhile
-  // scan the bins and build the bin-major word order
-  if (MODE == kByReserve && tid < kHistRows && s_run[tid])
-    s_base[tid] = atomicAdd(p.fill + tid, s_run[tid]);
+  // chunk offsets: the decoupled look-back (warp 0, publishing the aggregate
+  // first); the other warps meanwhile scan the bins and build the bin-major
+  // word order
   if (LOOKBACK && wid == 0) {
     publish_record(p.status, (uint32_t)chunk, s_run, chunk == 0 ? kRecIncl : kRecAgg,
                    chunk == 0 ? 2u : 1u);
