@@ -352,6 +352,31 @@ def bench_ours(args) -> None:
         torch.cuda.synchronize(dev)
         batch_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         batch_launches = bs.handle.launch_count() - batch_launches0
+
+        # ---- stats leg: the reference's full SortStats semantics on the
+        # device (order-preserving ingest, merge sort with inversion / K
+        # counts, per-bucket stats read back), text already in HBM
+        dtext = torch.frombuffer(bytearray(text), dtype=torch.uint8).to(dev)
+        hsx = Handle(local)
+        sstream = torch.cuda.ExternalStream(hsx.stream(), device=dev)
+        for _ in range(args.warmup):
+            hsx.ingest_text(None, device_ptr=dtext.data_ptr(), n=n)
+            hsx.sort(True)
+            hsx.bucket_stats(True)
+        stats_ms = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(sstream):
+                flush.zero_()
+            torch.cuda.synchronize(dev)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(sstream)
+            hsx.ingest_text(None, device_ptr=dtext.data_ptr(), n=n)
+            hsx.sort(True)
+            hsx.bucket_stats(True)
+            b.record(sstream)
+            torch.cuda.synchronize(dev)
+            stats_ms.append(a.elapsed_time(b))
     clocks = sampler.summary()
     # one extra (untimed) e2e step with per-phase events, for the timeline
     ts.handle.profile(reset=True)
@@ -364,6 +389,7 @@ def bench_ours(args) -> None:
     t_dev = max_over_ranks(statistics.mean(dev_ms))
     t_e2e = max_over_ranks(statistics.mean(e2e_ms))
     t_batch = max_over_ranks(batch_ms)
+    t_stats = max_over_ranks(statistics.mean(stats_ms))
     value = world * words / (t_dev * 1e-3)
     e2e_value = world * words / (t_e2e * 1e-3)
     batch_value = world * words / (t_batch * 1e-3)
@@ -436,6 +462,11 @@ def bench_ours(args) -> None:
                     "single": {"value": e2e_value, "ms_per_step": t_e2e,
                                "gpu_launches": e2e_launches,
                                "api": "ws_sort_text, one corpus per call, CUDA events"}},
+            "stats_mode": {"value": world * words / (t_stats * 1e-3), "unit": UNIT,
+                           "ms_per_step": t_stats,
+                           "api": "ws_ingest_text(DEVICE_PTR) + ws_sort(h, 1) + ws_bucket_stats: "
+                                  "corpus-order buckets, merge sort counting inversions and K, "
+                                  "the reference's SortStats per bucket"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,
@@ -453,6 +484,7 @@ def bench_ours(args) -> None:
         print(json.dumps(line), flush=True)
     ts.close()
     bs.close()
+    hsx.close()
     h.close()
     if world > 1:
         torch.distributed.destroy_process_group()
