@@ -164,6 +164,7 @@ struct ws_handle {
   DevBuf keys[2], idx[2];
   DevBuf keys_cap, status, ticket;  // single-pass ingest: capacity-bounded regions
   DevBuf fill;                      // reserve-mode counters (WS_INGEST_UNORDERED)
+  DevBuf run_at, run_cnt, run_off, longlist2;  // ordered reserve mode: runs to reorder
   DevBuf longlist, longgrp, rank, rank_tmp, lkeys[2], lidx[2];
   DevBuf tokens;
   DevBuf stat_inv, stat_k, stat_k_dummy;
@@ -665,8 +666,21 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     WS_CUDA(h->keys_cap.ensure(run + 256));
     WS_CUDA(h->longlist.ensure(((n + 1) / (kMaxPackedLen + 2) + 1) * sizeof(uint2)));
     if (keep_tokens) WS_CUDA(h->tokens.ensure(((n + 1) / 2 + 1) * sizeof(uint2)));
+    // chunk placement: payload-only -> reserve (any order); ordered without
+    // tokens -> reserve + runs reordered into corpus order afterwards;
+    // tokens (their global word index needs every predecessor) -> look-back
     const bool reserve = (flags & WS_INGEST_UNORDERED) && !keep_tokens;
-    if (!reserve) WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kLookbackRec * 4));
+    static const char* lb_env = getenv("WSORT_LOOKBACK");
+    const bool ordered_reserve = !reserve && !keep_tokens && !(lb_env && lb_env[0] == '1');
+    const bool lookback = !reserve && !ordered_reserve;
+    if (lookback) WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kLookbackRec * 4));
+    if (ordered_reserve) {
+      const size_t tb = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
+      WS_CUDA(h->run_at.ensure(tb));
+      WS_CUDA(h->run_cnt.ensure(tb));
+      WS_CUDA(h->run_off.ensure(tb));
+      WS_CUDA(h->longlist2.ensure(((n + 1) / (kMaxPackedLen + 2) + 1) * sizeof(uint2)));
+    }
     WS_CUDA(h->ticket.ensure(256));
     WS_CUDA(h->fill.ensure(kHistRows * 4));
     for (int b = 0; b < kMaxPackedLen; ++b) p.bin_base[b] = region[b];
@@ -678,10 +692,12 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     p.ticket = h->ticket.as<unsigned int>();
     p.status = h->status.as<uint32_t>();
     p.totals = h->totals.as<uint32_t>();
-    p.fill = reserve ? h->fill.as<uint32_t>() : nullptr;
-    const void* totals_src = reserve ? h->fill.p : h->totals.p;
+    p.fill = lookback ? nullptr : h->fill.as<uint32_t>();
+    p.run_at = ordered_reserve ? h->run_at.as<uint32_t>() : nullptr;
+    p.run_cnt = ordered_reserve ? h->run_cnt.as<uint32_t>() : nullptr;
+    const void* totals_src = lookback ? h->totals.p : h->fill.p;
     auto reset_chain = [&]() -> int {
-      if (reserve) {
+      if (!lookback) {
         WS_CUDA(cudaMemsetAsync(h->fill.p, 0, kHistRows * 4, h->st));
       } else {
         WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
@@ -722,7 +738,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ScatterParams pi = p;
           pi.avail = need == np - 1 ? 0 : edge[need + 1];
           const uint32_t c0 = (uint32_t)(edge[i] / cb), c1 = (uint32_t)((edge[i + 1] + cb - 1) / cb);
-          pi.chunk0 = reserve ? c0 : 0;  // look-back numbers chunks by its global ticket
+          pi.chunk0 = lookback ? 0 : c0;  // look-back numbers chunks by its global ticket
           Phase ph(h, "ingest", 2.27 * (double)(edge[i + 1] - edge[i]));
           launch_ingest_lookback(dtext, n, c1 - c0, pi, h->st);
           ++h->launches;
@@ -762,9 +778,39 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     total_words = tot_host[kNumBins];
     m = counts[kLongBin];
     WS_TRY(plan_packed(h, counts));  // compact layout of the sort buffers
-    for (auto& bk : h->buckets)
-      if (!bk.is_long)
-        bk.in_ptr = reinterpret_cast<const uint64_t*>(h->keys_cap.as<uint8_t>() + region[bk.len - 1]);
+    if (ordered_reserve && nchunks) {
+      // corpus order: runs of every (bin, chunk) move from their reserved place
+      // to the exclusive prefix of their bin over chunks, in the compact layout
+      launch_scan(h->run_cnt.as<uint32_t>(), h->run_off.as<uint32_t>(), h->totals.as<uint32_t>(),
+                  nchunks, kNumBins, h->st);
+      ReorderParams r;
+      memset(&r, 0, sizeof r);
+      r.nchunks = nchunks;
+      r.run_at = h->run_at.as<uint32_t>();
+      r.run_cnt = h->run_cnt.as<uint32_t>();
+      r.run_off = h->run_off.as<uint32_t>();
+      for (const auto& bk : h->buckets) {
+        const int b = (int)bk.len - 1;
+        r.src[b] = h->keys_cap.as<uint8_t>() + region[b];
+        r.dst[b] = reinterpret_cast<uint8_t*>(class_keys(h, 0, bk.lanes, bk.elem_off));
+        r.key_bytes[b] = (uint32_t)key_bytes(bk.lanes);
+      }
+      r.src[kLongBin] = h->longlist.as<uint8_t>();
+      r.dst[kLongBin] = h->longlist2.as<uint8_t>();
+      r.key_bytes[kLongBin] = sizeof(uint2);
+      {
+        Phase ph(h, "reorder", 2.0 * (double)(h->class_base[kClasses] + h->class_elems[kClasses] * key_bytes(kClasses)));
+        launch_reorder_runs(r, h->st);
+        h->launches += 2;
+      }
+      WS_TRY(check_launch("reorder_runs"));
+      std::swap(h->longlist, h->longlist2);  // the long list is now in corpus order
+    } else {
+      for (auto& bk : h->buckets)
+        if (!bk.is_long)
+          bk.in_ptr =
+              reinterpret_cast<const uint64_t*>(h->keys_cap.as<uint8_t>() + region[bk.len - 1]);
+    }
     if (keep_tokens) h->have_tokens = true;
     h->unordered = reserve;
   } else {
@@ -1400,6 +1446,7 @@ void ws_destroy(ws_handle* h) {
                     &h->stat_k_dummy, &h->out, &h->params, &h->splits[0], &h->splits[1],
                     &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5],
                     &h->keys_cap, &h->status, &h->ticket, &h->overflow, &h->fill,
+                    &h->run_at, &h->run_cnt, &h->run_off, &h->longlist2,
                     &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1]};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();

@@ -413,9 +413,12 @@ __device__ __forceinline__ void resolve_prefix_warp(uint32_t* __restrict__ statu
 // layout. kByLookback: CTAs take chunks in ticket order, chain their
 // per-bin offsets through a decoupled look-back and write into
 // capacity-bounded per-length regions (no count pass, no host round trip
-// before the scatter); the last chunk publishes the totals. (Payload-only
-// ingests use reserve_ingest_kernel below instead.)
-enum ScatterMode : int { kByScan = 0, kByLookback = 1 };
+// before the scatter); the last chunk publishes the totals. kByReserve: the
+// same stable in-chunk order, but each chunk reserves its bin runs with one
+// atomic per bin and records (position, count) per (bin, chunk); a scan over
+// chunks and reorder_runs_kernel then move the runs into corpus order (no
+// chain between chunks). (Payload-only ingests use reserve_ingest_kernel.)
+enum ScatterMode : int { kByScan = 0, kByLookback = 1, kByReserve = 2 };
 template <int MODE>
 __global__ void __launch_bounds__(kIngestThreads)
 scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __restrict__ off,
@@ -501,6 +504,13 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     s_run[tid] = run;
   }
   __syncthreads();
+  if (MODE == kByReserve && tid < kHistRows) {  // reserve the runs, record them for the reorder
+    const uint32_t cnt = s_run[tid];
+    const uint32_t at = cnt ? atomicAdd(p.fill + tid, cnt) : 0u;
+    s_base[tid] = at;
+    p.run_at[(uint64_t)tid * p.nchunks_total + chunk] = at;
+    p.run_cnt[(uint64_t)tid * p.nchunks_total + chunk] = cnt;
+  }
   // chunk offsets: the decoupled look-back (warp 0, publishing the aggregate
   // first); the other warps meanwhile scan the bins and build the bin-major
   // word order
@@ -658,6 +668,27 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
   }
 }
 
+// kByReserve follow-up: one CTA per chunk, one warp per bin run at a time:
+// copy the run's keys from their reserved place (ingest region of the bin)
+// to their corpus-order place (run_off = exclusive scan of run_cnt over
+// chunks) in the destination layout; long-word entries likewise.
+__global__ void __launch_bounds__(kIngestThreads)
+reorder_runs_kernel(ReorderParams r) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t chunk = blockIdx.x;
+  for (int bin = wid; bin < kNumBins; bin += kWarps) {
+    const uint64_t cell = (uint64_t)bin * r.nchunks + chunk;
+    const uint32_t cnt = r.run_cnt[cell];
+    if (!cnt) continue;
+    const uint32_t from = r.run_at[cell], to = r.run_off[cell];
+    const uint32_t ks = r.key_bytes[bin];  // 4, 8, 16, 24 (keys) or 8 (long-word entries)
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(r.src[bin] + (uint64_t)from * ks);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(r.dst[bin] + (uint64_t)to * ks);
+    const uint32_t words = cnt * (ks >> 2);
+    for (uint32_t i = lane; i < words; i += 32) dst[i] = src[i];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Word-list ingest (build_flat from a Python list): words are given as one
 // concatenated byte buffer + lengths. starts = exclusive scan of lengths is
@@ -799,13 +830,19 @@ void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32
 void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st) {
   if (!nchunks) return;
-  if (p.fill)
+  if (p.fill && p.run_at)
+    scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+  else if (p.fill)
     reserve_ingest_kernel<<<nchunks, kIngestThreads, 0, st>>>(text, n, p);
   else
     scatter_kernel<kByLookback><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }
+
+void launch_reorder_runs(const ReorderParams& r, cudaStream_t st) {
+  if (r.nchunks) reorder_runs_kernel<<<r.nchunks, kIngestThreads, 0, st>>>(r);
+}
 
 uint32_t chunk_count(uint64_t n) { return (uint32_t)((n + kChunk - 1) / kChunk); }
 

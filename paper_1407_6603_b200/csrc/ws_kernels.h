@@ -27,7 +27,22 @@ struct ScatterParams {
   // runs then land in completion order, so bucket order is not corpus order
   // (stats / permutations / tokens need the look-back). fill[] ends as totals.
   uint32_t* fill;               // [kHistRows] zeroed reservation counters, or nullptr
+  // ordered reserve mode (fill and run_at set): stable order inside a chunk,
+  // runs recorded per (bin, chunk) for the reorder into corpus order
+  uint32_t* run_at;             // [kHistRows][nchunks_total] reserved start of the run
+  uint32_t* run_cnt;            // [kHistRows][nchunks_total] words of the run
 };
+
+struct ReorderParams {
+  uint32_t nchunks;
+  const uint32_t* run_at;
+  const uint32_t* run_cnt;
+  const uint32_t* run_off;        // exclusive scan of run_cnt over chunks, per bin
+  const uint8_t* src[kNumBins];   // reserved regions (keys_cap / long list as filled)
+  uint8_t* dst[kNumBins];         // corpus-order destinations
+  uint32_t key_bytes[kNumBins];   // element bytes per bin
+};
+void launch_reorder_runs(const ReorderParams& r, cudaStream_t st);
 
 // ingest.cu
 uint32_t chunk_count(uint64_t n);
