@@ -181,3 +181,24 @@ def test_sort_texts_batch_matches_single_calls():
     with pytest.raises(ValueError):
         h.sort_texts([arrs[0]], [np.empty(3, dtype=np.uint8)], 2)
     h.close()
+
+
+def test_ordered_ingest_chunked_stats_and_permutation():
+    # > 16 MiB host text: chunked upload + ordered reserve ingest + reorder;
+    # the stats and a bucket permutation must match corpus order exactly
+    text = synth.generate(4, words=2_500_000, seed=12)
+    assert len(text) > (16 << 20)
+    want, info = oracle.sort_text(text, mode="fast")
+    dc = DeviceCorpus()
+    dc.ingest(text)
+    dc.sort(want_stats=True)
+    naive = dc.stats(naive=True)
+    for L, (n, inv, K, c, s, p) in info.items():
+        assert naive[L] == (c, s, p), L
+    assert dc.payload() == want
+    # the permutation of the L=3 bucket sorts the corpus-order words of length 3
+    words3 = [w for w in oracle.tokenize(text) if len(w) == 3]
+    lengths, counts, _ = dc.handle.buckets()
+    b = lengths.index(3)
+    perm = dc.handle.permutation(b, counts[b])
+    assert [words3[i] for i in perm] == sorted(words3)
