@@ -325,6 +325,57 @@ __device__ __forceinline__ void smem_to_global(const KW<LANES>* sk, const uint32
 
 // ---- tile pass -------------------------------------------------------------------
 
+// The on-chip sort of one tile already in shared memory (T keys, all-ones
+// sentinels after the first cnt): each thread takes E consecutive keys into
+// registers and runs odd-even transposition sort on them (E phases of
+// compare-exchange on strict '>'); merge-path levels in shared memory then
+// merge the runs. Levels stop once a run covers all cnt real keys (the
+// sentinels behind them are already in place). Leaves the thread's E
+// outputs of the sorted tile (blocked) in r / ri; idx0 = idx of key 0.
+template <int LANES, bool STATS>
+__device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cnt, uint32_t idx0,
+                                             Key<LANES> (&r)[TileCfg<LANES>::E],
+                                             uint32_t (&ri)[TileCfg<LANES>::E], uint64_t& inv) {
+  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    r[k] = ldk<LANES>(sk, tid * E + k);
+    ri[k] = STATS ? idx0 + (uint32_t)(tid * E + k) : 0u;
+  }
+  // Odd-even transposition sort of the thread's E keys: E phases, each a
+  // layer of independent compare-exchanges that swap on strictly-greater.
+#pragma unroll
+  for (int ph = 0; ph < E; ++ph) {
+#pragma unroll
+    for (int i = ph & 1; i + 1 < E; i += 2) {
+      const bool sw = key_lt<LANES>(r[i + 1], r[i]);
+      if (sw) {
+        Key<LANES> t = r[i];
+        r[i] = r[i + 1];
+        r[i + 1] = t;
+        uint32_t u = ri[i];
+        ri[i] = ri[i + 1];
+        ri[i + 1] = u;
+      }
+      if (STATS) inv += sw;
+    }
+  }
+  // Merge-path levels inside the tile.
+#pragma unroll 1
+  for (int run = E; run < T && run < cnt; run <<= 1) {
+    __syncthreads();
+    regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
+    __syncthreads();
+    const int gt = (2 * run) / E;  // threads per merged pair
+    const int a0 = (tid / gt) * 2 * run;
+    merge_path<LANES, E, STATS>(sk + (size_t)a0 * NW, run, sk + (size_t)(a0 + run) * NW, run,
+                                si + a0, si + a0 + run, (tid % gt) * E, run, r, ri, inv);
+  }
+}
+
+
 template <int LANES, bool STATS>
 __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_constant__ SortLaunch a) {
   constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
@@ -357,41 +408,8 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
 
   Key<LANES> r[E];
   uint32_t ri[E];
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    r[k] = ldk<LANES>(sk, tid * E + k);
-    ri[k] = STATS ? (uint32_t)(sd.idx_base + start + tid * E + k) : 0u;
-  }
-  // Odd-even transposition sort of the thread's E keys: E phases, each a
-  // layer of independent compare-exchanges that swap on strictly-greater.
   uint64_t inv = 0;
-#pragma unroll
-  for (int ph = 0; ph < E; ++ph) {
-#pragma unroll
-    for (int i = ph & 1; i + 1 < E; i += 2) {
-      const bool sw = key_lt<LANES>(r[i + 1], r[i]);
-      if (sw) {
-        Key<LANES> t = r[i];
-        r[i] = r[i + 1];
-        r[i + 1] = t;
-        uint32_t u = ri[i];
-        ri[i] = ri[i + 1];
-        ri[i + 1] = u;
-      }
-      if (STATS) inv += sw;
-    }
-  }
-  // Merge-path levels inside the tile.
-#pragma unroll 1
-  for (int run = E; run < T; run <<= 1) {
-    __syncthreads();
-    regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
-    __syncthreads();
-    const int gt = (2 * run) / E;  // threads per merged pair
-    const int a0 = (tid / gt) * 2 * run;
-    merge_path<LANES, E, STATS>(sk + (size_t)a0 * NW, run, sk + (size_t)(a0 + run) * NW, run,
-                                si + a0, si + a0 + run, (tid % gt) * E, run, r, ri, inv);
-  }
+  tile_network<LANES, STATS>(sk, si, cnt, (uint32_t)(sd.idx_base + start), r, ri, inv);
   long long kloc = 0;
   if (STATS && sd.n <= (uint32_t)T) {
 #pragma unroll
