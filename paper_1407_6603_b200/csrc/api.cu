@@ -172,6 +172,7 @@ struct ws_handle {
   DevBuf params;
   DevBuf splits[kClasses + 2];  // merge-path splits: [0] main stream, [1..4] class streams
   DevBuf rcounts[2], rtotals[2];  // radix passes of lane classes 0 and 1
+  DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
   uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
@@ -492,6 +493,72 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         if (pl.passes == p + 1) done.push_back(pl.s);
       if (!done.empty()) WS_TRY((*on_done)(done, st));
     }
+  }
+  return WS_OK;
+}
+
+// Payload-only sort of a multi-lane class (sort.cu, sample sort): every
+// bucket larger than a tile is cut by S - 1 sampled splitters into slots of
+// ~T/2 keys (plus one slot per splitter for keys equal to it), scattered into
+// the output buffer and sorted slot by slot on chip. Five launches per class
+// whatever the bucket sizes; the result is in buffer 1.
+int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* out_class,
+                         cudaStream_t st, const PassDoneHook* on_done) {
+  const uint32_t T = (uint32_t)tile_size(lanes);
+  uint32_t pmax = 1;
+  while (pmax * 2 <= (uint32_t)sample_max_keys(lanes)) pmax *= 2;
+  const uint32_t ptile = (uint32_t)part_tile_size();
+  std::vector<SampleSeg> d;
+  uint32_t slots = 0, splits = 0, tiles = 0;
+  for (auto& s : segs) {
+    s.final_buf = 1;
+    uint64_t S = s.n <= T ? 1 : (s.n + T / 2 - 1) / (T / 2);
+    S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 32));
+    SampleSeg g;
+    g.in = s.in_ptr;
+    g.key_off = (uint32_t)s.key_off;
+    g.n = s.n;
+    g.nsplit = (uint32_t)S - 1;
+    g.m = g.nsplit ? (uint32_t)std::min<uint64_t>(std::min<uint64_t>(32 * S, pmax), s.n) : 0u;
+    g.split_off = splits;
+    g.slot_base = slots;
+    g.tile_begin = tiles;
+    g.pad_ = 0;
+    d.push_back(g);
+    slots += 2 * g.nsplit + 1;
+    splits += g.nsplit;
+    tiles += (s.n + ptile - 1) / ptile;
+  }
+  if (d.empty() || !tiles) return WS_OK;
+  if (d.size() > (size_t)kInlineSegs) return fail(WS_ERR_STATE, "too many buckets in a class");
+  WS_CUDA(h->ss_split[lanes].ensure((size_t)std::max(splits, 1u) * key_bytes(lanes) + 64));
+  WS_CUDA(h->ss_slots[lanes].ensure((size_t)slots * 12 + 64));
+  SampleLaunch a;
+  std::copy(d.begin(), d.end(), a.inl);
+  a.segs = nullptr;
+  a.nsegs = (int)d.size();
+  a.nslots = slots;
+  a.work_items = tiles;
+  a.keys_out = out_class;
+  a.splitters = h->ss_split[lanes].as<uint64_t>();
+  a.hist = h->ss_slots[lanes].as<uint32_t>();
+  a.cursor = a.hist + slots;
+  a.slot_off = a.cursor + slots;
+  WS_CUDA(cudaMemsetAsync(a.hist, 0, (size_t)slots * 4, st));
+  double bytes = 0;
+  for (const auto& s : segs) bytes += 5.0 * s.n * key_bytes(lanes);
+  char name[32];
+  snprintf(name, sizeof name, "sample_l%d", lanes);
+  {
+    Phase ph(h, name, bytes, 0, st);
+    launch_sample_sort(lanes, a, st);
+    h->launches += 5;
+  }
+  WS_TRY(check_launch(name));
+  if (on_done) {
+    std::vector<const SegIn*> done;
+    for (auto& s : segs) done.push_back(&s);
+    WS_TRY((*on_done)(done, st));
   }
   return WS_OK;
 }
@@ -973,8 +1040,11 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     };
     static const char* no_radix = getenv("WSORT_NO_RADIX");
     const PassDoneHook* on_done = fe && !fe->per_class ? &hook : nullptr;
+    static const char* no_sample = getenv("WSORT_NO_SAMPLE");
     if (!stats && c == 0 && !(no_radix && no_radix[0] == '1')) {
       WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, on_done));
+    } else if (!stats && c >= 1 && !(no_sample && no_sample[0] == '1')) {
+      WS_TRY(sample_sort_segments(h, c, segs, k1, cst, on_done));
     } else {
       WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(),
                            h->idx[1].as<uint32_t>(), stats, inv, km, "", cst, on_done));
@@ -1447,7 +1517,9 @@ void ws_destroy(ws_handle* h) {
                     &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5],
                     &h->keys_cap, &h->status, &h->ticket, &h->overflow, &h->fill,
                     &h->run_at, &h->run_cnt, &h->run_off, &h->longlist2,
-                    &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1]};
+                    &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1],
+                    &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
+                    &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4]};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();

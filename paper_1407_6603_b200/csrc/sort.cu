@@ -579,6 +579,219 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
                                    STATS ? a.idx_out + sd.idx_off + out_begin : nullptr);
 }
 
+// ---- payload-mode sample sort (multi-lane classes) ------------------------------
+//
+// Payload mode only needs the sorted bytes, so a bucket larger than a tile is
+// split by value instead of merged level by level: S - 1 splitters taken
+// from a sorted, evenly spaced sample (32 per splitter) cut it into 2S - 1
+// slots (range slots between splitters, and one slot per splitter for keys
+// equal to it - repeated words need no sorting); keys are scattered to their
+// slot (positions reserved per CTA, order inside a slot arbitrary); every
+// range slot is then sorted on chip by the tile network. Slots beyond a tile
+// (rare: the sample bounds them to ~T/2 on average) fall back to an odd-even
+// transposition sort over half-tile blocks, done by the slot's CTA.
+
+constexpr int kSampleThreads = 1024;
+constexpr int kPartThreads = 256;
+constexpr int kPartPer = 8;
+constexpr int kPartTile = kPartThreads * kPartPer;
+
+__device__ __forceinline__ const SampleSeg& sseg_at(const SampleLaunch& a, int i) {
+  return a.segs ? a.segs[i] : a.inl[i];
+}
+
+// Slot of a key among nsplit sorted splitters: 2j for keys strictly between
+// splitters j-1 and j, 2j + 1 for keys equal to splitter j.
+template <int LANES>
+__device__ __forceinline__ uint32_t slot_of(const KW<LANES>* sp, uint32_t nsplit, const Key<LANES>& k) {
+  uint32_t lo = 0, len = nsplit;  // lower bound: first splitter >= k
+  while (len > 0) {
+    const uint32_t half = len >> 1, mid = lo + half;
+    const bool less = key_lt<LANES>(ldk<LANES>(sp, (int)mid), k);
+    lo = less ? mid + 1 : lo;
+    len = less ? len - half - 1 : half;
+  }
+  const bool eq = lo < nsplit && !key_lt<LANES>(k, ldk<LANES>(sp, (int)lo));
+  return 2 * lo + (eq ? 1u : 0u);
+}
+
+// One CTA per bucket: evenly spaced sample -> bitonic sort in shared memory
+// -> the nsplit splitters.
+template <int LANES>
+__global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
+  using W = KW<LANES>;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  extern __shared__ __align__(16) uint64_t smem[];
+  W* sk = reinterpret_cast<W*>(smem);
+  const SampleSeg& sg = sseg_at(a, blockIdx.x);
+  if (!sg.nsplit) return;
+  uint32_t P = 1;
+  while (P < sg.m) P <<= 1;
+  const W* in = kv<LANES>(sg.in);
+  for (uint32_t i = threadIdx.x; i < P; i += kSampleThreads) {
+    Key<LANES> k = key_max<LANES>();
+    if (i < sg.m) k = gld<LANES>(in, (int64_t)((uint64_t)i * sg.n / sg.m));
+    stk<LANES>(sk, (int)i, k);
+  }
+  __syncthreads();
+  for (uint32_t size = 2; size <= P; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t t = threadIdx.x; t < P / 2; t += kSampleThreads) {
+        const uint32_t i = 2 * t - (t & (stride - 1));  // lower element of the pair
+        const uint32_t j = i + stride;
+        const bool up = (i & size) == 0;
+        const Key<LANES> x = ldk<LANES>(sk, (int)i), y = ldk<LANES>(sk, (int)j);
+        if (key_lt<LANES>(y, x) == up) {
+          stk<LANES>(sk, (int)i, y);
+          stk<LANES>(sk, (int)j, x);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  W* sp = kv<LANES>(a.splitters) + (uint64_t)sg.split_off * NW;
+  for (uint32_t k = threadIdx.x; k < sg.nsplit; k += kSampleThreads)
+    stk<LANES>(sp, (int)k, ldk<LANES>(sk, (int)((uint64_t)(k + 1) * sg.m / (sg.nsplit + 1))));
+}
+
+__device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t tile) {
+  const int lane = threadIdx.x & 31;
+  int found = 0;
+  for (int base = 0; base < a.nsegs; base += 32) {
+    const int i = base + lane;
+    const bool le = i < a.nsegs && sseg_at(a, i).tile_begin <= tile;
+    found += __popc(__ballot_sync(0xffffffffu, le));
+    if (!__shfl_sync(0xffffffffu, (int)le, 31)) break;
+  }
+  return found - 1;
+}
+
+// Partition passes over one tile of a bucket. COUNT: per-slot counts into
+// a.hist. !COUNT: each key goes to cursor[slot] reservation + local rank.
+template <int LANES, bool COUNT>
+__global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_constant__ SampleLaunch a) {
+  using W = KW<LANES>;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  __shared__ __align__(16) W s_split[kMaxSplit * NW];
+  __shared__ uint32_t s_cnt[2 * kMaxSplit + 1];
+  __shared__ uint32_t s_base[2 * kMaxSplit + 1];
+  __shared__ int s_seg;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    const int sgi = part_segment_of(a, blockIdx.x);
+    if (tid == 0) s_seg = sgi;
+  }
+  __syncthreads();
+  const SampleSeg& sg = sseg_at(a, s_seg);
+  const uint32_t nslot = 2 * sg.nsplit + 1;
+  const W* gs = kv<LANES>(a.splitters) + (uint64_t)sg.split_off * NW;
+  for (uint32_t i = tid; i < sg.nsplit * NW; i += kPartThreads) s_split[i] = gs[i];
+  for (uint32_t i = tid; i < nslot; i += kPartThreads) s_cnt[i] = 0;
+  __syncthreads();
+  const uint64_t first = (uint64_t)(blockIdx.x - sg.tile_begin) * kPartTile;
+  const W* in = kv<LANES>(sg.in);
+  Key<LANES> k[kPartPer];
+  uint32_t slot[kPartPer], rank[kPartPer];
+#pragma unroll
+  for (int q = 0; q < kPartPer; ++q) {
+    const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
+    slot[q] = 0xFFFFFFFFu;
+    if (i < sg.n) {
+      k[q] = gld<LANES>(in, (int64_t)i);
+      slot[q] = slot_of<LANES>(s_split, sg.nsplit, k[q]);
+      rank[q] = atomicAdd(&s_cnt[slot[q]], 1u);
+    }
+  }
+  __syncthreads();
+  if (COUNT) {
+    for (uint32_t i = tid; i < nslot; i += kPartThreads)
+      if (s_cnt[i]) atomicAdd(a.hist + sg.slot_base + i, s_cnt[i]);
+    return;
+  }
+  for (uint32_t i = tid; i < nslot; i += kPartThreads)
+    if (s_cnt[i]) s_base[i] = atomicAdd(a.cursor + sg.slot_base + i, s_cnt[i]);
+  __syncthreads();
+  W* out = kv<LANES>(a.keys_out);
+#pragma unroll
+  for (int q = 0; q < kPartPer; ++q)
+    if (slot[q] != 0xFFFFFFFFu) stk<LANES>(out, (int)(s_base[slot[q]] + rank[q]), k[q]);
+}
+
+// Exclusive scan of the class's slot counts (one CTA): slot offsets, which
+// are class-relative element offsets because buckets lie back to back.
+__global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__ SampleLaunch a) {
+  __shared__ uint32_t s_w[32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) s_carry = sseg_at(a, 0).key_off;  // class-relative start of the first bucket
+  __syncthreads();
+  for (uint32_t base = 0; base < a.nslots; base += 1024) {
+    const uint32_t i = base + tid;
+    const uint32_t v = i < a.nslots ? a.hist[i] : 0u;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) s_w[wid] = inc;
+    __syncthreads();
+    uint32_t pre = s_carry;
+    for (int w = 0; w < wid; ++w) pre += s_w[w];
+    if (i < a.nslots) {
+      a.slot_off[i] = pre + inc - v;
+      a.cursor[i] = pre + inc - v;
+    }
+    __syncthreads();
+    if (tid == 1023) s_carry = pre + inc;
+    __syncthreads();
+  }
+}
+
+// One CTA per slot: sort a range slot in place (tile network; block
+// odd-even transposition over half tiles when it exceeds a tile).
+template <int LANES>
+__global__ void __launch_bounds__(kTileThreads) subsort_kernel(const __grid_constant__ SampleLaunch a) {
+  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  using W = KW<LANES>;
+  extern __shared__ __align__(16) uint64_t smem[];
+  W* sk = reinterpret_cast<W*>(smem);
+  const uint32_t s = blockIdx.x;
+  // bucket of the slot (segments ascend by slot_base)
+  int b = 0;
+  while (b + 1 < a.nsegs && sseg_at(a, b + 1).slot_base <= s) ++b;
+  if (((s - sseg_at(a, b).slot_base) & 1u) != 0) return;  // keys equal to a splitter
+  const uint32_t cnt = a.hist[s];
+  if (cnt < 2) return;
+  W* base = kv<LANES>(a.keys_out) + (uint64_t)a.slot_off[s] * NW;
+  Key<LANES> r[E];
+  uint32_t ri[E];
+  uint64_t inv = 0;
+  auto sort_span = [&](W* g, uint32_t c) {  // c <= T keys at g, sorted in place
+    for (uint32_t j = threadIdx.x; j < (uint32_t)T * NW; j += NT)
+      sk[j] = j < c * NW ? g[j] : ~W(0);
+    __syncthreads();
+    tile_network<LANES, false>(sk, nullptr, (int)c, 0u, r, ri, inv);
+    __syncthreads();
+    regs_to_smem<LANES, E, false>(sk, nullptr, threadIdx.x * E, r, ri);
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < c * NW; j += NT) g[j] = sk[j];
+    __syncthreads();
+  };
+  if (cnt <= (uint32_t)T) {
+    sort_span(base, cnt);
+    return;
+  }
+  constexpr uint32_t H = T / 2;
+  const uint32_t blocks = (cnt + H - 1) / H;
+  for (uint32_t round = 0; round < blocks; ++round)
+    for (uint32_t p = round & 1; p + 1 < blocks; p += 2) {
+      const uint32_t lo = p * H, hi = min(cnt, (p + 2) * H);
+      sort_span(base + (uint64_t)lo * NW, hi - lo);
+    }
+}
+
 // ---- host side ---------------------------------------------------------------------
 
 int tile_size(int lanes) {
@@ -603,6 +816,13 @@ int merge_tile_size(int lanes) {
 
 template <int LANES, bool STATS>
 static void set_attrs_t() {
+  if (!STATS && LANES >= 1) {
+    cudaFuncSetAttribute(sample_split_kernel<LANES < 1 ? 1 : LANES>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
+    cudaFuncSetAttribute(subsort_kernel<LANES < 1 ? 1 : LANES>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)pass_smem_bytes<(LANES < 1 ? 1 : LANES), TileCfg<(LANES < 1 ? 1 : LANES)>::T, false>());
+  }
   cudaFuncSetAttribute(tile_sort_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>());
   cudaFuncSetAttribute(merge_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -647,6 +867,33 @@ void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st) {
   if (!a.work_items) return;
   const bool stats = a.idx_out != nullptr;
   WS_DISPATCH_LANES(launch_tile_t, lanes, stats, a, st);
+}
+
+template <int LANES>
+static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
+  uint32_t P = 1;
+  uint32_t mmax = 0;
+  for (int i = 0; i < a.nsegs; ++i) mmax = std::max(mmax, a.inl[i].m);
+  while (P < mmax) P <<= 1;
+  const size_t split_smem = (size_t)P * key_bytes(LANES);
+  if (mmax) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, split_smem, st>>>(a);
+  partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
+  slot_scan_kernel<<<1, 1024, 0, st>>>(a);
+  partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
+  subsort_kernel<LANES><<<a.nslots, kTileThreads,
+                          pass_smem_bytes<LANES, TileCfg<LANES>::T, false>(), st>>>(a);
+}
+
+int sample_max_keys(int lanes) { return kSampleSmem / key_bytes(lanes); }
+int part_tile_size() { return kPartTile; }
+
+void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st) {
+  switch (lanes) {
+    case 1: launch_sample_t<1>(a, st); break;
+    case 2: launch_sample_t<2>(a, st); break;
+    case 3: launch_sample_t<3>(a, st); break;
+    default: launch_sample_t<4>(a, st); break;
+  }
 }
 
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st) {

@@ -83,6 +83,36 @@ struct SortLaunch {
   SegDesc inl[kInlineSegs];  // the segment table when it fits
 };
 int tile_size(int lanes);
+
+// payload-mode sample sort of multi-lane classes (sort.cu)
+constexpr int kMaxSplit = 511;            // splitters per bucket
+constexpr int kSampleSmem = 192 * 1024;   // bytes of the in-smem sample sort
+struct SampleSeg {
+  const uint64_t* in;   // unsorted keys of the bucket
+  uint32_t key_off;     // element offset of the bucket in the class region
+  uint32_t n;
+  uint32_t nsplit;      // S - 1 splitters (0: the bucket is one slot)
+  uint32_t m;           // sample size (0 when nsplit == 0)
+  uint32_t split_off;   // first splitter of the bucket in `splitters`
+  uint32_t slot_base;   // first of the bucket's 2 * nsplit + 1 slots
+  uint32_t tile_begin;  // first partition tile of the bucket
+  uint32_t pad_;
+};
+struct SampleLaunch {
+  const SampleSeg* segs;  // device table when nsegs > kInlineSegs, else nullptr
+  int nsegs;
+  uint32_t nslots;
+  uint32_t work_items;    // partition tiles of all buckets
+  uint64_t* keys_out;     // the class region of the output key buffer
+  uint64_t* splitters;
+  uint32_t* hist;         // per slot: keys (zeroed before the launch)
+  uint32_t* cursor;       // per slot: reservation cursor
+  uint32_t* slot_off;     // per slot: class-relative element offset
+  SampleSeg inl[kInlineSegs];
+};
+int sample_max_keys(int lanes);
+int part_tile_size();
+void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st);
 int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);
