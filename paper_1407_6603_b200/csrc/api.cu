@@ -985,7 +985,11 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   // packed buckets: one schedule per lane class, each class on its own stream
   // (the classes are independent; small classes fill the big one's bubbles)
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
-  for (int c = kClasses; c >= 0; --c) {  // small (multi-lane) classes are submitted first
+  // class 0 (radix: a chain of small passes, the longest) is submitted first
+  // on a high-priority stream; the multi-lane classes fill around it
+  static const int order[kClasses + 1] = {0, 4, 3, 2, 1};
+  for (int oi = 0; oi <= kClasses; ++oi) {
+    const int c = order[oi];
     std::vector<SegIn> segs;
     std::vector<int> which;
     for (int i = 0; i < nb; ++i) {
@@ -1471,15 +1475,15 @@ int ws_create(ws_handle** out, int32_t device) {
   h->device = device;
   const char* ser = getenv("WSORT_SERIAL");
   h->serial = ser && ser[0] == '1';
-  // Priorities: the multi-lane classes are small and their payload can reach
-  // the host while the 1-lane class still sorts, so they (and every emit /
-  // copy stream) outrank the 1-lane class's sort stream.
+  // Priorities: class 0's radix chain (four dependent passes of small
+  // kernels) is the longest path, so its stream (and every emit / copy
+  // stream) outranks the multi-lane classes' sort streams.
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
   // the one-word classes (0, 1) hold most keys and sort last
   for (int c = 0; c <= kClasses && e == cudaSuccess; ++c)
-    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, c <= 1 ? prio_lo : prio_hi);
+    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, c == 0 ? prio_hi : prio_lo);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->hs, cudaStreamNonBlocking, prio_hi);
   for (int c = 0; c <= kClasses && e == cudaSuccess; ++c) {
     e = cudaStreamCreateWithPriority(&h->es[c], cudaStreamNonBlocking, prio_hi);
