@@ -505,21 +505,28 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
 int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* out_class,
                          cudaStream_t st, const PassDoneHook* on_done) {
   const uint32_t T = (uint32_t)tile_size(lanes);
-  uint32_t pmax = 1;
-  while (pmax * 2 <= (uint32_t)sample_max_keys(lanes)) pmax *= 2;
+  uint32_t pmax = 1;  // sample prefixes sorted in shared memory (power of two, <= 4096)
+  while (pmax * 2 <= (uint32_t)std::min(sample_max_keys(lanes), 4096)) pmax *= 2;
   const uint32_t ptile = (uint32_t)part_tile_size();
   std::vector<SampleSeg> d;
   uint32_t slots = 0, splits = 0, tiles = 0;
   for (auto& s : segs) {
     s.final_buf = 1;
-    uint64_t S = s.n <= T ? 1 : (s.n + T / 2 - 1) / (T / 2);
-    S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 32));
+    // slots of ~T/3 on average; a sample of >= 8 keys per slot keeps the
+    // chance that a slot exceeds T (the slow fallback) negligible
+    const uint64_t target = (uint64_t)T / 3;
+    uint64_t S = s.n <= T ? 1 : (s.n + target - 1) / target;
+    S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 8));
     SampleSeg g;
     g.in = s.in_ptr;
     g.key_off = (uint32_t)s.key_off;
     g.n = s.n;
     g.nsplit = (uint32_t)S - 1;
-    g.m = g.nsplit ? (uint32_t)std::min<uint64_t>(std::min<uint64_t>(32 * S, pmax), s.n) : 0u;
+    g.m = 0;
+    if (g.nsplit) {  // >= 8 samples per splitter, a power of two (the bitonic sort's size)
+      g.m = 1;
+      while (g.m < 8 * S && 2ull * g.m <= std::min<uint64_t>(pmax, s.n)) g.m *= 2;
+    }
     g.split_off = splits;
     g.slot_base = slots;
     g.tile_begin = tiles;
@@ -531,7 +538,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   }
   if (d.empty() || !tiles) return WS_OK;
   if (d.size() > (size_t)kInlineSegs) return fail(WS_ERR_STATE, "too many buckets in a class");
-  WS_CUDA(h->ss_split[lanes].ensure((size_t)std::max(splits, 1u) * key_bytes(lanes) + 64));
+  WS_CUDA(h->ss_split[lanes].ensure((size_t)std::max(splits, 1u) * 8 + 64));
   WS_CUDA(h->ss_slots[lanes].ensure((size_t)slots * 12 + 64));
   SampleLaunch a;
   std::copy(d.begin(), d.end(), a.inl);

@@ -582,13 +582,15 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
 // ---- payload-mode sample sort (multi-lane classes) ------------------------------
 //
 // Payload mode only needs the sorted bytes, so a bucket larger than a tile is
-// split by value instead of merged level by level: S - 1 splitters taken
-// from a sorted, evenly spaced sample (32 per splitter) cut it into 2S - 1
-// slots (range slots between splitters, and one slot per splitter for keys
-// equal to it - repeated words need no sorting); keys are scattered to their
-// slot (positions reserved per CTA, order inside a slot arbitrary); every
-// range slot is then sorted on chip by the tile network. Slots beyond a tile
-// (rare: the sample bounds them to ~T/2 on average) fall back to an odd-even
+// split by value instead of merged level by level: S - 1 splitters (64-bit
+// key prefixes = the first word of the key) taken from a sorted, evenly
+// spaced sample (8 per splitter) cut it into 2S - 1 slots: range slots between
+// splitters, and one slot per splitter for keys whose prefix equals it
+// (repeated words land there and need no sorting; a slot whose keys differ
+// past the prefix is sorted like a range slot). Keys are scattered to their
+// slot (positions reserved per CTA, order inside a slot arbitrary) and every
+// slot is then sorted on chip by the tile network. Slots beyond a tile (rare:
+// the sample bounds them to ~0.4 T on average) fall back to an odd-even
 // transposition sort over half-tile blocks, done by the slot's CTA.
 
 constexpr int kSampleThreads = 1024;
@@ -600,58 +602,56 @@ __device__ __forceinline__ const SampleSeg& sseg_at(const SampleLaunch& a, int i
   return a.segs ? a.segs[i] : a.inl[i];
 }
 
-// Slot of a key among nsplit sorted splitters: 2j for keys strictly between
-// splitters j-1 and j, 2j + 1 for keys equal to splitter j.
+// 64-bit prefix of a key (its first word; class 0 keys are not sample-sorted).
 template <int LANES>
-__device__ __forceinline__ uint32_t slot_of(const KW<LANES>* sp, uint32_t nsplit, const Key<LANES>& k) {
-  uint32_t lo = 0, len = nsplit;  // lower bound: first splitter >= k
+__device__ __forceinline__ uint64_t prefix_of(const Key<LANES>& k) {
+  return (uint64_t)k.w[0];
+}
+
+// Slot of a prefix among nsplit sorted splitters: 2j for prefixes strictly
+// between splitters j-1 and j, 2j + 1 for a prefix equal to splitter j.
+__device__ __forceinline__ uint32_t slot_of(const uint64_t* sp, uint32_t nsplit, uint64_t p) {
+  uint32_t lo = 0, len = nsplit;  // lower bound: first splitter >= p
   while (len > 0) {
     const uint32_t half = len >> 1, mid = lo + half;
-    const bool less = key_lt<LANES>(ldk<LANES>(sp, (int)mid), k);
+    const bool less = sp[mid] < p;
     lo = less ? mid + 1 : lo;
     len = less ? len - half - 1 : half;
   }
-  const bool eq = lo < nsplit && !key_lt<LANES>(k, ldk<LANES>(sp, (int)lo));
-  return 2 * lo + (eq ? 1u : 0u);
+  return 2 * lo + ((lo < nsplit && sp[lo] == p) ? 1u : 0u);
 }
 
-// One CTA per bucket: evenly spaced sample -> bitonic sort in shared memory
-// -> the nsplit splitters.
+// One CTA per bucket: prefixes of an evenly spaced sample -> bitonic sort in
+// shared memory -> the nsplit splitters.
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
-  using W = KW<LANES>;
-  constexpr int NW = KeyTraits<LANES>::NW;
   extern __shared__ __align__(16) uint64_t smem[];
-  W* sk = reinterpret_cast<W*>(smem);
   const SampleSeg& sg = sseg_at(a, blockIdx.x);
   if (!sg.nsplit) return;
   uint32_t P = 1;
   while (P < sg.m) P <<= 1;
-  const W* in = kv<LANES>(sg.in);
-  for (uint32_t i = threadIdx.x; i < P; i += kSampleThreads) {
-    Key<LANES> k = key_max<LANES>();
-    if (i < sg.m) k = gld<LANES>(in, (int64_t)((uint64_t)i * sg.n / sg.m));
-    stk<LANES>(sk, (int)i, k);
-  }
+  const KW<LANES>* in = kv<LANES>(sg.in);
+  constexpr int NW = KeyTraits<LANES>::NW;
+  for (uint32_t i = threadIdx.x; i < P; i += kSampleThreads)
+    smem[i] = i < sg.m ? (uint64_t)__ldg(in + ((uint64_t)i * sg.n / sg.m) * NW) : ~0ull;
   __syncthreads();
   for (uint32_t size = 2; size <= P; size <<= 1) {
     for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
       for (uint32_t t = threadIdx.x; t < P / 2; t += kSampleThreads) {
         const uint32_t i = 2 * t - (t & (stride - 1));  // lower element of the pair
         const uint32_t j = i + stride;
-        const bool up = (i & size) == 0;
-        const Key<LANES> x = ldk<LANES>(sk, (int)i), y = ldk<LANES>(sk, (int)j);
-        if (key_lt<LANES>(y, x) == up) {
-          stk<LANES>(sk, (int)i, y);
-          stk<LANES>(sk, (int)j, x);
+        const uint64_t x = smem[i], y = smem[j];
+        if ((y < x) == ((i & size) == 0)) {
+          smem[i] = y;
+          smem[j] = x;
         }
       }
       __syncthreads();
     }
   }
-  W* sp = kv<LANES>(a.splitters) + (uint64_t)sg.split_off * NW;
+  uint64_t* sp = a.splitters + sg.split_off;
   for (uint32_t k = threadIdx.x; k < sg.nsplit; k += kSampleThreads)
-    stk<LANES>(sp, (int)k, ldk<LANES>(sk, (int)((uint64_t)(k + 1) * sg.m / (sg.nsplit + 1))));
+    sp[k] = smem[(uint64_t)(k + 1) * sg.m / (sg.nsplit + 1)];
 }
 
 __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t tile) {
@@ -671,8 +671,7 @@ __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t t
 template <int LANES, bool COUNT>
 __global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_constant__ SampleLaunch a) {
   using W = KW<LANES>;
-  constexpr int NW = KeyTraits<LANES>::NW;
-  __shared__ __align__(16) W s_split[kMaxSplit * NW];
+  __shared__ uint64_t s_split[kMaxSplit];
   __shared__ uint32_t s_cnt[2 * kMaxSplit + 1];
   __shared__ uint32_t s_base[2 * kMaxSplit + 1];
   __shared__ int s_seg;
@@ -684,8 +683,7 @@ __global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_co
   __syncthreads();
   const SampleSeg& sg = sseg_at(a, s_seg);
   const uint32_t nslot = 2 * sg.nsplit + 1;
-  const W* gs = kv<LANES>(a.splitters) + (uint64_t)sg.split_off * NW;
-  for (uint32_t i = tid; i < sg.nsplit * NW; i += kPartThreads) s_split[i] = gs[i];
+  for (uint32_t i = tid; i < sg.nsplit; i += kPartThreads) s_split[i] = a.splitters[sg.split_off + i];
   for (uint32_t i = tid; i < nslot; i += kPartThreads) s_cnt[i] = 0;
   __syncthreads();
   const uint64_t first = (uint64_t)(blockIdx.x - sg.tile_begin) * kPartTile;
@@ -698,7 +696,7 @@ __global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_co
     slot[q] = 0xFFFFFFFFu;
     if (i < sg.n) {
       k[q] = gld<LANES>(in, (int64_t)i);
-      slot[q] = slot_of<LANES>(s_split, sg.nsplit, k[q]);
+      slot[q] = slot_of(s_split, sg.nsplit, prefix_of<LANES>(k[q]));
       rank[q] = atomicAdd(&s_cnt[slot[q]], 1u);
     }
   }
@@ -748,23 +746,31 @@ __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__
   }
 }
 
-// One CTA per slot: sort a range slot in place (tile network; block
-// odd-even transposition over half tiles when it exceeds a tile).
+// One CTA per slot: sort the slot in place (tile network; block odd-even
+// transposition over half tiles when it exceeds a tile). A prefix-equal slot
+// whose keys are all identical (repeated words) is left as it is.
 template <int LANES>
 __global__ void __launch_bounds__(kTileThreads) subsort_kernel(const __grid_constant__ SampleLaunch a) {
   constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
   extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ int s_differs;
   W* sk = reinterpret_cast<W*>(smem);
   const uint32_t s = blockIdx.x;
-  // bucket of the slot (segments ascend by slot_base)
-  int b = 0;
-  while (b + 1 < a.nsegs && sseg_at(a, b + 1).slot_base <= s) ++b;
-  if (((s - sseg_at(a, b).slot_base) & 1u) != 0) return;  // keys equal to a splitter
   const uint32_t cnt = a.hist[s];
   if (cnt < 2) return;
   W* base = kv<LANES>(a.keys_out) + (uint64_t)a.slot_off[s] * NW;
+  int b = 0;  // bucket of the slot (segments ascend by slot_base)
+  while (b + 1 < a.nsegs && sseg_at(a, b + 1).slot_base <= s) ++b;
+  if (((s - sseg_at(a, b).slot_base) & 1u) != 0) {  // prefix-equal slot
+    if (threadIdx.x == 0) s_differs = 0;
+    __syncthreads();
+    const Key<LANES> k0 = ldk<LANES>(base, 0);
+    bool diff = false;
+    for (uint32_t i = threadIdx.x; i < cnt; i += NT) diff |= key_lt<LANES>(k0, ldk<LANES>(base, (int)i));
+    if (__syncthreads_or(diff) == 0) return;  // all copies of one word
+  }
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
@@ -875,7 +881,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   uint32_t mmax = 0;
   for (int i = 0; i < a.nsegs; ++i) mmax = std::max(mmax, a.inl[i].m);
   while (P < mmax) P <<= 1;
-  const size_t split_smem = (size_t)P * key_bytes(LANES);
+  const size_t split_smem = (size_t)P * 8;  // 64-bit prefixes
   if (mmax) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, split_smem, st>>>(a);
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
   slot_scan_kernel<<<1, 1024, 0, st>>>(a);
@@ -884,7 +890,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
                           pass_smem_bytes<LANES, TileCfg<LANES>::T, false>(), st>>>(a);
 }
 
-int sample_max_keys(int lanes) { return kSampleSmem / key_bytes(lanes); }
+int sample_max_keys(int) { return kSampleSmem / 8; }
 int part_tile_size() { return kPartTile; }
 
 void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st) {

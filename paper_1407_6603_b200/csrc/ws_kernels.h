@@ -104,7 +104,7 @@ struct SampleLaunch {
   uint32_t nslots;
   uint32_t work_items;    // partition tiles of all buckets
   uint64_t* keys_out;     // the class region of the output key buffer
-  uint64_t* splitters;
+  uint64_t* splitters;    // 64-bit key prefixes
   uint32_t* hist;         // per slot: keys (zeroed before the launch)
   uint32_t* cursor;       // per slot: reservation cursor
   uint32_t* slot_off;     // per slot: class-relative element offset
