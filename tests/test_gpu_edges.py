@@ -202,3 +202,36 @@ def test_ordered_ingest_chunked_stats_and_permutation():
     b = lengths.index(3)
     perm = dc.handle.permutation(b, counts[b])
     assert [words3[i] for i in perm] == sorted(words3)
+
+
+def _rand_words(rng, n, L, alphabet=synth.ALNUM):
+    al = np.frombuffer(alphabet, dtype=np.uint8)
+    return [bytes(r) for r in al[rng.integers(0, len(al), size=(n, L))]]
+
+
+def test_sample_sort_shared_prefixes_and_skew():
+    # payload-mode sample sort of the multi-lane classes: a splitter prefix
+    # shared by thousands of distinct words (a prefix-equal slot beyond a tile:
+    # the block odd-even fallback), a bucket half made of one word, uniform
+    # random buckets, and bucket sizes around the tile and slot sizes
+    rng = np.random.default_rng(77)
+    words = [b"Qwertyuiopa" + w for w in _rand_words(rng, 6000, 5)]          # L = 16
+    words += [b"Zz" * 6 + w for w in _rand_words(rng, 3000, 10)]              # L = 22
+    words += [b"samewordx"] * 4000 + _rand_words(rng, 4000, 9)                # L = 9
+    for L, n in ((12, 1791), (13, 1792), (14, 1793), (7, 3839), (8, 3840), (10, 3841),
+                 (25, 20000), (32, 9000), (6, 50000)):
+        words += _rand_words(rng, n, L)
+    rng.shuffle(words)
+    text = b" ".join(words)
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
+
+
+def test_sample_sort_descending_and_sorted_inputs():
+    rng = np.random.default_rng(78)
+    for L in (6, 11, 22):
+        ws = sorted(_rand_words(rng, 30000, L, b"abcdefghijklmnopqrstuvwxyz"))
+        for seq in (ws, ws[::-1]):
+            text = b"\n".join(seq)
+            want, _ = oracle.sort_text(text, mode="fast")
+            assert sort_text(text) == want
