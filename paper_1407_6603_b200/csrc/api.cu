@@ -994,7 +994,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
   // class 0 (radix: a chain of small passes, the longest) is submitted first
   // on a high-priority stream; the multi-lane classes fill around it
-  static const int order[kClasses + 1] = {0, 4, 3, 2, 1};
+  static const int order[kClasses + 1] = {0, 1, 2, 3, 4};
   for (int oi = 0; oi <= kClasses; ++oi) {
     const int c = order[oi];
     std::vector<SegIn> segs;
