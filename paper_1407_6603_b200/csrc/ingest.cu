@@ -668,24 +668,51 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
   }
 }
 
-// kByReserve follow-up: one CTA per chunk, one warp per bin run at a time:
-// copy the run's keys from their reserved place (ingest region of the bin)
-// to their corpus-order place (run_off = exclusive scan of run_cnt over
-// chunks) in the destination layout; long-word entries likewise.
+// kByReserve follow-up: one CTA per chunk moves the chunk's runs (one per
+// bin) from their reserved place (the bin's ingest region / the long list as
+// filled) to their corpus-order place (run_off = exclusive scan of run_cnt
+// over chunks) in the destination layout. Thread k copies element k of the
+// chunk's runs laid end to end (the run by a search over 33 prefix counts),
+// so small runs do not leave lanes idle.
 __global__ void __launch_bounds__(kIngestThreads)
 reorder_runs_kernel(ReorderParams r) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ uint32_t s_pre[kNumBins + 1];
+  __shared__ uint32_t s_from[kNumBins], s_to[kNumBins];
+  const int tid = threadIdx.x;
   const uint64_t chunk = blockIdx.x;
-  for (int bin = wid; bin < kNumBins; bin += kWarps) {
-    const uint64_t cell = (uint64_t)bin * r.nchunks + chunk;
-    const uint32_t cnt = r.run_cnt[cell];
-    if (!cnt) continue;
-    const uint32_t from = r.run_at[cell], to = r.run_off[cell];
-    const uint32_t ks = r.key_bytes[bin];  // 4, 8, 16, 24 (keys) or 8 (long-word entries)
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(r.src[bin] + (uint64_t)from * ks);
-    uint32_t* dst = reinterpret_cast<uint32_t*>(r.dst[bin] + (uint64_t)to * ks);
-    const uint32_t words = cnt * (ks >> 2);
-    for (uint32_t i = lane; i < words; i += 32) dst[i] = src[i];
+  if (tid < 32) {  // bins 0..31 in lanes, bin 32 folded into lane 31's second value
+    const uint64_t cell = (uint64_t)tid * r.nchunks + chunk;
+    const uint64_t cell2 = (uint64_t)kLongBin * r.nchunks + chunk;
+    const uint32_t c = r.run_cnt[cell];
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (tid >= d) inc += t;
+    }
+    s_pre[tid] = inc - c;
+    s_from[tid] = r.run_at[cell];
+    s_to[tid] = r.run_off[cell];
+    if (tid == 31) {
+      s_pre[kLongBin] = inc;
+      s_pre[kNumBins] = inc + r.run_cnt[cell2];
+      s_from[kLongBin] = r.run_at[cell2];
+      s_to[kLongBin] = r.run_off[cell2];
+    }
+  }
+  __syncthreads();
+  const uint32_t total = s_pre[kNumBins];
+  for (uint32_t k = tid; k < total; k += kIngestThreads) {
+    int lo = 0, hi = kLongBin;  // last bin whose run starts at or before element k
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pre[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t e = k - s_pre[lo], words = r.key_bytes[lo] >> 2;
+    const uint32_t* src =
+        reinterpret_cast<const uint32_t*>(r.src[lo]) + (uint64_t)(s_from[lo] + e) * words;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(r.dst[lo]) + (uint64_t)(s_to[lo] + e) * words;
+    for (uint32_t w = 0; w < words; ++w) dst[w] = src[w];
   }
 }
 
