@@ -346,8 +346,11 @@ __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cn
   }
   // Odd-even transposition sort of the thread's E keys: E phases, each a
   // layer of independent compare-exchanges that swap on strictly-greater.
+  // (Threads holding only sentinels skip the work.)
+  const bool real = tid * E < cnt;
 #pragma unroll
   for (int ph = 0; ph < E; ++ph) {
+    if (!real) break;
 #pragma unroll
     for (int i = ph & 1; i + 1 < E; i += 2) {
       const bool sw = key_lt<LANES>(r[i + 1], r[i]);
@@ -370,6 +373,7 @@ __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cn
     __syncthreads();
     const int gt = (2 * run) / E;  // threads per merged pair
     const int a0 = (tid / gt) * 2 * run;
+    if (a0 >= cnt) continue;  // a pair of sentinel runs: r already holds sentinels
     merge_path<LANES, E, STATS>(sk + (size_t)a0 * NW, run, sk + (size_t)(a0 + run) * NW, run,
                                 si + a0, si + a0 + run, (tid % gt) * E, run, r, ri, inv);
   }
