@@ -625,37 +625,78 @@ __device__ __forceinline__ uint32_t slot_of(const uint64_t* sp, uint32_t nsplit,
   return 2 * lo + ((lo < nsplit && sp[lo] == p) ? 1u : 0u);
 }
 
-// One CTA per bucket: prefixes of an evenly spaced sample -> bitonic sort in
-// shared memory -> the nsplit splitters.
+// One CTA per bucket: prefixes of an evenly spaced sample (padded with
+// all-ones to 4096) -> bitonic sort -> the nsplit splitters. Element i =
+// 128 w + 32 q + lane lives in register q of lane `lane` of warp w, so strides
+// below 32 are shuffles, 32 and 64 are register swaps, and only strides of
+// 128 and more (15 of the 78 stages) go through shared memory.
+constexpr int kBitonicN = 4096;
+static_assert(kBitonicN == kSampleThreads * 4, "4 prefixes per thread");
+
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
-  extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ uint64_t sm[kBitonicN];
   const SampleSeg& sg = sseg_at(a, blockIdx.x);
   if (!sg.nsplit) return;
-  uint32_t P = 1;
-  while (P < sg.m) P <<= 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const KW<LANES>* in = kv<LANES>(sg.in);
   constexpr int NW = KeyTraits<LANES>::NW;
-  for (uint32_t i = threadIdx.x; i < P; i += kSampleThreads)
-    smem[i] = i < sg.m ? (uint64_t)__ldg(in + ((uint64_t)i * sg.n / sg.m) * NW) : ~0ull;
-  __syncthreads();
-  for (uint32_t size = 2; size <= P; size <<= 1) {
+  uint64_t x[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t i = w * 128 + q * 32 + lane;
+    x[q] = i < sg.m ? (uint64_t)__ldg(in + ((uint64_t)i * sg.n / sg.m) * NW) : ~0ull;
+  }
+  for (uint32_t size = 2; size <= kBitonicN; size <<= 1) {
     for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-      for (uint32_t t = threadIdx.x; t < P / 2; t += kSampleThreads) {
-        const uint32_t i = 2 * t - (t & (stride - 1));  // lower element of the pair
-        const uint32_t j = i + stride;
-        const uint64_t x = smem[i], y = smem[j];
-        if ((y < x) == ((i & size) == 0)) {
-          smem[i] = y;
-          smem[j] = x;
+      if (stride >= 128) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sm[w * 128 + q * 32 + lane] = x[q];
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < kBitonicN / 2; t += kSampleThreads) {
+          const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
+          const uint64_t u = sm[i], v = sm[j];
+          if ((v < u) == ((i & size) == 0)) {
+            sm[i] = v;
+            sm[j] = u;
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = sm[w * 128 + q * 32 + lane];
+      } else if (stride >= 32) {  // partner in another register of the same lane
+        auto cas = [&](uint64_t& u, uint64_t& v, int q) {
+          const bool up = ((uint32_t)(w * 128 + q * 32 + lane) & size) == 0;
+          const bool sw = (v < u) == up;
+          const uint64_t a0 = u, b0 = v;
+          u = sw ? b0 : a0;
+          v = sw ? a0 : b0;
+        };
+        if (stride == 64) {
+          cas(x[0], x[2], 0);
+          cas(x[1], x[3], 1);
+        } else {
+          cas(x[0], x[1], 0);
+          cas(x[2], x[3], 2);
+        }
+      } else {  // partner in another lane of the warp
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t i = w * 128 + q * 32 + lane;
+          const bool up = (i & size) == 0, lower = (lane & stride) == 0;
+          const uint64_t y = __shfl_xor_sync(0xffffffffu, x[q], (int)stride);
+          const uint64_t lo = x[q] < y ? x[q] : y, hi = x[q] < y ? y : x[q];
+          x[q] = (lower == up) ? lo : hi;
         }
       }
-      __syncthreads();
     }
   }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sm[w * 128 + q * 32 + lane] = x[q];
+  __syncthreads();
   uint64_t* sp = a.splitters + sg.split_off;
   for (uint32_t k = threadIdx.x; k < sg.nsplit; k += kSampleThreads)
-    sp[k] = smem[(uint64_t)(k + 1) * sg.m / (sg.nsplit + 1)];
+    sp[k] = sm[(uint64_t)(k + 1) * sg.m / (sg.nsplit + 1)];
 }
 
 __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t tile) {
@@ -827,8 +868,6 @@ int merge_tile_size(int lanes) {
 template <int LANES, bool STATS>
 static void set_attrs_t() {
   if (!STATS && LANES >= 1) {
-    cudaFuncSetAttribute(sample_split_kernel<LANES < 1 ? 1 : LANES>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSampleSmem);
     cudaFuncSetAttribute(subsort_kernel<LANES < 1 ? 1 : LANES>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)pass_smem_bytes<(LANES < 1 ? 1 : LANES), TileCfg<(LANES < 1 ? 1 : LANES)>::T, false>());
@@ -885,8 +924,8 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   uint32_t mmax = 0;
   for (int i = 0; i < a.nsegs; ++i) mmax = std::max(mmax, a.inl[i].m);
   while (P < mmax) P <<= 1;
-  const size_t split_smem = (size_t)P * 8;  // 64-bit prefixes
-  if (mmax) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, split_smem, st>>>(a);
+  (void)P;
+  if (mmax) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
   slot_scan_kernel<<<1, 1024, 0, st>>>(a);
   partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
