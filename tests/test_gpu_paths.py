@@ -1,0 +1,50 @@
+"""Every alternative device path selected by a diagnostic knob produces the
+same payload and stats as the default path (each knob is read once per
+process, so every case runs in a fresh interpreter)."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parent.parent
+
+SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+from oracle import oracle
+from paper_1407_6603_b200 import synth
+from paper_1407_6603_b200.pipeline import DeviceCorpus, sort_text
+text = synth.generate(4, words={words}, seed=5) + b" " + b"x" * 70 + b" " + b"Zq" * 20
+want, info = oracle.sort_text(text, mode="fast")
+assert sort_text(text) == want, "payload"
+dc = DeviceCorpus()
+dc.ingest(text)
+dc.sort(want_stats=True)
+naive = dc.stats(naive=True)
+for L, (n, inv, K, c, s, p) in info.items():
+    assert naive[L] == (c, s, p), L
+assert dc.payload() == want, "stats-mode payload"
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("knob", [
+    "WSORT_NO_RADIX",         # class 0 by tile + merge path in payload mode
+    "WSORT_NO_SAMPLE",        # multi-lane classes by tile + merge path in payload mode
+    "WSORT_LOOKBACK",         # ordered ingest by the decoupled look-back
+    "WSORT_TWO_PASS",         # count + scan + scatter ingest
+    "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest
+    "WSORT_SERIAL",           # every kernel on the main stream
+    "WSORT_D2H_PER_CLASS",    # one emit + copy per lane class
+])
+def test_diagnostic_paths_agree(knob):
+    words = 2_600_000 if knob == "WSORT_NO_CHUNKED_H2D" else 300_000  # > 16 MiB for the H2D knob
+    env = dict(os.environ, **{knob: "1"})
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=str(ROOT), words=words)],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
