@@ -1,15 +1,20 @@
 // C-ABI runtime of libwsort_b200: handles, buffer planning, pass scheduling.
 //
-// A handle owns one CUDA stream and grow-only device buffers. A public call
-// stages its small parameter tables in a pinned arena, uploads them with one
-// copy, enqueues its kernels and synchronises once at the end (the ingest
-// path also synchronises once to read the 34-entry length histogram, which
-// sizes the key arena and the pass schedule).
+// A handle owns its streams (main, one sort / emit / copy stream per lane
+// class, one upload stream) and grow-only device buffers. A public call
+// enqueues its kernels and synchronises at the end; the ingest path also
+// synchronises once to read the 34-entry length histogram, which sizes the
+// key arena and the pass schedule. Small parameter tables travel in kernel
+// parameters (or, beyond 40 entries, through one pinned staging copy).
 //
-// Buckets: lengths 1..32 are packed-key buckets grouped by key width into 4
-// lane classes (one segmented launch per class and pass); lengths > 32 are
+// Buckets: lengths 1..32 are packed-key buckets grouped by key width into
+// lane classes 0..4 (0 = one uint32 word); each class sorts on its own stream
+// (payload mode: LSD radix for class 0, sample sort for the others; stats
+// mode: tile + merge-path levels with inversion counts). Lengths > 32 are
 // "long groups" sorted by an LSD sequence of stable 1-lane passes over their
 // 8-byte lanes (most significant last), with the text as the byte store.
+// Finished buckets are emitted (and copied to the host) on side streams while
+// later passes run. ws_sort_texts runs several corpora through peer handles.
 #include <algorithm>
 #include <chrono>
 #include <cstdio>

@@ -1,18 +1,21 @@
-// Ingest: raw text -> per-length buckets of packed keys, in one two-pass
-// stream over the text.
+// Ingest: raw text -> per-length buckets of packed keys.
 //
 // Replaces, for the flat layout:
 //   tokenize       = WORD_RE.findall        (ingest.py:15, 26-28)
 //   _group_by_length (stable, corpus order) (store.py:78-82)
 //   build_flat     (count, L) uint8 blocks   (store.py:90-96)
 //
-//   K1 count_kernel   : 4 KiB chunk per CTA, uint4 loads, SWAR byte classes,
-//                       start/end bitmasks, warp-aggregated length histogram
-//                       -> hist[bin][chunk]
-//   K2 scan_kernel    : one CTA per bin row: exclusive scan over chunks
-//   K3 scatter_kernel : re-tokenise the chunk from smem, stable per-bin rank
-//                       (warp word list + __match_any_sync), pack big-endian
-//                       uint64 lanes, write at bucket_base + rank.
+// Every kernel takes one 4 KiB chunk per 256-thread CTA: uint4 loads, SWAR
+// byte classes, start/end bitmasks, word lengths across thread / warp / CTA
+// edges (segmented suffix scan of per-thread alnum runs), 6-bit codes staged
+// in shared memory, keys packed in bin-major order and stored to consecutive
+// addresses. They differ in how a chunk learns where its runs go:
+//   reserve_ingest_kernel      payload mode: one atomic per bin, any order
+//   scatter_kernel<kByReserve> stats mode: stable in-chunk order, one atomic
+//                              per bin + (position, count) per run, then
+//                              reorder_runs_kernel puts runs in corpus order
+//   scatter_kernel<kByLookback> with tokens: decoupled look-back over chunks
+//   count + scan + scatter_kernel<kByScan>  two-pass fallback (> 512 MiB)
 // A word belongs to the chunk that holds its first byte; a word running past
 // its chunk is measured by scanning forward in global memory (the text is
 // zero padded, and zero is a separator).
