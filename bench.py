@@ -67,6 +67,19 @@ def rank_info():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def reduce_over_ranks(x: float, world: int, device, op: str = "max") -> float:
+    """Whole-job figure of a per-rank value: the slowest rank's time ("max")
+    or the job's total work ("sum"); identity on one rank."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def workload_name(cfg: int) -> str:
     from paper_1407_6603_b200 import synth
 
@@ -275,11 +288,7 @@ def bench_ours(args) -> None:
             torch.distributed.barrier()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(x, world, dev, "max")
 
     text = corpus(args.config, rank)
     n = len(text)

@@ -86,14 +86,16 @@ dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
 import bench
 from paper_1407_6603_b200 import synth
-# every rank builds its own replica corpus (no data exchange), weak scaling
-text = bench.corpus(0, rank) if False else synth.generate(0, seed=synth.BASE_SEED + 7919 * rank, words=2000)
-t = torch.tensor([float(len(text))], dtype=torch.float64)
-dist.all_reduce(t, op=dist.ReduceOp.MAX)
+# every rank builds its own replica corpus (bench.corpus seeds by rank; a
+# small word count stands in for config 4), no data exchange, weak scaling
+text = synth.generate(0, seed=synth.BASE_SEED + 7919 * rank, words=2000)
+ms = 10.0 + rank  # per-rank step time: the job's time is the slowest rank's
+t_job = bench.reduce_over_ranks(ms, world, torch.device("cpu"), "max")
+words = bench.reduce_over_ranks(2000.0, world, torch.device("cpu"), "sum")
 lens = [None] * world
 dist.all_gather_object(lens, len(text))
 if rank == 0:
-    print(json.dumps({"max": t.item(), "lens": lens}))
+    print(json.dumps({"t_job": t_job, "words": words, "lens": lens}))
 dist.barrier()
 dist.destroy_process_group()
 """
@@ -111,4 +113,5 @@ def test_replica_harness_gloo_world2(tmp_path):
     outs = [p.communicate(timeout=300) for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
     res = json.loads(outs[0][0].strip().splitlines()[-1])
-    assert res["max"] == max(res["lens"]) and res["lens"][0] != res["lens"][1]
+    assert res["t_job"] == 11.0 and res["words"] == 4000.0
+    assert res["lens"][0] != res["lens"][1]  # distinct replica corpora
