@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kRThreads) radix_scan_kernel(const __grid_cons
 }
 
 template <class K>
-__global__ void __launch_bounds__(kRThreads)
+__global__ void __launch_bounds__(kRThreads, 4)
 radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
   using C = RadixCfg<K>;
   __shared__ uint32_t wcnt[kRWarps][kDigits];
