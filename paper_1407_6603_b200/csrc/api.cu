@@ -791,7 +791,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         WS_CUDA(h->overflow.ensure(256));
         WS_CUDA(cudaMemsetAsync(h->overflow.p, 0, 4, h->st));
         p.overflow = h->overflow.as<unsigned int>();
-        const uint64_t cb = ingest_chunk_bytes();
+        const uint64_t cb = reserve ? reserve_chunk_bytes() : ingest_chunk_bytes();
         // pieces of >= 8 MB let the ingest start before the whole text has
         // landed; in batch mode (gate) other corpora fill that gap, and one
         // copy keeps PCIe faster while the device->host direction is busy
@@ -843,7 +843,10 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           // algorithmic bytes: text read + keys written (estimated from the text; exact
           // counts are only known afterwards)
           Phase ph(h, "ingest", (double)n + 1.27 * (double)n);
-          launch_ingest_lookback(dtext, n, nchunks, p, h->st);
+          launch_ingest_lookback(dtext, n, reserve ? (uint32_t)((n + reserve_chunk_bytes() - 1) /
+                                                                reserve_chunk_bytes())
+                                                   : nchunks,
+                                 p, h->st);
           ++h->launches;
         }
         WS_TRY(check_launch("ingest_kernel"));

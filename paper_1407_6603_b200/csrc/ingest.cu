@@ -141,6 +141,78 @@ __device__ __forceinline__ uint32_t word_len(const Segment16& s, int i) {
   return (uint32_t)(16 - i) + s.cont;
 }
 
+// 32-byte segments (payload-mode ingest: 8 KiB chunks, two uint4 loads per
+// thread): the same classification with 32-bit start / end masks, which
+// halves the per-byte share of the shuffles, scans and barriers.
+constexpr int kChunk32 = 2 * kChunk;
+
+__device__ __forceinline__ Segment16 classify_chunk32(const uint8_t* __restrict__ text, uint64_t n,
+                                                      uint64_t cbase, uint4& v0, uint4& v1,
+                                                      uint32_t* s_chain /*[kWarps]*/,
+                                                      uint64_t avail, unsigned int* overflow) {
+  __shared__ uint32_t s_edge[2 * kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t base = cbase + (uint64_t)tid * 32;
+  v0 = make_uint4(0, 0, 0, 0);
+  v1 = make_uint4(0, 0, 0, 0);
+  if (base < n) {
+    const uint4* p = reinterpret_cast<const uint4*>(text + base);
+    v0 = p[0];
+    v1 = p[1];  // the text buffer is padded: base + 32 <= n + kTextPad
+  }
+  const uint32_t m = alnum_mask16(v0) | (alnum_mask16(v1) << 16);
+  const uint32_t up = __shfl_up_sync(0xffffffffu, m, 1);
+  const uint32_t dn = __shfl_down_sync(0xffffffffu, m, 1);
+  uint32_t edge = 0;
+  if (wid == 0 && lane == 0)
+    edge = (base > 0 && base - 1 < n) ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
+  if (wid == kWarps - 1 && lane == 31)
+    edge = (base + 32 < n) ? (uint32_t)is_alnum_byte(text[base + 32]) : 0u;
+  uint32_t V = m == ~0u ? 32u : (uint32_t)__ffs(~m) - 1;  // leading alnum bytes
+  uint32_t F = V < 32;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t V2 = __shfl_down_sync(0xffffffffu, V, d);
+    const uint32_t F2 = __shfl_down_sync(0xffffffffu, F, d);
+    if (lane + d < 32 && !F) {
+      V += V2;
+      F = F2;
+    }
+  }
+  if (lane == 0) s_chain[wid] = V | (F << 31);
+  if (lane == 0) s_edge[2 * wid] = m & 1u;
+  if (lane == 31) s_edge[2 * wid + 1] = m >> 31;
+  uint32_t cV = __shfl_down_sync(0xffffffffu, V, 1);
+  uint32_t cF = __shfl_down_sync(0xffffffffu, F, 1);
+  if (lane == 31) cV = cF = 0;
+  __syncthreads();
+  uint32_t prev = up >> 31, next = dn & 1u;
+  if (lane == 0) prev = wid == 0 ? edge : s_edge[2 * wid - 1];
+  if (lane == 31) next = wid == kWarps - 1 ? edge : s_edge[2 * wid + 2];
+  Segment16 s;
+  s.starts = m & ~((m << 1) | prev);
+  s.ends = m & ~((m >> 1) | (next << 31));
+  const bool open = s.starts && !(s.ends >> (31 - __clz(s.starts)));
+  if (open && !cF) {
+    for (int w = wid + 1; w < kWarps; ++w) {
+      const uint32_t c = s_chain[w];
+      cV += c & 0x7FFFFFFFu;
+      if (c >> 31) {
+        cF = 1;
+        break;
+      }
+    }
+    if (!cF) cV += run_length_from(text, cbase + kChunk32, avail, overflow);
+  }
+  s.cont = cV;
+  return s;
+}
+
+__device__ __forceinline__ uint32_t word_len32(const Segment16& s, int i) {
+  const uint32_t rest = s.ends >> i;
+  return rest ? (uint32_t)__ffs(rest) : (uint32_t)(32 - i) + s.cont;
+}
+
 __global__ void __launch_bounds__(kIngestThreads)
 count_kernel(const uint8_t* __restrict__ text, uint64_t n, uint32_t* __restrict__ hist,
              uint32_t nchunks) {
@@ -591,8 +663,8 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
 // (uniform length per warp batch) and stored to consecutive addresses.
 __global__ void __launch_bounds__(kIngestThreads)
 reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
-  __shared__ __align__(16) uint32_t chunk32[(kChunk + 64) / 4];
-  __shared__ uint32_t ord[kChunk / 2];  // packed words in bin-major order: start | L << 16
+  __shared__ __align__(16) uint32_t chunk32[(kChunk32 + 64) / 4];
+  __shared__ uint32_t ord[kChunk32 / 2];  // packed words in bin-major order: start | L << 16
   __shared__ uint32_t s_cnt[kHistRows];
   __shared__ uint32_t s_cur[kNumBins];  // per-bin cursors into ord (long bin: into its run)
   __shared__ uint32_t s_base[kHistRows];
@@ -602,22 +674,23 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t chunk = p.chunk0 + blockIdx.x;
-  const uint64_t cbase = chunk * kChunk;
+  const uint64_t cbase = chunk * kChunk32;
   if (tid < kHistRows) s_cnt[tid] = 0;
 
-  uint4 v;
-  Segment16 seg = classify_chunk(text, n, cbase, v, s_chain, p.avail ? p.avail : ~0ull,
-                                 p.overflow);  // has a __syncthreads
+  uint4 v0, v1;
+  Segment16 seg = classify_chunk32(text, n, cbase, v0, v1, s_chain, p.avail ? p.avail : ~0ull,
+                                   p.overflow);  // has a __syncthreads
   const bool codes = p.enc == kEncAlnum6;
-  reinterpret_cast<uint4*>(chunk32)[tid] = codes ? alnum6_codes16(v) : v;
+  reinterpret_cast<uint4*>(chunk32)[2 * tid] = codes ? alnum6_codes16(v0) : v0;
+  reinterpret_cast<uint4*>(chunk32)[2 * tid + 1] = codes ? alnum6_codes16(v1) : v1;
   if (tid < 4) {
-    uint64_t a = cbase + kChunk + 16 * tid;
+    uint64_t a = cbase + kChunk32 + 16 * tid;
     uint4 la = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
-    reinterpret_cast<uint4*>(chunk32)[kChunk / 16 + tid] = codes ? alnum6_codes16(la) : la;
+    reinterpret_cast<uint4*>(chunk32)[kChunk32 / 16 + tid] = codes ? alnum6_codes16(la) : la;
   }
   // count the chunk's words per bin (no return value, nothing kept)
   for (uint32_t s = seg.starts; s; s &= s - 1)
-    atomicAdd(&s_cnt[bin_of_len(word_len(seg, __ffs(s) - 1))], 1u);
+    atomicAdd(&s_cnt[bin_of_len(word_len32(seg, __ffs(s) - 1))], 1u);
   const uint32_t words = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(seg.starts));
   if (lane == 0 && words) atomicAdd(&s_cnt[kNumBins], words);
   __syncthreads();  // also publishes chunk32
@@ -641,9 +714,9 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
   // place every word: packed ones into ord (bin-major), long ones into their run
   for (uint32_t s = seg.starts; s; s &= s - 1) {
     const int i = __ffs(s) - 1;
-    const uint32_t L = word_len(seg, i), bin = bin_of_len(L);
+    const uint32_t L = word_len32(seg, i), bin = bin_of_len(L);
     const uint32_t at = atomicAdd(&s_cur[bin], 1u);
-    const uint32_t start = (uint32_t)(tid * 16 + i);
+    const uint32_t start = (uint32_t)(tid * 32 + i);
     if (bin != (uint32_t)kLongBin)
       ord[at] = start | (L << 16);
     else if (p.keys)
@@ -869,6 +942,7 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }
+uint32_t reserve_chunk_bytes() { return kChunk32; }
 
 void launch_reorder_runs(const ReorderParams& r, cudaStream_t st) {
   if (r.nchunks) reorder_runs_kernel<<<r.nchunks, kIngestThreads, 0, st>>>(r);

@@ -55,6 +55,7 @@ void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32
 void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st);
 uint32_t ingest_chunk_bytes();
+uint32_t reserve_chunk_bytes();  // payload-mode (reserve_ingest_kernel) chunks
 void launch_words_hist(const uint32_t* lens, uint64_t nwords, uint32_t wpw, uint32_t* whist,
                        uint32_t nwarps, cudaStream_t st);
 void launch_words_scatter(const uint8_t* bytes, const uint64_t* starts, const uint32_t* lens,
