@@ -71,8 +71,9 @@ __device__ __forceinline__ uint32_t alnum_mask4(uint32_t v) {
   const uint32_t f = x | 0x20202020u;
   const uint32_t l = (f + 0x1f1f1f1fu) & ~(f + 0x05050505u);
   uint32_t m = (d | l) & 0x80808080u & ~hi;
-  // gather bit 7 of each byte into bits 0..3
-  return ((m >> 7) & 1u) | ((m >> 14) & 2u) | ((m >> 21) & 4u) | ((m >> 28) & 8u);
+  // gather bit 7 of each byte into bits 0..3: the multiply by 2^0 + 2^7 +
+  // 2^14 + 2^21 lands bits 7, 15, 23, 31 on 28, 29, 30, 31 without carries
+  return (m * 0x00204081u) >> 28;
 }
 
 __device__ __forceinline__ uint32_t alnum_mask16(uint4 v) {
