@@ -1482,6 +1482,7 @@ int ws_create(ws_handle** out, int32_t device) {
     std::lock_guard<std::mutex> lk(mu);
     if (!(attr_done & (1ull << device))) {
       set_sort_attributes();
+      set_ingest_attributes();
       WS_CUDA(cudaGetLastError());
       attr_done |= 1ull << device;
     }

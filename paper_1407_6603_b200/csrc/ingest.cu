@@ -19,12 +19,17 @@
 // A word belongs to the chunk that holds its first byte; a word running past
 // its chunk is measured by scanning forward in global memory (the text is
 // zero padded, and zero is a separator).
+#include <type_traits>
+
 #include "ws_common.cuh"
 #include "ws_kernels.h"
 
 namespace ws {
 
 constexpr int kChunk = 4096;
+#ifndef WS_RESERVE_SB
+#define WS_RESERVE_SB 32  // bytes per thread of the payload-mode ingest (32 or 64; 64 measured slower)
+#endif
 constexpr int kIngestThreads = 256;  // 16 bytes per thread
 constexpr int kWarps = kIngestThreads / 32;
 constexpr int kMaxWordsPerWarp = 256;  // 512 bytes per warp, <= 1 start per 2 bytes
@@ -141,35 +146,49 @@ __device__ __forceinline__ uint32_t word_len(const Segment16& s, int i) {
   return (uint32_t)(16 - i) + s.cont;
 }
 
-// 32-byte segments (payload-mode ingest: 8 KiB chunks, two uint4 loads per
-// thread): the same classification with 32-bit start / end masks, which
-// halves the per-byte share of the shuffles, scans and barriers.
-constexpr int kChunk32 = 2 * kChunk;
+// Wide segments (payload-mode ingest): SB = 32 or 64 bytes per thread, i.e.
+// 8 or 16 KiB chunks per CTA, SB / 16 uint4 loads per thread and SB-bit start
+// / end masks. The per-thread share of the shuffles, scans and barriers is
+// spread over 2-4x the bytes of the 16-byte classification above.
+template <int SB>
+struct SegW {
+  using M = typename std::conditional<SB == 64, unsigned long long, uint32_t>::type;
+  M starts, ends;
+  uint32_t cont;
+};
 
-__device__ __forceinline__ Segment16 classify_chunk32(const uint8_t* __restrict__ text, uint64_t n,
-                                                      uint64_t cbase, uint4& v0, uint4& v1,
-                                                      uint32_t* s_chain /*[kWarps]*/,
-                                                      uint64_t avail, unsigned int* overflow) {
+template <int SB>
+__device__ __forceinline__ int ffsw(typename SegW<SB>::M x) {
+  if constexpr (SB == 64) return __ffsll((long long)x); else return __ffs((int)x);
+}
+
+template <int SB>
+__device__ __forceinline__ SegW<SB> classify_wide(const uint8_t* __restrict__ text, uint64_t n,
+                                                  uint64_t cbase, uint4 (&v)[SB / 16],
+                                                  uint32_t* s_chain /*[kWarps]*/, uint64_t avail,
+                                                  unsigned int* overflow) {
+  using M = typename SegW<SB>::M;
+  constexpr int NV = SB / 16;
+  constexpr uint64_t kCB = (uint64_t)SB * kIngestThreads;
   __shared__ uint32_t s_edge[2 * kWarps];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint64_t base = cbase + (uint64_t)tid * 32;
-  v0 = make_uint4(0, 0, 0, 0);
-  v1 = make_uint4(0, 0, 0, 0);
-  if (base < n) {
-    const uint4* p = reinterpret_cast<const uint4*>(text + base);
-    v0 = p[0];
-    v1 = p[1];  // the text buffer is padded: base + 32 <= n + kTextPad
+  const uint64_t base = cbase + (uint64_t)tid * SB;
+  M m = 0;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    v[k] = make_uint4(0, 0, 0, 0);
+    if (base < n) v[k] = reinterpret_cast<const uint4*>(text + base)[k];  // padded text
+    m |= (M)alnum_mask16(v[k]) << (16 * k);
   }
-  const uint32_t m = alnum_mask16(v0) | (alnum_mask16(v1) << 16);
-  const uint32_t up = __shfl_up_sync(0xffffffffu, m, 1);
-  const uint32_t dn = __shfl_down_sync(0xffffffffu, m, 1);
+  const M up = __shfl_up_sync(0xffffffffu, m, 1);
+  const M dn = __shfl_down_sync(0xffffffffu, m, 1);
   uint32_t edge = 0;
   if (wid == 0 && lane == 0)
     edge = (base > 0 && base - 1 < n) ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u;
   if (wid == kWarps - 1 && lane == 31)
-    edge = (base + 32 < n) ? (uint32_t)is_alnum_byte(text[base + 32]) : 0u;
-  uint32_t V = m == ~0u ? 32u : (uint32_t)__ffs(~m) - 1;  // leading alnum bytes
-  uint32_t F = V < 32;
+    edge = (base + SB < n) ? (uint32_t)is_alnum_byte(text[base + SB]) : 0u;
+  uint32_t V = m == (M)~(M)0 ? (uint32_t)SB : (uint32_t)ffsw<SB>(~m) - 1;  // leading alnum bytes
+  uint32_t F = V < (uint32_t)SB;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
     const uint32_t V2 = __shfl_down_sync(0xffffffffu, V, d);
@@ -180,19 +199,21 @@ __device__ __forceinline__ Segment16 classify_chunk32(const uint8_t* __restrict_
     }
   }
   if (lane == 0) s_chain[wid] = V | (F << 31);
-  if (lane == 0) s_edge[2 * wid] = m & 1u;
-  if (lane == 31) s_edge[2 * wid + 1] = m >> 31;
+  if (lane == 0) s_edge[2 * wid] = (uint32_t)(m & 1u);
+  if (lane == 31) s_edge[2 * wid + 1] = (uint32_t)(m >> (SB - 1));
   uint32_t cV = __shfl_down_sync(0xffffffffu, V, 1);
   uint32_t cF = __shfl_down_sync(0xffffffffu, F, 1);
   if (lane == 31) cV = cF = 0;
   __syncthreads();
-  uint32_t prev = up >> 31, next = dn & 1u;
+  M prev = up >> (SB - 1), next = dn & 1u;
   if (lane == 0) prev = wid == 0 ? edge : s_edge[2 * wid - 1];
   if (lane == 31) next = wid == kWarps - 1 ? edge : s_edge[2 * wid + 2];
-  Segment16 s;
+  SegW<SB> s;
   s.starts = m & ~((m << 1) | prev);
-  s.ends = m & ~((m >> 1) | (next << 31));
-  const bool open = s.starts && !(s.ends >> (31 - __clz(s.starts)));
+  s.ends = m & ~((m >> 1) | (next << (SB - 1)));
+  int last = 0;  // highest start bit
+  if constexpr (SB == 64) last = 63 - __clzll((long long)s.starts); else last = 31 - __clz((int)s.starts);
+  const bool open = s.starts && !(s.ends >> last);
   if (open && !cF) {
     for (int w = wid + 1; w < kWarps; ++w) {
       const uint32_t c = s_chain[w];
@@ -202,15 +223,16 @@ __device__ __forceinline__ Segment16 classify_chunk32(const uint8_t* __restrict_
         break;
       }
     }
-    if (!cF) cV += run_length_from(text, cbase + kChunk32, avail, overflow);
+    if (!cF) cV += run_length_from(text, cbase + kCB, avail, overflow);
   }
   s.cont = cV;
   return s;
 }
 
-__device__ __forceinline__ uint32_t word_len32(const Segment16& s, int i) {
-  const uint32_t rest = s.ends >> i;
-  return rest ? (uint32_t)__ffs(rest) : (uint32_t)(32 - i) + s.cont;
+template <int SB>
+__device__ __forceinline__ uint32_t word_len_w(const SegW<SB>& s, int i) {
+  const typename SegW<SB>::M rest = s.ends >> i;
+  return rest ? (uint32_t)ffsw<SB>(rest) : (uint32_t)(SB - i) + s.cont;
 }
 
 __global__ void __launch_bounds__(kIngestThreads)
@@ -661,10 +683,14 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
 // atomic (no per-warp ranking pass), and each chunk reserves its bin runs in
 // HBM with one global atomic per bin. Keys are then packed in bin-major order
 // (uniform length per warp batch) and stored to consecutive addresses.
+template <int SB>
 __global__ void __launch_bounds__(kIngestThreads)
 reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
-  __shared__ __align__(16) uint32_t chunk32[(kChunk32 + 64) / 4];
-  __shared__ uint32_t ord[kChunk32 / 2];  // packed words in bin-major order: start | L << 16
+  constexpr int kCB = SB * kIngestThreads;  // chunk bytes
+  constexpr int NV = SB / 16;
+  extern __shared__ __align__(16) uint32_t dyn_smem[];
+  uint32_t* chunk32 = dyn_smem;                  // (kCB + 64) bytes of 6-bit codes
+  uint32_t* ord = dyn_smem + (kCB + 64) / 4;     // kCB / 2 words, bin-major
   __shared__ uint32_t s_cnt[kHistRows];
   __shared__ uint32_t s_cur[kNumBins];  // per-bin cursors into ord (long bin: into its run)
   __shared__ uint32_t s_base[kHistRows];
@@ -674,24 +700,28 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint64_t chunk = p.chunk0 + blockIdx.x;
-  const uint64_t cbase = chunk * kChunk32;
+  const uint64_t cbase = chunk * kCB;
   if (tid < kHistRows) s_cnt[tid] = 0;
 
-  uint4 v0, v1;
-  Segment16 seg = classify_chunk32(text, n, cbase, v0, v1, s_chain, p.avail ? p.avail : ~0ull,
-                                   p.overflow);  // has a __syncthreads
+  uint4 v[NV];
+  const SegW<SB> seg = classify_wide<SB>(text, n, cbase, v, s_chain, p.avail ? p.avail : ~0ull,
+                                         p.overflow);  // has a __syncthreads
   const bool codes = p.enc == kEncAlnum6;
-  reinterpret_cast<uint4*>(chunk32)[2 * tid] = codes ? alnum6_codes16(v0) : v0;
-  reinterpret_cast<uint4*>(chunk32)[2 * tid + 1] = codes ? alnum6_codes16(v1) : v1;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+    reinterpret_cast<uint4*>(chunk32)[NV * tid + q] = codes ? alnum6_codes16(v[q]) : v[q];
   if (tid < 4) {
-    uint64_t a = cbase + kChunk32 + 16 * tid;
+    uint64_t a = cbase + kCB + 16 * tid;
     uint4 la = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
-    reinterpret_cast<uint4*>(chunk32)[kChunk32 / 16 + tid] = codes ? alnum6_codes16(la) : la;
+    reinterpret_cast<uint4*>(chunk32)[kCB / 16 + tid] = codes ? alnum6_codes16(la) : la;
   }
   // count the chunk's words per bin (no return value, nothing kept)
-  for (uint32_t s = seg.starts; s; s &= s - 1)
-    atomicAdd(&s_cnt[bin_of_len(word_len32(seg, __ffs(s) - 1))], 1u);
-  const uint32_t words = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(seg.starts));
+  using M = typename SegW<SB>::M;
+  for (M s = seg.starts; s; s &= s - 1)
+    atomicAdd(&s_cnt[bin_of_len(word_len_w<SB>(seg, ffsw<SB>(s) - 1))], 1u);
+  uint32_t nw = 0;
+  if constexpr (SB == 64) nw = __popcll(seg.starts); else nw = __popc(seg.starts);
+  const uint32_t words = __reduce_add_sync(0xffffffffu, nw);
   if (lane == 0 && words) atomicAdd(&s_cnt[kNumBins], words);
   __syncthreads();  // also publishes chunk32
   if (tid < kHistRows && s_cnt[tid]) s_base[tid] = atomicAdd(p.fill + tid, s_cnt[tid]);
@@ -712,11 +742,11 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
   }
   __syncthreads();
   // place every word: packed ones into ord (bin-major), long ones into their run
-  for (uint32_t s = seg.starts; s; s &= s - 1) {
-    const int i = __ffs(s) - 1;
-    const uint32_t L = word_len32(seg, i), bin = bin_of_len(L);
+  for (M s = seg.starts; s; s &= s - 1) {
+    const int i = ffsw<SB>(s) - 1;
+    const uint32_t L = word_len_w<SB>(seg, i), bin = bin_of_len(L);
     const uint32_t at = atomicAdd(&s_cur[bin], 1u);
-    const uint32_t start = (uint32_t)(tid * 32 + i);
+    const uint32_t start = (uint32_t)(tid * SB + i);
     if (bin != (uint32_t)kLongBin)
       ord[at] = start | (L << 16);
     else if (p.keys)
@@ -930,19 +960,30 @@ void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32
   if (nchunks) scatter_kernel<kByScan><<<nchunks, kIngestThreads, 0, st>>>(text, n, off, nchunks, p);
 }
 
+constexpr int kReserveSB = WS_RESERVE_SB;
+static_assert(kReserveSB == 32 || kReserveSB == 64, "payload ingest: 32 or 64 bytes per thread");
+static size_t reserve_smem_bytes() {
+  return (size_t)(kReserveSB * kIngestThreads + 64) + (size_t)kReserveSB * kIngestThreads / 2 * 4;
+}
+
+void set_ingest_attributes() {
+  cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve_smem_bytes());
+}
+
 void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st) {
   if (!nchunks) return;
   if (p.fill && p.run_at)
     scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
   else if (p.fill)
-    reserve_ingest_kernel<<<nchunks, kIngestThreads, 0, st>>>(text, n, p);
+    reserve_ingest_kernel<kReserveSB><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(text, n, p);
   else
     scatter_kernel<kByLookback><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }
-uint32_t reserve_chunk_bytes() { return kChunk32; }
+uint32_t reserve_chunk_bytes() { return kReserveSB * kIngestThreads; }
 
 void launch_reorder_runs(const ReorderParams& r, cudaStream_t st) {
   if (r.nchunks) reorder_runs_kernel<<<r.nchunks, kIngestThreads, 0, st>>>(r);
