@@ -61,15 +61,15 @@ __device__ __forceinline__ uint32_t digit_of(K key, uint32_t shift) {
 }
 
 // Lanes of the warp holding the same 8-bit digit (8 ballots; invalid lanes,
-// ok == false, match nobody valid). Cheaper than match.any on sm_100.
+// ok == false, match nobody valid). Measured no slower than match.any.
 __device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool ok) {
   uint32_t peers = __ballot_sync(0xffffffffu, ok);
   if (!ok) peers = ~peers;
 #pragma unroll
   for (int b = 0; b < 8; ++b) {
-    const bool bit = (d >> b) & 1u;
+    const uint32_t bit = (d >> b) & 1u;
     const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-    peers &= bit ? bal : ~bal;
+    peers &= bal ^ (bit - 1u);  // lanes whose bit b equals mine (one LOP3)
   }
   return peers;
 }
