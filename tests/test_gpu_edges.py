@@ -50,12 +50,25 @@ def test_separator_bytes():
 
 
 def test_words_crossing_chunk_boundaries():
-    # words straddling the 16-byte, 512-byte (warp) and 4096-byte (CTA) edges
+    # words straddling the 16/32-byte (thread), warp and 4/8 KiB (CTA chunk:
+    # ordered / payload ingest) edges
     parts = []
-    for edge in (16, 512, 4096, 8192):
+    for edge in (16, 32, 512, 1024, 4096, 8192, 16384):
         pad = b"x " * ((edge - 7) // 2)
         parts.append(pad + b" ab" + b"C" * 9 + b"d" * 30 + b" ")
     check_text(b"".join(parts) * 3)
+
+
+def test_word_spanning_whole_chunks_payload_mode():
+    # a word covering several whole 8 KiB payload-mode chunks (no start or end
+    # inside them) next to words that start / end exactly on chunk edges
+    big = b"W" * 20000
+    text = b"ab " * 2730 + b"c" + big + b" " + b"d" * 8191 + b" e" + b" f" * 9000
+    want, _ = oracle.sort_text(text, mode="fast", max_len=40000)
+    assert sort_text(text) == want
+    for shift in range(1, 40, 7):
+        t = b" " * shift + text
+        assert sort_text(t) == want
 
 
 @pytest.mark.parametrize("L", [1, 7, 8, 9, 16, 17, 24, 25, 32, 33, 40, 64, 65, 100, 1000])
