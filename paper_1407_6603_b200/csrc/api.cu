@@ -517,9 +517,9 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   uint32_t slots = 0, splits = 0, tiles = 0;
   for (auto& s : segs) {
     s.final_buf = 1;
-    // slots of ~T/3 on average; a sample of >= 8 keys per slot keeps the
-    // chance that a slot exceeds T (the slow fallback) negligible
-    const uint64_t target = (uint64_t)T / 3;
+    // slots of half a slot-sort tile on average; a sample of >= 8 keys per
+    // slot keeps slots beyond the tile (the slower fallback) rare
+    const uint64_t target = (uint64_t)subsort_tile_size(lanes) / 2;
     uint64_t S = s.n <= T ? 1 : (s.n + target - 1) / target;
     S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 8));
     SampleSeg g;

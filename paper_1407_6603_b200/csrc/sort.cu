@@ -332,13 +332,14 @@ __device__ __forceinline__ void smem_to_global(const KW<LANES>* sk, const uint32
 // merge the runs. Levels stop once a run covers all cnt real keys (the
 // sentinels behind them are already in place). Leaves the thread's E
 // outputs of the sorted tile (blocked) in r / ri; idx0 = idx of key 0.
-template <int LANES, bool STATS>
+// NT = the CTA's threads (the tile holds NT * E keys).
+template <int LANES, bool STATS, int NT = kTileThreads>
 __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cnt, uint32_t idx0,
                                              Key<LANES> (&r)[TileCfg<LANES>::E],
                                              uint32_t (&ri)[TileCfg<LANES>::E], uint64_t& inv) {
-  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T;
+  constexpr int E = TileCfg<LANES>::E, T = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
-  const int tid = threadIdx.x;
+  const int tid = (int)threadIdx.x;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     r[k] = ldk<LANES>(sk, tid * E + k);
@@ -791,16 +792,18 @@ __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__
   }
 }
 
-// One CTA per slot: sort the slot in place (tile network; block odd-even
-// transposition over half tiles when it exceeds a tile). A prefix-equal slot
-// whose keys are all identical (repeated words) is left as it is.
+// One 128-thread CTA per slot: the slot is sorted in place by the tile
+// network of a half-size tile (slots average half of it), or - beyond it, rare
+// - by block odd-even transposition over quarter-size blocks. A prefix-equal
+// slot whose keys are all identical (repeated words) is left as it is.
+constexpr int kSubThreads = 128;
+
 template <int LANES>
-__global__ void __launch_bounds__(kTileThreads) subsort_kernel(const __grid_constant__ SampleLaunch a) {
-  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
+__global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_constant__ SampleLaunch a) {
+  constexpr int E = TileCfg<LANES>::E, NT = kSubThreads, TS = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
   extern __shared__ __align__(16) uint64_t smem[];
-  __shared__ int s_differs;
   W* sk = reinterpret_cast<W*>(smem);
   const uint32_t s = blockIdx.x;
   const uint32_t cnt = a.hist[s];
@@ -809,8 +812,6 @@ __global__ void __launch_bounds__(kTileThreads) subsort_kernel(const __grid_cons
   int b = 0;  // bucket of the slot (segments ascend by slot_base)
   while (b + 1 < a.nsegs && sseg_at(a, b + 1).slot_base <= s) ++b;
   if (((s - sseg_at(a, b).slot_base) & 1u) != 0) {  // prefix-equal slot
-    if (threadIdx.x == 0) s_differs = 0;
-    __syncthreads();
     const Key<LANES> k0 = ldk<LANES>(base, 0);
     bool diff = false;
     for (uint32_t i = threadIdx.x; i < cnt; i += NT) diff |= key_lt<LANES>(k0, ldk<LANES>(base, (int)i));
@@ -819,26 +820,26 @@ __global__ void __launch_bounds__(kTileThreads) subsort_kernel(const __grid_cons
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
-  auto sort_span = [&](W* g, uint32_t c) {  // c <= T keys at g, sorted in place
-    for (uint32_t j = threadIdx.x; j < (uint32_t)T * NW; j += NT)
+  auto sort_span = [&](W* g, uint32_t c) {  // c <= TS keys at g, sorted in place
+    for (uint32_t j = threadIdx.x; j < (uint32_t)TS * NW; j += NT)
       sk[j] = j < c * NW ? g[j] : ~W(0);
     __syncthreads();
-    tile_network<LANES, false>(sk, nullptr, (int)c, 0u, r, ri, inv);
+    tile_network<LANES, false, NT>(sk, nullptr, (int)c, 0u, r, ri, inv);
     __syncthreads();
     regs_to_smem<LANES, E, false>(sk, nullptr, threadIdx.x * E, r, ri);
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < c * NW; j += NT) g[j] = sk[j];
     __syncthreads();
   };
-  if (cnt <= (uint32_t)T) {
+  if (cnt <= (uint32_t)TS) {
     sort_span(base, cnt);
     return;
   }
-  constexpr uint32_t H = T / 2;
-  const uint32_t blocks = (cnt + H - 1) / H;
+  constexpr uint32_t HB = TS / 2;
+  const uint32_t blocks = (cnt + HB - 1) / HB;
   for (uint32_t round = 0; round < blocks; ++round)
     for (uint32_t p = round & 1; p + 1 < blocks; p += 2) {
-      const uint32_t lo = p * H, hi = min(cnt, (p + 2) * H);
+      const uint32_t lo = p * HB, hi = min(cnt, (p + 2) * HB);
       sort_span(base + (uint64_t)lo * NW, hi - lo);
     }
 }
@@ -870,7 +871,8 @@ static void set_attrs_t() {
   if (!STATS && LANES >= 1) {
     cudaFuncSetAttribute(subsort_kernel<LANES < 1 ? 1 : LANES>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)pass_smem_bytes<(LANES < 1 ? 1 : LANES), TileCfg<(LANES < 1 ? 1 : LANES)>::T, false>());
+                         (int)pass_smem_bytes<(LANES < 1 ? 1 : LANES),
+                                              kSubThreads * TileCfg<(LANES < 1 ? 1 : LANES)>::E, false>());
   }
   cudaFuncSetAttribute(tile_sort_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>());
@@ -929,12 +931,13 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
   slot_scan_kernel<<<1, 1024, 0, st>>>(a);
   partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
-  subsort_kernel<LANES><<<a.nslots, kTileThreads,
-                          pass_smem_bytes<LANES, TileCfg<LANES>::T, false>(), st>>>(a);
+  subsort_kernel<LANES><<<a.nslots, kSubThreads,
+                          pass_smem_bytes<LANES, kSubThreads * TileCfg<LANES>::E, false>(), st>>>(a);
 }
 
 int sample_max_keys(int) { return kSampleSmem / 8; }
 int part_tile_size() { return kPartTile; }
+int subsort_tile_size(int lanes) { return kSubThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E); }
 
 void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st) {
   switch (lanes) {

@@ -114,6 +114,7 @@ struct SampleLaunch {
 };
 int sample_max_keys(int lanes);
 int part_tile_size();
+int subsort_tile_size(int lanes);  // keys one slot-sort CTA sorts in one network
 void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st);
 int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
