@@ -519,7 +519,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
     s.final_buf = 1;
     // slots of half a slot-sort tile on average; a sample of >= 8 keys per
     // slot keeps slots beyond the tile (the slower fallback) rare
-    const uint64_t target = (uint64_t)subsort_tile_size(lanes) / 2;
+    const uint64_t target = (uint64_t)subsort_tile_size(lanes) / 2;  // (measured: T/1.4..T/3 within noise)
     uint64_t S = s.n <= T ? 1 : (s.n + target - 1) / target;
     S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 8));
     SampleSeg g;
