@@ -355,4 +355,6 @@ def test_verify_words_all_layouts():
 #    path spawns no worker threads (one segmented launch replaces the pool).
 #  * test_acceptance.py criterion 7/8 and test_bench.py strip<sort -- timing
 #    relations of the CPU implementation.
-#  * bench CLI subcommand -- the CPU scaling harness is out of scope.
+# test_bench.py (speedup / efficiency arithmetic, CSV / JSON / plot reports,
+# the timing matrix and the `bench` subcommand) is restated in
+# tests/test_harness.py against paper_1407_6603_b200/harness.py.
