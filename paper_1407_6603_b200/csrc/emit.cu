@@ -75,14 +75,27 @@ emit_kernel(const __grid_constant__ EmitTable t, uint8_t* __restrict__ out, int 
   const uint64_t o0 = sg.out_off + w0 * stride;
   const int mis = (int)(o0 & 15);
   constexpr int NL = LANES < 1 ? 1 : LANES;  // lanes of the unpacked key
-  for (int j = threadIdx.x; j < cnt; j += kEmitThreads) {
-    uint64_t k[NL];
-    if constexpr (LANES == 0) {  // one uint32 word: the top half of a lane
-      k[0] = (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(sg.keys) + w0 + j) << 32;
-    } else {
+  constexpr int PER = kEmitWords / kEmitThreads;
+  uint64_t kk[PER][NL];  // every key of the thread in flight before the first unpack
 #pragma unroll
-      for (int l = 0; l < LANES; ++l) k[l] = __ldg(sg.keys + (w0 + j) * LANES + l);
+  for (int q = 0; q < PER; ++q) {
+    const int j = threadIdx.x + q * kEmitThreads;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) kk[q][l] = 0;
+    if (j < cnt) {
+      if constexpr (LANES == 0) {  // one uint32 word: the top half of a lane
+        kk[q][0] = (uint64_t)__ldg(reinterpret_cast<const uint32_t*>(sg.keys) + w0 + j) << 32;
+      } else {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) kk[q][l] = __ldg(sg.keys + (w0 + j) * LANES + l);
+      }
     }
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int j = threadIdx.x + q * kEmitThreads;
+    if (j >= cnt) break;
+    const uint64_t (&k)[NL] = kk[q];
     uint8_t* dst = buf + mis + j * stride;
     if constexpr (ENC == kEncAlnum6) {
       unpack6<NL>(k, L, dst);
