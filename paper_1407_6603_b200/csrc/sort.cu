@@ -737,11 +737,15 @@ __global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_co
   Key<LANES> k[kPartPer];
   uint32_t slot[kPartPer], rank[kPartPer];
 #pragma unroll
+  for (int q = 0; q < kPartPer; ++q) {  // every load in flight before the first search
+    const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
+    if (i < sg.n) k[q] = gld<LANES>(in, (int64_t)i);
+  }
+#pragma unroll
   for (int q = 0; q < kPartPer; ++q) {
     const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
     slot[q] = 0xFFFFFFFFu;
     if (i < sg.n) {
-      k[q] = gld<LANES>(in, (int64_t)i);
       slot[q] = slot_of(s_split, sg.nsplit, prefix_of<LANES>(k[q]));
       rank[q] = atomicAdd(&s_cnt[slot[q]], 1u);
     }
@@ -821,8 +825,15 @@ __global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_const
   uint32_t ri[E];
   uint64_t inv = 0;
   auto sort_span = [&](W* g, uint32_t c) {  // c <= TS keys at g, sorted in place
-    for (uint32_t j = threadIdx.x; j < (uint32_t)TS * NW; j += NT)
-      sk[j] = j < c * NW ? g[j] : ~W(0);
+    constexpr int PW = E * NW;  // words per thread: all loads in flight, then the stores
+    W v[PW];
+#pragma unroll
+    for (int q = 0; q < PW; ++q) {
+      const uint32_t j = threadIdx.x + q * NT;
+      v[q] = j < c * NW ? g[j] : ~W(0);
+    }
+#pragma unroll
+    for (int q = 0; q < PW; ++q) sk[threadIdx.x + q * NT] = v[q];
     __syncthreads();
     tile_network<LANES, false, NT>(sk, nullptr, (int)c, 0u, r, ri, inv);
     __syncthreads();
