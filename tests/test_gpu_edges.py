@@ -248,3 +248,25 @@ def test_sample_sort_descending_and_sorted_inputs():
             text = b"\n".join(seq)
             want, _ = oracle.sort_text(text, mode="fast")
             assert sort_text(text) == want
+
+
+def test_payload_mode_raw_byte_words():
+    # word lists with arbitrary bytes (raw 8-bit keys) sorted without stats:
+    # class 0 by the radix passes, the wider classes by the sample sort with
+    # 8-byte prefixes (shared prefixes, 0x00 / 0xff bytes, many duplicates)
+    rng = np.random.default_rng(90)
+    words = []
+    for L, n in ((1, 3000), (3, 9000), (4, 40000), (5, 30000), (8, 20000), (9, 25000),
+                 (12, 20000), (17, 8000), (24, 6000), (31, 5000), (32, 4000), (40, 500)):
+        rows = rng.integers(0, 256, size=(n, L), dtype=np.uint8)
+        rows[::5] = rows[0]                       # duplicates
+        rows[::7, : min(L, 9)] = 0xFF             # shared high prefixes
+        rows[::11, : min(L, 8)] = 0x00            # shared low prefixes
+        words += [bytes(r) for r in rows]
+    rng.shuffle(words)
+    h = _native.Handle(0)
+    h.ingest_words(words)
+    h.sort(False)
+    want = b"".join(w + b"\n" for w in sorted(words, key=lambda w: (len(w), w)))
+    assert h.emit_lines().tobytes() == want
+    h.close()
