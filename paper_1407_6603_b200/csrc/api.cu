@@ -507,6 +507,12 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
 // ~T/2 keys (plus one slot per splitter for keys equal to it), scattered into
 // the output buffer and sorted slot by slot on chip. Five launches per class
 // whatever the bucket sizes; the result is in buffer 1.
+// Largest bucket the sample sort keeps at its slot size (the splitter and
+// sample budget: kMaxSplit + 1 slots of half a slot-sort tile).
+uint64_t sample_bucket_limit(int lanes) {
+  return (uint64_t)(kMaxSplit + 1) * (uint64_t)(subsort_tile_size(lanes) / 2);
+}
+
 int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* out_class,
                          cudaStream_t st, const PassDoneHook* on_done) {
   const uint32_t T = (uint32_t)tile_size(lanes);
@@ -1063,7 +1069,23 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     if (!stats && c == 0 && !(no_radix && no_radix[0] == '1')) {
       WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, on_done));
     } else if (!stats && c >= 1 && !(no_sample && no_sample[0] == '1')) {
-      WS_TRY(sample_sort_segments(h, c, segs, k1, cst, on_done));
+      // buckets beyond what the splitter budget keeps at slot size go through
+      // the merge path (same stream; both leave per-bucket final buffers)
+      std::vector<SegIn> fit, big;
+      std::vector<int> fit_w, big_w;
+      const uint64_t cap = sample_bucket_limit(c);
+      for (size_t j = 0; j < segs.size(); ++j) {
+        if (segs[j].n <= cap) { fit.push_back(segs[j]); fit_w.push_back(which[j]); }
+        else { big.push_back(segs[j]); big_w.push_back(which[j]); }
+      }
+      if (!fit.empty()) WS_TRY(sample_sort_segments(h, c, fit, k1, cst, on_done));
+      if (!big.empty())
+        WS_TRY(sort_segments(h, c, big, k0, k1, h->idx[0].as<uint32_t>(), h->idx[1].as<uint32_t>(),
+                             false, nullptr, nullptr, "", cst, on_done));
+      size_t fi = 0, bi = 0;  // final buffers back into the class's segment order
+      for (size_t j = 0; j < segs.size(); ++j)
+        segs[j].final_buf = segs[j].n <= cap ? fit[fi++].final_buf : big[bi++].final_buf;
+      (void)fit_w; (void)big_w;
     } else {
       WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(),
                            h->idx[1].as<uint32_t>(), stats, inv, km, "", cst, on_done));

@@ -765,17 +765,20 @@ __global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_co
     if (slot[q] != 0xFFFFFFFFu) stk<LANES>(out, (int)(s_base[slot[q]] + rank[q]), k[q]);
 }
 
-// Exclusive scan of the class's slot counts (one CTA): slot offsets, which
-// are class-relative element offsets because buckets lie back to back.
+// Exclusive scan of each bucket's slot counts (one CTA per bucket), started
+// at the bucket's class-relative key offset: the slot offsets, valid for any
+// subset of a class's buckets.
 __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__ SampleLaunch a) {
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) s_carry = sseg_at(a, 0).key_off;  // class-relative start of the first bucket
+  const SampleSeg& sg = sseg_at(a, blockIdx.x);
+  const uint32_t nslot = 2 * sg.nsplit + 1;
+  if (tid == 0) s_carry = sg.key_off;
   __syncthreads();
-  for (uint32_t base = 0; base < a.nslots; base += 1024) {
+  for (uint32_t base = 0; base < nslot; base += 1024) {
     const uint32_t i = base + tid;
-    const uint32_t v = i < a.nslots ? a.hist[i] : 0u;
+    const uint32_t v = i < nslot ? a.hist[sg.slot_base + i] : 0u;
     uint32_t inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -786,9 +789,9 @@ __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__
     __syncthreads();
     uint32_t pre = s_carry;
     for (int w = 0; w < wid; ++w) pre += s_w[w];
-    if (i < a.nslots) {
-      a.slot_off[i] = pre + inc - v;
-      a.cursor[i] = pre + inc - v;
+    if (i < nslot) {
+      a.slot_off[sg.slot_base + i] = pre + inc - v;
+      a.cursor[sg.slot_base + i] = pre + inc - v;
     }
     __syncthreads();
     if (tid == 1023) s_carry = pre + inc;
@@ -940,7 +943,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   (void)P;
   if (mmax) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
-  slot_scan_kernel<<<1, 1024, 0, st>>>(a);
+  slot_scan_kernel<<<a.nsegs, 1024, 0, st>>>(a);
   partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
   subsort_kernel<LANES><<<a.nslots, kSubThreads,
                           pass_smem_bytes<LANES, kSubThreads * TileCfg<LANES>::E, false>(), st>>>(a);

@@ -270,3 +270,15 @@ def test_payload_mode_raw_byte_words():
     want = b"".join(w + b"\n" for w in sorted(words, key=lambda w: (len(w), w)))
     assert h.emit_lines().tobytes() == want
     h.close()
+
+
+def test_multilane_buckets_beyond_the_sample_budget():
+    # buckets larger than the sample sort's splitter budget (class 2: 512
+    # slots of 448 keys) take the merge path inside the same class
+    rng = np.random.default_rng(91)
+    words = _rand_words(rng, 260_000, 12) + _rand_words(rng, 50_000, 14) + _rand_words(rng, 9000, 7)
+    words += [b"Repeatedword"] * 20_000
+    rng.shuffle(words)
+    text = b" ".join(words)
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
