@@ -282,3 +282,23 @@ def test_multilane_buckets_beyond_the_sample_budget():
     text = b" ".join(words)
     want, _ = oracle.sort_text(text, mode="fast")
     assert sort_text(text) == want
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.lists(st.tuples(st.integers(1, 45), st.sampled_from([b"ab", b"aZ09", synth.ALNUM, b"q"]),
+                          st.integers(1, 40)), min_size=0, max_size=12),
+       st.sampled_from([b" ", b"\n", b"., ", b"\x00", b"\xff-"]), st.integers(0, 2**31))
+def test_payload_and_stats_property(groups, sep, seed):
+    # random mixtures of word lengths, alphabets (few symbols = many
+    # duplicates), separators and counts: payload mode (radix / sample sort)
+    # and stats mode (merge path) must both match the oracle
+    rng = np.random.default_rng(seed)
+    words = []
+    for L, alphabet, count in groups:
+        al = np.frombuffer(alphabet, dtype=np.uint8)
+        words += [bytes(r) for r in al[rng.integers(0, len(al), size=(count * 37, L))]]
+    rng.shuffle(words)
+    check_text(sep.join(words))
