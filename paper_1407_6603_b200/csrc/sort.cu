@@ -821,7 +821,10 @@ __global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_const
   if (((s - sseg_at(a, b).slot_base) & 1u) != 0) {  // prefix-equal slot
     const Key<LANES> k0 = ldk<LANES>(base, 0);
     bool diff = false;
-    for (uint32_t i = threadIdx.x; i < cnt; i += NT) diff |= key_lt<LANES>(k0, ldk<LANES>(base, (int)i));
+    for (uint32_t i = threadIdx.x; i < cnt; i += NT) {  // any key different from the first one
+      const Key<LANES> ki = ldk<LANES>(base, (int)i);
+      diff |= key_lt<LANES>(k0, ki) | key_lt<LANES>(ki, k0);
+    }
     if (__syncthreads_or(diff) == 0) return;  // all copies of one word
   }
   Key<LANES> r[E];

@@ -302,3 +302,18 @@ def test_payload_and_stats_property(groups, sep, seed):
         words += [bytes(r) for r in al[rng.integers(0, len(al), size=(count * 37, L))]]
     rng.shuffle(words)
     check_text(sep.join(words))
+
+
+def test_prefix_equal_slot_with_two_tails():
+    # thousands of 9-byte words share their first 8 bytes (one prefix-equal
+    # slot) and differ only in the last byte: the slot must be sorted whichever
+    # key lands first in it (scatter order is arbitrary)
+    h = _native.Handle(0)
+    for rep in range(12):
+        words = [b"\x00" * 8 + bytes([1 + (i + rep) % 2]) for i in range(6000)]
+        words += [bytes([65 + i % 20]) * 9 for i in range(3000)]
+        h.ingest_words(words)
+        h.sort(False)
+        want = b"".join(w + b"\n" for w in sorted(words))
+        assert h.emit_lines().tobytes() == want, rep
+    h.close()
