@@ -30,6 +30,16 @@ while time.time() - t0 < budget:
         naive = dc.stats(naive=True)
         ok = ok and all(naive[L] == (c, s, p) for L, (n, inv, K, c, s, p) in info.items())
         ok = ok and dc.payload() == want
+    if rng.random() < 0.15:  # a batch of several corpora through ws_sort_texts
+        texts = [text] + [synth.generate(0, seed=int(rng.integers(1 << 30))) for _ in range(int(rng.integers(1, 5)))]
+        wants = [want] + [oracle.sort_text(t, mode="fast")[0] for t in texts[1:]]
+        arrs = [np.frombuffer(t, dtype=np.uint8) if t else np.zeros(0, np.uint8) for t in texts]
+        outs = [np.empty(len(t) + 1, dtype=np.uint8) for t in texts]
+        sizes = shared.sort_texts(arrs, outs, int(rng.integers(1, 5)))
+        ok = ok and all(o[:z].tobytes() == w for o, z, w in zip(outs, sizes, wants))
+    if rng.random() < 0.05:  # > 16 MiB: chunked upload overlapped with the ingest
+        big = synth.generate(4, words=int(rng.integers(2_200_000, 3_000_000)), seed=int(rng.integers(1 << 30)))
+        ok = ok and sort_text(big) == oracle.sort_text(big, mode="fast")[0]
     cases += 1
     if not ok:
         fails += 1
