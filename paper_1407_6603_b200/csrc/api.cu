@@ -177,6 +177,8 @@ struct ws_handle {
   DevBuf params;
   DevBuf splits[kClasses + 2];  // merge-path splits: [0] main stream, [1..4] class streams
   DevBuf rcounts[2], rtotals[2];  // radix passes of lane classes 0 and 1
+  DevBuf rstatus[2];              // one-sweep look-back words
+  uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
@@ -448,11 +450,82 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
   if (plan.empty()) return WS_OK;
   DevBuf& cb = h->rcounts[lanes];
   DevBuf& tb = h->rtotals[lanes];
+  uint8_t* kb[2] = {reinterpret_cast<uint8_t*>(keys0), reinterpret_cast<uint8_t*>(keys1)};
+  static const char* rts_env = getenv("WSORT_RADIX_RTS");
+  if (!(rts_env && rts_env[0] == '1')) {
+    // one-sweep: one histogram launch for the digit totals of every pass, then
+    // one look-back launch per pass
+    const size_t tot_words = plan.size() * kRadixMaxPasses * 256;
+    WS_CUDA(tb.ensure(tot_words * 4 + kRadixMaxPasses * 4 + 64));
+    WS_CUDA(cudaMemsetAsync(tb.p, 0, tot_words * 4 + kRadixMaxPasses * 4, st));
+    uint32_t* totals = tb.as<uint32_t>();
+    uint32_t* tickets = totals + tot_words;
+    uint32_t all_tiles = 0;
+    for (auto& pl : plan) all_tiles += pl.ntiles;
+    DevBuf& sb = h->rstatus[lanes];
+    const void* before = sb.p;
+    const size_t cap0 = sb.cap;
+    WS_CUDA(sb.ensure((size_t)all_tiles * 256 * 8));
+    if (sb.p != before || sb.cap != cap0) WS_CUDA(cudaMemsetAsync(sb.p, 0, sb.cap, st));  // no stale epochs
+    char name[32];
+    snprintf(name, sizeof name, "radix_l%d", lanes);
+    for (int p = -1; p < max_passes; ++p) {  // p = -1: the histogram launch
+      std::vector<RadixSeg> d;
+      uint32_t work = 0;
+      double bytes = 0;
+      for (size_t i = 0; i < plan.size(); ++i) {
+        const Plan& pl = plan[i];
+        if (pl.passes <= std::max(p, 0) && p >= 0) continue;
+        RadixSeg r;
+        memset(&r, 0, sizeof r);
+        const uint64_t off = pl.s->key_off * kb_bytes;
+        r.in = p <= 0 ? static_cast<const void*>(pl.s->in_ptr) : kb[p & 1] + off;
+        r.out = kb[(p + 1) & 1] + off;
+        r.n = pl.s->n;
+        r.tile_begin = work;
+        r.ntiles = pl.ntiles;
+        r.shift = pl.shift0 + 8 * std::max(p, 0);
+        r.sid = (uint32_t)i;
+        r.passes = (uint32_t)pl.passes;
+        d.push_back(r);
+        work += pl.ntiles;
+        bytes += (p < 0 ? 1.0 : 2.0) * pl.s->n * kb_bytes;
+      }
+      RadixLaunch a;
+      memset(&a, 0, sizeof a);
+      if (d.size() <= (size_t)kInlineSegs) {
+        std::copy(d.begin(), d.end(), a.inl);
+        a.segs = nullptr;
+      } else {
+        WS_TRY(params_upload(h, d, &a.segs, st));
+      }
+      a.nsegs = (int)d.size();
+      a.work_items = work;
+      a.totals = totals;
+      a.status = sb.as<uint64_t>();
+      a.pass = (uint32_t)std::max(p, 0);
+      a.ticket = tickets + a.pass;
+      if (++h->radix_epoch >= (1u << 30)) h->radix_epoch = 1;
+      a.epoch = h->radix_epoch;
+      Phase ph(h, name, bytes, 0, st);
+      if (p < 0) launch_radix_hist(lanes, a, st);
+      else launch_radix_onesweep(lanes, a, st);
+      ++h->launches;
+      ph.end();
+      WS_TRY(check_launch(name));
+      if (on_done && p >= 0) {
+        std::vector<const SegIn*> done;
+        for (auto& pl : plan)
+          if (pl.passes == p + 1) done.push_back(pl.s);
+        if (!done.empty()) WS_TRY((*on_done)(done, st));
+      }
+    }
+    return WS_OK;
+  }
   WS_CUDA(cb.ensure(count_words * 4 + 64));
   const size_t tot_bytes = (size_t)max_passes * plan.size() * 256 * 4;
   WS_CUDA(tb.ensure(tot_bytes));
   WS_CUDA(cudaMemsetAsync(tb.p, 0, tot_bytes, st));
-  uint8_t* kb[2] = {reinterpret_cast<uint8_t*>(keys0), reinterpret_cast<uint8_t*>(keys1)};
   for (int p = 0; p < max_passes; ++p) {
     std::vector<RadixSeg> d;
     uint32_t work = 0;
@@ -1559,7 +1632,7 @@ void ws_destroy(ws_handle* h) {
                     &h->splits[2], &h->splits[3], &h->splits[4], &h->splits[5],
                     &h->keys_cap, &h->status, &h->ticket, &h->overflow, &h->fill,
                     &h->run_at, &h->run_cnt, &h->run_off, &h->longlist2,
-                    &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1],
+                    &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1], &h->rstatus[0], &h->rstatus[1],
                     &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
                     &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4]};
   for (DevBuf* b : bufs) b->release();

@@ -257,7 +257,219 @@ radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// One-sweep variant: the digit totals of every pass come from one histogram
+// launch over the unsorted keys (a digit's count does not depend on the key
+// order), and each pass is a single launch whose tiles find their per-digit
+// offsets by a decoupled look-back over the preceding tiles of their segment
+// (tiles taken in ticket order, so every awaited tile is already running).
+//
+// Status word per (tile, digit): epoch (bits 63..34, unique per launch, so no
+// clearing between passes) | flag (bits 33..32: 1 tile count, 2 inclusive
+// prefix within the segment) | value (bits 31..0). One 64-bit store carries
+// flag and value together.
+constexpr uint64_t kStAgg = 1ull << 32, kStInc = 2ull << 32;
+constexpr uint64_t kStEpochMask = ~0x3FFFFFFFFull;
+#ifndef WS_LOOK_W
+#define WS_LOOK_W 4
+#endif
+constexpr int kLookW = WS_LOOK_W;  // predecessors loaded per look-back round
+#ifndef WS_OS_MINB
+#define WS_OS_MINB 3  // 80 registers, no spills (4: 64 with spills, measured slower)
+#endif
+
+__device__ __forceinline__ void st_status(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Digit histograms of all passes of every segment: totals[sid][p][256].
+template <class K>
+__global__ void __launch_bounds__(kRThreads)
+radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
+  using C = RadixCfg<K>;
+  constexpr int kP = (int)sizeof(K);  // at most one pass per key byte
+  __shared__ uint32_t hist[kP][kDigits];
+  __shared__ int s_seg;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t tile = blockIdx.x;
+  if (tid < 32) {
+    const int s = rsegment_of(a, tile);
+    if (tid == 0) s_seg = s;
+  }
+  for (int i = tid; i < kP * kDigits; i += kRThreads) (&hist[0][0])[i] = 0;
+  __syncthreads();
+  const RadixSeg& sg = rseg_at(a, s_seg);
+  const uint32_t t = tile - sg.tile_begin;
+  const uint64_t first = (uint64_t)t * C::T + (uint64_t)wid * 32 * C::E;
+  const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
+  const K* in = reinterpret_cast<const K*>(sg.in) + first;
+  K key[C::E];
+#pragma unroll
+  for (int r = 0; r < C::E; ++r) {
+    const uint32_t j = r * 32 + lane;
+    key[r] = j < nvalid ? in[j] : K(0);  // default caching: the first pass re-reads from L2
+  }
+  const int passes = (int)sg.passes;
+#pragma unroll
+  for (int p = 0; p < kP; ++p) {
+    if (p >= passes) break;
+    const uint32_t sh = sg.shift + 8 * p;
+#pragma unroll
+    for (int r = 0; r < C::E; ++r)
+      if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&hist[p][digit_of<K>(key[r], sh)], 1u);
+  }
+  __syncthreads();
+  for (int p = 0; p < passes; ++p) {
+    const uint32_t c = hist[p][tid];
+    if (c) atomicAdd(a.totals + ((uint64_t)sg.sid * kRadixMaxPasses + p) * kDigits + tid, c);
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kRThreads, WS_OS_MINB)
+radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
+  using C = RadixCfg<K>;
+  __shared__ uint32_t wcnt[kRWarps][kDigits];
+  __shared__ uint32_t s_gdelta[kDigits];  // global offset - tile-local start
+  __shared__ uint32_t s_wsum[2][kRWarps];
+  __shared__ __align__(16) K stage[C::T];
+  __shared__ int s_seg;
+  __shared__ uint32_t s_tile;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < 32) {  // ticket order: every tile this one waits for has started
+    uint32_t tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1u);
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    const int s = rsegment_of(a, tk);
+    if (lane == 0) {
+      s_seg = s;
+      s_tile = tk;
+    }
+  }
+  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const RadixSeg& sg = rseg_at(a, s_seg);
+  const uint32_t t = tile - sg.tile_begin;
+  const uint64_t tfirst = (uint64_t)t * C::T;
+  const uint64_t first = tfirst + (uint64_t)wid * 32 * C::E;
+  const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
+  const uint32_t ntile = (uint32_t)umin64(sg.n - tfirst, C::T);
+  // this pass's digit total (-> the digit's base in the segment), early
+  const uint32_t tot = a.totals[((uint64_t)sg.sid * kRadixMaxPasses + a.pass) * kDigits + tid];
+  const K* in = reinterpret_cast<const K*>(sg.in) + first;
+  K key[C::E];
+#pragma unroll
+  for (int r = 0; r < C::E; ++r) {
+    const uint32_t j = r * 32 + lane;
+    key[r] = j < nvalid ? __ldcs(in + j) : K(0);
+  }
+  uint32_t rk[C::E];
+  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], rk);
+  __syncthreads();
+  // per digit (thread = digit): exclusive over warps; the tile's count
+  uint32_t run = 0;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) {
+    const uint32_t c = wcnt[w][tid];
+    wcnt[w][tid] = run;
+    run += c;
+  }
+  uint64_t* status = a.status + (uint64_t)tile * kDigits + tid;
+  const uint64_t ep = (uint64_t)a.epoch << 34;
+  const bool head = t == 0;  // the segment's first tile: its prefix is 0
+  st_status(status, ep | (head ? kStInc : kStAgg) | run);
+  // tile-local digit starts and the digits' bases in the segment (two scans)
+  uint32_t inc = run, inc2 = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    const uint32_t u2 = __shfl_up_sync(0xffffffffu, inc2, o);
+    if (lane >= o) {
+      inc += u;
+      inc2 += u2;
+    }
+  }
+  if (lane == 31) {
+    s_wsum[0][wid] = inc;
+    s_wsum[1][wid] = inc2;
+  }
+  __syncthreads();
+  uint32_t wpre = 0, wpre2 = 0;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) {
+    wpre += w < wid ? s_wsum[0][w] : 0u;
+    wpre2 += w < wid ? s_wsum[1][w] : 0u;
+  }
+  const uint32_t doff = wpre + inc - run;
+  const uint32_t dbase = wpre2 + inc2 - tot;
+#pragma unroll
+  for (int w = 0; w < kRWarps; ++w) wcnt[w][tid] += doff;  // tile-local start of (warp, digit)
+  __syncthreads();
+  // regroup the tile by digit in shared memory first (keys and ranks are
+  // dead before the look-back's loads are in flight)
+#pragma unroll
+  for (int r = 0; r < C::E; ++r) {
+    const uint32_t j = r * 32 + lane;
+    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk[r]] = key[r];
+  }
+  // look-back over the segment's preceding tiles for this digit: a window of
+  // kLookW predecessors per load round, nearest first; the segment's first
+  // tile is always inclusive, so the walk stops there
+  uint32_t excl = 0;
+  if (!head) {
+    uint32_t back = 1;  // distance of the nearest predecessor not yet consumed
+    for (;;) {
+      uint64_t v[kLookW];
+#pragma unroll
+      for (int w = 0; w < kLookW; ++w)
+        v[w] = back + w <= t ? ld_status(status - (uint64_t)(back + w) * kDigits) : (ep | kStInc);
+      uint32_t used = 0;
+      bool found = false;
+#pragma unroll
+      for (int w = 0; w < kLookW; ++w) {
+        if (found || used < (uint32_t)w) continue;     // stopped earlier in this window
+        if ((v[w] & kStEpochMask) != ep) continue;     // not yet published in this launch
+        excl += (uint32_t)v[w];
+        found = (v[w] & kStInc) != 0;
+        used = w + 1;
+      }
+      if (found) break;
+      back += used;
+    }
+    st_status(status, ep | kStInc | (excl + run));
+  }
+  s_gdelta[tid] = dbase + excl - doff;
+  __syncthreads();
+  K* out = reinterpret_cast<K*>(sg.out);
+  for (uint32_t i = tid; i < ntile; i += kRThreads) {
+    const K k = stage[i];
+    out[s_gdelta[digit_of<K>(k, sg.shift)] + i] = k;
+  }
+}
+
 }  // namespace
+
+void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st) {
+  if (!a.work_items) return;
+  if (lanes == 0)
+    radix_hist_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
+  else
+    radix_hist_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+}
+
+void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st) {
+  if (!a.work_items) return;
+  if (lanes == 0)
+    radix_onesweep_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
+  else
+    radix_onesweep_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+}
 
 int radix_tile_size(int lanes) { return lanes == 0 ? RadixCfg<uint32_t>::T : RadixCfg<uint64_t>::T; }
 

@@ -128,18 +128,28 @@ struct RadixSeg {
   uint32_t n;
   uint32_t tile_begin;  // first tile (work item) of the segment
   uint32_t ntiles;
-  uint32_t shift;       // bit position of this pass's 8-bit digit
+  uint32_t shift;       // bit position of this pass's 8-bit digit (histogram: of pass 0)
+  uint32_t sid;         // one-sweep: the segment's row in the totals table
+  uint32_t passes;      // one-sweep histogram: passes of the segment
 };
+constexpr int kRadixMaxPasses = 8;  // one per key byte
 struct RadixLaunch {
   const RadixSeg* segs;  // device table when nsegs > kInlineSegs, else nullptr
   int nsegs;
   uint32_t work_items;   // tiles of all segments
   uint32_t* counts;      // per segment [256][ntiles] tile histograms -> offsets
-  uint32_t* totals;      // [nsegs][256] digit totals of this pass (zeroed)
+  uint32_t* totals;      // reduce-then-scan: [nsegs][256] digit totals of this pass (zeroed);
+                         // one-sweep: [sid][kRadixMaxPasses][256] (zeroed before the histogram)
+  uint64_t* status;      // one-sweep: [work_items][256] look-back words
+  uint32_t* ticket;      // one-sweep: this launch's tile counter (zeroed)
+  uint32_t epoch;        // one-sweep: unique per launch, < 2^30, != 0
+  uint32_t pass;
   RadixSeg inl[kInlineSegs];
 };
 int radix_tile_size(int lanes);
 void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st);
+void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st);
+void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st);
 
 // emit.cu
 struct EmitSeg {

@@ -317,3 +317,30 @@ def test_prefix_equal_slot_with_two_tails():
         want = b"".join(w + b"\n" for w in sorted(words))
         assert h.emit_lines().tobytes() == want, rep
     h.close()
+
+
+def _short_word_text(rng, n, L=None, alphabet=synth.ALNUM):
+    """n words of length L (or 1..5 at random) over `alphabet`, space-separated."""
+    al = np.frombuffer(alphabet, dtype=np.uint8)
+    lens = np.full(n, L) if L else rng.integers(1, 6, n)
+    buf = np.full(int(lens.sum()) + n, ord(" "), dtype=np.uint8)
+    ends = np.cumsum(lens + 1) - 1
+    starts = ends - lens
+    pos = np.repeat(starts, lens) + (np.arange(int(lens.sum())) - np.repeat(np.cumsum(lens) - lens, lens))
+    buf[pos] = al[rng.integers(0, len(al), int(lens.sum()))]
+    return buf.tobytes()
+
+
+def test_radix_one_sweep_tiles_and_reuse():
+    # class-0 buckets (<= 5 characters) of 1 .. ~300 radix tiles (4096 keys),
+    # exact tile multiples, heavy duplicates; one handle reused across growing
+    # and shrinking corpora (look-back status buffer growth, per-launch epochs)
+    rng = np.random.default_rng(77)
+    cases = [(1, 5, synth.ALNUM), (4095, 5, synth.ALNUM), (4096, 5, synth.ALNUM),
+             (4097, 5, synth.ALNUM), (3 * 4096, 4, synth.ALNUM), (300_000, None, synth.ALNUM),
+             (1_200_000, 5, b"ab"), (1_200_000, 5, synth.ALNUM), (5000, None, b"xyz"),
+             (4096 * 7, 3, synth.ALNUM), (2, 5, synth.ALNUM)]
+    for n, L, al in cases:
+        text = _short_word_text(rng, n, L, al)
+        want, _ = oracle.sort_text(text, mode="fast")
+        assert sort_text(text) == want, (n, L, al)

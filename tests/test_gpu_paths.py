@@ -36,6 +36,7 @@ print("ok")
 @pytest.mark.parametrize("knob", [
     "WSORT_NO_RADIX",         # class 0 by tile + merge path in payload mode
     "WSORT_NO_SAMPLE",        # multi-lane classes by tile + merge path in payload mode
+    "WSORT_RADIX_RTS",        # class-0 radix by upsweep + scan + downsweep (no look-back)
     "WSORT_LOOKBACK",         # ordered ingest by the decoupled look-back
     "WSORT_TWO_PASS",         # count + scan + scatter ingest
     "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest
