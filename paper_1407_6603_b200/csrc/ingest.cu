@@ -683,7 +683,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
 // atomic (no per-warp ranking pass), and each chunk reserves its bin runs in
 // HBM with one global atomic per bin. Keys are then packed in bin-major order
 // (uniform length per warp batch) and stored to consecutive addresses.
-template <int SB>
+template <int SB, int ENC>
 __global__ void __launch_bounds__(kIngestThreads)
 reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
   constexpr int kCB = SB * kIngestThreads;  // chunk bytes
@@ -706,7 +706,7 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
   uint4 v[NV];
   const SegW<SB> seg = classify_wide<SB>(text, n, cbase, v, s_chain, p.avail ? p.avail : ~0ull,
                                          p.overflow);  // has a __syncthreads
-  const bool codes = p.enc == kEncAlnum6;
+  constexpr bool codes = ENC == kEncAlnum6;  // text ingest: 6-bit codes (else raw bytes)
 #pragma unroll
   for (int q = 0; q < NV; ++q)
     reinterpret_cast<uint4*>(chunk32)[NV * tid + q] = codes ? alnum6_codes16(v[q]) : v[q];
@@ -753,7 +753,7 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
       p.longlist[s_base[kLongBin] + at] = make_uint2((uint32_t)(cbase + start), L);
   }
   if (tid < kMaxPackedLen) {
-    const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc(tid + 1, p.enc));
+    const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc(tid + 1, ENC));
     s_dst[tid] = p.bin_base[tid] + ((uint64_t)s_base[tid] - s_boff[tid]) * ks;
   }
   __syncthreads();
@@ -763,9 +763,9 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
     for (uint32_t k = tid; k < npacked; k += kIngestThreads) {
       const uint32_t e = ord[k];
       const uint32_t start = e & 0xFFFFu, L = e >> 16;
-      const int lanes = lanes_for_len_enc(L, p.enc);
+      const int lanes = lanes_for_len_enc(L, ENC);
       uint64_t key[4];
-      if (codes)
+      if constexpr (codes)
         pack6_fast(chunk32, start, L, lanes, key);
       else
         pack_from_smem(chunk32, start, L, lanes, key);
@@ -967,7 +967,9 @@ static size_t reserve_smem_bytes() {
 }
 
 void set_ingest_attributes() {
-  cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB>,
+  cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncAlnum6>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve_smem_bytes());
+  cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncRaw8>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve_smem_bytes());
 }
 
@@ -976,8 +978,12 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
   if (!nchunks) return;
   if (p.fill && p.run_at)
     scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+  else if (p.fill && p.enc == kEncAlnum6)
+    reserve_ingest_kernel<kReserveSB, kEncAlnum6><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(
+        text, n, p);
   else if (p.fill)
-    reserve_ingest_kernel<kReserveSB><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(text, n, p);
+    reserve_ingest_kernel<kReserveSB, kEncRaw8><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(
+        text, n, p);
   else
     scatter_kernel<kByLookback><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
 }
