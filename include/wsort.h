@@ -122,7 +122,10 @@ int ws_emit_rows(ws_handle* h, uint8_t* out, uint64_t cap, uint64_t* written);
 
 /* --- fused end-to-end ---------------------------------------------------- */
 /* The whole `wordsort sort FILE` path after load_text (cli.py:83-103): text
- * bytes in, payload bytes out (host buffers; pinned memory is fastest). */
+ * bytes in, payload bytes out (host buffers; pinned memory is fastest).
+ * Buckets may be written straight from the last sort pass as payload, so
+ * afterwards (also after ws_sort_resident) ws_emit_lines / ws_emit_rows
+ * return WS_ERR_STATE until a ws_sort on the same ingest. */
 int ws_sort_text(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
                  uint64_t* written);
 

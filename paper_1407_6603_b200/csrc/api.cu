@@ -147,6 +147,7 @@ struct SegIn {
   uint32_t idx_base;
   int final_buf;  // out
   const uint64_t* in_ptr = nullptr;  // unsorted keys for the tile pass (default: keys0)
+  bool emitted = false;  // out: the last pass wrote the payload records (no keys)
 };
 
 }  // namespace
@@ -178,6 +179,7 @@ struct ws_handle {
   DevBuf splits[kClasses + 2];  // merge-path splits: [0] main stream, [1..4] class streams
   DevBuf rcounts[2], rtotals[2];  // radix passes of lane classes 0 and 1
   DevBuf rstatus[2];              // one-sweep look-back words
+  bool payload_only = false;      // a fused sort wrote some buckets' payload without their keys
   uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   PinBuf pin_params, pin_small;
@@ -424,7 +426,8 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
 // reads buffer p & 1 (pass 0: the segment's in_ptr) and writes (p + 1) & 1;
 // a bucket is done after ceil(bits / 8) passes.
 int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* keys0,
-                        uint64_t* keys1, cudaStream_t st, const PassDoneHook* on_done) {
+                        uint64_t* keys1, cudaStream_t st, const PassDoneHook* on_done,
+                        uint8_t* pay = nullptr, const std::vector<uint64_t>* pay_off = nullptr) {
   const int kb_bytes = key_bytes(lanes);
   const int keybits = 8 * kb_bytes;
   const int cbits = h->enc == kEncAlnum6 ? 6 : 8;  // bits per character
@@ -487,6 +490,11 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         r.shift = pl.shift0 + 8 * std::max(p, 0);
         r.sid = (uint32_t)i;
         r.passes = (uint32_t)pl.passes;
+        if (pay && p == pl.passes - 1) {  // last pass: payload records instead of keys
+          r.pay = pay + (*pay_off)[pl.s->stat_slot];
+          r.len = h->buckets[pl.s->stat_slot].len;
+          pl.s->emitted = true;
+        }
         d.push_back(r);
         work += pl.ntiles;
         bytes += (p < 0 ? 1.0 : 2.0) * pl.s->n * kb_bytes;
@@ -504,6 +512,7 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       a.totals = totals;
       a.status = sb.as<uint64_t>();
       a.pass = (uint32_t)std::max(p, 0);
+      a.enc = h->enc;
       a.ticket = tickets + a.pass;
       if (++h->radix_epoch >= (1u << 30)) h->radix_epoch = 1;
       a.epoch = h->radix_epoch;
@@ -772,7 +781,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   } else if (n && !text) {
     return fail(WS_ERR_ARG, "null text");
   }
-  h->ingested = h->sorted = h->have_stats = false;
+  h->ingested = h->sorted = h->have_stats = h->payload_only = false;
   h->have_tokens = false;
   h->unordered = false;
   h->buckets.clear();
@@ -1064,6 +1073,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   if (stats && h->unordered)
     return fail(WS_ERR_STATE, "stats need corpus order: ingest without WS_INGEST_UNORDERED");
   if (fe) h->sorted = true;  // bucket final buffers are fixed at planning time
+  h->payload_only = false;
   const int nb = (int)h->buckets.size();
   if (stats) {
     WS_CUDA(h->idx[0].ensure(std::max<uint64_t>(h->idx_total, 1) * 4 + 64));
@@ -1104,17 +1114,18 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     // the pass that completes it, on side streams, while later passes run.
     PassDoneHook hook = [&, est, dst](const std::vector<const SegIn*>& done,
                                       cudaStream_t st) -> int {
-      std::vector<int> bids;
+      std::vector<int> bids, to_emit;
       for (const SegIn* sg : done) {
         h->buckets[sg->stat_slot].final_buf = sg->final_buf;
         bids.push_back((int)sg->stat_slot);
+        if (!sg->emitted) to_emit.push_back((int)sg->stat_slot);
       }
       if (est != st) {
         cudaEvent_t ev = sync_event(h);
         WS_CUDA(cudaEventRecord(ev, st));
         WS_CUDA(cudaStreamWaitEvent(est, ev, 0));
       }
-      WS_TRY(emit_device(h, fe->dout, true, nullptr, -1, est, &bids));
+      if (!to_emit.empty()) WS_TRY(emit_device(h, fe->dout, true, nullptr, -1, est, &to_emit));
       if (!fe->host) return WS_OK;
       if (dst != est) {
         cudaEvent_t ev2 = sync_event(h);
@@ -1140,7 +1151,12 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     const PassDoneHook* on_done = fe && !fe->per_class ? &hook : nullptr;
     static const char* no_sample = getenv("WSORT_NO_SAMPLE");
     if (!stats && c == 0 && !(no_radix && no_radix[0] == '1')) {
-      WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, on_done));
+      // the last pass of each bucket writes its payload records directly
+      static const char* no_fuse = getenv("WSORT_NO_FUSED_PAYLOAD");
+      const bool fuse = on_done && !(no_fuse && no_fuse[0] == '1');
+      WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, on_done, fuse ? fe->dout : nullptr,
+                                 fuse ? &fe->off : nullptr));
+      for (const SegIn& sg : segs) h->payload_only |= sg.emitted;
     } else if (!stats && c >= 1 && !(no_sample && no_sample[0] == '1')) {
       // buckets beyond what the splitter budget keeps at slot size go through
       // the merge path (same stream; both leave per-bucket final buffers)
@@ -1349,6 +1365,8 @@ uint64_t emit_size(ws_handle* h, bool lines) {
 
 int emit_to_host(ws_handle* h, bool lines, uint8_t* out, uint64_t cap, uint64_t* written) {
   if (!h->ingested) return fail(WS_ERR_STATE, "emit before ingest");
+  if (h->payload_only)
+    return fail(WS_ERR_STATE, "the handle holds the payload of a fused sort, not sorted keys: ws_sort first");
   const uint64_t size = emit_size(h, lines);
   if (written) *written = size;
   if (!out && cap == 0) return WS_OK;  // size query
@@ -1372,7 +1390,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
                        const int64_t* counts, const int32_t* widths, bool allow_dup,
                        std::vector<int>* block_of_bucket) {
   if (nblocks < 0) return fail(WS_ERR_ARG, "negative block count");
-  h->ingested = h->sorted = h->have_stats = false;
+  h->ingested = h->sorted = h->have_stats = h->payload_only = false;
   h->have_tokens = false;
   h->unordered = false;
   h->text_valid = false;
@@ -1467,7 +1485,7 @@ int ingest_blocks_impl(ws_handle* h, int32_t nblocks, const uint8_t* const* rows
 }
 
 int ingest_words_impl(ws_handle* h, const uint8_t* concat, const uint32_t* lens, uint64_t nwords) {
-  h->ingested = h->sorted = h->have_stats = false;
+  h->ingested = h->sorted = h->have_stats = h->payload_only = false;
   h->have_tokens = false;
   h->unordered = false;
   h->text_valid = false;
@@ -1593,8 +1611,19 @@ int ws_create(ws_handle** out, int32_t device) {
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   e = cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking);
   // the one-word classes (0, 1) hold most keys and sort last
+  int cprio[kClasses + 1];
+  for (int c = 0; c <= kClasses; ++c) cprio[c] = c == 0 ? prio_hi : prio_lo;
+  if (const char* cp = getenv("WSORT_CLASS_PRIO")) {  // experiment: per-class priorities
+    for (int c = 0; c <= kClasses && *cp; ++c) {
+      char* endp = nullptr;
+      const long v = strtol(cp, &endp, 10);
+      if (endp == cp) break;
+      cprio[c] = std::min(prio_lo, std::max(prio_hi, (int)v));
+      cp = *endp == ',' ? endp + 1 : endp;
+    }
+  }
   for (int c = 0; c <= kClasses && e == cudaSuccess; ++c)
-    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, c == 0 ? prio_hi : prio_lo);
+    e = cudaStreamCreateWithPriority(&h->cs[c], cudaStreamNonBlocking, cprio[c]);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->hs, cudaStreamNonBlocking, prio_hi);
   for (int c = 0; c <= kClasses && e == cudaSuccess; ++c) {
     e = cudaStreamCreateWithPriority(&h->es[c], cudaStreamNonBlocking, prio_hi);

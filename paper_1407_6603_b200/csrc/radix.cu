@@ -446,6 +446,25 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   }
   s_gdelta[tid] = dbase + excl - doff;
   __syncthreads();
+  if (sg.pay) {  // the segment's last pass: payload records (characters + '\n') at rank * (L + 1)
+    const uint32_t L = sg.len;
+    constexpr int kBits = 8 * (int)sizeof(K);
+    for (uint32_t i = tid; i < ntile; i += kRThreads) {
+      const K k = stage[i];
+      uint8_t* dst = sg.pay + (uint64_t)(s_gdelta[digit_of<K>(k, sg.shift)] + i) * (L + 1);
+      if (a.enc == kEncAlnum6) {
+#pragma unroll
+        for (int c = 0; c < kBits / 6; ++c)
+          if (c < (int)L) dst[c] = (uint8_t)alnum6_byte((uint32_t)(k >> (kBits - 6 - 6 * c)) & 63u);
+      } else {
+#pragma unroll
+        for (int c = 0; c < kBits / 8; ++c)
+          if (c < (int)L) dst[c] = (uint8_t)(k >> (kBits - 8 - 8 * c));
+      }
+      dst[L] = '\n';
+    }
+    return;
+  }
   K* out = reinterpret_cast<K*>(sg.out);
   for (uint32_t i = tid; i < ntile; i += kRThreads) {
     const K k = stage[i];

@@ -131,6 +131,8 @@ struct RadixSeg {
   uint32_t shift;       // bit position of this pass's 8-bit digit (histogram: of pass 0)
   uint32_t sid;         // one-sweep: the segment's row in the totals table
   uint32_t passes;      // one-sweep histogram: passes of the segment
+  uint8_t* pay;         // one-sweep, segment's last pass: write payload records here instead
+  uint32_t len;         //   of keys (word length; record = characters + '\n')
 };
 constexpr int kRadixMaxPasses = 8;  // one per key byte
 struct RadixLaunch {
@@ -144,6 +146,7 @@ struct RadixLaunch {
   uint32_t* ticket;      // one-sweep: this launch's tile counter (zeroed)
   uint32_t epoch;        // one-sweep: unique per launch, < 2^30, != 0
   uint32_t pass;
+  int enc;               // key encoding (kEncAlnum6 / kEncRaw8), for payload records
   RadixSeg inl[kInlineSegs];
 };
 int radix_tile_size(int lanes);

@@ -344,3 +344,20 @@ def test_radix_one_sweep_tiles_and_reuse():
         text = _short_word_text(rng, n, L, al)
         want, _ = oracle.sort_text(text, mode="fast")
         assert sort_text(text) == want, (n, L, al)
+
+
+def test_fused_payload_sort_then_emit_needs_sort():
+    # ws_sort_text writes short-word buckets straight from the last radix pass
+    # as payload (no sorted keys): a later emit is refused until ws_sort
+    text = synth.generate(4, words=200_000, seed=8)
+    want, _ = oracle.sort_text(text, mode="fast")
+    h = _native.Handle(0)
+    src = np.frombuffer(text, dtype=np.uint8)
+    out = np.empty(len(text) + 64, dtype=np.uint8)
+    n = h.sort_text(src, out)
+    assert out[:n].tobytes() == want
+    with pytest.raises(RuntimeError, match="fused sort"):
+        h.emit_lines()
+    h.sort(False)
+    assert h.emit_lines().tobytes() == want
+    h.close()
