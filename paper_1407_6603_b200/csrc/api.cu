@@ -596,7 +596,9 @@ uint64_t sample_bucket_limit(int lanes) {
 }
 
 int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* out_class,
-                         cudaStream_t st, const PassDoneHook* on_done) {
+                         cudaStream_t st, const PassDoneHook* on_done, uint8_t* pay = nullptr,
+                         const std::vector<uint64_t>* pay_off = nullptr) {
+  if (h->enc != kEncAlnum6) pay = nullptr;  // fused records decode 6-bit text keys only
   const uint32_t T = (uint32_t)tile_size(lanes);
   uint32_t pmax = 1;  // sample prefixes sorted in shared memory (power of two, <= 4096)
   while (pmax * 2 <= (uint32_t)std::min(sample_max_keys(lanes), 4096)) pmax *= 2;
@@ -623,7 +625,12 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
     g.split_off = splits;
     g.slot_base = slots;
     g.tile_begin = tiles;
-    g.pad_ = 0;
+    g.len = h->buckets[s.stat_slot].len;
+    g.pay = nullptr;
+    if (pay) {  // the slot sorts write this bucket's payload records
+      g.pay = pay + (*pay_off)[s.stat_slot];
+      s.emitted = true;
+    }
     d.push_back(g);
     slots += 2 * g.nsplit + 1;
     splits += g.nsplit;
@@ -1167,13 +1174,20 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
         if (segs[j].n <= cap) { fit.push_back(segs[j]); fit_w.push_back(which[j]); }
         else { big.push_back(segs[j]); big_w.push_back(which[j]); }
       }
-      if (!fit.empty()) WS_TRY(sample_sort_segments(h, c, fit, k1, cst, on_done));
+      static const char* no_fuse_s = getenv("WSORT_NO_FUSED_PAYLOAD");
+      static const char* no_fuse_slots = getenv("WSORT_NO_FUSED_SLOTS");
+      const bool fuse_s = on_done && !(no_fuse_s && no_fuse_s[0] == '1') &&
+                          !(no_fuse_slots && no_fuse_slots[0] == '1');
+      if (!fit.empty())
+        WS_TRY(sample_sort_segments(h, c, fit, k1, cst, on_done, fuse_s ? fe->dout : nullptr,
+                                    fuse_s ? &fe->off : nullptr));
       if (!big.empty())
         WS_TRY(sort_segments(h, c, big, k0, k1, h->idx[0].as<uint32_t>(), h->idx[1].as<uint32_t>(),
                              false, nullptr, nullptr, "", cst, on_done));
       size_t fi = 0, bi = 0;  // final buffers back into the class's segment order
       for (size_t j = 0; j < segs.size(); ++j)
         segs[j].final_buf = segs[j].n <= cap ? fit[fi++].final_buf : big[bi++].final_buf;
+      for (const SegIn& sg : fit) h->payload_only |= sg.emitted;
       (void)fit_w; (void)big_w;
     } else {
       WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(),

@@ -9,6 +9,7 @@
 // Words with L > 32 are copied from the text by (start, len).
 #include <algorithm>
 
+#include "payload.cuh"
 #include "ws_common.cuh"
 #include "ws_kernels.h"
 
@@ -29,25 +30,6 @@ __device__ __forceinline__ void copy_span_out(const uint8_t* __restrict__ buf, i
   for (uint64_t q = ab + 16ull * threadIdx.x; q < ae; q += 16ull * kEmitThreads)
     *reinterpret_cast<uint4*>(out + q) = *reinterpret_cast<const uint4*>(buf + (q - o0 + mis));
   for (uint64_t q = ae + threadIdx.x; q < g_end; q += kEmitThreads) out[q] = buf[q - o0 + mis];
-}
-
-// Unpack one 6-bit alnum key (character k of the big-endian bit string).
-template <int LANES>
-__device__ __forceinline__ void unpack6(const uint64_t (&k)[LANES], int L, uint8_t* dst) {
-  static_assert(LANES <= 3, "6-bit keys use at most 3 lanes");
-#define WS_UNPACK6_CHAR(I)                                                    \
-  if constexpr ((6 * (I) + 5) / 64 < LANES) {                                 \
-    if ((I) < L) dst[I] = (uint8_t)alnum6_byte(code6_at<I>(k));               \
-  }
-  WS_UNPACK6_CHAR(0) WS_UNPACK6_CHAR(1) WS_UNPACK6_CHAR(2) WS_UNPACK6_CHAR(3)
-  WS_UNPACK6_CHAR(4) WS_UNPACK6_CHAR(5) WS_UNPACK6_CHAR(6) WS_UNPACK6_CHAR(7)
-  WS_UNPACK6_CHAR(8) WS_UNPACK6_CHAR(9) WS_UNPACK6_CHAR(10) WS_UNPACK6_CHAR(11)
-  WS_UNPACK6_CHAR(12) WS_UNPACK6_CHAR(13) WS_UNPACK6_CHAR(14) WS_UNPACK6_CHAR(15)
-  WS_UNPACK6_CHAR(16) WS_UNPACK6_CHAR(17) WS_UNPACK6_CHAR(18) WS_UNPACK6_CHAR(19)
-  WS_UNPACK6_CHAR(20) WS_UNPACK6_CHAR(21) WS_UNPACK6_CHAR(22) WS_UNPACK6_CHAR(23)
-  WS_UNPACK6_CHAR(24) WS_UNPACK6_CHAR(25) WS_UNPACK6_CHAR(26) WS_UNPACK6_CHAR(27)
-  WS_UNPACK6_CHAR(28) WS_UNPACK6_CHAR(29) WS_UNPACK6_CHAR(30) WS_UNPACK6_CHAR(31)
-#undef WS_UNPACK6_CHAR
 }
 
 template <int LANES, int ENC>

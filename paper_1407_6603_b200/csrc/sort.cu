@@ -38,6 +38,7 @@
 
 #include "ws_common.cuh"
 #include "ws_kernels.h"
+#include "payload.cuh"
 
 namespace ws {
 
@@ -805,6 +806,19 @@ __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__
 // slot whose keys are all identical (repeated words) is left as it is.
 constexpr int kSubThreads = 128;
 
+// Fused emission (SampleSeg::pay set: 6-bit text keys, payload mode): the
+// slot's sorted keys leave as payload records at their final place
+// (pay + rank in bucket * (L + 1)) instead of going back to the key buffer,
+// so no emit pass re-reads them; a slot of one repeated word is filled with
+// the record pattern. Staging buffer after the keys in dynamic smem.
+constexpr int kSubPayBuf = kSubThreads * (kMaxPackedLen + 1) + 64;
+
+template <int LANES>
+__device__ __forceinline__ void sub_emit(const KW<LANES>* keys, uint32_t cnt, int L, uint8_t* out,
+                                         uint8_t* pbuf) {
+  if constexpr (LANES <= 3) emit_records_cta<LANES, kSubThreads>(keys, cnt, L, out, pbuf);
+}
+
 template <int LANES>
 __global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_constant__ SampleLaunch a) {
   constexpr int E = TileCfg<LANES>::E, NT = kSubThreads, TS = NT * E;
@@ -812,25 +826,37 @@ __global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_const
   using W = KW<LANES>;
   extern __shared__ __align__(16) uint64_t smem[];
   W* sk = reinterpret_cast<W*>(smem);
+  uint8_t* pbuf = reinterpret_cast<uint8_t*>(smem) + keys_smem_bytes<LANES, TS, false>();
   const uint32_t s = blockIdx.x;
   const uint32_t cnt = a.hist[s];
-  if (cnt < 2) return;
-  W* base = kv<LANES>(a.keys_out) + (uint64_t)a.slot_off[s] * NW;
+  if (cnt == 0) return;
   int b = 0;  // bucket of the slot (segments ascend by slot_base)
   while (b + 1 < a.nsegs && sseg_at(a, b + 1).slot_base <= s) ++b;
-  if (((s - sseg_at(a, b).slot_base) & 1u) != 0) {  // prefix-equal slot
+  const SampleSeg& sg = sseg_at(a, b);
+  W* base = kv<LANES>(a.keys_out) + (uint64_t)a.slot_off[s] * NW;
+  const int L = (int)sg.len;
+  uint8_t* const out = (LANES <= 3 && sg.pay) ? sg.pay + (uint64_t)(a.slot_off[s] - sg.key_off) * (L + 1) : nullptr;
+  if (cnt < 2) {
+    if (out) sub_emit<LANES>(base, cnt, L, out, pbuf);
+    return;
+  }
+  if (((s - sg.slot_base) & 1u) != 0) {  // prefix-equal slot
     const Key<LANES> k0 = ldk<LANES>(base, 0);
     bool diff = false;
     for (uint32_t i = threadIdx.x; i < cnt; i += NT) {  // any key different from the first one
       const Key<LANES> ki = ldk<LANES>(base, (int)i);
       diff |= key_lt<LANES>(k0, ki) | key_lt<LANES>(ki, k0);
     }
-    if (__syncthreads_or(diff) == 0) return;  // all copies of one word
+    if (__syncthreads_or(diff) == 0) {  // all copies of one word
+      if constexpr (LANES <= 3)
+        if (out) fill_records_cta<LANES, NT>(k0, cnt, L, out, pbuf);
+      return;
+    }
   }
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
-  auto sort_span = [&](W* g, uint32_t c) {  // c <= TS keys at g, sorted in place
+  auto sort_span = [&](W* g, uint32_t c, bool emit) {  // c <= TS keys at g, sorted in place
     constexpr int PW = E * NW;  // words per thread: all loads in flight, then the stores
     W v[PW];
 #pragma unroll
@@ -845,11 +871,15 @@ __global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_const
     __syncthreads();
     regs_to_smem<LANES, E, false>(sk, nullptr, threadIdx.x * E, r, ri);
     __syncthreads();
+    if (emit) {  // the whole slot is in sk: records straight out
+      sub_emit<LANES>(sk, c, L, out, pbuf);
+      return;
+    }
     for (uint32_t j = threadIdx.x; j < c * NW; j += NT) g[j] = sk[j];
     __syncthreads();
   };
   if (cnt <= (uint32_t)TS) {
-    sort_span(base, cnt);
+    sort_span(base, cnt, out != nullptr);
     return;
   }
   constexpr uint32_t HB = TS / 2;
@@ -857,11 +887,17 @@ __global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_const
   for (uint32_t round = 0; round < blocks; ++round)
     for (uint32_t p = round & 1; p + 1 < blocks; p += 2) {
       const uint32_t lo = p * HB, hi = min(cnt, (p + 2) * HB);
-      sort_span(base + (uint64_t)lo * NW, hi - lo);
+      sort_span(base + (uint64_t)lo * NW, hi - lo, false);
     }
+  if (out) sub_emit<LANES>(base, cnt, L, out, pbuf);  // the block sort's stores are visible to the CTA
 }
 
 // ---- host side ---------------------------------------------------------------------
+
+template <int LANES>
+static constexpr size_t subsort_smem_bytes() {
+  return keys_smem_bytes<LANES, kSubThreads * TileCfg<LANES>::E, false>() + kSubPayBuf;
+}
 
 int tile_size(int lanes) {
   switch (lanes) {
@@ -888,8 +924,7 @@ static void set_attrs_t() {
   if (!STATS && LANES >= 1) {
     cudaFuncSetAttribute(subsort_kernel<LANES < 1 ? 1 : LANES>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)pass_smem_bytes<(LANES < 1 ? 1 : LANES),
-                                              kSubThreads * TileCfg<(LANES < 1 ? 1 : LANES)>::E, false>());
+                         (int)subsort_smem_bytes<(LANES < 1 ? 1 : LANES)>());
   }
   cudaFuncSetAttribute(tile_sort_kernel<LANES, STATS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>());
@@ -948,8 +983,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
   slot_scan_kernel<<<a.nsegs, 1024, 0, st>>>(a);
   partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
-  subsort_kernel<LANES><<<a.nslots, kSubThreads,
-                          pass_smem_bytes<LANES, kSubThreads * TileCfg<LANES>::E, false>(), st>>>(a);
+  subsort_kernel<LANES><<<a.nslots, kSubThreads, subsort_smem_bytes<LANES>(), st>>>(a);
 }
 
 int sample_max_keys(int) { return kSampleSmem / 8; }

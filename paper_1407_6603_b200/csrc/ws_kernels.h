@@ -98,7 +98,8 @@ struct SampleSeg {
   uint32_t split_off;   // first splitter of the bucket in `splitters`
   uint32_t slot_base;   // first of the bucket's 2 * nsplit + 1 slots
   uint32_t tile_begin;  // first partition tile of the bucket
-  uint32_t pad_;
+  uint32_t len;         // word length L of the bucket
+  uint8_t* pay;         // fused emission: the bucket's payload records (6-bit text keys), or null
 };
 struct SampleLaunch {
   const SampleSeg* segs;  // device table when nsegs > kInlineSegs, else nullptr

@@ -37,7 +37,8 @@ print("ok")
     "WSORT_NO_RADIX",         # class 0 by tile + merge path in payload mode
     "WSORT_NO_SAMPLE",        # multi-lane classes by tile + merge path in payload mode
     "WSORT_RADIX_RTS",        # class-0 radix by upsweep + scan + downsweep (no look-back)
-    "WSORT_NO_FUSED_PAYLOAD", # class-0 payload by the emit kernel after the last radix pass
+    "WSORT_NO_FUSED_PAYLOAD", # payload by the emit kernels after the last radix pass / slot sorts
+    "WSORT_NO_FUSED_SLOTS",   # multi-lane payload by the emit kernels after the slot sorts
     "WSORT_LOOKBACK",         # ordered ingest by the decoupled look-back
     "WSORT_TWO_PASS",         # count + scan + scatter ingest
     "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest

@@ -1,6 +1,6 @@
 """Quick A/B of library variants on the device-resident step (config 4).
 
-usage: python tools/ab_quick.py VARIANT... (default | a build/variants/ name)
+usage: python tools/ab_quick.py VARIANT... (default | env:NAME=VALUE | a build/variants/ name)
 Each variant runs in its own process (WSORT_LIB); prints the median step time
 (CUDA events on the library stream, 256 MiB L2 flush between steps) and the
 per-phase times of one profiled step. Two rounds, interleaved.
@@ -48,7 +48,10 @@ def main(variants):
         for v in variants:
             env = dict(os.environ)
             env.pop("WSORT_LIB", None)
-            if v != "default":
+            if v.startswith("env:"):  # env:NAME=VALUE on the default library
+                k, _, val = v[4:].partition("=")
+                env[k] = val
+            elif v != "default":
                 env["WSORT_LIB"] = f"build/variants/{v}/libwsort_b200.so"
             out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-400:]
