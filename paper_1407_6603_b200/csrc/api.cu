@@ -425,6 +425,43 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
 // passes over 8-bit digits of the bits each bucket uses (radix.cu). Pass p
 // reads buffer p & 1 (pass 0: the segment's in_ptr) and writes (p + 1) & 1;
 // a bucket is done after ceil(bits / 8) passes.
+// WSORT_OS_PROF=1: per-tile phase durations of one one-sweep pass (stderr).
+void print_os_profile(DevBuf& prof, uint32_t work, int pass, cudaStream_t st) {
+  std::vector<unsigned long long> v((size_t)work * 8);
+  cudaMemcpyAsync(v.data(), prof.p, v.size() * 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  unsigned long long t0 = ~0ull, t1 = 0;
+  double ph[4] = {0, 0, 0, 0}, mx[4] = {0, 0, 0, 0};
+  for (uint32_t i = 0; i < work; ++i) {
+    const unsigned long long* r = &v[(size_t)i * 8];
+    t0 = std::min(t0, r[0]);
+    t1 = std::max(t1, r[4]);
+    for (int k = 0; k < 4; ++k) {
+      const double d = (double)(r[k + 1] - r[k]);
+      ph[k] += d;
+      mx[k] = std::max(mx[k], d);
+    }
+  }
+  double rounds = 0, stalls = 0;
+  for (uint32_t i = 0; i < work; ++i) {
+    rounds += (double)v[(size_t)i * 8 + 5];
+    stalls += (double)v[(size_t)i * 8 + 6];
+  }
+  fprintf(stderr, "os_prof pass %d tiles %u span %.1f us | mean us: rank %.2f scan %.2f lookback %.2f "
+          "scatter %.2f | max: %.2f %.2f %.2f %.2f | look-back rounds %.1f (not-ready %.1f)\n",
+          pass, work, (t1 - t0) / 1e3, ph[0] / work / 1e3, ph[1] / work / 1e3, ph[2] / work / 1e3,
+          ph[3] / work / 1e3, mx[0] / 1e3, mx[1] / 1e3, mx[2] / 1e3, mx[3] / 1e3, rounds / work,
+          stalls / work);
+  // in-flight tiles over time (8 samples)
+  for (int s = 1; s < 8; ++s) {
+    const unsigned long long t = t0 + (t1 - t0) * s / 8;
+    int live = 0;
+    for (uint32_t i = 0; i < work; ++i) live += v[(size_t)i * 8] <= t && v[(size_t)i * 8 + 4] > t;
+    fprintf(stderr, " %d", live);
+  }
+  fprintf(stderr, " (tiles in flight)\n");
+}
+
 int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* keys0,
                         uint64_t* keys1, cudaStream_t st, const PassDoneHook* on_done,
                         uint8_t* pay = nullptr, const std::vector<uint64_t>* pay_off = nullptr) {
@@ -516,11 +553,22 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       a.ticket = tickets + a.pass;
       if (++h->radix_epoch >= (1u << 30)) h->radix_epoch = 1;
       a.epoch = h->radix_epoch;
+      static const char* os_prof = getenv("WSORT_OS_PROF");  // diagnostics: per-tile phase stamps
+      DevBuf prof;
+      if (os_prof && os_prof[0] == '1' && p >= 0) {
+        WS_CUDA(prof.ensure((size_t)work * 64));
+        WS_CUDA(cudaMemsetAsync(prof.p, 0, (size_t)work * 64, st));
+        a.prof = prof.as<unsigned long long>();
+      }
       Phase ph(h, name, bytes, 0, st);
       if (p < 0) launch_radix_hist(lanes, a, st);
       else launch_radix_onesweep(lanes, a, st);
       ++h->launches;
       ph.end();
+      if (a.prof) {
+        print_os_profile(prof, work, p, st);
+        prof.release();
+      }
       WS_TRY(check_launch(name));
       if (on_done && p >= 0) {
         std::vector<const SegIn*> done;

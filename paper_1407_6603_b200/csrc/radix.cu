@@ -85,9 +85,42 @@ __device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool ok) {
 #ifndef WS_RANK_OR
 #define WS_RANK_OR 0  // 1 measured ~2 % slower on the step (fewer instructions, latency-bound)
 #endif
+// Ranks of a thread's keys: two 16-bit ranks per register (a tile holds <
+// 2^16 keys), which keeps the one-sweep kernel within 64 registers.
+#ifndef WS_PACK_RK
+#define WS_PACK_RK 1
+#endif
+template <int E>
+struct Ranks {
+  static constexpr int N = WS_PACK_RK ? (E + 1) / 2 : E;
+  uint32_t v[N];
+  template <int R>
+  __device__ __forceinline__ void set(uint32_t x) {
+    if constexpr (WS_PACK_RK) {
+      if constexpr (R & 1) v[R >> 1] |= x << 16; else v[R >> 1] = x;
+    } else {
+      v[R] = x;
+    }
+  }
+  __device__ __forceinline__ uint32_t get(int r) const {
+    if (WS_PACK_RK) return (v[r >> 1] >> (16 * (r & 1))) & 0xFFFFu;
+    return v[r];
+  }
+};
+template <int R, int E>
+struct RankSetter {
+  __device__ __forceinline__ static void set(Ranks<E>& rk, int r, uint32_t x) {
+    if (r == R) rk.template set<R>(x); else RankSetter<R + 1, E>::set(rk, r, x);
+  }
+};
+template <int E>
+struct RankSetter<E, E> {
+  __device__ __forceinline__ static void set(Ranks<E>&, int, uint32_t) {}
+};
+
 template <class K, int E>
 __device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, uint32_t shift,
-                                          uint32_t* wcnt, uint32_t* wmask, uint32_t (&rk)[E]) {
+                                          uint32_t* wcnt, uint32_t* wmask, Ranks<E>& rk) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -102,7 +135,7 @@ __device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, ui
       peers = wmask[d];
       base = wcnt[d];
     }
-    rk[r] = base + __popc(peers & lt);
+    RankSetter<0, E>::set(rk, r, base + __popc(peers & lt));
     __syncwarp();
     if (ok && lane == 31 - __clz(peers)) {
       wcnt[d] = base + __popc(peers);
@@ -114,7 +147,7 @@ __device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, ui
     const uint32_t peers = match_digit8(d, ok);
     uint32_t base = 0;
     if (ok) base = wcnt[d];
-    rk[r] = base + __popc(peers & lt);
+    RankSetter<0, E>::set(rk, r, base + __popc(peers & lt));
     __syncwarp();
     if (ok && lane == 31 - __clz(peers)) wcnt[d] = base + __popc(peers);
     __syncwarp();
@@ -246,7 +279,7 @@ radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
     const uint32_t j = r * 32 + lane;
     key[r] = j < nvalid ? __ldcs(in + j) : K(0);
   }
-  uint32_t rk[C::E];
+  Ranks<C::E> rk;
   warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], wmask[WS_RANK_OR ? wid : 0], rk);
   __syncthreads();
   // per digit (thread = digit): exclusive over warps, then over digits
@@ -277,7 +310,7 @@ radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
 #pragma unroll
   for (int r = 0; r < C::E; ++r) {
     const uint32_t j = r * 32 + lane;
-    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk[r]] = key[r];
+    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk.get(r)] = key[r];
   }
   __syncthreads();
   // per-digit runs to their global offsets (consecutive threads, consecutive addresses)
@@ -305,6 +338,9 @@ constexpr uint64_t kStEpochMask = ~0x3FFFFFFFFull;
 #define WS_LOOK_W 4
 #endif
 constexpr int kLookW = WS_LOOK_W;  // predecessors loaded per look-back round
+#ifndef WS_OS_EARLY
+#define WS_OS_EARLY 0  // 1: tile histogram + look-back before the ranking (measured 2 % slower)
+#endif
 #ifndef WS_OS_MINB
 #define WS_OS_MINB 3  // 80 registers, no spills (4: 64 with spills, measured slower)
 #endif
@@ -317,6 +353,17 @@ __device__ __forceinline__ uint64_t ld_status(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// Diagnostics: thread 0 stamps phase k of this tile (globaltimer, ns).
+#define WS_OS_STAMP(k)                                                         \
+  do {                                                                         \
+    if (a.prof && threadIdx.x == 0) a.prof[(uint64_t)tile * 8 + (k)] = gtimer(); \
+  } while (0)
 
 // Digit histograms of all passes of every segment: totals[sid][p][256].
 template <class K>
@@ -372,6 +419,10 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   __shared__ __align__(16) K stage[C::T];
   __shared__ int s_seg;
   __shared__ uint32_t s_tile;
+#if WS_OS_EARLY
+  __shared__ uint32_t s_hist[kDigits];
+  s_hist[threadIdx.x] = 0;
+#endif
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 32) {  // ticket order: every tile this one waits for has started
     uint32_t tk = 0;
@@ -389,6 +440,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   }
   __syncthreads();
   const uint32_t tile = s_tile;
+  WS_OS_STAMP(0);
   const RadixSeg& sg = rseg_at(a, s_seg);
   const uint32_t t = tile - sg.tile_begin;
   const uint64_t tfirst = (uint64_t)t * C::T;
@@ -404,9 +456,22 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     const uint32_t j = r * 32 + lane;
     key[r] = j < nvalid ? __ldcs(in + j) : K(0);
   }
-  uint32_t rk[C::E];
+#if WS_OS_EARLY
+  // The tile's digit counts first (shared atomics, no ranking), so its
+  // aggregate is published - and its look-back done and its inclusive prefix
+  // published - before the ranking: successors find inclusive prefixes
+  // nearer, which shortens every look-back walk.
+#pragma unroll
+  for (int r = 0; r < C::E; ++r)
+    if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&s_hist[digit_of<K>(key[r], sg.shift)], 1u);
+  __syncthreads();
+  WS_OS_STAMP(1);
+  const uint32_t run = s_hist[tid];
+#else
+  Ranks<C::E> rk;
   warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], wmask[WS_RANK_OR ? wid : 0], rk);
   __syncthreads();
+  WS_OS_STAMP(1);
   // per digit (thread = digit): exclusive over warps; the tile's count
   uint32_t run = 0;
 #pragma unroll
@@ -415,6 +480,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     wcnt[w][tid] = run;
     run += c;
   }
+#endif
   uint64_t* status = a.status + (uint64_t)tile * kDigits + tid;
   const uint64_t ep = (uint64_t)a.epoch << 34;
   const bool head = t == 0;  // the segment's first tile: its prefix is 0
@@ -443,6 +509,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   }
   const uint32_t doff = wpre + inc - run;
   const uint32_t dbase = wpre2 + inc2 - tot;
+#if !WS_OS_EARLY
 #pragma unroll
   for (int w = 0; w < kRWarps; ++w) wcnt[w][tid] += doff;  // tile-local start of (warp, digit)
   __syncthreads();
@@ -451,15 +518,19 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
 #pragma unroll
   for (int r = 0; r < C::E; ++r) {
     const uint32_t j = r * 32 + lane;
-    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk[r]] = key[r];
+    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk.get(r)] = key[r];
   }
+#endif
   // look-back over the segment's preceding tiles for this digit: a window of
   // kLookW predecessors per load round, nearest first; the segment's first
   // tile is always inclusive, so the walk stops there
+  WS_OS_STAMP(2);
   uint32_t excl = 0;
+  uint32_t rounds = 0, stalls = 0;  // diagnostics (WSORT_OS_PROF)
   if (!head) {
     uint32_t back = 1;  // distance of the nearest predecessor not yet consumed
     for (;;) {
+      ++rounds;
       uint64_t v[kLookW];
 #pragma unroll
       for (int w = 0; w < kLookW; ++w)
@@ -475,18 +546,78 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
         used = w + 1;
       }
       if (found) break;
+      stalls += used < (uint32_t)kLookW;
       back += used;
     }
     st_status(status, ep | kStInc | (excl + run));
   }
+  if (a.prof && tid == 0) {
+    a.prof[(uint64_t)tile * 8 + 5] = rounds;
+    a.prof[(uint64_t)tile * 8 + 6] = stalls;
+  }
+#if WS_OS_EARLY
+  {
+    // now rank (stable, per warp) and regroup the tile by digit in shared memory
+    Ranks<C::E> rk;
+    warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], wmask[WS_RANK_OR ? wid : 0], rk);
+    __syncthreads();
+    uint32_t st = doff;  // tile-local start of (warp, digit): doff + earlier warps' counts
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) {
+      const uint32_t c = wcnt[w][tid];
+      wcnt[w][tid] = st;
+      st += c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < C::E; ++r) {
+      const uint32_t j = r * 32 + lane;
+      if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk.get(r)] = key[r];
+    }
+  }
+#endif
   s_gdelta[tid] = dbase + excl - doff;
   __syncthreads();
+  WS_OS_STAMP(3);
   if (sg.pay) {  // the segment's last pass: payload records (characters + '\n') at rank * (L + 1)
     const uint32_t L = sg.len;
     constexpr int kBits = 8 * (int)sizeof(K);
     for (uint32_t i = tid; i < ntile; i += kRThreads) {
       const K k = stage[i];
       uint8_t* dst = sg.pay + (uint64_t)(s_gdelta[digit_of<K>(k, sg.shift)] + i) * (L + 1);
+      if constexpr (sizeof(K) == 4) {
+        // one-word keys: the record (<= 6 bytes) assembled little-endian in a
+        // register and written with the fewest aligned stores (1/2/4 bytes)
+        uint64_t rec = (uint64_t)'\n' << (8 * L);
+        if (a.enc == kEncAlnum6) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c)
+            if (c < (int)L) rec |= (uint64_t)alnum6_byte((uint32_t)(k >> (26 - 6 * c)) & 63u) << (8 * c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < (int)L) rec |= (uint64_t)((uint32_t)(k >> (24 - 8 * c)) & 0xFFu) << (8 * c);
+        }
+        uint32_t rem = L + 1;
+        if (((uintptr_t)dst & 1) != 0) {
+          *dst = (uint8_t)rec;
+          rec >>= 8; ++dst; --rem;
+        }
+        if (((uintptr_t)dst & 2) != 0 && rem >= 2) {
+          *reinterpret_cast<uint16_t*>(dst) = (uint16_t)rec;
+          rec >>= 16; dst += 2; rem -= 2;
+        }
+        if (rem >= 4) {
+          *reinterpret_cast<uint32_t*>(dst) = (uint32_t)rec;
+          rec >>= 32; dst += 4; rem -= 4;
+        }
+        if (rem >= 2) {
+          *reinterpret_cast<uint16_t*>(dst) = (uint16_t)rec;
+          rec >>= 16; dst += 2; rem -= 2;
+        }
+        if (rem) *dst = (uint8_t)rec;
+        continue;
+      }
       if (a.enc == kEncAlnum6) {
 #pragma unroll
         for (int c = 0; c < kBits / 6; ++c)
@@ -498,12 +629,20 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
       }
       dst[L] = '\n';
     }
+    if (a.prof) {
+      __syncthreads();
+      WS_OS_STAMP(4);
+    }
     return;
   }
   K* out = reinterpret_cast<K*>(sg.out);
   for (uint32_t i = tid; i < ntile; i += kRThreads) {
     const K k = stage[i];
     out[s_gdelta[digit_of<K>(k, sg.shift)] + i] = k;
+  }
+  if (a.prof) {
+    __syncthreads();
+    WS_OS_STAMP(4);
   }
 }
 

@@ -148,6 +148,7 @@ struct RadixLaunch {
   uint32_t epoch;        // one-sweep: unique per launch, < 2^30, != 0
   uint32_t pass;
   int enc;               // key encoding (kEncAlnum6 / kEncRaw8), for payload records
+  unsigned long long* prof;  // diagnostics (WSORT_OS_PROF): [tile][8] phase timestamps, or null
   RadixSeg inl[kInlineSegs];
 };
 int radix_tile_size(int lanes);
