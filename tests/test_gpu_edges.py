@@ -361,3 +361,31 @@ def test_fused_payload_sort_then_emit_needs_sort():
     h.sort(False)
     assert h.emit_lines().tobytes() == want
     h.close()
+
+
+def test_fused_slot_records_repeats_singletons_and_alignment():
+    # multi-lane buckets (6..32 characters) whose slot sorts write payload
+    # records directly: one word repeated 1..90k times (pattern fill at every
+    # 16-byte phase), singleton slots, slots beyond a slot-sort tile (many
+    # words sharing a 10-character prefix), mixed with random words
+    rng = np.random.default_rng(2026)
+    al = np.frombuffer(synth.ALNUM, dtype=np.uint8)
+    words = []
+    for L in (6, 7, 10, 11, 13, 21, 22, 31, 32):
+        for reps in (1, 2, 3, 17, 255, 5000, 90_000 if L in (6, 22) else 1200):
+            w = bytes(al[rng.integers(0, len(al), L)])
+            words += [w] * reps
+        words += [bytes(r) for r in al[rng.integers(0, len(al), size=(4000, L))]]
+        pre = bytes(al[rng.integers(0, len(al), min(L - 1, 10))])
+        words += [pre + bytes(r) for r in al[rng.integers(0, len(al), size=(3000, L - len(pre)))]]
+    order = rng.permutation(len(words))
+    text = b" ".join(words[i] for i in order)
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
+    h = _native.Handle(0)
+    src = np.frombuffer(text, dtype=np.uint8)
+    out = np.empty(len(text) + 64, dtype=np.uint8)
+    for shift in range(3):  # the same corpus again on a reused handle
+        n = h.sort_text(src, out)
+        assert out[:n].tobytes() == want, shift
+    h.close()
