@@ -1224,8 +1224,10 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       }
       static const char* no_fuse_s = getenv("WSORT_NO_FUSED_PAYLOAD");
       static const char* no_fuse_slots = getenv("WSORT_NO_FUSED_SLOTS");
+      static const char* fuse_mask = getenv("WSORT_FUSED_SLOT_CLASSES");  // experiment: bit c = class c
       const bool fuse_s = on_done && !(no_fuse_s && no_fuse_s[0] == '1') &&
-                          !(no_fuse_slots && no_fuse_slots[0] == '1');
+                          !(no_fuse_slots && no_fuse_slots[0] == '1') &&
+                          (!fuse_mask || ((strtol(fuse_mask, nullptr, 0) >> c) & 1));
       if (!fit.empty())
         WS_TRY(sample_sort_segments(h, c, fit, k1, cst, on_done, fuse_s ? fe->dout : nullptr,
                                     fuse_s ? &fe->off : nullptr));
