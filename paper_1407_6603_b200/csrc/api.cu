@@ -473,16 +473,26 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
     SegIn* s;
     int passes;
     uint32_t shift0, ntiles;
+    uint32_t jbits;  // > 0: no passes, payload from the whole-key counts
   };
   std::vector<Plan> plan;
   int max_passes = 0;
   uint64_t count_words = 0;
+  static const char* rts_env = getenv("WSORT_RADIX_RTS");
+  const bool rts = rts_env && rts_env[0] == '1';
+  static const char* nj_env = getenv("WSORT_NO_JOINT");
+  const bool joint_ok = pay && lanes == 0 && !rts && !(nj_env && nj_env[0] == '1');
   for (auto& s : segs) {
     s.final_buf = 0;
     if (!s.n) continue;
     const int bits = std::min(keybits, cbits * (int)h->buckets[s.stat_slot].len);
-    const int passes = std::max(1, (bits + 7) / 8);
-    plan.push_back(Plan{&s, passes, (uint32_t)(keybits - bits), (s.n + T - 1) / T});
+    int passes = std::max(1, (bits + 7) / 8);
+    uint32_t jbits = 0;
+    if (joint_ok && bits <= 12) {  // <= 4096 distinct keys: counted, not sorted
+      jbits = (uint32_t)bits;
+      passes = 0;
+    }
+    plan.push_back(Plan{&s, passes, (uint32_t)(keybits - bits), (s.n + T - 1) / T, jbits});
     max_passes = std::max(max_passes, passes);
     count_words += 256ull * plan.back().ntiles;
     s.final_buf = passes & 1;
@@ -491,15 +501,24 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
   DevBuf& cb = h->rcounts[lanes];
   DevBuf& tb = h->rtotals[lanes];
   uint8_t* kb[2] = {reinterpret_cast<uint8_t*>(keys0), reinterpret_cast<uint8_t*>(keys1)};
-  static const char* rts_env = getenv("WSORT_RADIX_RTS");
-  if (!(rts_env && rts_env[0] == '1')) {
+  if (!rts) {
     // one-sweep: one histogram launch for the digit totals of every pass, then
     // one look-back launch per pass
     const size_t tot_words = plan.size() * kRadixMaxPasses * 256;
-    WS_CUDA(tb.ensure(tot_words * 4 + kRadixMaxPasses * 4 + 64));
-    WS_CUDA(cudaMemsetAsync(tb.p, 0, tot_words * 4 + kRadixMaxPasses * 4, st));
+    size_t joint_words = 0;
+    uint32_t njoint = 0, jblocks = 0;
+    for (auto& pl : plan)
+      if (pl.jbits) {
+        joint_words += 2u << pl.jbits;  // counts, then their exclusive prefix
+        jblocks += 1u << pl.jbits;
+        ++njoint;
+      }
+    const size_t zero_bytes = (tot_words + kRadixMaxPasses + joint_words) * 4;
+    WS_CUDA(tb.ensure(zero_bytes + 64));
+    WS_CUDA(cudaMemsetAsync(tb.p, 0, zero_bytes, st));
     uint32_t* totals = tb.as<uint32_t>();
     uint32_t* tickets = totals + tot_words;
+    uint32_t* joint = tickets + kRadixMaxPasses;
     uint32_t all_tiles = 0;
     for (auto& pl : plan) all_tiles += pl.ntiles;
     DevBuf& sb = h->rstatus[lanes];
@@ -510,6 +529,7 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
     char name[32];
     snprintf(name, sizeof name, "radix_l%d", lanes);
     for (int p = -1; p < max_passes; ++p) {  // p = -1: the histogram launch
+      uint32_t joff = 0;
       std::vector<RadixSeg> d;
       uint32_t work = 0;
       double bytes = 0;
@@ -527,6 +547,14 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         r.shift = pl.shift0 + 8 * std::max(p, 0);
         r.sid = (uint32_t)i;
         r.passes = (uint32_t)pl.passes;
+        if (p < 0 && pl.jbits) {
+          r.jbits = pl.jbits;
+          r.joff = joff;
+          joff += 2u << pl.jbits;
+          r.pay = pay + (*pay_off)[pl.s->stat_slot];
+          r.len = h->buckets[pl.s->stat_slot].len;
+          pl.s->emitted = true;
+        }
         if (pay && p == pl.passes - 1) {  // last pass: payload records instead of keys
           r.pay = pay + (*pay_off)[pl.s->stat_slot];
           r.len = h->buckets[pl.s->stat_slot].len;
@@ -553,6 +581,7 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       a.ticket = tickets + a.pass;
       if (++h->radix_epoch >= (1u << 30)) h->radix_epoch = 1;
       a.epoch = h->radix_epoch;
+      a.joint = joint;
       static const char* os_prof = getenv("WSORT_OS_PROF");  // diagnostics: per-tile phase stamps
       DevBuf prof;
       if (os_prof && os_prof[0] == '1' && p >= 0) {
@@ -568,6 +597,17 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       if (a.prof) {
         print_os_profile(prof, work, p, st);
         prof.release();
+      }
+      if (p < 0 && njoint) {  // the counted segments are done: payload from their counts
+        launch_joint_expand(a, jblocks, njoint, st);
+        h->launches += 2;
+        WS_TRY(check_launch("joint_expand"));
+        if (on_done) {
+          std::vector<const SegIn*> done;
+          for (auto& pl : plan)
+            if (pl.jbits) done.push_back(pl.s);
+          WS_TRY((*on_done)(done, st));
+        }
       }
       WS_TRY(check_launch(name));
       if (on_done && p >= 0) {

@@ -21,6 +21,7 @@
 
 #include "ws_common.cuh"
 #include "ws_kernels.h"
+#include "payload.cuh"
 
 namespace ws {
 namespace {
@@ -366,12 +367,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 // Digit histograms of all passes of every segment: totals[sid][p][256].
+// Segments whose keys have <= 12 bits (6-bit text words of 1-2 characters,
+// raw words of 1 byte) with a payload destination skip the passes: the
+// histogram launch counts whole keys (joint[]) and joint_expand_kernel writes
+// each distinct word as often as it occurs, at its rank.
+constexpr int kJointMax = 1 << 12;
+
 template <class K>
 __global__ void __launch_bounds__(kRThreads)
 radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
   using C = RadixCfg<K>;
   constexpr int kP = (int)sizeof(K);  // at most one pass per key byte
-  __shared__ uint32_t hist[kP][kDigits];
+  constexpr int kSm = kP * kDigits > kJointMax ? kP * kDigits : kJointMax;
+  __shared__ uint32_t sm[kSm];  // hist[kP][256], or the joint counts of a jbits segment
+  uint32_t (*hist)[kDigits] = reinterpret_cast<uint32_t (*)[kDigits]>(sm);
   __shared__ int s_seg;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t tile = blockIdx.x;
@@ -379,9 +388,12 @@ radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
     const int s = rsegment_of(a, tile);
     if (tid == 0) s_seg = s;
   }
-  for (int i = tid; i < kP * kDigits; i += kRThreads) (&hist[0][0])[i] = 0;
   __syncthreads();
   const RadixSeg& sg = rseg_at(a, s_seg);
+  const uint32_t jbits = sizeof(K) == 4 ? sg.jbits : 0u;
+  const int nzero = jbits ? (1 << jbits) : kP * kDigits;
+  for (int i = tid; i < nzero; i += kRThreads) sm[i] = 0;
+  __syncthreads();
   const uint32_t t = tile - sg.tile_begin;
   const uint64_t first = (uint64_t)t * C::T + (uint64_t)wid * 32 * C::E;
   const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
@@ -391,6 +403,15 @@ radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
   for (int r = 0; r < C::E; ++r) {
     const uint32_t j = r * 32 + lane;
     key[r] = j < nvalid ? in[j] : K(0);  // default caching: the first pass re-reads from L2
+  }
+  if (jbits) {
+#pragma unroll
+    for (int r = 0; r < C::E; ++r)
+      if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&sm[(uint32_t)(key[r] >> (32 - jbits))], 1u);
+    __syncthreads();
+    for (int v = tid; v < (1 << jbits); v += kRThreads)
+      if (sm[v]) atomicAdd(a.joint + sg.joff + v, sm[v]);
+    return;
   }
   const int passes = (int)sg.passes;
 #pragma unroll
@@ -405,6 +426,83 @@ radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
   for (int p = 0; p < passes; ++p) {
     const uint32_t c = hist[p][tid];
     if (c) atomicAdd(a.totals + ((uint64_t)sg.sid * kRadixMaxPasses + p) * kDigits + tid, c);
+  }
+}
+
+// One CTA per jbits segment: exclusive prefix of its 2^jbits counts, stored
+// right after them.
+// The b-th jbits segment of the launch (counting in segment order).
+__device__ __forceinline__ int jseg_at(const RadixLaunch& a, uint32_t b) {
+  for (int i = 0; i < a.nsegs; ++i)
+    if (rseg_at(a, i).jbits && b-- == 0) return i;
+  return 0;
+}
+
+__global__ void __launch_bounds__(1024) joint_scan_kernel(const __grid_constant__ RadixLaunch a) {
+  __shared__ uint32_t s_w[32];
+  const RadixSeg& sg = rseg_at(a, jseg_at(a, blockIdx.x));
+  uint32_t* cnt = a.joint + sg.joff;
+  const uint32_t nv = 1u << sg.jbits;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t v[4], sum = 0;  // 4 consecutive values per thread (nv <= 4096)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t i = 4 * tid + q;
+    v[q] = i < nv ? cnt[i] : 0u;
+    sum += v[q];
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_w[wid] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum;
+  for (int w = 0; w < wid; ++w) run += s_w[w];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t i = 4 * tid + q;
+    if (i < nv) cnt[nv + i] = run;
+    run += v[q];
+  }
+}
+
+// One CTA per (jbits segment, key value, part): the value's copies [part
+// share] as payload records at pay + (prefix + first copy) * (L + 1).
+constexpr int kExpandThreads = 128;
+constexpr int kExpandParts = 4;
+__global__ void __launch_bounds__(kExpandThreads)
+joint_expand_kernel(const __grid_constant__ RadixLaunch a) {
+  __shared__ __align__(16) uint8_t pbuf[64 + 16 * 40];
+  uint32_t v = blockIdx.x;  // blocks: the jbits segments' values back to back
+  int si = 0;
+  for (; si < a.nsegs; ++si) {
+    const uint32_t jb = rseg_at(a, si).jbits;
+    if (!jb) continue;
+    if (v < (1u << jb)) break;
+    v -= 1u << jb;
+  }
+  if (si == a.nsegs) return;
+  const RadixSeg& sg = rseg_at(a, si);
+  const uint32_t* cnt = a.joint + sg.joff;
+  const uint32_t c = cnt[v];
+  const uint32_t part = blockIdx.y;
+  const uint32_t c0 = (uint32_t)((uint64_t)c * part / kExpandParts);
+  const uint32_t c1 = (uint32_t)((uint64_t)c * (part + 1) / kExpandParts);
+  if (c1 <= c0) return;
+  const uint32_t pre = cnt[(1u << sg.jbits) + v];  // copies of smaller values (joint_scan_kernel)
+  const int L = (int)sg.len;
+  Key<0> k0;
+  k0.w[0] = v << (32 - sg.jbits);
+  uint8_t* out = sg.pay + (uint64_t)(pre + c0) * (L + 1);
+  if (a.enc == kEncAlnum6) {
+    fill_records_cta<0, kExpandThreads>(k0, c1 - c0, L, out, pbuf);
+  } else {  // raw one-byte words: the record is the byte + '\n'
+    const uint64_t n = (uint64_t)(c1 - c0) * 2;
+    const uint8_t b = (uint8_t)v;
+    for (uint64_t q = threadIdx.x; q < n; q += kExpandThreads) out[q] = (q & 1) ? '\n' : b;
   }
 }
 
@@ -654,6 +752,12 @@ void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st) {
     radix_hist_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
   else
     radix_hist_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+}
+
+void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs, cudaStream_t st) {
+  if (!blocks) return;
+  joint_scan_kernel<<<njsegs, 1024, 0, st>>>(a);
+  joint_expand_kernel<<<dim3(blocks, kExpandParts), kExpandThreads, 0, st>>>(a);
 }
 
 void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st) {

@@ -134,6 +134,8 @@ struct RadixSeg {
   uint32_t passes;      // one-sweep histogram: passes of the segment
   uint8_t* pay;         // one-sweep, segment's last pass: write payload records here instead
   uint32_t len;         //   of keys (word length; record = characters + '\n')
+  uint32_t jbits;       // histogram launch: > 0 = count whole keys (key >> (32 - jbits), one-word
+  uint32_t joff;        //   keys of <= 12 bits) into joint[joff ..]; the segment then takes no pass
 };
 constexpr int kRadixMaxPasses = 8;  // one per key byte
 struct RadixLaunch {
@@ -149,11 +151,16 @@ struct RadixLaunch {
   uint32_t pass;
   int enc;               // key encoding (kEncAlnum6 / kEncRaw8), for payload records
   unsigned long long* prof;  // diagnostics (WSORT_OS_PROF): [tile][8] phase timestamps, or null
+  uint32_t* joint;       // whole-key counters of the jbits segments (zeroed with the totals)
   RadixSeg inl[kInlineSegs];
 };
 int radix_tile_size(int lanes);
 void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st);
 void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st);
+// Payload of the jbits segments straight from their whole-key counts: value v
+// of segment i repeated joint[v] times at its rank (the exclusive prefix).
+// blocks = sum of 2^jbits over the launch's jbits segments (njsegs of them).
+void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs, cudaStream_t st);
 void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st);
 
 // emit.cu

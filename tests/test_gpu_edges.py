@@ -389,3 +389,20 @@ def test_fused_slot_records_repeats_singletons_and_alignment():
         n = h.sort_text(src, out)
         assert out[:n].tobytes() == want, shift
     h.close()
+
+
+def test_counted_short_buckets_every_value_and_hot_words():
+    # 1- and 2-character buckets are counted, not sorted (payload from
+    # whole-key counts): every one of the 62 / 3844 values, hot values with
+    # 10^5-10^6 copies (split over CTA parts), absent values, odd counts
+    rng = np.random.default_rng(31)
+    al = synth.ALNUM
+    words = [bytes([c]) for c in al] + [bytes([a, b]) for a in al for b in al]
+    words += [b"a"] * 1_000_003 + [b"Zz"] * 123_457 + [b"9"] * 7 + [b"q"] * 65_537
+    words += [bytes([al[i % 62]]) * (1 + i % 2) for i in rng.integers(0, 62, 200_000)]
+    order = rng.permutation(len(words))
+    text = b"\n".join(words[i] for i in order)
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
+    sparse = b" ".join([b"x"] * 5 + [b"Q1"] * 3 + [b"abcdef"])
+    assert sort_text(sparse) == oracle.sort_text(sparse, mode="fast")[0]

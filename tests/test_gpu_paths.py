@@ -39,6 +39,7 @@ print("ok")
     "WSORT_RADIX_RTS",        # class-0 radix by upsweep + scan + downsweep (no look-back)
     "WSORT_NO_FUSED_PAYLOAD", # payload by the emit kernels after the last radix pass / slot sorts
     "WSORT_NO_FUSED_SLOTS",   # multi-lane payload by the emit kernels after the slot sorts
+    "WSORT_NO_JOINT",         # 1-2 character buckets by radix passes instead of whole-key counts
     "WSORT_LOOKBACK",         # ordered ingest by the decoupled look-back
     "WSORT_TWO_PASS",         # count + scan + scatter ingest
     "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest
