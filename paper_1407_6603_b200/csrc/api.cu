@@ -182,6 +182,7 @@ struct ws_handle {
   bool payload_only = false;      // a fused sort wrote some buckets' payload without their keys
   uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
+  DevBuf ss_ids[kClasses + 1];                            // per-key slot ids
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
   uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
@@ -728,6 +729,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   if (d.size() > (size_t)kInlineSegs) return fail(WS_ERR_STATE, "too many buckets in a class");
   WS_CUDA(h->ss_split[lanes].ensure((size_t)std::max(splits, 1u) * 8 + 64));
   WS_CUDA(h->ss_slots[lanes].ensure((size_t)slots * 12 + 64));
+  WS_CUDA(h->ss_ids[lanes].ensure((size_t)tiles * part_tile_size() * 2 + 64));
   SampleLaunch a;
   std::copy(d.begin(), d.end(), a.inl);
   a.segs = nullptr;
@@ -739,6 +741,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   a.hist = h->ss_slots[lanes].as<uint32_t>();
   a.cursor = a.hist + slots;
   a.slot_off = a.cursor + slots;
+  a.slot_ids = h->ss_ids[lanes].as<uint16_t>();
   WS_CUDA(cudaMemsetAsync(a.hist, 0, (size_t)slots * 4, st));
   double bytes = 0;
   for (const auto& s : segs) bytes += 5.0 * s.n * key_bytes(lanes);
@@ -1767,7 +1770,8 @@ void ws_destroy(ws_handle* h) {
                     &h->run_at, &h->run_cnt, &h->run_off, &h->longlist2,
                     &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1], &h->rstatus[0], &h->rstatus[1],
                     &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
-                    &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4]};
+                    &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4],
+                    &h->ss_ids[1], &h->ss_ids[2], &h->ss_ids[3], &h->ss_ids[4]};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();

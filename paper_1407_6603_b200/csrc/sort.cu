@@ -730,25 +730,39 @@ __global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_co
   __syncthreads();
   const SampleSeg& sg = sseg_at(a, s_seg);
   const uint32_t nslot = 2 * sg.nsplit + 1;
-  for (uint32_t i = tid; i < sg.nsplit; i += kPartThreads) s_split[i] = a.splitters[sg.split_off + i];
+  if (COUNT)  // the scatter pass reads the slots the count pass found
+    for (uint32_t i = tid; i < sg.nsplit; i += kPartThreads) s_split[i] = a.splitters[sg.split_off + i];
   for (uint32_t i = tid; i < nslot; i += kPartThreads) s_cnt[i] = 0;
   __syncthreads();
   const uint64_t first = (uint64_t)(blockIdx.x - sg.tile_begin) * kPartTile;
   const W* in = kv<LANES>(sg.in);
+  uint16_t* ids = a.slot_ids + (uint64_t)blockIdx.x * kPartTile;
   Key<LANES> k[kPartPer];
   uint32_t slot[kPartPer], rank[kPartPer];
 #pragma unroll
   for (int q = 0; q < kPartPer; ++q) {  // every load in flight before the first search
     const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
-    if (i < sg.n) k[q] = gld<LANES>(in, (int64_t)i);
+    if (i < sg.n) {
+      if (COUNT) {
+        k[q].w[0] = __ldg(in + i * KeyTraits<LANES>::NW);  // the 64-bit prefix is all it needs
+        slot[q] = 0;
+      } else {
+        k[q] = gld<LANES>(in, (int64_t)i);
+        slot[q] = ids[q * kPartThreads + tid];
+      }
+    }
   }
 #pragma unroll
   for (int q = 0; q < kPartPer; ++q) {
     const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
-    slot[q] = 0xFFFFFFFFu;
     if (i < sg.n) {
-      slot[q] = slot_of(s_split, sg.nsplit, prefix_of<LANES>(k[q]));
+      if (COUNT) {
+        slot[q] = slot_of(s_split, sg.nsplit, prefix_of<LANES>(k[q]));
+        ids[q * kPartThreads + tid] = (uint16_t)slot[q];
+      }
       rank[q] = atomicAdd(&s_cnt[slot[q]], 1u);
+    } else {
+      slot[q] = 0xFFFFFFFFu;
     }
   }
   __syncthreads();

@@ -111,6 +111,7 @@ struct SampleLaunch {
   uint32_t* hist;         // per slot: keys (zeroed before the launch)
   uint32_t* cursor;       // per slot: reservation cursor
   uint32_t* slot_off;     // per slot: class-relative element offset
+  uint16_t* slot_ids;     // per key, in partition-tile order: its slot (count pass -> scatter pass)
   SampleSeg inl[kInlineSegs];
 };
 int sample_max_keys(int lanes);
