@@ -180,6 +180,9 @@ struct ws_handle {
   DevBuf rcounts[2], rtotals[2];  // radix passes of lane classes 0 and 1
   DevBuf rstatus[2];              // one-sweep look-back words
   bool payload_only = false;      // a fused sort wrote some buckets' payload without their keys
+  bool early_req = false;         // the next ingest launches the class-0 histogram itself
+  bool early_done = false;        // ... and did (valid for the sort that follows)
+  bool early_joint = false;       //     with whole-key counts for <= 12-bit keys
   uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   DevBuf ss_ids[kClasses + 1];                            // per-key slot ids
@@ -505,7 +508,12 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
   if (!rts) {
     // one-sweep: one histogram launch for the digit totals of every pass, then
     // one look-back launch per pass
-    const size_t tot_words = plan.size() * kRadixMaxPasses * 256;
+    const size_t tot_words = (lanes == 0 ? std::max<size_t>(kRadixC0Segs, plan.size()) : plan.size()) *
+                             kRadixMaxPasses * 256;
+    // the ingest already ran this histogram launch (same plan rules, same stream)
+    const bool early = h->early_done && lanes == 0 && pay && joint_ok == h->early_joint &&
+                       plan.size() <= (size_t)kRadixC0Segs;
+    h->early_done = false;
     size_t joint_words = 0;
     uint32_t njoint = 0, jblocks = 0;
     for (auto& pl : plan)
@@ -515,8 +523,10 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         ++njoint;
       }
     const size_t zero_bytes = (tot_words + kRadixMaxPasses + joint_words) * 4;
-    WS_CUDA(tb.ensure(zero_bytes + 64));
-    WS_CUDA(cudaMemsetAsync(tb.p, 0, zero_bytes, st));
+    if (!early) {
+      WS_CUDA(tb.ensure(zero_bytes + 64));
+      WS_CUDA(cudaMemsetAsync(tb.p, 0, zero_bytes, st));
+    }
     uint32_t* totals = tb.as<uint32_t>();
     uint32_t* tickets = totals + tot_words;
     uint32_t* joint = tickets + kRadixMaxPasses;
@@ -529,6 +539,8 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
     if (sb.p != before || sb.cap != cap0) WS_CUDA(cudaMemsetAsync(sb.p, 0, sb.cap, st));  // no stale epochs
     char name[32];
     snprintf(name, sizeof name, "radix_l%d", lanes);
+    RadixLaunch jlaunch;  // the histogram launch's table (jbits segments and their counters)
+    memset(&jlaunch, 0, sizeof jlaunch);
     for (int p = -1; p < max_passes; ++p) {  // p = -1: the histogram launch
       uint32_t joff = 0;
       std::vector<RadixSeg> d;
@@ -591,31 +603,32 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         a.prof = prof.as<unsigned long long>();
       }
       Phase ph(h, name, bytes, 0, st);
-      if (p < 0) launch_radix_hist(lanes, a, st);
-      else launch_radix_onesweep(lanes, a, st);
-      ++h->launches;
+      if (p >= 0) launch_radix_onesweep(lanes, a, st);
+      else if (!early) launch_radix_hist(lanes, a, st);
+      if (p >= 0 || !early) ++h->launches;
       ph.end();
       if (a.prof) {
         print_os_profile(prof, work, p, st);
         prof.release();
       }
-      if (p < 0 && njoint) {  // the counted segments are done: payload from their counts
-        launch_joint_expand(a, jblocks, njoint, st);
-        h->launches += 2;
-        WS_TRY(check_launch("joint_expand"));
-        if (on_done) {
-          std::vector<const SegIn*> done;
-          for (auto& pl : plan)
-            if (pl.jbits) done.push_back(pl.s);
-          WS_TRY((*on_done)(done, st));
-        }
-      }
+      if (p < 0 && njoint) jlaunch = a;  // the counted segments: expanded after the passes
       WS_TRY(check_launch(name));
       if (on_done && p >= 0) {
         std::vector<const SegIn*> done;
         for (auto& pl : plan)
           if (pl.passes == p + 1) done.push_back(pl.s);
         if (!done.empty()) WS_TRY((*on_done)(done, st));
+      }
+    }
+    if (njoint) {  // off the passes' chain: payload of the counted segments from their counts
+      launch_joint_expand(jlaunch, jblocks, njoint, st);
+      h->launches += 2;
+      WS_TRY(check_launch("joint_expand"));
+      if (on_done) {
+        std::vector<const SegIn*> done;
+        for (auto& pl : plan)
+          if (pl.jbits) done.push_back(pl.s);
+        WS_TRY((*on_done)(done, st));
       }
     }
     return WS_OK;
@@ -866,6 +879,51 @@ int finish_ingest(ws_handle* h) {
   return WS_OK;
 }
 
+static bool env_on(const char* v) {
+  const char* e = getenv(v);
+  return e && e[0] == '1';
+}
+
+// The fused payload sorts (ws_sort_text / ws_sort_resident / batches) let the
+// ingest start class 0's histogram launch on the class-0 stream, planned on the
+// device from the fill counters, so it overlaps the host's read-back and plan.
+bool early_hist_wanted() {
+  static const bool ok = !env_on("WSORT_NO_EARLY_HIST") && !env_on("WSORT_D2H_PER_CLASS") &&
+                         !env_on("WSORT_NO_FUSED_PAYLOAD") && !env_on("WSORT_NO_RADIX") &&
+                         !env_on("WSORT_RADIX_RTS");
+  return ok;
+}
+
+size_t radix_c0_zero_bytes() {  // totals + tickets + whole-key counters of class 0
+  return ((size_t)kRadixC0Segs * kRadixMaxPasses * 256 + kRadixMaxPasses + (2u << 6) + (2u << 12)) * 4;
+}
+
+int launch_early_hist(ws_handle* h, const uint64_t* region) {
+  cudaStream_t cst = h->serial ? h->st : h->cs[0];
+  DevBuf& tb = h->rtotals[0];
+  WS_CUDA(tb.ensure(radix_c0_zero_bytes() + 64));
+  if (cst != h->st) {
+    cudaEvent_t ev = sync_event(h);
+    WS_CUDA(cudaEventRecord(ev, h->st));
+    WS_CUDA(cudaStreamWaitEvent(cst, ev, 0));
+  }
+  WS_CUDA(cudaMemsetAsync(tb.p, 0, radix_c0_zero_bytes(), cst));
+  EarlyHist e;
+  memset(&e, 0, sizeof e);
+  e.fill = h->fill.as<uint32_t>();
+  e.keys_cap = h->keys_cap.as<uint8_t>();
+  for (int b = 0; b < 5; ++b) e.region[b] = region[b];
+  e.totals = tb.as<uint32_t>();
+  e.joint = e.totals + (size_t)kRadixC0Segs * kRadixMaxPasses * 256 + kRadixMaxPasses;
+  e.joint_ok = !env_on("WSORT_NO_JOINT");
+  launch_radix_hist_early(e, cst);
+  ++h->launches;
+  WS_TRY(check_launch("radix_hist_early"));
+  h->early_done = true;
+  h->early_joint = e.joint_ok != 0;
+  return WS_OK;
+}
+
 int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags,
                      std::mutex* gate = nullptr) {
   // batch mode: `gate` is held while this corpus crosses PCIe host->device
@@ -882,6 +940,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   h->ingested = h->sorted = h->have_stats = h->payload_only = false;
   h->have_tokens = false;
   h->unordered = false;
+  h->early_done = false;
   h->buckets.clear();
   h->n_text = n;
   h->text_valid = false;
@@ -1014,6 +1073,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           gate_lk.unlock();
           if (getenv("WSORT_TRACE")) fprintf(stderr, "wsort-trace handle=%p h2d_landed=%.3f\n", (void*)h, trace_ms());
         }
+        if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
         WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
                                 h->st));
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1021,6 +1081,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         redo = tot_host[kHistRows] != 0;  // a word spanned a whole piece: ingest again
         if (redo) {
           p.overflow = nullptr;
+          h->early_done = false;
           WS_TRY(reset_chain());
         }
       }
@@ -1036,6 +1097,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ++h->launches;
         }
         WS_TRY(check_launch("ingest_kernel"));
+        if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
       }
@@ -1189,7 +1251,17 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
   // class 0 (radix: a chain of small passes, the longest) is submitted first
   // on a high-priority stream; the multi-lane classes fill around it
-  static const int order[kClasses + 1] = {0, 1, 2, 3, 4};
+  static int order[kClasses + 1] = {0, 1, 2, 3, 4};
+  static const bool order_set = [] {  // experiment: WSORT_CLASS_ORDER=3,2,1,0,4
+    if (const char* o = getenv("WSORT_CLASS_ORDER")) {
+      for (int i = 0; i <= kClasses && *o; ++i) {
+        order[i] = *o - '0';
+        o += (o[1] == ',') ? 2 : 1;
+      }
+    }
+    return true;
+  }();
+  (void)order_set;
   for (int oi = 0; oi <= kClasses; ++oi) {
     const int c = order[oi];
     std::vector<SegIn> segs;
@@ -1914,7 +1986,10 @@ int sort_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, 
                    uint64_t* written, std::mutex* gate) {
   static const bool trace = getenv("WSORT_TRACE") && getenv("WSORT_TRACE")[0] == '1';
   const double t_begin = trace ? trace_ms() : 0;
-  WS_TRY(ingest_text_impl(h, text, n, WS_INGEST_UNORDERED, gate));  // ends with a sync
+  h->early_req = early_hist_wanted();
+  const int irc = ingest_text_impl(h, text, n, WS_INGEST_UNORDERED, gate);  // ends with a sync
+  h->early_req = false;
+  WS_TRY(irc);
   const double t_ingested = trace ? trace_ms() : 0;
   params_reset(h);  // the ingest synchronised: staging space is free again
   const uint64_t size = emit_size(h, true);
@@ -1982,7 +2057,13 @@ int ws_sort_texts(ws_handle* h, int32_t count, const uint8_t* const* texts, cons
 
 int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   WS_TRY(begin_call(h));
-  WS_TRY(ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT | WS_INGEST_UNORDERED));
+  static const bool trace = env_on("WSORT_TRACE");
+  const double t_begin = trace ? trace_ms() : 0;
+  h->early_req = early_hist_wanted();
+  const int irc = ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT | WS_INGEST_UNORDERED);
+  h->early_req = false;
+  WS_TRY(irc);
+  const double t_ingested = trace ? trace_ms() : 0;
   params_reset(h);
   const uint64_t size = emit_size(h, true);
   WS_CUDA(h->out.ensure(size + 64));
@@ -1991,9 +2072,13 @@ int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   fe.host = nullptr;
   fe.off = emit_offsets(h, true);
   WS_TRY(sort_impl(h, false, &fe));  // each class emits as soon as it is sorted
+  const double t_enqueued = trace ? trace_ms() : 0;
   h->out_size = size;
   if (written) *written = size;
   WS_CUDA(cudaStreamSynchronize(h->st));
+  if (trace)
+    fprintf(stderr, "wsort-trace resident ingest_host=%.3f enqueue_host=%.3f wait=%.3f ms\n",
+            t_ingested - t_begin, t_enqueued - t_ingested, trace_ms() - t_enqueued);
   return WS_OK;
 }
 

@@ -373,28 +373,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // each distinct word as often as it occurs, at its rank.
 constexpr int kJointMax = 1 << 12;
 
+// Histogram of one tile t of segment sg (all threads of the CTA): digit
+// counts of every pass into totals[sid][p][256], or whole-key counts into
+// joint[] for a jbits segment. sm: the CTA's shared counters (see kSm).
 template <class K>
-__global__ void __launch_bounds__(kRThreads)
-radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
+__device__ __forceinline__ void hist_tile(const RadixSeg& sg, uint32_t t, uint32_t* sm,
+                                          uint32_t* __restrict__ totals, uint32_t* __restrict__ joint) {
   using C = RadixCfg<K>;
   constexpr int kP = (int)sizeof(K);  // at most one pass per key byte
-  constexpr int kSm = kP * kDigits > kJointMax ? kP * kDigits : kJointMax;
-  __shared__ uint32_t sm[kSm];  // hist[kP][256], or the joint counts of a jbits segment
   uint32_t (*hist)[kDigits] = reinterpret_cast<uint32_t (*)[kDigits]>(sm);
-  __shared__ int s_seg;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t tile = blockIdx.x;
-  if (tid < 32) {
-    const int s = rsegment_of(a, tile);
-    if (tid == 0) s_seg = s;
-  }
-  __syncthreads();
-  const RadixSeg& sg = rseg_at(a, s_seg);
   const uint32_t jbits = sizeof(K) == 4 ? sg.jbits : 0u;
   const int nzero = jbits ? (1 << jbits) : kP * kDigits;
   for (int i = tid; i < nzero; i += kRThreads) sm[i] = 0;
   __syncthreads();
-  const uint32_t t = tile - sg.tile_begin;
   const uint64_t first = (uint64_t)t * C::T + (uint64_t)wid * 32 * C::E;
   const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
   const K* in = reinterpret_cast<const K*>(sg.in) + first;
@@ -410,22 +402,79 @@ radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
       if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&sm[(uint32_t)(key[r] >> (32 - jbits))], 1u);
     __syncthreads();
     for (int v = tid; v < (1 << jbits); v += kRThreads)
-      if (sm[v]) atomicAdd(a.joint + sg.joff + v, sm[v]);
-    return;
+      if (sm[v]) atomicAdd(joint + sg.joff + v, sm[v]);
+  } else {
+    const int passes = (int)sg.passes;
+#pragma unroll
+    for (int p = 0; p < kP; ++p) {
+      if (p >= passes) break;
+      const uint32_t sh = sg.shift + 8 * p;
+#pragma unroll
+      for (int r = 0; r < C::E; ++r)
+        if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&hist[p][digit_of<K>(key[r], sh)], 1u);
+    }
+    __syncthreads();
+    for (int p = 0; p < passes; ++p) {
+      const uint32_t c = hist[p][tid];
+      if (c) atomicAdd(totals + ((uint64_t)sg.sid * kRadixMaxPasses + p) * kDigits + tid, c);
+    }
   }
-  const int passes = (int)sg.passes;
-#pragma unroll
-  for (int p = 0; p < kP; ++p) {
-    if (p >= passes) break;
-    const uint32_t sh = sg.shift + 8 * p;
-#pragma unroll
-    for (int r = 0; r < C::E; ++r)
-      if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&hist[p][digit_of<K>(key[r], sh)], 1u);
+  __syncthreads();  // sm is reused by the CTA's next tile
+}
+
+template <class K>
+__global__ void __launch_bounds__(kRThreads)
+radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
+  constexpr int kP = (int)sizeof(K);
+  constexpr int kSm = kP * kDigits > kJointMax ? kP * kDigits : kJointMax;
+  __shared__ uint32_t sm[kSm];  // hist[kP][256], or the joint counts of a jbits segment
+  __shared__ int s_seg;
+  const uint32_t tile = blockIdx.x;
+  if (threadIdx.x < 32) {
+    const int s = rsegment_of(a, tile);
+    if (threadIdx.x == 0) s_seg = s;
   }
   __syncthreads();
-  for (int p = 0; p < passes; ++p) {
-    const uint32_t c = hist[p][tid];
-    if (c) atomicAdd(a.totals + ((uint64_t)sg.sid * kRadixMaxPasses + p) * kDigits + tid, c);
+  const RadixSeg& sg = rseg_at(a, s_seg);
+  hist_tile<K>(sg, tile - sg.tile_begin, sm, a.totals, a.joint);
+}
+
+// The histogram launch of the 6-bit class-0 buckets (L = 1..5) planned on the
+// device from the ingest's per-length counts, so it can run while the host
+// reads those counts and plans the passes. Tiles are visited grid-stride; the
+// segment table is the one radix_sort_segments builds (nonzero buckets in
+// ascending length; whole-key counts for <= 12-bit keys when allowed).
+__global__ void __launch_bounds__(kRThreads) radix_hist_early_kernel(const __grid_constant__ EarlyHist e) {
+  __shared__ uint32_t sm[kJointMax];
+  constexpr uint32_t T = RadixCfg<uint32_t>::T;
+  RadixSeg seg[5];
+  uint32_t nseg = 0, tiles = 0, joff = 0;
+  for (int b = 0; b < 5; ++b) {
+    const uint32_t n = e.fill[b];
+    if (!n) continue;
+    const uint32_t bits = 6u * (uint32_t)(b + 1);
+    RadixSeg r;
+    memset(&r, 0, sizeof r);
+    r.in = e.keys_cap + e.region[b];
+    r.n = n;
+    r.tile_begin = tiles;
+    r.ntiles = (n + T - 1) / T;
+    r.shift = 32u - bits;
+    r.sid = nseg;
+    r.passes = (bits + 7) / 8;
+    if (e.joint_ok && bits <= 12) {
+      r.jbits = bits;
+      r.joff = joff;
+      joff += 2u << bits;
+      r.passes = 0;
+    }
+    tiles += r.ntiles;
+    seg[nseg++] = r;
+  }
+  for (uint32_t g = blockIdx.x; g < tiles; g += gridDim.x) {
+    uint32_t s = 0;
+    while (s + 1 < nseg && seg[s + 1].tile_begin <= g) ++s;
+    hist_tile<uint32_t>(seg[s], g - seg[s].tile_begin, sm, e.totals, e.joint);
   }
 }
 
@@ -752,6 +801,13 @@ void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st) {
     radix_hist_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
   else
     radix_hist_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+}
+
+void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  radix_hist_early_kernel<<<4 * sms, kRThreads, 0, st>>>(e);
 }
 
 void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs, cudaStream_t st) {

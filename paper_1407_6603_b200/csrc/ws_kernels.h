@@ -158,6 +158,18 @@ struct RadixLaunch {
 int radix_tile_size(int lanes);
 void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st);
 void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st);
+// Class-0 histogram launch planned on the device (6-bit text keys, payload
+// mode): counts of lengths 1..5 from the ingest's fill counters.
+struct EarlyHist {
+  const uint32_t* fill;     // per-length word counts (bins 0..4 used)
+  const uint8_t* keys_cap;  // the ingest's per-length key regions
+  uint64_t region[5];       // byte offsets of lengths 1..5 in keys_cap
+  uint32_t* totals;         // [5][kRadixMaxPasses][256], zeroed
+  uint32_t* joint;          // whole-key counters, zeroed
+  int joint_ok;             // count (not sort) keys of <= 12 bits
+};
+constexpr int kRadixC0Segs = 5;  // class-0 buckets at most (the totals table is sized for them)
+void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st);
 // Payload of the jbits segments straight from their whole-key counts: value v
 // of segment i repeated joint[v] times at its rank (the exclusive prefix).
 // blocks = sum of 2^jbits over the launch's jbits segments (njsegs of them).
