@@ -834,7 +834,10 @@ __device__ __forceinline__ void sub_emit(const KW<LANES>* keys, uint32_t cnt, in
 }
 
 template <int LANES>
-__global__ void __launch_bounds__(kSubThreads) subsort_kernel(const __grid_constant__ SampleLaunch a) {
+#ifndef WS_SUB_MINB
+#define WS_SUB_MINB 6  // CTAs per SM the slot sort is compiled for (80 registers; 1: up to 128, 4 % slower)
+#endif
+__global__ void __launch_bounds__(kSubThreads, WS_SUB_MINB) subsort_kernel(const __grid_constant__ SampleLaunch a) {
   constexpr int E = TileCfg<LANES>::E, NT = kSubThreads, TS = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
