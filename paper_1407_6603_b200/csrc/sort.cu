@@ -716,7 +716,10 @@ __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t t
 // Partition passes over one tile of a bucket. COUNT: per-slot counts into
 // a.hist. !COUNT: each key goes to cursor[slot] reservation + local rank.
 template <int LANES, bool COUNT>
-__global__ void __launch_bounds__(kPartThreads) partition_kernel(const __grid_constant__ SampleLaunch a) {
+#ifndef WS_PART_MINB
+#define WS_PART_MINB 1
+#endif
+__global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(const __grid_constant__ SampleLaunch a) {
   using W = KW<LANES>;
   __shared__ uint64_t s_split[kMaxSplit];
   __shared__ uint32_t s_cnt[2 * kMaxSplit + 1];

@@ -332,12 +332,15 @@ def _short_word_text(rng, n, L=None, alphabet=synth.ALNUM):
 
 
 def test_radix_one_sweep_tiles_and_reuse():
-    # class-0 buckets (<= 5 characters) of 1 .. ~300 radix tiles (4096 keys),
+    # class-0 buckets (<= 5 characters) of 1 .. ~300 radix tiles (5120 keys),
     # exact tile multiples, heavy duplicates; one handle reused across growing
     # and shrinking corpora (look-back status buffer growth, per-launch epochs)
     rng = np.random.default_rng(77)
+    T = 5120  # radix.cu: 256 threads x WS_RADIX_E4 (20) keys per tile
     cases = [(1, 5, synth.ALNUM), (4095, 5, synth.ALNUM), (4096, 5, synth.ALNUM),
              (4097, 5, synth.ALNUM), (3 * 4096, 4, synth.ALNUM), (300_000, None, synth.ALNUM),
+             (T - 1, 5, synth.ALNUM), (T, 5, synth.ALNUM), (T + 1, 3, synth.ALNUM),
+             (5 * T, 4, synth.ALNUM), (5 * T + 1, 5, synth.ALNUM),
              (1_200_000, 5, b"ab"), (1_200_000, 5, synth.ALNUM), (5000, None, b"xyz"),
              (4096 * 7, 3, synth.ALNUM), (2, 5, synth.ALNUM)]
     for n, L, al in cases:
