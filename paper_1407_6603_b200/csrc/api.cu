@@ -755,7 +755,6 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   a.cursor = a.hist + slots;
   a.slot_off = a.cursor + slots;
   a.slot_ids = h->ss_ids[lanes].as<uint16_t>();
-  WS_CUDA(cudaMemsetAsync(a.hist, 0, (size_t)slots * 4, st));
   double bytes = 0;
   for (const auto& s : segs) bytes += 5.0 * s.n * key_bytes(lanes);
   char name[32];
@@ -1262,8 +1261,14 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     return true;
   }();
   (void)order_set;
+  static const bool trace_cls = env_on("WSORT_TRACE");
+  double t_cls = trace_cls ? trace_ms() : 0;
   for (int oi = 0; oi <= kClasses; ++oi) {
     const int c = order[oi];
+    if (trace_cls && oi) {
+      fprintf(stderr, "wsort-trace enqueue class %d: %.3f ms\n", order[oi - 1], trace_ms() - t_cls);
+      t_cls = trace_ms();
+    }
     std::vector<SegIn> segs;
     std::vector<int> which;
     for (int i = 0; i < nb; ++i) {
@@ -1282,6 +1287,9 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     uint64_t* k1 = class_keys(h, 1, c, 0);
     // Fused emission: a bucket is emitted (and copied to the host) right after
     // the pass that completes it, on side streams, while later passes run.
+    // side streams used by this class (only those are joined back; a fused
+    // bucket needs no emit, and device-resident output needs no copy)
+    bool used_est = fe && fe->per_class, used_dst = fe && fe->per_class;
     PassDoneHook hook = [&, est, dst](const std::vector<const SegIn*>& done,
                                       cudaStream_t st) -> int {
       std::vector<int> bids, to_emit;
@@ -1290,18 +1298,24 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
         bids.push_back((int)sg->stat_slot);
         if (!sg->emitted) to_emit.push_back((int)sg->stat_slot);
       }
-      if (est != st) {
-        cudaEvent_t ev = sync_event(h);
-        WS_CUDA(cudaEventRecord(ev, st));
-        WS_CUDA(cudaStreamWaitEvent(est, ev, 0));
+      cudaStream_t ready = st;  // the stream after which the buckets' records are complete
+      if (!to_emit.empty()) {
+        if (est != st) {
+          cudaEvent_t ev = sync_event(h);
+          WS_CUDA(cudaEventRecord(ev, st));
+          WS_CUDA(cudaStreamWaitEvent(est, ev, 0));
+        }
+        WS_TRY(emit_device(h, fe->dout, true, nullptr, -1, est, &to_emit));
+        ready = est;
+        used_est = true;
       }
-      if (!to_emit.empty()) WS_TRY(emit_device(h, fe->dout, true, nullptr, -1, est, &to_emit));
       if (!fe->host) return WS_OK;
-      if (dst != est) {
+      if (dst != ready) {
         cudaEvent_t ev2 = sync_event(h);
-        WS_CUDA(cudaEventRecord(ev2, est));
+        WS_CUDA(cudaEventRecord(ev2, ready));
         WS_CUDA(cudaStreamWaitEvent(dst, ev2, 0));
       }
+      used_dst = true;
       std::sort(bids.begin(), bids.end());
       size_t k = 0;
       while (k < bids.size()) {  // coalesce adjacent output ranges
@@ -1365,10 +1379,13 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     for (size_t j = 0; j < segs.size(); ++j) h->buckets[which[j]].final_buf = segs[j].final_buf;
     WS_CUDA(cudaEventRecord(h->ev_join[c], cst));
     WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_join[c], 0));
-    if (fe && est != h->st) {
-      cudaEvent_t e1 = sync_event(h), e2 = sync_event(h);
+    if (fe && used_est && est != h->st) {
+      cudaEvent_t e1 = sync_event(h);
       WS_CUDA(cudaEventRecord(e1, est));
       WS_CUDA(cudaStreamWaitEvent(h->st, e1, 0));
+    }
+    if (fe && used_dst && dst != h->st) {
+      cudaEvent_t e2 = sync_event(h);
       WS_CUDA(cudaEventRecord(e2, dst));
       WS_CUDA(cudaStreamWaitEvent(h->st, e2, 0));
     }

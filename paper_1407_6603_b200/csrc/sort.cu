@@ -639,6 +639,8 @@ template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
   __shared__ uint64_t sm[kBitonicN];
   const SampleSeg& sg = sseg_at(a, blockIdx.x);
+  for (uint32_t i = threadIdx.x; i < 2 * sg.nsplit + 1; i += kSampleThreads)
+    a.hist[sg.slot_base + i] = 0;  // the bucket's slot counters (the count pass follows)
   if (!sg.nsplit) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const KW<LANES>* in = kv<LANES>(sg.in);
@@ -999,7 +1001,8 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   for (int i = 0; i < a.nsegs; ++i) mmax = std::max(mmax, a.inl[i].m);
   while (P < mmax) P <<= 1;
   (void)P;
-  if (mmax) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
+  (void)mmax;  // every bucket's CTA zeroes its slot counters, sampled or not
+  sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
   slot_scan_kernel<<<a.nsegs, 1024, 0, st>>>(a);
   partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);

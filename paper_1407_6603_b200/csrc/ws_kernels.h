@@ -68,7 +68,7 @@ void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t*
 // sort.cu
 // Segment tables of up to kInlineSegs entries travel in the kernel
 // parameters (constant bank): no host->device copy sits between passes.
-constexpr int kInlineSegs = 40;
+constexpr int kInlineSegs = 12;  // >= the buckets of any lane class (11); kernel parameters stay small (launch cost)
 
 struct SortLaunch {
   const uint64_t* keys_in;
