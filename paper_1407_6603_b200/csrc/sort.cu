@@ -840,9 +840,13 @@ __device__ __forceinline__ void sub_emit(const KW<LANES>* keys, uint32_t cnt, in
 
 template <int LANES>
 #ifndef WS_SUB_MINB
-#define WS_SUB_MINB 6  // CTAs per SM the slot sort is compiled for (80 registers; 1: up to 128, 4 % slower)
+#define WS_SUB_MINB 6  // CTAs per SM the multi-word slot sorts are compiled for (80 registers;
+                       // 1: up to 128, 4 % slower)
 #endif
-__global__ void __launch_bounds__(kSubThreads, WS_SUB_MINB) subsort_kernel(const __grid_constant__ SampleLaunch a) {
+#ifndef WS_SUB1_MINB
+#define WS_SUB1_MINB 7  // one-word keys: 72 registers (1: 109, slot sort 63 -> 43 us at 7)
+#endif
+__global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SUB_MINB) subsort_kernel(const __grid_constant__ SampleLaunch a) {
   constexpr int E = TileCfg<LANES>::E, NT = kSubThreads, TS = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
