@@ -183,6 +183,7 @@ struct ws_handle {
   bool early_req = false;         // the next ingest launches the class-0 histogram itself
   bool early_done = false;        // ... and did (valid for the sort that follows)
   bool early_joint = false;       //     with whole-key counts for <= 12-bit keys
+  bool split_early[kClasses + 1] = {false};  // ... and each multi-lane class's split launch
   uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   DevBuf ss_ids[kClasses + 1];                            // per-key slot ids
@@ -755,6 +756,9 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   a.cursor = a.hist + slots;
   a.slot_off = a.cursor + slots;
   a.slot_ids = h->ss_ids[lanes].as<uint16_t>();
+  // the ingest ran this class's split launch (same rules, same stream)
+  a.split_done = h->split_early[lanes] ? 1 : 0;
+  h->split_early[lanes] = false;
   double bytes = 0;
   for (const auto& s : segs) bytes += 5.0 * s.n * key_bytes(lanes);
   char name[32];
@@ -920,6 +924,42 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   WS_TRY(check_launch("radix_hist_early"));
   h->early_done = true;
   h->early_joint = e.joint_ok != 0;
+  // the multi-lane classes' split launches (payload-mode sample sort), each on
+  // its class stream, buffers at their maximum size (no regrowth later)
+  static const bool split_ok = !env_on("WSORT_NO_SAMPLE") && !env_on("WSORT_NO_EARLY_SPLIT");
+  if (!split_ok) return WS_OK;
+  uint32_t pmax = 1;
+  while (pmax * 2 <= (uint32_t)std::min(sample_max_keys(1), 4096)) pmax *= 2;
+  for (int c = 1; c <= 3; ++c) {  // 6-bit text keys: lengths 6-10, 11-21, 22-32
+    const int lmin = c == 1 ? 6 : (c == 2 ? 11 : 22), lmax = c == 1 ? 10 : (c == 2 ? 21 : 32);
+    const int nb = lmax - lmin + 1;
+    WS_CUDA(h->ss_split[c].ensure((size_t)nb * kMaxSplit * 8 + 64));
+    WS_CUDA(h->ss_slots[c].ensure((size_t)nb * (2 * kMaxSplit + 1) * 12 + 64));
+    cudaStream_t sst = h->serial ? h->st : h->cs[c];
+    if (sst != h->st) {
+      cudaEvent_t ev = sync_event(h);
+      WS_CUDA(cudaEventRecord(ev, h->st));
+      WS_CUDA(cudaStreamWaitEvent(sst, ev, 0));
+    }
+    SplitEarly se;
+    memset(&se, 0, sizeof se);
+    se.fill = h->fill.as<uint32_t>();
+    se.keys_cap = h->keys_cap.as<uint8_t>();
+    for (int b = 0; b < 32; ++b) se.region[b] = region[b];
+    se.lmin = lmin;
+    se.lmax = lmax;
+    se.T = (uint32_t)tile_size(c);
+    se.target = (uint32_t)subsort_tile_size(c) / 2;
+    se.pmax = pmax;
+    se.smax = std::min<uint32_t>(kMaxSplit + 1, pmax / 8);
+    se.cap = sample_bucket_limit(c);
+    se.splitters = h->ss_split[c].as<uint64_t>();
+    se.hist = h->ss_slots[c].as<uint32_t>();
+    launch_sample_split_early(c, se, sst);
+    ++h->launches;
+    h->split_early[c] = true;
+  }
+  WS_TRY(check_launch("sample_split_early"));
   return WS_OK;
 }
 
@@ -940,6 +980,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   h->have_tokens = false;
   h->unordered = false;
   h->early_done = false;
+  for (bool& f : h->split_early) f = false;
   h->buckets.clear();
   h->n_text = n;
   h->text_valid = false;
@@ -1081,6 +1122,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         if (redo) {
           p.overflow = nullptr;
           h->early_done = false;
+          for (bool& f : h->split_early) f = false;
           WS_TRY(reset_chain());
         }
       }
@@ -1459,6 +1501,8 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     }
   }
   WS_TRY(check_launch("sort"));
+  h->early_done = false;  // early launches serve only the sort right after their ingest
+  for (bool& f : h->split_early) f = false;
   h->sorted = true;
   h->have_stats = stats;
   return WS_OK;

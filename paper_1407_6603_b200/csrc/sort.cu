@@ -635,12 +635,13 @@ __device__ __forceinline__ uint32_t slot_of(const uint64_t* sp, uint32_t nsplit,
 constexpr int kBitonicN = 4096;
 static_assert(kBitonicN == kSampleThreads * 4, "4 prefixes per thread");
 
+// The splitters of one bucket (all threads of a 1024-thread CTA); also zeroes
+// the bucket's slot counters for the count pass.
 template <int LANES>
-__global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
-  __shared__ uint64_t sm[kBitonicN];
-  const SampleSeg& sg = sseg_at(a, blockIdx.x);
+__device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __restrict__ splitters,
+                                             uint32_t* __restrict__ hist, uint64_t* sm) {
   for (uint32_t i = threadIdx.x; i < 2 * sg.nsplit + 1; i += kSampleThreads)
-    a.hist[sg.slot_base + i] = 0;  // the bucket's slot counters (the count pass follows)
+    hist[sg.slot_base + i] = 0;  // the bucket's slot counters (the count pass follows)
   if (!sg.nsplit) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const KW<LANES>* in = kv<LANES>(sg.in);
@@ -698,9 +699,55 @@ __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __gr
 #pragma unroll
   for (int q = 0; q < 4; ++q) sm[w * 128 + q * 32 + lane] = x[q];
   __syncthreads();
-  uint64_t* sp = a.splitters + sg.split_off;
+  uint64_t* sp = splitters + sg.split_off;
   for (uint32_t k = threadIdx.x; k < sg.nsplit; k += kSampleThreads)
     sp[k] = sm[(uint64_t)(k + 1) * sg.m / (sg.nsplit + 1)];
+}
+
+
+template <int LANES>
+__global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
+  __shared__ uint64_t sm[kBitonicN];
+  split_bucket<LANES>(sseg_at(a, blockIdx.x), a.splitters, a.hist, sm);
+}
+
+// The split launch planned on the device from the ingest's per-length counts
+// (same rules as sample_sort_segments: slots of half a slot-sort tile, >= 8
+// samples per splitter, buckets beyond the splitter budget left to the merge
+// path), so it runs while the host reads the counts back. CTA b: length
+// lmin + b.
+template <int LANES>
+__global__ void __launch_bounds__(kSampleThreads) sample_split_early_kernel(const __grid_constant__ SplitEarly e) {
+  __shared__ uint64_t sm[kBitonicN];
+  SampleSeg sg;
+  memset(&sg, 0, sizeof sg);
+  uint32_t slots = 0, splits = 0;
+  bool mine = false;
+  for (int L = e.lmin; L <= e.lmax; ++L) {
+    const uint32_t n = e.fill[L - 1];
+    if (!n || n > e.cap) continue;
+    uint64_t S = n <= e.T ? 1 : (n + e.target - 1) / e.target;
+    S = S < e.smax ? S : e.smax;
+    const uint32_t nsplit = (uint32_t)S - 1;
+    uint32_t m = 0;
+    if (nsplit) {
+      m = 1;
+      const uint32_t lim = e.pmax < n ? e.pmax : n;
+      while (m < 8 * S && 2ull * m <= lim) m *= 2;
+    }
+    if (L == e.lmin + (int)blockIdx.x) {
+      sg.in = reinterpret_cast<const uint64_t*>(e.keys_cap + e.region[L - 1]);
+      sg.n = n;
+      sg.nsplit = nsplit;
+      sg.m = m;
+      sg.split_off = splits;
+      sg.slot_base = slots;
+      mine = true;
+    }
+    slots += 2 * nsplit + 1;
+    splits += nsplit;
+  }
+  if (mine) split_bucket<LANES>(sg, e.splitters, e.hist, sm);
 }
 
 __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t tile) {
@@ -1006,7 +1053,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   while (P < mmax) P <<= 1;
   (void)P;
   (void)mmax;  // every bucket's CTA zeroes its slot counters, sampled or not
-  sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
+  if (!a.split_done) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
   partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
   slot_scan_kernel<<<a.nsegs, 1024, 0, st>>>(a);
   partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
@@ -1016,6 +1063,16 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
 int sample_max_keys(int) { return kSampleSmem / 8; }
 int part_tile_size() { return kPartTile; }
 int subsort_tile_size(int lanes) { return kSubThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E); }
+
+void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st) {
+  const unsigned nb = (unsigned)(e.lmax - e.lmin + 1);
+  switch (lanes) {
+    case 1: sample_split_early_kernel<1><<<nb, kSampleThreads, 0, st>>>(e); break;
+    case 2: sample_split_early_kernel<2><<<nb, kSampleThreads, 0, st>>>(e); break;
+    case 3: sample_split_early_kernel<3><<<nb, kSampleThreads, 0, st>>>(e); break;
+    default: sample_split_early_kernel<4><<<nb, kSampleThreads, 0, st>>>(e); break;
+  }
+}
 
 void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st) {
   switch (lanes) {

@@ -112,8 +112,22 @@ struct SampleLaunch {
   uint32_t* cursor;       // per slot: reservation cursor
   uint32_t* slot_off;     // per slot: class-relative element offset
   uint16_t* slot_ids;     // per key, in partition-tile order: its slot (count pass -> scatter pass)
+  int split_done;         // the ingest already ran the split launch (sample_split_early_kernel)
   SampleSeg inl[kInlineSegs];
 };
+// Split launch of one lane class planned on the device (6-bit text keys,
+// payload mode): lengths lmin..lmax, counts from the ingest's fill counters.
+struct SplitEarly {
+  const uint32_t* fill;
+  const uint8_t* keys_cap;
+  uint64_t region[32];     // byte offsets of lengths 1..32 in keys_cap
+  int lmin, lmax;
+  uint32_t T, target, pmax, smax;  // sample_sort_segments' rules
+  uint64_t cap;            // larger buckets take the merge path
+  uint64_t* splitters;     // the class's splitter and slot-counter buffers (max size)
+  uint32_t* hist;
+};
+void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st);
 int sample_max_keys(int lanes);
 int part_tile_size();
 int subsort_tile_size(int lanes);  // keys one slot-sort CTA sorts in one network
