@@ -80,7 +80,7 @@ emit_kernel(const __grid_constant__ EmitTable t, uint8_t* __restrict__ out, int 
     const uint64_t (&k)[NL] = kk[q];
     uint8_t* dst = buf + mis + j * stride;
     if constexpr (ENC == kEncAlnum6) {
-      unpack6<NL>(k, L, dst);
+      unpack6_swar<NL>(k, L, dst);
     } else {
 #pragma unroll
       for (int l = 0; l < NL; ++l) {

@@ -26,6 +26,51 @@ __device__ __forceinline__ void unpack6(const uint64_t (&k)[LANES], int L, uint8
 #undef WS_UNPACK6_CHAR
 }
 
+// 24 bits of a 6-bit code string at bit offset O from its top (4 characters;
+// bits past the last lane read as zero).
+template <int NL, int O>
+__device__ __forceinline__ uint32_t code_bits24(const uint64_t (&k)[NL]) {
+  constexpr int w = O / 64, off = O % 64;
+  if constexpr (w >= NL) {
+    return 0u;
+  } else if constexpr (off <= 40) {
+    return (uint32_t)(k[w] >> (40 - off)) & 0xFFFFFFu;
+  } else if constexpr (w + 1 < NL) {
+    return (uint32_t)((k[w] << (off - 40)) | (k[w + 1] >> (104 - off))) & 0xFFFFFFu;
+  } else {
+    return (uint32_t)(k[w] << (off - 40)) & 0xFFFFFFu;
+  }
+}
+
+// Characters of 4 codes at once: the codes spread to bytes (first character
+// lowest) and mapped to ASCII with two SWAR range tests (codes are 1..62, so
+// no byte carries): 1..10 -> '0'..'9', 11..36 -> 'A'..'Z', 37..62 -> 'a'..'z'.
+__device__ __forceinline__ uint32_t ascii4_of_codes(uint32_t x) {
+  uint32_t u = ((x >> 18) & 0x3Fu) | ((x >> 4) & 0x3F00u) | ((x << 10) & 0x3F0000u) | ((x << 24) & 0x3F000000u);
+  const uint32_t ge11 = ((u + 0x75757575u) & 0x80808080u) >> 7;
+  const uint32_t ge37 = ((u + 0x5B5B5B5Bu) & 0x80808080u) >> 7;
+  return u + 0x2F2F2F2Fu + ge11 * 7u + ge37 * 6u;
+}
+
+template <int NL, int G>
+__device__ __forceinline__ void unpack6_group(const uint64_t (&k)[NL], int L, uint8_t* dst) {
+  if constexpr (4 * G < (NL * 64) / 6) {
+    if (4 * G >= L) return;
+    const uint32_t a = ascii4_of_codes(code_bits24<NL, 24 * G>(k));
+    dst[4 * G] = (uint8_t)a;
+    if (4 * G + 1 < L) dst[4 * G + 1] = (uint8_t)(a >> 8);
+    if (4 * G + 2 < L) dst[4 * G + 2] = (uint8_t)(a >> 16);
+    if (4 * G + 3 < L) dst[4 * G + 3] = (uint8_t)(a >> 24);
+    unpack6_group<NL, G + 1>(k, L, dst);
+  }
+}
+
+// unpack6 four characters at a time.
+template <int NL>
+__device__ __forceinline__ void unpack6_swar(const uint64_t (&k)[NL], int L, uint8_t* dst) {
+  unpack6_group<NL, 0>(k, L, dst);
+}
+
 // buf[mis, mis + total) -> out[0, total), where mis = out & 15: aligned
 // 16-byte stores for the body, byte stores for the ragged head and tail.
 template <int NT>
@@ -68,7 +113,7 @@ __device__ void emit_records_cta(const typename KeyTraits<LANES>::W* keys, uint3
         for (int l = 0; l < NL; ++l) k[l] = kp[l];
       }
       uint8_t* dst = pbuf + mis + threadIdx.x * R;
-      unpack6<NL>(k, L, dst);
+      unpack6_swar<NL>(k, L, dst);
       dst[L] = '\n';
     }
     __syncthreads();
