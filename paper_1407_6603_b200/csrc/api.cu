@@ -56,6 +56,13 @@ double trace_ms() {
   return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
+// WSORT_TRACE=2: host timestamps of the resident step's milestones (stderr).
+thread_local std::vector<std::pair<const char*, double>> g_marks;
+inline void tmark(const char* what) {
+  static const bool on = getenv("WSORT_TRACE") && getenv("WSORT_TRACE")[0] == '2';
+  if (on) g_marks.emplace_back(what, trace_ms());
+}
+
 #define WS_CUDA(x)                                             \
   do {                                                         \
     cudaError_t e_ = (x);                                      \
@@ -604,7 +611,9 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         a.prof = prof.as<unsigned long long>();
       }
       Phase ph(h, name, bytes, 0, st);
+      if (p == 0) tmark("pass0_launch");
       if (p >= 0) launch_radix_onesweep(lanes, a, st);
+      if (p == 0) tmark("pass0_launched");
       else if (!early) launch_radix_hist(lanes, a, st);
       if (p >= 0 || !early) ++h->launches;
       ph.end();
@@ -1139,8 +1148,10 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         }
         WS_TRY(check_launch("ingest_kernel"));
         if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        tmark("early_enq");
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
+        tmark("sync_ret");
       }
     } else {
       memset(tot_host, 0, kHistRows * 4);
@@ -1148,7 +1159,9 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     for (int b = 0; b < kNumBins; ++b) counts[b] = tot_host[b];
     total_words = tot_host[kNumBins];
     m = counts[kLongBin];
+    tmark("synced");
     WS_TRY(plan_packed(h, counts));  // compact layout of the sort buffers
+    tmark("planned");
     if (ordered_reserve && nchunks) {
       // corpus order: runs of every (bin, chunk) move from their reserved place
       // to the exclusive prefix of their bin over chunks, in the compact layout
@@ -1228,6 +1241,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     WS_TRY(check_launch("scatter_kernel"));
   }
   WS_TRY(group_long_words(h, m));
+  tmark("grouped");
   h->words = total_words;
   h->text_valid = true;
   return finish_ingest(h);
@@ -1270,6 +1284,7 @@ int fused_class_copy(ws_handle* h, FusedEmit* fe, int cls, cudaStream_t st) {
 }
 
 int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
+  tmark("sort_impl");
   if (!h->ingested) return fail(WS_ERR_STATE, "ws_sort before ingest");
   if (stats && h->unordered)
     return fail(WS_ERR_STATE, "stats need corpus order: ingest without WS_INGEST_UNORDERED");
@@ -2118,13 +2133,15 @@ int ws_sort_texts(ws_handle* h, int32_t count, const uint8_t* const* texts, cons
 
 int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   WS_TRY(begin_call(h));
-  static const bool trace = env_on("WSORT_TRACE");
+  static const bool trace = env_on("WSORT_TRACE") || (getenv("WSORT_TRACE") && getenv("WSORT_TRACE")[0] == '2');
   const double t_begin = trace ? trace_ms() : 0;
+  tmark("begin");
   h->early_req = early_hist_wanted();
   const int irc = ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT | WS_INGEST_UNORDERED);
   h->early_req = false;
   WS_TRY(irc);
   const double t_ingested = trace ? trace_ms() : 0;
+  tmark("ingest_ret");
   params_reset(h);
   const uint64_t size = emit_size(h, true);
   WS_CUDA(h->out.ensure(size + 64));
@@ -2132,6 +2149,7 @@ int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   fe.dout = h->out.as<uint8_t>();
   fe.host = nullptr;
   fe.off = emit_offsets(h, true);
+  tmark("offsets");
   WS_TRY(sort_impl(h, false, &fe));  // each class emits as soon as it is sorted
   const double t_enqueued = trace ? trace_ms() : 0;
   h->out_size = size;
@@ -2140,6 +2158,12 @@ int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   if (trace)
     fprintf(stderr, "wsort-trace resident ingest_host=%.3f enqueue_host=%.3f wait=%.3f ms\n",
             t_ingested - t_begin, t_enqueued - t_ingested, trace_ms() - t_enqueued);
+  if (!g_marks.empty()) {
+    fprintf(stderr, "wsort-marks");
+    for (auto& m : g_marks) fprintf(stderr, " %s=%.1f", m.first, (m.second - t_begin) * 1e3);
+    fprintf(stderr, " (us from call start)\n");
+    g_marks.clear();
+  }
   return WS_OK;
 }
 

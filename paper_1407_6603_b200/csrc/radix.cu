@@ -803,11 +803,14 @@ void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st) {
     radix_hist_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
 }
 
+#ifndef WS_HIST_EARLY_CTAS
+#define WS_HIST_EARLY_CTAS 8  // per SM (grid-stride over the tiles)
+#endif
 void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  radix_hist_early_kernel<<<4 * sms, kRThreads, 0, st>>>(e);
+  radix_hist_early_kernel<<<WS_HIST_EARLY_CTAS * sms, kRThreads, 0, st>>>(e);
 }
 
 void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs, cudaStream_t st) {
