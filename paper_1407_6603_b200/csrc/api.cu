@@ -612,9 +612,12 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       }
       Phase ph(h, name, bytes, 0, st);
       if (p == 0) tmark("pass0_launch");
-      if (p >= 0) launch_radix_onesweep(lanes, a, st);
-      if (p == 0) tmark("pass0_launched");
-      else if (!early) launch_radix_hist(lanes, a, st);
+      if (p >= 0) {
+        launch_radix_onesweep(lanes, a, st);
+        if (p == 0) tmark("pass0_launched");
+      } else if (!early) {
+        launch_radix_hist(lanes, a, st);
+      }
       if (p >= 0 || !early) ++h->launches;
       ph.end();
       if (a.prof) {

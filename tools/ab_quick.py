@@ -1,6 +1,7 @@
 """Quick A/B of library variants on the device-resident step (config 4).
 
 usage: python tools/ab_quick.py VARIANT... (default | env:NAME=VALUE | a build/variants/ name)
+AB_STATS=1 times the stats-mode step (ordered ingest + merge sort + SortStats) instead.
 Each variant runs in its own process (WSORT_LIB); prints the median step time
 (CUDA events on the library stream, 256 MiB L2 flush between steps) and the
 per-phase times of one profiled step. Two rounds, interleaved.
@@ -21,19 +22,28 @@ h = Handle(0)
 h.ingest_text(text)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device='cuda')
 st = torch.cuda.ExternalStream(h.stream_ptr()) if hasattr(h, 'stream_ptr') else torch.cuda.current_stream()
+import os
+stats = os.environ.get("AB_STATS") == "1"
+if stats:
+    d = torch.frombuffer(bytearray(text), dtype=torch.uint8).cuda()
+def step():
+    if stats:  # ordered ingest + merge sort with SortStats
+        h.ingest_text(None, device_ptr=d.data_ptr(), n=len(text)); h.sort(True); h.bucket_stats(True)
+    else:
+        h.sort_resident(len(text))
 ts = []
 for i in range(25):
     flush.zero_()
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record()
-    h.sort_resident(len(text))
+    step()
     torch.cuda.synchronize()
     b.record(); torch.cuda.synchronize()
     if i >= 5: ts.append(a.elapsed_time(b))
 h.profile(reset=True)
 h.set_profiling(True)
-h.sort_resident(len(text))
+step()
 h.set_profiling(False)
 ph = h.profile(reset=True)
 agg = {}
