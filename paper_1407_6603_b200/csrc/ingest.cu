@@ -27,6 +27,14 @@
 namespace ws {
 
 constexpr int kChunk = 4096;
+#ifndef WS_TEXT_STREAM
+#define WS_TEXT_STREAM 1
+#endif
+#if WS_TEXT_STREAM
+#define WS_TEXT_LD(p) __ldcs(p)
+#else
+#define WS_TEXT_LD(p) (*(p))
+#endif
 #ifndef WS_RESERVE_SB
 #define WS_RESERVE_SB 32  // bytes per thread of the payload-mode ingest (32 or 64; 64 measured slower)
 #endif
@@ -177,7 +185,8 @@ __device__ __forceinline__ SegW<SB> classify_wide(const uint8_t* __restrict__ te
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     v[k] = make_uint4(0, 0, 0, 0);
-    if (base < n) v[k] = reinterpret_cast<const uint4*>(text + base)[k];  // padded text
+    // padded text; streamed once (evict-first), so the keys written behind it stay in L2
+    if (base < n) v[k] = WS_TEXT_LD(reinterpret_cast<const uint4*>(text + base) + k);
     m |= (M)alnum_mask16(v[k]) << (16 * k);
   }
   const M up = __shfl_up_sync(0xffffffffu, m, 1);
