@@ -66,7 +66,13 @@ __device__ __forceinline__ uint32_t digit_of(K key, uint32_t shift) {
 
 // Lanes of the warp holding the same 8-bit digit (8 ballots; invalid lanes,
 // ok == false, match nobody valid). Measured no slower than match.any.
+#ifndef WS_MATCH_ANY
+#define WS_MATCH_ANY 1  // 0: 8 ballots (the one-sweep passes 3 % slower alone, same step)
+#endif
 __device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool ok) {
+#if WS_MATCH_ANY  // one MATCH.ANY (off the ALU pipe); invalid lanes get unique values > 255
+  return __match_any_sync(0xffffffffu, ok ? d : 0x100u + (threadIdx.x & 31));
+#endif
   uint32_t peers = __ballot_sync(0xffffffffu, ok);
   if (!ok) peers = ~peers;
 #pragma unroll
