@@ -714,7 +714,6 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
                          cudaStream_t st, const PassDoneHook* on_done, uint8_t* pay = nullptr,
                          const std::vector<uint64_t>* pay_off = nullptr) {
   if (h->enc != kEncAlnum6) pay = nullptr;  // fused records decode 6-bit text keys only
-  const uint32_t T = (uint32_t)tile_size(lanes);
   uint32_t pmax = 1;  // sample prefixes sorted in shared memory (power of two, <= 4096)
   while (pmax * 2 <= (uint32_t)std::min(sample_max_keys(lanes), 4096)) pmax *= 2;
   const uint32_t ptile = (uint32_t)part_tile_size();
@@ -725,7 +724,9 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
     // slots of half a slot-sort tile on average; a sample of >= 8 keys per
     // slot keeps slots beyond the tile (the slower fallback) rare
     const uint64_t target = (uint64_t)subsort_tile_size(lanes) / 2;  // (measured: T/1.4..T/3 within noise)
-    uint64_t S = s.n <= T ? 1 : (s.n + target - 1) / target;
+    // one slot only when it fits one slot sort's tile (larger single slots
+    // take the slow block-transposition fallback)
+    uint64_t S = s.n <= 2 * target ? 1 : (s.n + target - 1) / target;
     S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 8));
     SampleSeg g;
     g.in = s.in_ptr;
@@ -960,7 +961,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     for (int b = 0; b < 32; ++b) se.region[b] = region[b];
     se.lmin = lmin;
     se.lmax = lmax;
-    se.T = (uint32_t)tile_size(c);
+    se.T = (uint32_t)subsort_tile_size(c);  // one slot up to a slot-sort tile (= 2 * target)
     se.target = (uint32_t)subsort_tile_size(c) / 2;
     se.pmax = pmax;
     se.smax = std::min<uint32_t>(kMaxSplit + 1, pmax / 8);
