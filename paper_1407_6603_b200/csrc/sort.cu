@@ -615,7 +615,10 @@ __device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __re
     const uint32_t i = w * 128 + q * 32 + lane;
     x[q] = i < sg.m ? (uint64_t)__ldg(in + ((uint64_t)i * sg.n / sg.m) * NW) : ~0ull;
   }
-  for (uint32_t size = 2; size <= kBitonicN; size <<= 1) {
+  // only the first m (a power of two) prefixes are samples: the network's
+  // stages up to size m sort them (the padding blocks are already sorted)
+  const uint32_t P = sg.m < 2 ? 2u : (sg.m > kBitonicN ? (uint32_t)kBitonicN : sg.m);
+  for (uint32_t size = 2; size <= P; size <<= 1) {
     for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
       if (stride >= 128) {
 #pragma unroll
