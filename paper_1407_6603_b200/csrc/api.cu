@@ -713,6 +713,7 @@ uint64_t sample_bucket_limit(int lanes) {
 int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* out_class,
                          cudaStream_t st, const PassDoneHook* on_done, uint8_t* pay = nullptr,
                          const std::vector<uint64_t>* pay_off = nullptr) {
+  tmark("ss_begin");
   if (h->enc != kEncAlnum6) pay = nullptr;  // fused records decode 6-bit text keys only
   uint32_t pmax = 1;  // sample prefixes sorted in shared memory (power of two, <= 4096)
   while (pmax * 2 <= (uint32_t)std::min(sample_max_keys(lanes), 4096)) pmax *= 2;
@@ -778,15 +779,19 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   snprintf(name, sizeof name, "sample_l%d", lanes);
   {
     Phase ph(h, name, bytes, 0, st);
+    tmark("ss_launch");
     launch_sample_sort(lanes, a, st);
+    tmark("ss_launched");
     h->launches += 5;
   }
   WS_TRY(check_launch(name));
+  tmark("ss_checked");
   if (on_done) {
     std::vector<const SegIn*> done;
     for (auto& s : segs) done.push_back(&s);
     WS_TRY((*on_done)(done, st));
   }
+  tmark("ss_hooked");
   return WS_OK;
 }
 
