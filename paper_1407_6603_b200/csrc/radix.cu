@@ -86,12 +86,6 @@ __device__ __forceinline__ uint32_t match_digit8(uint32_t d, bool ok) {
 
 // Per-warp stable digit ranks of the warp's keys (round r, lane l <-> key
 // r * 32 + l of the warp's slice): rank = earlier keys of the same digit.
-// Peers of a digit are found either by 8 ballots (WS_RANK_OR=0) or by one
-// shared-memory atomic OR per key into a per-warp digit mask array that the
-// digit's last lane clears again (WS_RANK_OR=1, ~half the instructions).
-#ifndef WS_RANK_OR
-#define WS_RANK_OR 0  // 1 measured ~2 % slower on the step (fewer instructions, latency-bound)
-#endif
 // Ranks of a thread's keys: two 16-bit ranks per register (a tile holds <
 // 2^16 keys), which keeps the one-sweep kernel within 64 registers.
 #ifndef WS_PACK_RK
@@ -127,30 +121,13 @@ struct RankSetter<E, E> {
 
 template <class K, int E>
 __device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, uint32_t shift,
-                                          uint32_t* wcnt, uint32_t* wmask, Ranks<E>& rk) {
+                                          uint32_t* wcnt, Ranks<E>& rk) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const bool ok = (uint32_t)(r * 32 + lane) < nvalid;
     const uint32_t d = digit_of<K>(key[r], shift);
-#if WS_RANK_OR
-    if (ok) atomicOr(wmask + d, 1u << lane);
-    __syncwarp();
-    uint32_t peers = 0, base = 0;
-    if (ok) {
-      peers = wmask[d];
-      base = wcnt[d];
-    }
-    RankSetter<0, E>::set(rk, r, base + __popc(peers & lt));
-    __syncwarp();
-    if (ok && lane == 31 - __clz(peers)) {
-      wcnt[d] = base + __popc(peers);
-      wmask[d] = 0;
-    }
-    __syncwarp();
-#else
-    (void)wmask;
     const uint32_t peers = match_digit8(d, ok);
     uint32_t base = 0;
     if (ok) base = wcnt[d];
@@ -158,7 +135,6 @@ __device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, ui
     __syncwarp();
     if (ok && lane == 31 - __clz(peers)) wcnt[d] = base + __popc(peers);
     __syncwarp();
-#endif
   }
 }
 
@@ -255,7 +231,6 @@ __global__ void __launch_bounds__(kRThreads, 4)
 radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
   using C = RadixCfg<K>;
   __shared__ uint32_t wcnt[kRWarps][kDigits];
-  __shared__ uint32_t wmask[WS_RANK_OR ? kRWarps : 1][kDigits];
   __shared__ uint32_t s_gdelta[kDigits];  // global offset - tile-local start
   __shared__ uint32_t s_wsum[kRWarps];
   __shared__ __align__(16) K stage[C::T];
@@ -266,10 +241,7 @@ radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
     const int s = rsegment_of(a, tile);
     if (tid == 0) s_seg = s;
   }
-  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) {
-    (&wcnt[0][0])[i] = 0;
-    if (WS_RANK_OR) (&wmask[0][0])[i] = 0;
-  }
+  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const RadixSeg& sg = rseg_at(a, s_seg);
   const uint32_t t = tile - sg.tile_begin;
@@ -287,7 +259,7 @@ radix_downsweep_kernel(const __grid_constant__ RadixLaunch a) {
     key[r] = j < nvalid ? __ldcs(in + j) : K(0);
   }
   Ranks<C::E> rk;
-  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], wmask[WS_RANK_OR ? wid : 0], rk);
+  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], rk);
   __syncthreads();
   // per digit (thread = digit): exclusive over warps, then over digits
   uint32_t run = 0;
@@ -345,9 +317,6 @@ constexpr uint64_t kStEpochMask = ~0x3FFFFFFFFull;
 #define WS_LOOK_W 4
 #endif
 constexpr int kLookW = WS_LOOK_W;  // predecessors loaded per look-back round
-#ifndef WS_OS_EARLY
-#define WS_OS_EARLY 0  // 1: tile histogram + look-back before the ranking (measured 2 % slower)
-#endif
 #ifndef WS_OS_MINB
 #define WS_OS_MINB 3  // 80 registers, no spills (4: 64 with spills, measured slower)
 #endif
@@ -566,16 +535,11 @@ __global__ void __launch_bounds__(kRThreads, WS_OS_MINB)
 radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   using C = RadixCfg<K>;
   __shared__ uint32_t wcnt[kRWarps][kDigits];
-  __shared__ uint32_t wmask[WS_RANK_OR ? kRWarps : 1][kDigits];
   __shared__ uint32_t s_gdelta[kDigits];  // global offset - tile-local start
   __shared__ uint32_t s_wsum[2][kRWarps];
   __shared__ __align__(16) K stage[C::T];
   __shared__ int s_seg;
   __shared__ uint32_t s_tile;
-#if WS_OS_EARLY
-  __shared__ uint32_t s_hist[kDigits];
-  s_hist[threadIdx.x] = 0;
-#endif
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < 32) {  // ticket order: every tile this one waits for has started
     uint32_t tk = 0;
@@ -587,10 +551,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
       s_tile = tk;
     }
   }
-  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) {
-    (&wcnt[0][0])[i] = 0;
-    if (WS_RANK_OR) (&wmask[0][0])[i] = 0;
-  }
+  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const uint32_t tile = s_tile;
   WS_OS_STAMP(0);
@@ -609,20 +570,8 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     const uint32_t j = r * 32 + lane;
     key[r] = j < nvalid ? __ldcs(in + j) : K(0);
   }
-#if WS_OS_EARLY
-  // The tile's digit counts first (shared atomics, no ranking), so its
-  // aggregate is published - and its look-back done and its inclusive prefix
-  // published - before the ranking: successors find inclusive prefixes
-  // nearer, which shortens every look-back walk.
-#pragma unroll
-  for (int r = 0; r < C::E; ++r)
-    if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&s_hist[digit_of<K>(key[r], sg.shift)], 1u);
-  __syncthreads();
-  WS_OS_STAMP(1);
-  const uint32_t run = s_hist[tid];
-#else
   Ranks<C::E> rk;
-  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], wmask[WS_RANK_OR ? wid : 0], rk);
+  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], rk);
   __syncthreads();
   WS_OS_STAMP(1);
   // per digit (thread = digit): exclusive over warps; the tile's count
@@ -633,7 +582,6 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     wcnt[w][tid] = run;
     run += c;
   }
-#endif
   uint64_t* status = a.status + (uint64_t)tile * kDigits + tid;
   const uint64_t ep = (uint64_t)a.epoch << 34;
   const bool head = t == 0;  // the segment's first tile: its prefix is 0
@@ -662,7 +610,6 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   }
   const uint32_t doff = wpre + inc - run;
   const uint32_t dbase = wpre2 + inc2 - tot;
-#if !WS_OS_EARLY
 #pragma unroll
   for (int w = 0; w < kRWarps; ++w) wcnt[w][tid] += doff;  // tile-local start of (warp, digit)
   __syncthreads();
@@ -673,7 +620,6 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     const uint32_t j = r * 32 + lane;
     if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk.get(r)] = key[r];
   }
-#endif
   // look-back over the segment's preceding tiles for this digit: a window of
   // kLookW predecessors per load round, nearest first; the segment's first
   // tile is always inclusive, so the walk stops there
@@ -708,27 +654,6 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     a.prof[(uint64_t)tile * 8 + 5] = rounds;
     a.prof[(uint64_t)tile * 8 + 6] = stalls;
   }
-#if WS_OS_EARLY
-  {
-    // now rank (stable, per warp) and regroup the tile by digit in shared memory
-    Ranks<C::E> rk;
-    warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], wmask[WS_RANK_OR ? wid : 0], rk);
-    __syncthreads();
-    uint32_t st = doff;  // tile-local start of (warp, digit): doff + earlier warps' counts
-#pragma unroll
-    for (int w = 0; w < kRWarps; ++w) {
-      const uint32_t c = wcnt[w][tid];
-      wcnt[w][tid] = st;
-      st += c;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < C::E; ++r) {
-      const uint32_t j = r * 32 + lane;
-      if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk.get(r)] = key[r];
-    }
-  }
-#endif
   s_gdelta[tid] = dbase + excl - doff;
   __syncthreads();
   WS_OS_STAMP(3);
