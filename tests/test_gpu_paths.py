@@ -47,10 +47,16 @@ print("ok")
     "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest
     "WSORT_SERIAL",           # every kernel on the main stream
     "WSORT_D2H_PER_CLASS",    # one emit + copy per lane class
+    # A/B knobs used in the measurements (profiles/r01_ab_*.txt)
+    "WSORT_CLASS_ORDER=3,2,1,0,4",
+    "WSORT_CLASS_PRIO=0,-5,-5,-5,0",
+    "WSORT_FUSED_SLOT_CLASSES=2",
+    "CUDA_DEVICE_MAX_CONNECTIONS=32",
 ])
 def test_diagnostic_paths_agree(knob):
     words = 2_600_000 if knob == "WSORT_NO_CHUNKED_H2D" else 300_000  # > 16 MiB for the H2D knob
-    env = dict(os.environ, **{knob: "1"})
+    name, _, value = knob.partition("=")
+    env = dict(os.environ, **{name: value or "1"})
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=str(ROOT), words=words)],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
