@@ -533,6 +533,7 @@ joint_expand_kernel(const __grid_constant__ RadixLaunch a) {
 template <class K>
 __global__ void __launch_bounds__(kRThreads, WS_OS_MINB)
 radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
+  pdl_wait();
   using C = RadixCfg<K>;
   __shared__ uint32_t wcnt[kRWarps][kDigits];
   __shared__ uint32_t s_gdelta[kDigits];  // global offset - tile-local start
@@ -753,9 +754,9 @@ void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs,
 void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st) {
   if (!a.work_items) return;
   if (lanes == 0)
-    radix_onesweep_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
+    launch_pdl(radix_onesweep_kernel<uint32_t>, a.work_items, kRThreads, 0, st, a);
   else
-    radix_onesweep_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+    launch_pdl(radix_onesweep_kernel<uint64_t>, a.work_items, kRThreads, 0, st, a);
 }
 
 int radix_tile_size(int lanes) { return lanes == 0 ? RadixCfg<uint32_t>::T : RadixCfg<uint64_t>::T; }

@@ -735,6 +735,7 @@ template <int LANES, bool COUNT>
 #define WS_PART_MINB 1
 #endif
 __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(const __grid_constant__ SampleLaunch a) {
+  pdl_wait();
   using W = KW<LANES>;
   __shared__ uint64_t s_split[kMaxSplit];
   __shared__ uint32_t s_cnt[2 * kMaxSplit + 1];
@@ -802,6 +803,7 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
 // at the bucket's class-relative key offset: the slot offsets, valid for any
 // subset of a class's buckets.
 __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__ SampleLaunch a) {
+  pdl_wait();
   __shared__ uint32_t s_w[32];
   __shared__ uint32_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -860,6 +862,7 @@ template <int LANES>
 #define WS_SUB1_MINB 7  // one-word keys: 72 registers (1: 109, slot sort 63 -> 43 us at 7)
 #endif
 __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SUB_MINB) subsort_kernel(const __grid_constant__ SampleLaunch a) {
+  pdl_wait();
   constexpr int E = TileCfg<LANES>::E, NT = kSubThreads, TS = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
@@ -1020,10 +1023,11 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   (void)P;
   (void)mmax;  // every bucket's CTA zeroes its slot counters, sampled or not
   if (!a.split_done) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
-  partition_kernel<LANES, true><<<a.work_items, kPartThreads, 0, st>>>(a);
-  slot_scan_kernel<<<a.nsegs, 1024, 0, st>>>(a);
-  partition_kernel<LANES, false><<<a.work_items, kPartThreads, 0, st>>>(a);
-  subsort_kernel<LANES><<<a.nslots, kSubThreads, subsort_smem_bytes<LANES>(), st>>>(a);
+  // the chain's kernels start while their predecessor drains (pdl_wait first)
+  launch_pdl(partition_kernel<LANES, true>, a.work_items, kPartThreads, 0, st, a);
+  launch_pdl(slot_scan_kernel, a.nsegs, 1024, 0, st, a);
+  launch_pdl(partition_kernel<LANES, false>, a.work_items, kPartThreads, 0, st, a);
+  launch_pdl(subsort_kernel<LANES>, a.nslots, kSubThreads, subsort_smem_bytes<LANES>(), st, a);
 }
 
 int sample_max_keys(int) { return kSampleSmem / 8; }

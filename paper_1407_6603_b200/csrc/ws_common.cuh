@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace ws {
 
@@ -136,6 +137,30 @@ __device__ __forceinline__ uint32_t code6_at(const uint64_t* key) {
   } else {
     return (uint32_t)((key[w] << (o - 58)) | (key[w + 1] >> (122 - o))) & 63u;
   }
+}
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while its predecessor in the stream drains; it waits here before touching
+// anything the predecessor wrote (a no-op for a normal launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#ifndef WS_PDL
+#define WS_PDL 1
+#endif
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = WS_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // One sort segment: a bucket (or a long-word group / LSD pass) whose keys
