@@ -347,6 +347,7 @@ __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cn
 
 template <int LANES, bool STATS>
 __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_constant__ SortLaunch a) {
+  pdl_wait();
   constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kTileThreads;
   constexpr int NW = KeyTraits<LANES>::NW, KB = key_bytes(LANES);
   using W = KW<LANES>;
@@ -452,6 +453,7 @@ __device__ __forceinline__ PairGeom pair_geom(const SegDesc& sd, uint32_t item, 
 // its own lookup.
 template <int LANES>
 __global__ void __launch_bounds__(256) merge_split_kernel(const __grid_constant__ SortLaunch a) {
+  pdl_wait();
   constexpr int T = MergeCfg<LANES>::T;
   const uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (item >= a.work_items) return;
@@ -474,6 +476,7 @@ __global__ void __launch_bounds__(256) merge_split_kernel(const __grid_constant_
 template <int LANES, bool STATS>
 __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
     merge_kernel(const __grid_constant__ SortLaunch a) {
+  pdl_wait();
   constexpr int E = MergeCfg<LANES>::E, T = MergeCfg<LANES>::T, NT = kMergeThreads;
   constexpr int NW = KeyTraits<LANES>::NW, KB = key_bytes(LANES);
   using W = KW<LANES>;
@@ -986,15 +989,15 @@ void set_sort_attributes() {
 
 template <int LANES, bool STATS>
 static void launch_tile_t(const SortLaunch& a, cudaStream_t st) {
-  tile_sort_kernel<LANES, STATS><<<a.work_items, kTileThreads,
-                                   pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>(), st>>>(a);
+  launch_pdl(tile_sort_kernel<LANES, STATS>, a.work_items, kTileThreads,
+             pass_smem_bytes<LANES, TileCfg<LANES>::T, STATS>(), st, a);
 }
 
 template <int LANES, bool STATS>
 static void launch_merge_t(const SortLaunch& a, cudaStream_t st) {
-  merge_split_kernel<LANES><<<(a.work_items * 32 + 255) / 256, 256, 0, st>>>(a);
-  merge_kernel<LANES, STATS><<<a.work_items, kMergeThreads,
-                               pass_smem_bytes<LANES, MergeCfg<LANES>::T, STATS>(), st>>>(a);
+  launch_pdl(merge_split_kernel<LANES>, (a.work_items * 32 + 255) / 256, 256, 0, st, a);
+  launch_pdl(merge_kernel<LANES, STATS>, a.work_items, kMergeThreads,
+             pass_smem_bytes<LANES, MergeCfg<LANES>::T, STATS>(), st, a);
 }
 
 #define WS_DISPATCH_LANES(fn, lanes, stats, ...)                                    \
