@@ -280,6 +280,7 @@ count_kernel(const uint8_t* __restrict__ text, uint64_t n, uint32_t* __restrict_
 __global__ void __launch_bounds__(1024)
 scan_kernel(const uint32_t* __restrict__ hist, uint32_t* __restrict__ off,
             uint32_t* __restrict__ totals, uint32_t nchunks) {
+  pdl_wait();
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry_s;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -791,6 +792,7 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
 // so small runs do not leave lanes idle.
 __global__ void __launch_bounds__(kIngestThreads)
 reorder_runs_kernel(ReorderParams r) {
+  pdl_wait();
   __shared__ uint32_t s_pre[kNumBins + 1];
   __shared__ uint32_t s_from[kNumBins], s_to[kNumBins];
   const int tid = threadIdx.x;
@@ -961,7 +963,7 @@ void launch_count(const uint8_t* text, uint64_t n, uint32_t* hist, uint32_t nchu
 
 void launch_scan(const uint32_t* hist, uint32_t* off, uint32_t* totals, uint32_t nchunks,
                  int rows, cudaStream_t st) {
-  scan_kernel<<<rows, 1024, 0, st>>>(hist, off, totals, nchunks);
+  launch_pdl(scan_kernel, rows, 1024, 0, st, hist, off, totals, nchunks);
 }
 
 void launch_scatter(const uint8_t* text, uint64_t n, const uint32_t* off, uint32_t nchunks,
@@ -1001,7 +1003,7 @@ uint32_t ingest_chunk_bytes() { return kChunk; }
 uint32_t reserve_chunk_bytes() { return kReserveSB * kIngestThreads; }
 
 void launch_reorder_runs(const ReorderParams& r, cudaStream_t st) {
-  if (r.nchunks) reorder_runs_kernel<<<r.nchunks, kIngestThreads, 0, st>>>(r);
+  if (r.nchunks) launch_pdl(reorder_runs_kernel, r.nchunks, kIngestThreads, 0, st, r);
 }
 
 uint32_t chunk_count(uint64_t n) { return (uint32_t)((n + kChunk - 1) / kChunk); }

@@ -463,6 +463,7 @@ __device__ __forceinline__ int jseg_at(const RadixLaunch& a, uint32_t b) {
 }
 
 __global__ void __launch_bounds__(1024) joint_scan_kernel(const __grid_constant__ RadixLaunch a) {
+  pdl_wait();
   __shared__ uint32_t s_w[32];
   const RadixSeg& sg = rseg_at(a, jseg_at(a, blockIdx.x));
   uint32_t* cnt = a.joint + sg.joff;
@@ -499,6 +500,7 @@ constexpr int kExpandThreads = 128;
 constexpr int kExpandParts = 4;
 __global__ void __launch_bounds__(kExpandThreads)
 joint_expand_kernel(const __grid_constant__ RadixLaunch a) {
+  pdl_wait();
   __shared__ __align__(16) uint8_t pbuf[64 + 16 * 40];
   uint32_t v = blockIdx.x;  // blocks: the jbits segments' values back to back
   int si = 0;
@@ -747,8 +749,8 @@ void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st) {
 
 void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs, cudaStream_t st) {
   if (!blocks) return;
-  joint_scan_kernel<<<njsegs, 1024, 0, st>>>(a);
-  joint_expand_kernel<<<dim3(blocks, kExpandParts), kExpandThreads, 0, st>>>(a);
+  launch_pdl(joint_scan_kernel, njsegs, 1024, 0, st, a);
+  launch_pdl(joint_expand_kernel, dim3(blocks, kExpandParts), kExpandThreads, 0, st, a);
 }
 
 void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st) {
