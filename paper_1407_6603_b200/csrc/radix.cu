@@ -400,6 +400,7 @@ __device__ __forceinline__ void hist_tile(const RadixSeg& sg, uint32_t t, uint32
 template <class K>
 __global__ void __launch_bounds__(kRThreads)
 radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
+  pdl_wait();
   constexpr int kP = (int)sizeof(K);
   constexpr int kSm = kP * kDigits > kJointMax ? kP * kDigits : kJointMax;
   __shared__ uint32_t sm[kSm];  // hist[kP][256], or the joint counts of a jbits segment
@@ -732,9 +733,9 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
 void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st) {
   if (!a.work_items) return;
   if (lanes == 0)
-    radix_hist_kernel<uint32_t><<<a.work_items, kRThreads, 0, st>>>(a);
+    launch_pdl(radix_hist_kernel<uint32_t>, a.work_items, kRThreads, 0, st, a);
   else
-    radix_hist_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
+    launch_pdl(radix_hist_kernel<uint64_t>, a.work_items, kRThreads, 0, st, a);
 }
 
 #ifndef WS_HIST_EARLY_CTAS

@@ -676,6 +676,7 @@ __device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __re
 
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
+  pdl_wait();
   __shared__ uint64_t sm[kBitonicN];
   split_bucket<LANES>(sseg_at(a, blockIdx.x), a.splitters, a.hist, sm);
 }
@@ -1025,7 +1026,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
   while (P < mmax) P <<= 1;
   (void)P;
   (void)mmax;  // every bucket's CTA zeroes its slot counters, sampled or not
-  if (!a.split_done) sample_split_kernel<LANES><<<a.nsegs, kSampleThreads, 0, st>>>(a);
+  if (!a.split_done) launch_pdl(sample_split_kernel<LANES>, a.nsegs, kSampleThreads, 0, st, a);
   // the chain's kernels start while their predecessor drains (pdl_wait first)
   launch_pdl(partition_kernel<LANES, true>, a.work_items, kPartThreads, 0, st, a);
   launch_pdl(slot_scan_kernel, a.nsegs, 1024, 0, st, a);
