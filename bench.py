@@ -17,11 +17,18 @@ One JSON line on rank 0:
              + all kernels + D2H of the payload in every step: a batch of K
              corpora through ws_sort_texts (3 in flight, wall clock around the
              call); e2e.single = one ws_sort_text call per step (CUDA events).
-  roofline   dominant kernel: algorithmic bytes per launch / its CUDA-event
-             duration inside the timed steps, against MEASURED_PEAKS.json.
-  cpu_baseline  the reference algorithm (oracle/ C port of _bubble_rows etc.)
-             on the host cores, on a bounded prefix sample of the same text.
-`--impl reference` times that CPU path alone (rank 0; other ranks exit 0).
+  roofline   the kernel family with the largest serialised share of the step:
+             algorithmic bytes per launch / its CUDA-event duration (events
+             around every launch in K profiled steps run after the timed
+             ones), against MEASURED_PEAKS.json; roofline_rows lists every
+             family (ingest, one-sweep radix, radix histogram, sample split,
+             partition, slot sort; stats mode: ingest, tile sort, merge).
+  cpu_baseline  the unmodified reference (baseline/_ref, numba _bubble_rows on
+             a worker pool; tools/vendor_reference.sh) on the host cores, on a
+             bounded prefix of the same text, with the oracle's C port of the
+             same algorithm beside it ("port").
+`--impl reference` times the reference's CPU path alone (rank 0; other ranks
+exit 0). Every leg's output is byte-compared with the oracle after its loop.
 Multi-GPU: independent replicas (one corpus per rank, no collective in the
 data path), weak scaling, max-over-ranks timing.
 """
@@ -44,6 +51,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "sorted words/sec on 1 B200 (end-to-end) and % of HBM/int-pipe roofline; bit-exact"
 UNIT = "words/s"
 CPU_SAMPLE_WORDS = 120_000
+REF_SAMPLE_WORDS = 60_000  # reference arm: per-step sample (~3 s of numba work on 16 threads)
 FLUSH_BYTES = 256 << 20
 INFLIGHT = 3  # corpora in flight in the serving (batch) e2e leg
 
@@ -56,6 +64,8 @@ def parse_args():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-sample-words", type=int, default=CPU_SAMPLE_WORDS)
+    ap.add_argument("--ref-sample-words", type=int, default=REF_SAMPLE_WORDS,
+                    help="--impl reference: words of the per-step sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true", help="skip the oracle payload check")
     ap.add_argument("--profile-json", default=None, help="also write per-phase timings here")
@@ -122,7 +132,17 @@ def extrapolate(full_hist: dict, sample_info: dict, timings: dict, threads: int)
     return max(loads) if loads else None
 
 
+def physical_cores() -> int | None:
+    try:
+        import psutil
+
+        return psutil.cpu_count(logical=False)
+    except Exception:
+        return None
+
+
 def run_cpu(text: bytes, sample_words: int, threads: int, full_hist: dict | None):
+    """The oracle's C restatement of the reference pipeline (kind "port")."""
     from oracle import oracle
 
     sample = cpu_sample(text, sample_words)
@@ -135,6 +155,7 @@ def run_cpu(text: bytes, sample_words: int, threads: int, full_hist: dict | None
         "value": n_words / dt,
         "unit": UNIT,
         "cores": threads,
+        "physical_cores": physical_cores(),
         "kind": "port",
         "sample": (f"first {n_words} words ({len(sample)} bytes) of the same seeded text; "
                    "tokenize + group-by-length + per-bucket bubble sort (engine.py:89-114 "
@@ -146,7 +167,51 @@ def run_cpu(text: bytes, sample_words: int, threads: int, full_hist: dict | None
         if ex:
             res["extrapolated_full_seconds"] = ex
             res["extrapolated_full_words_per_s"] = sum(full_hist.values()) / ex
-    return res, dt, n_words
+    return res, dt, n_words, payload
+
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_module():
+    """The UNMODIFIED reference package installed by tools/vendor_reference.sh
+    (git-ignored, shipped to the GPU box), or None when it is absent."""
+    if not (REF_DIR / "wordsort" / "__init__.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_wordsort")
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    try:
+        import wordsort  # noqa: F401
+        from wordsort import cli, engine, ingest, store
+    except Exception:
+        return None
+    return {"ingest": ingest, "store": store, "engine": engine, "cli": cli}
+
+
+def run_reference(text: bytes, sample_words: int, threads: int):
+    """The reference's own pipeline through its public API, as `wordsort sort`
+    runs it with the CLI defaults (cli.py:83-103: flat layout, NAIVE, STATIC,
+    os.cpu_count() threads): tokenize -> build_store -> sort_all_parallel (the
+    numba _bubble_rows, engine.py:89-114) -> emit_sorted -> payload join.
+    Returns (seconds, words, payload) or None when the reference is absent."""
+    ref = reference_module()
+    if ref is None:
+        return None
+    sample = cpu_sample(text, sample_words)
+    eng, st, ing = ref["engine"], ref["store"], ref["ingest"]
+    cfg = eng.SortConfig(layout=st.LayoutKind.FLAT, variant=eng.SortVariant.NAIVE,
+                         threads=threads, schedule=eng.SchedulePolicy.STATIC_BLOCK)
+    t0 = time.perf_counter()
+    words = ing.tokenize(sample)
+    store = st.build_store(words, cfg.layout)
+    if threads == 1:
+        eng.sort_all_sequential(store, cfg.variant)
+    else:
+        eng.sort_all_parallel(store, cfg)
+    payload = b"".join(w + b"\n" for w in st.emit_sorted(store))
+    dt = time.perf_counter() - t0
+    return dt, len(words), payload
 
 
 # ---------------------------------------------------------------------------
@@ -240,19 +305,38 @@ def ncu_traffic(workload: str, kernel: str):
 # ---------------------------------------------------------------------------
 
 def bench_reference(args) -> None:
+    """--impl reference: the reference's own CPU path (baseline/_ref, the
+    unmodified wordsort package: numba _bubble_rows on a worker pool) on the
+    host cores, a bounded prefix of the same workload per step; the oracle's
+    C port when the reference is not installed. Rank 0 only."""
     rank, world, _ = rank_info()
     if rank != 0:
         return
     text = corpus(args.config, 0)
     threads = os.cpu_count() or 1
+    have_ref = reference_module() is not None
     times = []
     n_words = 0
+    payload = b""
     for i in range(args.warmup + args.steps):
-        _, dt, n_words = run_cpu(text, args.cpu_sample_words, threads, None)
+        if have_ref:
+            dt, n_words, payload = run_reference(text, args.ref_sample_words, threads)
+        else:
+            _, dt, n_words, payload = run_cpu(text, args.ref_sample_words, threads, None)
         if i >= args.warmup:
             times.append(dt)
     t = statistics.mean(times)
     value = n_words / t
+    kind = "reference" if have_ref else "port"
+    what = ("the unmodified reference (baseline/_ref wordsort: tokenize, build_store flat, "
+            "sort_all_parallel NAIVE/STATIC with the numba _bubble_rows, emit_sorted, payload join)"
+            if have_ref else "the reference bubble sort restated in C (oracle/wsort_oracle.c)")
+    parity = None
+    if not args.no_check:
+        from oracle import oracle
+
+        want, _ = oracle.sort_text(cpu_sample(text, args.ref_sample_words), mode="fast")
+        parity = payload == want
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -260,19 +344,60 @@ def bench_reference(args) -> None:
         "data": "synthetic", "impl": "reference",
         "config": {"workload": workload_name(args.config),
                    "sample_words": n_words, "l2_flush": "n/a (CPU)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads,
+                         "physical_cores": physical_cores(), "kind": kind,
                          "sample": (f"first {n_words} words of the seeded config-{args.config} "
-                                    "text per step (reference bubble sort restated in C, "
-                                    "oracle/wsort_oracle.c)")},
+                                    f"text per step through {what}")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parity_vs_oracle": parity,
     }
     print(json.dumps(line), flush=True)
+
+
+# Kernel families of the step and the profiling records (ws_profile names) that
+# time them; each record carries its launch's algorithmic bytes.
+FAMILIES = {
+    "ingest": ("ingest",),
+    "radix_onesweep": ("radix_l0",),
+    "radix_hist": ("radix_hist_l0",),
+    "sample_split": ("split_l1", "split_l2", "split_l3", "split_l4"),
+    "partition": ("part_count_l1", "part_count_l2", "part_count_l3", "part_count_l4",
+                  "part_scatter_l1", "part_scatter_l2", "part_scatter_l3", "part_scatter_l4"),
+    "slot_sort": ("subsort_l1", "subsort_l2", "subsort_l3", "subsort_l4"),
+}
+STATS_FAMILIES = {
+    "stats_ingest": ("ingest", "reorder"),
+    "stats_tile_sort": ("tile_l0", "tile_l1", "tile_l2", "tile_l3", "tile_l4"),
+    "stats_merge": ("merge_l0", "merge_l1", "merge_l2", "merge_l3", "merge_l4"),
+}
+
+
+def family_rows(phases: list, families: dict, steps: int, peak: float, workload: str,
+                override_bytes: dict | None = None) -> dict:
+    """Per kernel family: algorithmic bytes and CUDA-event time of its launches
+    (profiled steps), achieved GB/s and the fraction of the measured peak."""
+    rows = {}
+    for fam, names in families.items():
+        recs = [p for p in phases if p["name"] in names and p["launches"] > 0]
+        ms = sum(p["ms"] for p in recs)
+        nbytes = sum(p["bytes"] for p in recs)
+        launches = sum(p["launches"] for p in recs)
+        if override_bytes and fam in override_bytes:
+            nbytes = override_bytes[fam]
+        if ms <= 0 or launches == 0:
+            continue
+        ach = nbytes / (ms * 1e-3) / 1e9
+        rows[fam] = {"ms_per_step": ms / steps, "launches_per_step": launches / steps,
+                     "algorithmic_bytes_per_launch": nbytes / launches,
+                     "ms_per_launch": ms / launches, "achieved": ach, "unit": "GB/s",
+                     "frac": ach / peak, "traffic": ncu_traffic(workload, fam)}
+    return rows
 
 
 def bench_ours(args) -> None:
     import torch
 
-    from paper_1407_6603_b200._native import Handle
+    from paper_1407_6603_b200._native import Handle, device_bytes
     from paper_1407_6603_b200.pipeline import BatchSorter, TextSorter
 
     rank, world, local = rank_info()
@@ -293,6 +418,11 @@ def bench_ours(args) -> None:
     text = corpus(args.config, rank)
     n = len(text)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    want = None
+    if not args.no_check:
+        from oracle import oracle
+
+        want, _ = oracle.sort_text(text, mode="fast")  # checker only, outside every timed region
 
     # ---- device-resident leg --------------------------------------------
     h = Handle(local)
@@ -303,11 +433,24 @@ def bench_ours(args) -> None:
     written = 0
     for _ in range(args.warmup):
         written = h.sort_resident(n)
+
+    def profiled(step, hh, s) -> list:
+        """K more steps with per-kernel CUDA events, kernels serialised on one
+        stream so each event pair times one launch alone (not the timed steps)."""
+        hh.profile(reset=True)
+        hh.set_profiling(2)
+        for _ in range(args.steps):
+            with torch.cuda.stream(s):
+                flush.zero_()
+            torch.cuda.synchronize(dev)
+            step()
+        torch.cuda.synchronize(dev)
+        hh.set_profiling(False)
+        return hh.profile(reset=True)
+
     sampler = ClockSampler(local)
     dev_ms = []
     with sampler:
-        h.profile(reset=True)
-        h.set_profiling(True)
         launches0 = h.launch_count()
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
@@ -322,8 +465,11 @@ def bench_ours(args) -> None:
             torch.cuda.synchronize(dev)
             dev_ms.append(a.elapsed_time(b))
         launches = h.launch_count() - launches0
-        h.set_profiling(False)
-        phases = h.profile(reset=True)
+        # the timed path's own output, byte-compared after the loop
+        resident_ok = None
+        if want is not None:
+            resident_ok = device_bytes(*h.output_device()) == want
+        phases = profiled(lambda: h.sort_resident(n), h, stream)
 
         # ---- end-to-end leg through the C ABI with host buffers -------------
         ts = TextSorter(n, device=local)
@@ -346,11 +492,13 @@ def bench_ours(args) -> None:
             torch.cuda.synchronize(dev)
             e2e_ms.append(a.elapsed_time(b))
         e2e_launches = ts.handle.launch_count() - e2e_launches0
+        single_ok = None if want is None else ts.payload(e2e_written) == want
 
         # ---- serving leg: the same corpus as a batch of K jobs through
         # ws_sort_texts, INFLIGHT in flight (H2D of one overlaps the sort and
-        # D2H of the previous ones); every job's H2D and D2H is in the region
-        bs = BatchSorter(n, inflight=INFLIGHT, device=local)
+        # D2H of the previous ones); every job's H2D and D2H is in the region,
+        # every job writes its own pinned output buffer (all K checked)
+        bs = BatchSorter(n, inflight=INFLIGHT, device=local, outputs=max(args.steps, INFLIGHT))
         bs.load(text)
         bs.run(max(args.warmup, INFLIGHT))
         batch_launches0 = bs.handle.launch_count()
@@ -361,6 +509,9 @@ def bench_ours(args) -> None:
         torch.cuda.synchronize(dev)
         batch_ms = (time.perf_counter() - t0) * 1e3 / args.steps
         batch_launches = bs.handle.launch_count() - batch_launches0
+        batch_ok = None
+        if want is not None:
+            batch_ok = all(bs.payload(k, sz) == want for k, sz in enumerate(batch_sizes))
 
         # ---- stats leg: the reference's full SortStats semantics on the
         # device (order-preserving ingest, merge sort with inversion / K
@@ -368,10 +519,14 @@ def bench_ours(args) -> None:
         dtext = torch.frombuffer(bytearray(text), dtype=torch.uint8).to(dev)
         hsx = Handle(local)
         sstream = torch.cuda.ExternalStream(hsx.stream(), device=dev)
-        for _ in range(args.warmup):
+
+        def stats_step():
             hsx.ingest_text(None, device_ptr=dtext.data_ptr(), n=n)
             hsx.sort(True)
-            hsx.bucket_stats(True)
+            return hsx.bucket_stats(True)
+
+        for _ in range(args.warmup):
+            stats_step()
         stats_ms = []
         for _ in range(args.steps):
             with torch.cuda.stream(sstream):
@@ -380,12 +535,11 @@ def bench_ours(args) -> None:
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(sstream)
-            hsx.ingest_text(None, device_ptr=dtext.data_ptr(), n=n)
-            hsx.sort(True)
-            hsx.bucket_stats(True)
+            st_rows = stats_step()
             b.record(sstream)
             torch.cuda.synchronize(dev)
             stats_ms.append(a.elapsed_time(b))
+        stats_phases = profiled(stats_step, hsx, sstream)
     clocks = sampler.summary()
     # one extra (untimed) e2e step with per-phase events, for the timeline
     ts.handle.profile(reset=True)
@@ -403,55 +557,54 @@ def bench_ours(args) -> None:
     e2e_value = world * words / (t_e2e * 1e-3)
     batch_value = world * words / (t_batch * 1e-3)
 
-    # per-phase aggregation (CUDA events on the library stream, timed steps)
-    agg: dict = {}
-    for p in phases:
-        a_ = agg.setdefault(p["name"], {"ms": 0.0, "bytes": 0.0, "launches": 0, "kind": p["kind"]})
-        a_["ms"] += p["ms"]
-        a_["bytes"] += p["bytes"]
-        a_["launches"] += max(p["launches"], 1)
-    kern = {k: v for k, v in agg.items() if v["kind"] == 0}
-    step_ms = sum(dev_ms)
-    # The roofline kernel is the ingest: the largest single kernel of the step
-    # in the serialised ncu launch list (profiles/), and the only one that runs
-    # alone (before the per-class streams fork), so its events time it cleanly.
-    # Its algorithmic bytes are exact: the text read once + every packed key
-    # written once + 8 B per long-word (start, len) entry.
-    if "ingest" in kern:
-        dom = "ingest"
-        kern["ingest"]["bytes"] = args.steps * ingest_algorithmic_bytes(n, hist)
-    else:
-        dom = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
+    # ---- rooflines: every kernel family of the step (CUDA events per launch
+    # in K profiled steps after the timed ones), against the measured peak.
+    # The ingest's bytes are exact: text read once + every packed key written
+    # once + 8 B per long-word entry; the others come from the library's
+    # per-launch accounting (keys read + keys or payload records written).
     peak, peak_src = measured_peak()
+    wl = workload_name(args.config)
+    rows = family_rows(phases, FAMILIES, args.steps, peak, wl,
+                       {"ingest": args.steps * ingest_algorithmic_bytes(n, hist)})
+    stats_rows = family_rows(stats_phases, STATS_FAMILIES, args.steps, peak, wl)
+    serial_ms = sum(r["ms_per_step"] for r in rows.values())
     roofline = None
-    if dom:
-        d = kern[dom]
-        per_launch_bytes = d["bytes"] / d["launches"]
-        per_launch_ms = d["ms"] / d["launches"]
-        achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
-        roofline = {
-            "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
-            "traffic": ncu_traffic(workload_name(args.config), dom),
-            "algorithmic_bytes_per_launch": per_launch_bytes,
-            "ms_per_launch": per_launch_ms, "share_of_step": d["ms"] / step_ms,
-        }
+    if rows:
+        dom = max(rows, key=lambda k: rows[k]["ms_per_step"])  # largest serialised share
+        d = rows[dom]
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": d["achieved"], "peak": peak,
+                    "unit": "GB/s", "frac": d["frac"],
+                    "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                    "traffic": d["traffic"],
+                    "algorithmic_bytes_per_launch": d["algorithmic_bytes_per_launch"],
+                    "ms_per_launch": d["ms_per_launch"],
+                    "share_of_step": d["ms_per_step"] / serial_ms if serial_ms else None,
+                    "timing": "CUDA events per launch over K profiled steps after the timed ones, "
+                              "kernels serialised on one stream"}
+        for r in rows.values():
+            r["share_of_step"] = r["ms_per_step"] / serial_ms if serial_ms else None
 
     parity = None
     cpu = None
     if rank == 0:
-        if not args.no_check:
-            from oracle import oracle
-
-            want, _ = oracle.sort_text(text, mode="fast")
-            parity = bool(ts.payload(e2e_written) == want)
-            parity = parity and all(sz == len(want) for sz in batch_sizes)
-            parity = parity and all(bs.payload(k, batch_sizes[0]) == want
-                                    for k in range(min(INFLIGHT, args.steps)))
-            dptr, dsize = h.output_device()
-            parity = parity and (dsize == len(want))
+        if want is not None:
+            parity = bool(resident_ok and single_ok and batch_ok)
         if world == 1 and not args.no_cpu_baseline:
-            cpu, _, _ = run_cpu(text, args.cpu_sample_words, os.cpu_count() or 1, hist)
+            threads = os.cpu_count() or 1
+            port, _, _, port_payload = run_cpu(text, args.cpu_sample_words, threads, hist)
+            ref = run_reference(text, args.cpu_sample_words, threads)
+            if ref is not None:  # the reference's own numba path, beside the port
+                dt, nw, ref_payload = ref
+                cpu = {"value": nw / dt, "unit": UNIT, "cores": threads,
+                       "physical_cores": physical_cores(), "kind": "reference",
+                       "sample": (f"first {nw} words of the same seeded text through the "
+                                  "unmodified reference (baseline/_ref wordsort: tokenize, "
+                                  "build_store flat, sort_all_parallel NAIVE/STATIC with the "
+                                  "numba _bubble_rows on a thread pool, emit_sorted, payload join)"),
+                       "seconds": dt, "payload_equals_port": ref_payload == port_payload,
+                       "port": port}
+            else:
+                cpu = port
 
     if rank == 0:
         line = {
@@ -459,7 +612,7 @@ def bench_ours(args) -> None:
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_dev, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": workload_name(args.config), "words": words,
+            "config": {"workload": wl, "words": words,
                        "text_bytes": n, "payload_bytes": written, "buckets": len(lengths),
                        "l2_flush": "256 MiB memset on the timed stream between steps",
                        "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
@@ -467,26 +620,31 @@ def bench_ours(args) -> None:
                     "d2h_bytes_per_step": batch_sizes[0] if batch_sizes else 0,
                     "ms_per_step": t_batch, "gpu_launches": batch_launches,
                     "api": f"ws_sort_texts, batch of {args.steps} corpora, {INFLIGHT} in flight, "
-                           "pinned host buffers, wall clock around the call",
+                           "pinned host buffers (one output buffer per corpus), wall clock "
+                           "around the call",
                     "single": {"value": e2e_value, "ms_per_step": t_e2e,
                                "gpu_launches": e2e_launches,
                                "api": "ws_sort_text, one corpus per call, CUDA events"}},
             "stats_mode": {"value": world * words / (t_stats * 1e-3), "unit": UNIT,
-                           "ms_per_step": t_stats,
+                           "ms_per_step": t_stats, "roofline_rows": stats_rows,
                            "api": "ws_ingest_text(DEVICE_PTR) + ws_sort(h, 1) + ws_bucket_stats: "
                                   "corpus-order buckets, merge sort counting inversions and K, "
                                   "the reference's SortStats per bucket"},
             "roofline": roofline,
+            "roofline_rows": rows,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches,
             "parity_vs_oracle": parity,
-            "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in agg.items()},
+            "parity_detail": {"resident_output": resident_ok, "single_call": single_ok,
+                              "batch_all_outputs": batch_ok,
+                              "batch_outputs_checked": len(batch_sizes)},
         }
         line["e2e_timeline_ms"] = [[p["name"], round(p["start_ms"], 3), round(p["ms"], 3),
                                     int(p["bytes"])] for p in e2e_phases]
         if args.profile_json:
-            Path(args.profile_json).write_text(json.dumps({"phases": agg, "steps": args.steps,
+            Path(args.profile_json).write_text(json.dumps({"phases": phases, "steps": args.steps,
+                                                           "stats_phases": stats_phases,
                                                            "dev_ms": dev_ms, "e2e_ms": e2e_ms,
                                                            "e2e_phases": e2e_phases},
                                                           indent=1))

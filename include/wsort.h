@@ -177,7 +177,9 @@ typedef struct ws_phase {
   double start_ms;   /* start relative to the first recorded phase            */
 } ws_phase;
 
-/* Record CUDA events around every phase while enabled. */
+/* Record CUDA events around every phase while enabled (on = 1); on = 2 also
+ * runs every kernel on the handle's main stream, so each event pair times one
+ * launch alone (a serialised per-kernel profile). 0 turns both off. */
 int ws_set_profiling(ws_handle* h, int32_t on);
 /* Phases recorded since the last reset (synchronises the handle's stream). */
 int ws_profile(ws_handle* h, ws_phase* out, int32_t cap, int32_t* n);

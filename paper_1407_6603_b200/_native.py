@@ -144,6 +144,25 @@ def ptr(arr) -> int:
     raise TypeError(type(arr))
 
 
+class _DeviceSpan:
+    """A raw device byte range exposed through __cuda_array_interface__."""
+
+    def __init__(self, address: int, size: int):
+        self.__cuda_array_interface__ = {"shape": (size,), "typestr": "|u1",
+                                         "data": (address, False), "version": 3}
+
+
+def device_bytes(address: int, size: int) -> bytes:
+    """Copy `size` bytes at device address `address` (e.g. ws_output_device)
+    back to the host; the caller's work on the library stream must be done."""
+    if size == 0:
+        return b""
+    import torch
+
+    t = torch.as_tensor(_DeviceSpan(address, size), device="cuda")
+    return t.cpu().numpy().tobytes()
+
+
 def device_count() -> int:
     n = ctypes.c_int32(0)
     check(load_library().ws_device_count(ctypes.byref(n)))
@@ -327,8 +346,10 @@ class Handle:
         return int(p.value or 0), int(size.value)
 
     # -- profiling --------------------------------------------------------------
-    def set_profiling(self, on: bool) -> None:
-        check(self.lib.ws_set_profiling(self.h, 1 if on else 0))
+    def set_profiling(self, on: bool | int) -> None:
+        """True / 1: CUDA events around every phase; 2: also serialise the
+        kernels on the main stream (one launch per event pair)."""
+        check(self.lib.ws_set_profiling(self.h, int(on)))
 
     def profile(self, reset: bool = True) -> list[dict]:
         n = ctypes.c_int32(0)

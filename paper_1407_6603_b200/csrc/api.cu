@@ -29,6 +29,7 @@
 #include "wsort.h"
 #include "ws_common.cuh"
 #include "ws_kernels.h"
+#include "plan.cuh"
 
 using namespace ws;
 
@@ -214,6 +215,8 @@ struct ws_handle {
 
   bool prof = false;
   bool serial = false;  // WSORT_SERIAL=1: every kernel on the main stream (diagnostics)
+  bool serial_env = false;  // ... as the environment set it (ws_set_profiling(h, 2) serialises too)
+  size_t early_phase_first = 0;  // profiling: 1 + index of the early launches' first record
   std::vector<PhaseRec> phases;
   std::vector<cudaEvent_t> event_pool;
   uint64_t launches = 0;
@@ -583,7 +586,10 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         }
         d.push_back(r);
         work += pl.ntiles;
-        bytes += (p < 0 ? 1.0 : 2.0) * pl.s->n * kb_bytes;
+        // keys read; keys written, or the payload records of a fused last pass
+        bytes += (double)pl.s->n * kb_bytes;
+        if (p >= 0)
+          bytes += (double)pl.s->n * (r.pay ? (double)(r.len + 1) : (double)kb_bytes);
       }
       RadixLaunch a;
       memset(&a, 0, sizeof a);
@@ -610,7 +616,9 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         WS_CUDA(cudaMemsetAsync(prof.p, 0, (size_t)work * 64, st));
         a.prof = prof.as<unsigned long long>();
       }
-      Phase ph(h, name, bytes, 0, st);
+      char pname[32];
+      snprintf(pname, sizeof pname, p < 0 ? "radix_hist_l%d" : "radix_l%d", lanes);
+      Phase ph(h, pname, bytes, 0, st);
       if (p == 0) tmark("pass0_launch");
       if (p >= 0) {
         launch_radix_onesweep(lanes, a, st);
@@ -706,6 +714,17 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
 // whatever the bucket sizes; the result is in buffer 1.
 // Largest bucket the sample sort keeps at its slot size (the splitter and
 // sample budget: kMaxSplit + 1 slots of half a slot-sort tile).
+// Slots per bucket at most: the splitter budget, and >= 8 samples per splitter.
+// WSORT_SAMPLE_SMAX=k lowers it (tests: forces slots beyond a tile, i.e. the
+// slot sorts' merge-sort route, at small sizes; the merge-path cap below is
+// unchanged, so those buckets stay in the sample sort).
+uint32_t sample_smax(uint32_t pmax) {
+  static const char* e = getenv("WSORT_SAMPLE_SMAX");
+  uint32_t v = std::min<uint32_t>(kMaxSplit + 1, pmax / 8);
+  if (e && atoi(e) >= 1) v = std::min<uint32_t>(v, (uint32_t)atoi(e));
+  return v;
+}
+
 uint64_t sample_bucket_limit(int lanes) {
   return (uint64_t)(kMaxSplit + 1) * (uint64_t)(subsort_tile_size(lanes) / 2);
 }
@@ -722,23 +741,15 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   uint32_t slots = 0, splits = 0, tiles = 0;
   for (auto& s : segs) {
     s.final_buf = 1;
-    // slots of half a slot-sort tile on average; a sample of >= 8 keys per
-    // slot keeps slots beyond the tile (the slower fallback) rare
-    const uint64_t target = (uint64_t)subsort_tile_size(lanes) / 2;  // (measured: T/1.4..T/3 within noise)
-    // one slot only when it fits one slot sort's tile (larger single slots
-    // take the slow block-transposition fallback)
-    uint64_t S = s.n <= 2 * target ? 1 : (s.n + target - 1) / target;
-    S = std::min<uint64_t>(S, std::min<uint64_t>(kMaxSplit + 1, pmax / 8));
+    // slots of half a slot-sort tile on average, one slot when the bucket fits
+    // one slot sort's tile (plan.cuh, shared with sample_split_early_kernel)
+    const SamplePlan pl = sample_plan(s.n, (uint32_t)subsort_tile_size(lanes), pmax, sample_smax(pmax));
     SampleSeg g;
     g.in = s.in_ptr;
     g.key_off = (uint32_t)s.key_off;
     g.n = s.n;
-    g.nsplit = (uint32_t)S - 1;
-    g.m = 0;
-    if (g.nsplit) {  // >= 8 samples per splitter, a power of two (the bitonic sort's size)
-      g.m = 1;
-      while (g.m < 8 * S && 2ull * g.m <= std::min<uint64_t>(pmax, s.n)) g.m *= 2;
-    }
+    g.nsplit = pl.nsplit;
+    g.m = pl.m;
     g.split_off = splits;
     g.slot_base = slots;
     g.tile_begin = tiles;
@@ -755,7 +766,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   }
   if (d.empty() || !tiles) return WS_OK;
   if (d.size() > (size_t)kInlineSegs) return fail(WS_ERR_STATE, "too many buckets in a class");
-  WS_CUDA(h->ss_split[lanes].ensure((size_t)std::max(splits, 1u) * 8 + 64));
+  WS_CUDA(h->ss_split[lanes].ensure((size_t)std::max(splits, 1u) * key_bytes(lanes) + 64));  // full keys
   WS_CUDA(h->ss_slots[lanes].ensure((size_t)slots * 12 + 64));
   WS_CUDA(h->ss_ids[lanes].ensure((size_t)tiles * part_tile_size() * 2 + 64));
   SampleLaunch a;
@@ -773,16 +784,43 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   // the ingest ran this class's split launch (same rules, same stream)
   a.split_done = h->split_early[lanes] ? 1 : 0;
   h->split_early[lanes] = false;
-  double bytes = 0;
-  for (const auto& s : segs) bytes += 5.0 * s.n * key_bytes(lanes);
+  double bytes = 0, nkeys = 0, pay_bytes = 0;
+  for (const auto& s : segs) {
+    bytes += 5.0 * s.n * key_bytes(lanes);
+    nkeys += s.n;
+    pay_bytes += (double)s.n * (h->buckets[s.stat_slot].len + 1);
+  }
   char name[32];
   snprintf(name, sizeof name, "sample_l%d", lanes);
   {
     Phase ph(h, name, bytes, 0, st);
     tmark("ss_launch");
-    launch_sample_sort(lanes, a, st);
+    cudaEvent_t ev[10];  // distinct events per record (ws_profile_reset pools them)
+    if (h->prof)
+      for (auto& e : ev) e = get_event(h);
+    launch_sample_sort(lanes, a, st, h->prof ? ev : nullptr);
     tmark("ss_launched");
     h->launches += 5;
+    if (h->prof) {  // one record per kernel of the chain (kind 2: inside a phase)
+      const double kb = key_bytes(lanes);
+      const double split_b = a.split_done ? 0.0 : 8.0 * kb * std::min<double>(nkeys, 4096.0 * d.size());
+      const struct { const char* nm; double bytes; } k[5] = {
+          {"split", split_b},
+          {"part_count", nkeys * (8.0 + 2.0)},            // first words read, slot ids written
+          {"slot_scan", 8.0 * slots},
+          {"part_scatter", nkeys * (2.0 * kb + 2.0)},     // keys read + written, slot ids read
+          {"subsort", nkeys * kb + (pay ? pay_bytes : nkeys * kb)}};  // keys in, records (or keys) out
+      for (int i = 0; i < 5; ++i) {
+        PhaseRec r;
+        r.name = std::string(k[i].nm) + "_l" + std::to_string(lanes);
+        r.a = ev[2 * i];
+        r.b = ev[2 * i + 1];
+        r.bytes = k[i].bytes;
+        r.launches = (i == 0 && a.split_done) ? 0 : 1;
+        r.kind = 2;
+        h->phases.push_back(r);
+      }
+    }
   }
   WS_TRY(check_launch(name));
   tmark("ss_checked");
@@ -937,8 +975,12 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   e.totals = tb.as<uint32_t>();
   e.joint = e.totals + (size_t)kRadixC0Segs * kRadixMaxPasses * 256 + kRadixMaxPasses;
   e.joint_ok = !env_on("WSORT_NO_JOINT");
-  launch_radix_hist_early(e, cst);
-  ++h->launches;
+  {
+    Phase ph(h, "radix_hist_l0", 0.0, 0, cst);  // bytes patched once the counts are known
+    launch_radix_hist_early(e, cst);
+    ++h->launches;
+    if (h->prof) h->early_phase_first = h->phases.size() + 1;  // this record's index + 1
+  }
   WS_TRY(check_launch("radix_hist_early"));
   h->early_done = true;
   h->early_joint = e.joint_ok != 0;
@@ -951,7 +993,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   for (int c = 1; c <= 3; ++c) {  // 6-bit text keys: lengths 6-10, 11-21, 22-32
     const int lmin = c == 1 ? 6 : (c == 2 ? 11 : 22), lmax = c == 1 ? 10 : (c == 2 ? 21 : 32);
     const int nb = lmax - lmin + 1;
-    WS_CUDA(h->ss_split[c].ensure((size_t)nb * kMaxSplit * 8 + 64));
+    WS_CUDA(h->ss_split[c].ensure((size_t)nb * kMaxSplit * key_bytes(c) + 64));
     WS_CUDA(h->ss_slots[c].ensure((size_t)nb * (2 * kMaxSplit + 1) * 12 + 64));
     cudaStream_t sst = h->serial ? h->st : h->cs[c];
     if (sst != h->st) {
@@ -969,12 +1011,17 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     se.T = (uint32_t)subsort_tile_size(c);  // one slot up to a slot-sort tile (= 2 * target)
     se.target = (uint32_t)subsort_tile_size(c) / 2;
     se.pmax = pmax;
-    se.smax = std::min<uint32_t>(kMaxSplit + 1, pmax / 8);
+    se.smax = sample_smax(pmax);
     se.cap = sample_bucket_limit(c);
     se.splitters = h->ss_split[c].as<uint64_t>();
     se.hist = h->ss_slots[c].as<uint32_t>();
-    launch_sample_split_early(c, se, sst);
-    ++h->launches;
+    {
+      char nm[16];
+      snprintf(nm, sizeof nm, "split_l%d", c);
+      Phase ph(h, nm, 0.0, 0, sst);
+      launch_sample_split_early(c, se, sst);
+      ++h->launches;
+    }
     h->split_early[c] = true;
   }
   WS_TRY(check_launch("sample_split_early"));
@@ -1171,6 +1218,24 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     tmark("synced");
     WS_TRY(plan_packed(h, counts));  // compact layout of the sort buffers
     tmark("planned");
+    if (h->prof && h->early_phase_first) {  // bytes of the device-planned early launches
+      for (size_t i = h->early_phase_first - 1; i < h->phases.size(); ++i) {
+        PhaseRec& r = h->phases[i];
+        double b = r.bytes;
+        if (r.name == "radix_hist_l0") {
+          b = 0;
+          for (int L = 1; L <= 5; ++L) b += 4.0 * (double)counts[L - 1];  // keys read once
+        } else if (r.name.rfind("split_l", 0) == 0) {
+          const int c = r.name[7] - '0';
+          b = 0;
+          for (int L = 1; L <= kMaxPackedLen; ++L)  // sampled keys read
+            if (lanes_for_len_enc(L, h->enc) == c && counts[L - 1])
+              b += (double)key_bytes(c) * std::min<double>((double)counts[L - 1], 4096.0);
+        }
+        r.bytes = b;
+      }
+      h->early_phase_first = 0;
+    }
     if (ordered_reserve && nchunks) {
       // corpus order: runs of every (bin, chunk) move from their reserved place
       // to the exclusive prefix of their bin over chunks, in the compact layout
@@ -1867,7 +1932,7 @@ int ws_create(ws_handle** out, int32_t device) {
   ws_handle* h = new ws_handle();
   h->device = device;
   const char* ser = getenv("WSORT_SERIAL");
-  h->serial = ser && ser[0] == '1';
+  h->serial = h->serial_env = ser && ser[0] == '1';
   // Priorities: class 0's radix chain (four dependent passes of small
   // kernels) is the longest path, so its stream (and every emit / copy
   // stream) outranks the multi-lane classes' sort streams.
@@ -2248,6 +2313,9 @@ int ws_sort_blocks(int32_t nblocks, uint8_t* const* rows, const int64_t* counts,
 int ws_set_profiling(ws_handle* h, int32_t on) {
   if (!h) return fail(WS_ERR_ARG, "null handle");
   h->prof = on != 0;
+  // 2: also run every kernel on the main stream, so each event pair brackets
+  // its own launch alone (serialised, like an ncu launch list)
+  h->serial = on == 2 ? true : h->serial_env;
   return WS_OK;
 }
 

@@ -40,6 +40,7 @@
 #include "ws_kernels.h"
 #include "payload.cuh"
 #include "tma.cuh"
+#include "plan.cuh"
 
 namespace ws {
 
@@ -574,52 +575,86 @@ __device__ __forceinline__ const SampleSeg& sseg_at(const SampleLaunch& a, int i
   return a.segs ? a.segs[i] : a.inl[i];
 }
 
-// 64-bit prefix of a key (its first word; class 0 keys are not sample-sorted).
+// Slot of a key among nsplit sorted full-key splitters: 2j for keys strictly
+// between splitters j-1 and j, 2j + 1 for a key equal to splitter j. `sp`
+// holds the splitters' first words (shared memory), `spk` the full splitters
+// (global, NW words each). The first-word search decides almost every key;
+// only a key whose first word equals a splitter's loads its remaining words
+// and searches the splitters sharing that word on them.
 template <int LANES>
-__device__ __forceinline__ uint64_t prefix_of(const Key<LANES>& k) {
-  return (uint64_t)k.w[0];
-}
-
-// Slot of a prefix among nsplit sorted splitters: 2j for prefixes strictly
-// between splitters j-1 and j, 2j + 1 for a prefix equal to splitter j.
-__device__ __forceinline__ uint32_t slot_of(const uint64_t* sp, uint32_t nsplit, uint64_t p) {
-  uint32_t lo = 0, len = nsplit;  // lower bound: first splitter >= p
+__device__ __forceinline__ uint32_t slot_of(const uint64_t* sp, const uint64_t* __restrict__ spk,
+                                            uint32_t nsplit, uint64_t p,
+                                            const KW<LANES>* __restrict__ in, uint64_t i) {
+  uint32_t lo = 0, len = nsplit;  // lower bound: first splitter with first word >= p
   while (len > 0) {
     const uint32_t half = len >> 1, mid = lo + half;
     const bool less = sp[mid] < p;
     lo = less ? mid + 1 : lo;
     len = less ? len - half - 1 : half;
   }
-  return 2 * lo + ((lo < nsplit && sp[lo] == p) ? 1u : 0u);
+  if (lo >= nsplit || sp[lo] != p) return 2 * lo;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  if constexpr (NW == 1) {
+    return 2 * lo + 1;
+  } else {
+    uint32_t hi = lo + 1, l2 = nsplit - hi;  // first splitter with first word > p
+    while (l2 > 0) {
+      const uint32_t half = l2 >> 1, mid = hi + half;
+      const bool le = sp[mid] <= p;
+      hi = le ? mid + 1 : hi;
+      l2 = le ? l2 - half - 1 : half;
+    }
+    const Key<LANES> k = gld<LANES>(in, (int64_t)i);
+    uint32_t a = lo, l3 = hi - lo;  // first splitter in [lo, hi) >= k
+    while (l3 > 0) {
+      const uint32_t half = l3 >> 1, mid = a + half;
+      const bool less = key_lt<LANES>(gld<LANES>(reinterpret_cast<const KW<LANES>*>(spk), mid), k);
+      a = less ? mid + 1 : a;
+      l3 = less ? l3 - half - 1 : half;
+    }
+    const bool eq = a < hi && !key_lt<LANES>(k, gld<LANES>(reinterpret_cast<const KW<LANES>*>(spk), a));
+    return 2 * a + (eq ? 1u : 0u);
+  }
 }
 
-// One CTA per bucket: prefixes of an evenly spaced sample (padded with
-// all-ones to 4096) -> bitonic sort -> the nsplit splitters. Element i =
-// 128 w + 32 q + lane lives in register q of lane `lane` of warp w, so strides
-// below 32 are shuffles, 32 and 64 are register swaps, and only strides of
-// 128 and more (15 of the 78 stages) go through shared memory.
+// One CTA per bucket: the full keys of an evenly spaced sample (padded with
+// all-ones to 4096) -> bitonic sort -> the nsplit splitters, full keys too, so
+// keys that share their first word (timestamps, IDs, URLs) are split like any
+// others. Element i = 128 w + 32 q + lane lives in register set q of lane
+// `lane` of warp w, so strides below 32 are shuffles, 32 and 64 are register
+// swaps, and only strides of 128 and more (15 of the 78 stages) go through
+// shared memory (kBitonicN keys of the class's width, dynamic).
 constexpr int kBitonicN = 4096;
-static_assert(kBitonicN == kSampleThreads * 4, "4 prefixes per thread");
+static_assert(kBitonicN == kSampleThreads * 4, "4 keys per thread");
+
+template <int LANES>
+constexpr size_t split_smem_bytes() { return (size_t)kBitonicN * key_bytes(LANES); }
 
 // The splitters of one bucket (all threads of a 1024-thread CTA); also zeroes
 // the bucket's slot counters for the count pass.
 template <int LANES>
 __device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __restrict__ splitters,
-                                             uint32_t* __restrict__ hist, uint64_t* sm) {
+                                             uint32_t* __restrict__ hist, Key<LANES>* sm) {
   for (uint32_t i = threadIdx.x; i < 2 * sg.nsplit + 1; i += kSampleThreads)
     hist[sg.slot_base + i] = 0;  // the bucket's slot counters (the count pass follows)
   if (!sg.nsplit) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const KW<LANES>* in = kv<LANES>(sg.in);
   constexpr int NW = KeyTraits<LANES>::NW;
-  uint64_t x[4];
+  Key<LANES> x[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint32_t i = w * 128 + q * 32 + lane;
-    x[q] = i < sg.m ? (uint64_t)__ldg(in + ((uint64_t)i * sg.n / sg.m) * NW) : ~0ull;
+    x[q] = i < sg.m ? gld<LANES>(in, (int64_t)((uint64_t)i * sg.n / sg.m)) : key_max<LANES>();
   }
-  // only the first m (a power of two) prefixes are samples: the network's
-  // stages up to size m sort them (the padding blocks are already sorted)
+  auto cas = [&](Key<LANES>& u, Key<LANES>& v, bool up) {  // ascending when up
+    const bool sw = key_lt<LANES>(v, u) == up;
+    const Key<LANES> a0 = u, b0 = v;
+    u = sw ? b0 : a0;
+    v = sw ? a0 : b0;
+  };
+  // only the first m (a power of two) keys are samples: the network's stages
+  // up to size m sort them (the padding blocks are already sorted)
   const uint32_t P = sg.m < 2 ? 2u : (sg.m > kBitonicN ? (uint32_t)kBitonicN : sg.m);
   for (uint32_t size = 2; size <= P; size <<= 1) {
     for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
@@ -629,8 +664,8 @@ __device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __re
         __syncthreads();
         for (uint32_t t = threadIdx.x; t < kBitonicN / 2; t += kSampleThreads) {
           const uint32_t i = 2 * t - (t & (stride - 1)), j = i + stride;
-          const uint64_t u = sm[i], v = sm[j];
-          if ((v < u) == ((i & size) == 0)) {
+          Key<LANES> u = sm[i], v = sm[j];
+          if (key_lt<LANES>(v, u) == ((i & size) == 0)) {
             sm[i] = v;
             sm[j] = u;
           }
@@ -638,29 +673,25 @@ __device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __re
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < 4; ++q) x[q] = sm[w * 128 + q * 32 + lane];
-      } else if (stride >= 32) {  // partner in another register of the same lane
-        auto cas = [&](uint64_t& u, uint64_t& v, int q) {
-          const bool up = ((uint32_t)(w * 128 + q * 32 + lane) & size) == 0;
-          const bool sw = (v < u) == up;
-          const uint64_t a0 = u, b0 = v;
-          u = sw ? b0 : a0;
-          v = sw ? a0 : b0;
-        };
+      } else if (stride >= 32) {  // partner in another register set of the same lane
         if (stride == 64) {
-          cas(x[0], x[2], 0);
-          cas(x[1], x[3], 1);
+          cas(x[0], x[2], ((uint32_t)(w * 128 + lane) & size) == 0);
+          cas(x[1], x[3], ((uint32_t)(w * 128 + 32 + lane) & size) == 0);
         } else {
-          cas(x[0], x[1], 0);
-          cas(x[2], x[3], 2);
+          cas(x[0], x[1], ((uint32_t)(w * 128 + lane) & size) == 0);
+          cas(x[2], x[3], ((uint32_t)(w * 128 + 64 + lane) & size) == 0);
         }
       } else {  // partner in another lane of the warp
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint32_t i = w * 128 + q * 32 + lane;
           const bool up = (i & size) == 0, lower = (lane & stride) == 0;
-          const uint64_t y = __shfl_xor_sync(0xffffffffu, x[q], (int)stride);
-          const uint64_t lo = x[q] < y ? x[q] : y, hi = x[q] < y ? y : x[q];
-          x[q] = (lower == up) ? lo : hi;
+          Key<LANES> y;
+#pragma unroll
+          for (int l = 0; l < NW; ++l) y.w[l] = __shfl_xor_sync(0xffffffffu, x[q].w[l], (int)stride);
+          const bool lt = key_lt<LANES>(x[q], y);
+          const bool keep = (lower == up) == lt;  // lower==up wants the smaller one
+          x[q] = keep ? x[q] : y;
         }
       }
     }
@@ -668,27 +699,29 @@ __device__ __forceinline__ void split_bucket(const SampleSeg& sg, uint64_t* __re
 #pragma unroll
   for (int q = 0; q < 4; ++q) sm[w * 128 + q * 32 + lane] = x[q];
   __syncthreads();
-  uint64_t* sp = splitters + sg.split_off;
-  for (uint32_t k = threadIdx.x; k < sg.nsplit; k += kSampleThreads)
-    sp[k] = sm[(uint64_t)(k + 1) * sg.m / (sg.nsplit + 1)];
+  uint64_t* sp = splitters + (uint64_t)sg.split_off * NW;
+  for (uint32_t k = threadIdx.x; k < sg.nsplit; k += kSampleThreads) {
+    const Key<LANES> v = sm[(uint64_t)(k + 1) * sg.m / (sg.nsplit + 1)];
+#pragma unroll
+    for (int l = 0; l < NW; ++l) sp[(uint64_t)k * NW + l] = (uint64_t)v.w[l];
+  }
 }
 
 
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __grid_constant__ SampleLaunch a) {
   pdl_wait();
-  __shared__ uint64_t sm[kBitonicN];
-  split_bucket<LANES>(sseg_at(a, blockIdx.x), a.splitters, a.hist, sm);
+  extern __shared__ __align__(16) uint64_t dsm[];
+  split_bucket<LANES>(sseg_at(a, blockIdx.x), a.splitters, a.hist, reinterpret_cast<Key<LANES>*>(dsm));
 }
 
 // The split launch planned on the device from the ingest's per-length counts
-// (same rules as sample_sort_segments: slots of half a slot-sort tile, >= 8
-// samples per splitter, buckets beyond the splitter budget left to the merge
-// path), so it runs while the host reads the counts back. CTA b: length
-// lmin + b.
+// (sample_plan, the host's rule; buckets beyond the splitter budget are left
+// to the merge path), so it runs while the host reads the counts back. CTA b:
+// length lmin + b.
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_early_kernel(const __grid_constant__ SplitEarly e) {
-  __shared__ uint64_t sm[kBitonicN];
+  extern __shared__ __align__(16) uint64_t dsm[];
   SampleSeg sg;
   memset(&sg, 0, sizeof sg);
   uint32_t slots = 0, splits = 0;
@@ -696,28 +729,20 @@ __global__ void __launch_bounds__(kSampleThreads) sample_split_early_kernel(cons
   for (int L = e.lmin; L <= e.lmax; ++L) {
     const uint32_t n = e.fill[L - 1];
     if (!n || n > e.cap) continue;
-    uint64_t S = n <= e.T ? 1 : (n + e.target - 1) / e.target;
-    S = S < e.smax ? S : e.smax;
-    const uint32_t nsplit = (uint32_t)S - 1;
-    uint32_t m = 0;
-    if (nsplit) {
-      m = 1;
-      const uint32_t lim = e.pmax < n ? e.pmax : n;
-      while (m < 8 * S && 2ull * m <= lim) m *= 2;
-    }
+    const SamplePlan pl = sample_plan(n, e.T, e.pmax, e.smax);
     if (L == e.lmin + (int)blockIdx.x) {
       sg.in = reinterpret_cast<const uint64_t*>(e.keys_cap + e.region[L - 1]);
       sg.n = n;
-      sg.nsplit = nsplit;
-      sg.m = m;
+      sg.nsplit = pl.nsplit;
+      sg.m = pl.m;
       sg.split_off = splits;
       sg.slot_base = slots;
       mine = true;
     }
-    slots += 2 * nsplit + 1;
-    splits += nsplit;
+    slots += 2 * pl.nsplit + 1;
+    splits += pl.nsplit;
   }
-  if (mine) split_bucket<LANES>(sg, e.splitters, e.hist, sm);
+  if (mine) split_bucket<LANES>(sg, e.splitters, e.hist, reinterpret_cast<Key<LANES>*>(dsm));
 }
 
 __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t tile) {
@@ -754,7 +779,8 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
   const SampleSeg& sg = sseg_at(a, s_seg);
   const uint32_t nslot = 2 * sg.nsplit + 1;
   if (COUNT)  // the scatter pass reads the slots the count pass found
-    for (uint32_t i = tid; i < sg.nsplit; i += kPartThreads) s_split[i] = a.splitters[sg.split_off + i];
+    for (uint32_t i = tid; i < sg.nsplit; i += kPartThreads)
+      s_split[i] = a.splitters[((uint64_t)sg.split_off + i) * KeyTraits<LANES>::NW];
   for (uint32_t i = tid; i < nslot; i += kPartThreads) s_cnt[i] = 0;
   __syncthreads();
   const uint64_t first = (uint64_t)(blockIdx.x - sg.tile_begin) * kPartTile;
@@ -780,7 +806,8 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
     const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
     if (i < sg.n) {
       if (COUNT) {
-        slot[q] = slot_of(s_split, sg.nsplit, prefix_of<LANES>(k[q]));
+        slot[q] = slot_of<LANES>(s_split, a.splitters + (uint64_t)sg.split_off * KeyTraits<LANES>::NW,
+                                 sg.nsplit, (uint64_t)k[q].w[0], in, i);
         ids[q * kPartThreads + tid] = (uint16_t)slot[q];
       }
       rank[q] = atomicAdd(&s_cnt[slot[q]], 1u);
@@ -839,9 +866,9 @@ __global__ void __launch_bounds__(1024) slot_scan_kernel(const __grid_constant__
 }
 
 // One 128-thread CTA per slot: the slot is sorted in place by the tile
-// network of a half-size tile (slots average half of it), or - beyond it, rare
-// - by block odd-even transposition over quarter-size blocks. A prefix-equal
-// slot whose keys are all identical (repeated words) is left as it is.
+// network of a slot-sort tile (slots average half of it), or - beyond it, rare
+// - by an in-CTA merge sort. A key-equal slot (copies of one word) is left as
+// it is (payload: filled with the record pattern).
 constexpr int kSubThreads = 128;
 
 // Fused emission (SampleSeg::pay set: 6-bit text keys, payload mode): the
@@ -886,23 +913,16 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
     if (out) sub_emit<LANES>(base, cnt, L, out, pbuf);
     return;
   }
-  if (((s - sg.slot_base) & 1u) != 0) {  // prefix-equal slot
-    const Key<LANES> k0 = ldk<LANES>(base, 0);
-    bool diff = false;
-    for (uint32_t i = threadIdx.x; i < cnt; i += NT) {  // any key different from the first one
-      const Key<LANES> ki = ldk<LANES>(base, (int)i);
-      diff |= key_lt<LANES>(k0, ki) | key_lt<LANES>(ki, k0);
-    }
-    if (__syncthreads_or(diff) == 0) {  // all copies of one word
-      if constexpr (LANES <= 3)
-        if (out) fill_records_cta<LANES, NT>(k0, cnt, L, out, pbuf);
-      return;
-    }
+  if (((s - sg.slot_base) & 1u) != 0) {  // key-equal slot: copies of one word (full-key splitters)
+    if constexpr (LANES <= 3)
+      if (out) fill_records_cta<LANES, NT>(ldk<LANES>(base, 0), cnt, L, out, pbuf);
+    return;
   }
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
-  auto sort_span = [&](W* g, uint32_t c, bool emit) {  // c <= TS keys at g, sorted in place
+  // c <= TS keys at g sorted on chip, written to d (may be g), or emitted
+  auto sort_span = [&](const W* g, uint32_t c, W* d, bool emit) {
     constexpr int PW = E * NW;  // words per thread: all loads in flight, then the stores
     W v[PW];
 #pragma unroll
@@ -921,21 +941,66 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
       sub_emit<LANES>(sk, c, L, out, pbuf);
       return;
     }
-    for (uint32_t j = threadIdx.x; j < c * NW; j += NT) g[j] = sk[j];
+    for (uint32_t j = threadIdx.x; j < c * NW; j += NT) d[j] = sk[j];
     __syncthreads();
   };
   if (cnt <= (uint32_t)TS) {
-    sort_span(base, cnt, out != nullptr);
+    sort_span(base, cnt, base, out != nullptr);
     return;
   }
-  constexpr uint32_t HB = TS / 2;
-  const uint32_t blocks = (cnt + HB - 1) / HB;
-  for (uint32_t round = 0; round < blocks; ++round)
-    for (uint32_t p = round & 1; p + 1 < blocks; p += 2) {
-      const uint32_t lo = p * HB, hi = min(cnt, (p + 2) * HB);
-      sort_span(base + (uint64_t)lo * NW, hi - lo, false);
+  // A slot beyond one tile (sampling variance, or a sample that misses the
+  // bucket's spread): merge sort in O(cnt log cnt) by this CTA. Tiles of TS
+  // keys are sorted on chip, then merge-path levels ping-pong between the
+  // slot and its scratch: the same range of the bucket's input keys, which no
+  // one reads after the scatter pass. The block pass writes to the side that
+  // makes the last level land in the slot.
+  W* const scratch = const_cast<W*>(kv<LANES>(sg.in)) + (uint64_t)(a.slot_off[s] - sg.key_off) * NW;
+  const uint32_t blocks = (cnt + TS - 1) / TS;
+  int levels = 0;
+  while ((1u << levels) < blocks) ++levels;
+  W* cur = (levels & 1) ? scratch : base;
+  for (uint32_t bk = 0; bk < blocks; ++bk) {
+    const uint32_t lo = bk * TS;
+    sort_span(base + (uint64_t)lo * NW, min((uint32_t)TS, cnt - lo), cur + (uint64_t)lo * NW, false);
+  }
+  __shared__ int64_t s_split;
+  for (uint32_t run = TS; run < cnt; run <<= 1) {
+    W* const nxt = cur == base ? scratch : base;
+    for (uint32_t p0 = 0; p0 < cnt; p0 += 2 * run) {
+      const W* A = cur + (uint64_t)p0 * NW;
+      const uint32_t na = min(run, cnt - p0);
+      const uint32_t nb = cnt - p0 > run ? min(run, cnt - p0 - run) : 0u;
+      const W* B = A + (uint64_t)na * NW;
+      int64_t a0 = 0;
+      for (uint32_t d0 = 0; d0 < na + nb; d0 += TS) {  // one output tile of TS keys per step
+        const uint32_t d1 = min(d0 + (uint32_t)TS, na + nb);
+        if (threadIdx.x < 32) {
+          const int64_t a1 = d1 == na + nb ? (int64_t)na
+                                           : merge_path_search_global<LANES>(A, na, B, nb, d1);
+          if (threadIdx.x == 0) s_split = a1;
+        }
+        __syncthreads();
+        const int64_t a1 = s_split;
+        const int la = (int)(a1 - a0), lb = (int)((d1 - a1) - (d0 - a0));
+        const W* Ag = A + (uint64_t)a0 * NW;
+        const W* Bg = B + (uint64_t)(d0 - a0) * NW;
+        for (int j = threadIdx.x; j < la * NW; j += NT) sk[j] = Ag[j];
+        for (int j = threadIdx.x; j < lb * NW; j += NT) sk[la * NW + j] = Bg[j];
+        __syncthreads();
+        merge_path<LANES, E, false>(sk, la, sk + (size_t)la * NW, lb, nullptr, nullptr,
+                                    min((int)threadIdx.x * E, la + lb), 0, r, ri, inv);
+        __syncthreads();
+        if ((int)threadIdx.x * E < la + lb) regs_to_smem<LANES, E, false>(sk, nullptr, threadIdx.x * E, r, ri);
+        __syncthreads();
+        W* o = nxt + (uint64_t)(p0 + d0) * NW;
+        for (int j = threadIdx.x; j < (la + lb) * NW; j += NT) o[j] = sk[j];
+        __syncthreads();
+        a0 = a1;
+      }
     }
-  if (out) sub_emit<LANES>(base, cnt, L, out, pbuf);  // the block sort's stores are visible to the CTA
+    cur = nxt;
+  }
+  if (out) sub_emit<LANES>(base, cnt, L, out, pbuf);  // the merges' stores are visible to the CTA
 }
 
 // ---- host side ---------------------------------------------------------------------
@@ -968,6 +1033,11 @@ int merge_tile_size(int lanes) {
 template <int LANES, bool STATS>
 static void set_attrs_t() {
   if (!STATS && LANES >= 1) {
+    constexpr int SL = LANES < 1 ? 1 : LANES;
+    cudaFuncSetAttribute(sample_split_kernel<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)split_smem_bytes<SL>());
+    cudaFuncSetAttribute(sample_split_early_kernel<SL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)split_smem_bytes<SL>());
     cudaFuncSetAttribute(subsort_kernel<LANES < 1 ? 1 : LANES>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)subsort_smem_bytes<(LANES < 1 ? 1 : LANES)>());
@@ -1019,19 +1089,27 @@ void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st) {
 }
 
 template <int LANES>
-static void launch_sample_t(const SampleLaunch& a, cudaStream_t st) {
-  uint32_t P = 1;
-  uint32_t mmax = 0;
-  for (int i = 0; i < a.nsegs; ++i) mmax = std::max(mmax, a.inl[i].m);
-  while (P < mmax) P <<= 1;
-  (void)P;
-  (void)mmax;  // every bucket's CTA zeroes its slot counters, sampled or not
-  if (!a.split_done) launch_pdl(sample_split_kernel<LANES>, a.nsegs, kSampleThreads, 0, st, a);
-  // the chain's kernels start while their predecessor drains (pdl_wait first)
+static void launch_sample_t(const SampleLaunch& a, cudaStream_t st, cudaEvent_t* ev) {
+  // every bucket's CTA zeroes its slot counters, sampled or not; the chain's
+  // kernels start while their predecessor drains (pdl_wait first). `ev`
+  // (profiling): 10 events, a start / end pair per launch.
+  auto mark = [&](int i) {  // end of launch i - 1 (ev[2i - 1]), start of launch i (ev[2i])
+    if (!ev) return;
+    if (i > 0) cudaEventRecord(ev[2 * i - 1], st);
+    if (i < 5) cudaEventRecord(ev[2 * i], st);
+  };
+  mark(0);
+  if (!a.split_done)
+    launch_pdl(sample_split_kernel<LANES>, a.nsegs, kSampleThreads, split_smem_bytes<LANES>(), st, a);
+  mark(1);
   launch_pdl(partition_kernel<LANES, true>, a.work_items, kPartThreads, 0, st, a);
+  mark(2);
   launch_pdl(slot_scan_kernel, a.nsegs, 1024, 0, st, a);
+  mark(3);
   launch_pdl(partition_kernel<LANES, false>, a.work_items, kPartThreads, 0, st, a);
+  mark(4);
   launch_pdl(subsort_kernel<LANES>, a.nslots, kSubThreads, subsort_smem_bytes<LANES>(), st, a);
+  mark(5);
 }
 
 int sample_max_keys(int) { return kSampleSmem / 8; }
@@ -1041,19 +1119,19 @@ int subsort_tile_size(int lanes) { return kSubThreads * (lanes <= 1 ? TileCfg<1>
 void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st) {
   const unsigned nb = (unsigned)(e.lmax - e.lmin + 1);
   switch (lanes) {
-    case 1: sample_split_early_kernel<1><<<nb, kSampleThreads, 0, st>>>(e); break;
-    case 2: sample_split_early_kernel<2><<<nb, kSampleThreads, 0, st>>>(e); break;
-    case 3: sample_split_early_kernel<3><<<nb, kSampleThreads, 0, st>>>(e); break;
-    default: sample_split_early_kernel<4><<<nb, kSampleThreads, 0, st>>>(e); break;
+    case 1: sample_split_early_kernel<1><<<nb, kSampleThreads, split_smem_bytes<1>(), st>>>(e); break;
+    case 2: sample_split_early_kernel<2><<<nb, kSampleThreads, split_smem_bytes<2>(), st>>>(e); break;
+    case 3: sample_split_early_kernel<3><<<nb, kSampleThreads, split_smem_bytes<3>(), st>>>(e); break;
+    default: sample_split_early_kernel<4><<<nb, kSampleThreads, split_smem_bytes<4>(), st>>>(e); break;
   }
 }
 
-void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st) {
+void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st, cudaEvent_t* ev) {
   switch (lanes) {
-    case 1: launch_sample_t<1>(a, st); break;
-    case 2: launch_sample_t<2>(a, st); break;
-    case 3: launch_sample_t<3>(a, st); break;
-    default: launch_sample_t<4>(a, st); break;
+    case 1: launch_sample_t<1>(a, st, ev); break;
+    case 2: launch_sample_t<2>(a, st, ev); break;
+    case 3: launch_sample_t<3>(a, st, ev); break;
+    default: launch_sample_t<4>(a, st, ev); break;
   }
 }
 

@@ -131,7 +131,8 @@ void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st);
 int sample_max_keys(int lanes);
 int part_tile_size();
 int subsort_tile_size(int lanes);  // keys one slot-sort CTA sorts in one network
-void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st);
+// ev (profiling, or null): 10 events, a start / end pair around each of the 5 launches
+void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st, cudaEvent_t* ev = nullptr);
 int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);

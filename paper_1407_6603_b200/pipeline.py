@@ -66,11 +66,15 @@ class BatchSorter:
     of them in flight, so one corpus crosses PCIe host->device while earlier
     ones sort and come back (each output is byte-identical to ``sort_text``)."""
 
-    def __init__(self, max_text: int, inflight: int = 3, device: int | None = None):
+    def __init__(self, max_text: int, inflight: int = 3, device: int | None = None,
+                 outputs: int | None = None):
+        """`outputs`: distinct pinned output buffers, used round robin (default
+        `inflight`); job i of a run writes buffer i % outputs."""
         self.handle = Handle(device_index() if device is None else device)
         self.inflight = inflight
         self.text = PinnedBuffer(max_text)
-        self.outs = [PinnedBuffer(payload_bound(max_text)) for _ in range(inflight)]
+        nout = max(inflight, outputs or inflight)
+        self.outs = [PinnedBuffer(payload_bound(max_text)) for _ in range(nout)]
         self._n = 0
 
     def load(self, text: bytes) -> int:
@@ -84,7 +88,7 @@ class BatchSorter:
     def run(self, count: int) -> list[int]:
         """Sort the loaded corpus `count` times as a batch; payload sizes."""
         texts = [self.text.array[: self._n]] * count
-        outs = [self.outs[i % self.inflight].array for i in range(count)]
+        outs = [self.outs[i % len(self.outs)].array for i in range(count)]
         return self.handle.sort_texts(texts, outs, self.inflight)
 
     def payload(self, slot: int, size: int) -> bytes:

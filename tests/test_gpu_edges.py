@@ -409,3 +409,76 @@ def test_counted_short_buckets_every_value_and_hot_words():
     assert sort_text(text) == want
     sparse = b" ".join([b"x"] * 5 + [b"Q1"] * 3 + [b"abcdef"])
     assert sort_text(sparse) == oracle.sort_text(sparse, mode="fast")[0]
+
+
+def test_slot_sort_shared_prefix_200k_is_n_log_n():
+    # 200k distinct 14-character tokens sharing their first 10 characters
+    # (timestamps / IDs): full-key splitters split them like any other words;
+    # before, they all fell into one prefix-equal slot sorted by block
+    # odd-even transposition, O((n / T)^2) tile sorts on one CTA.
+    import time
+
+    import torch
+
+    from paper_1407_6603_b200._native import Handle
+
+    rng2 = np.random.default_rng(7)
+    words = [bytes(b"2024102010" + bytes(r)) for r in
+             np.frombuffer(synth.ALNUM, np.uint8)[rng2.integers(0, 62, size=(200_000, 4))]]
+    assert len(set(words)) > 190_000
+    rng2.shuffle(words)
+    text = b" ".join(words)
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
+    h = Handle(0)
+    h.ingest_text(text, unordered=True)
+    for _ in range(2):
+        h.sort_resident(len(text))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h.sort_resident(len(text))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    from paper_1407_6603_b200._native import device_bytes
+
+    assert device_bytes(*h.output_device()) == want
+    h.close()
+    assert dt < 5e-3, f"shared-prefix bucket took {dt * 1e3:.2f} ms"
+
+
+_MERGE_ROUTE = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+from oracle import oracle
+from paper_1407_6603_b200 import synth
+from paper_1407_6603_b200.pipeline import sort_text
+rng = np.random.default_rng(9)
+al = np.frombuffer(synth.ALNUM, np.uint8)
+words = []
+for L, n in ((7, 30000), (9, 4001), (12, 25000), (16, 7000), (23, 9001), (31, 2500)):
+    words += [bytes(r) for r in al[rng.integers(0, 62, size=(n, L))]]
+words += [b"Repeatedword"] * 5000 + [b"samewordx"] * 3000
+rng.shuffle(words)
+text = b" ".join(words)
+want, _ = oracle.sort_text(text, mode="fast")
+assert sort_text(text) == want
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("smax", ["2", "3", "5"])
+def test_slot_merge_sort_route(smax):
+    # WSORT_SAMPLE_SMAX caps the slots per bucket, so most slots exceed one
+    # slot-sort tile and take the in-CTA merge sort (odd and even level counts,
+    # a partial last pair, key-equal slots of repeated words)
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, WSORT_SAMPLE_SMAX=smax)
+    r = subprocess.run([sys.executable, "-c", _MERGE_ROUTE.format(root=str(root))], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
