@@ -303,9 +303,15 @@ int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev,
   size_t bytes = v.size() * sizeof(T);
   size_t off = (h->param_used + 255) & ~size_t(255);
   if (off + bytes > h->pin_params.cap || off + bytes > h->params.cap) {
-    // growing needs every stream of the handle idle (old staging bytes may be in flight)
+    // growing needs every stream of the handle idle (old staging bytes may be
+    // in flight on any of them: class, emit, copy and upload streams)
     WS_CUDA(cudaStreamSynchronize(h->st));
-    for (int c = 0; c <= kClasses; ++c) WS_CUDA(cudaStreamSynchronize(h->cs[c]));
+    for (int c = 0; c <= kClasses; ++c) {
+      if (h->cs[c]) WS_CUDA(cudaStreamSynchronize(h->cs[c]));
+      if (h->es[c]) WS_CUDA(cudaStreamSynchronize(h->es[c]));
+      if (h->ds[c]) WS_CUDA(cudaStreamSynchronize(h->ds[c]));
+    }
+    if (h->hs) WS_CUDA(cudaStreamSynchronize(h->hs));
     size_t need = std::max<size_t>(2 * (off + bytes), 1 << 20);
     if (need > h->pin_params.cap) {
       h->pin_params.release();
@@ -1067,6 +1073,12 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
                                                              : cudaMemcpyHostToDevice,
                               h->st));
     WS_CUDA(cudaMemsetAsync(static_cast<uint8_t*>(h->text.p) + n, 0, kTextPad, h->st));
+    if (gate_lk.owns_lock()) {  // batch mode: the next corpus may start its upload now
+      cudaEvent_t up = sync_event(h);
+      WS_CUDA(cudaEventRecord(up, h->st));
+      WS_CUDA(cudaEventSynchronize(up));
+      gate_lk.unlock();
+    }
   }
   const uint32_t nchunks = chunk_count(n);
   h->nchunks = nchunks;

@@ -19,6 +19,7 @@
 // A word belongs to the chunk that holds its first byte; a word running past
 // its chunk is measured by scanning forward in global memory (the text is
 // zero padded, and zero is a separator).
+#include <cstdlib>
 #include <type_traits>
 
 #include "ws_common.cuh"
@@ -784,6 +785,221 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
   }
 }
 
+// Payload-mode text ingest, word-parallel (6-bit keys). The per-byte front
+// end classifies and encodes 32 bytes per thread; after it, every per-word
+// step runs on full warps over a per-warp word list instead of one thread per
+// byte segment looping over its own words (which left half of the lanes idle):
+//   A  classify, 6-bit codes -> smem, start / end masks (ends -> smem), warp
+//      scan of the start counts, each thread lists its starts (the only
+//      per-thread loop left: one shared store per word)
+//   C  per listed word: length from the end masks (a word may run into later
+//      segments, rarely past the chunk), bin, rank in the warp's bin (shared
+//      atomic on a warp-private counter); L > 32 goes straight to the long list
+//   D  warp bin-major order: exclusive scan of the warp's 32 bin counts
+//      (lane = bin), every word moved to its bin-major slot (16-bit entries)
+//   CTA  per bin: one global atomic reserves the chunk's run; each warp's
+//      sub-run gets its key address
+//   E  pack + store in warp bin-major order: a 32-word batch spans 1-3 bins,
+//      so lanes store to consecutive addresses and share one packing path.
+// Word starts are warp-local byte offsets (0..1023); the CTA's chunk is 8 KiB.
+constexpr int kW6Threads = 256;
+constexpr int kW6Warps = kW6Threads / 32;
+constexpr int kW6SB = 32;                          // bytes per thread
+constexpr int kW6CB = kW6SB * kW6Threads;          // chunk bytes
+constexpr int kW6WB = kW6SB * 32;                  // bytes per warp
+constexpr int kW6MaxWords = kW6WB / 2;             // words per warp at most
+constexpr uint32_t kW6Long = 0x80000000u;          // word-list flag: L > 32 (done in C)
+constexpr int kW6OrdCap = kW6MaxWords + 4 * 32;    // + each lane class padded to 32 entries
+constexpr uint16_t kW6Pad = 0xFFFFu;               // padding entry of ord
+
+struct W6Smem {
+  uint32_t codes[(kW6CB + 64) / 4];                // 6-bit codes, one byte per text byte
+  uint32_t ends[kW6Threads + 1];                   // per-thread end masks (+ a zero one)
+  uint32_t wl[kW6Warps][kW6MaxWords];              // word list: start | bin << 10 | pos << 15
+  uint16_t ord[kW6Warps][kW6OrdCap];               // class-aligned bin-major: start | bin << 10
+  uint32_t wcnt[kW6Warps][32];                     // per-warp bin counters
+  uint32_t wboff[kW6Warps][32];                    // per-warp bin-major offsets
+  unsigned long long dst[kW6Warps][32];            // key address of (warp, bin) slot 0
+  uint32_t edge_first[kW6Warps], edge_last[kW6Warps];  // alnum masks of lanes 0 / 31
+  uint32_t wtot[kW6Warps];
+};
+
+// Length of a word that runs past the end of its thread's segment (rare path):
+// `len` bytes so far, continuing at segment t.
+__device__ __noinline__ uint32_t w6_long_tail(const W6Smem& sm, uint32_t t, uint32_t len,
+                                              const uint8_t* __restrict__ text, uint64_t cbase,
+                                              uint64_t avail, unsigned int* overflow) {
+  for (; t < (uint32_t)kW6Threads; ++t) {
+    const uint32_t e = sm.ends[t];
+    if (e) return len + (uint32_t)__ffs(e);
+    len += 32;
+  }
+  return len + run_length_from(text, cbase + kW6CB, avail, overflow);
+}
+
+__global__ void __launch_bounds__(kW6Threads)
+ingest6_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
+  extern __shared__ __align__(16) uint8_t w6_raw[];
+  W6Smem& sm = *reinterpret_cast<W6Smem*>(w6_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t chunk = p.chunk0 + blockIdx.x;
+  const uint64_t cbase = chunk * kW6CB;
+  const uint64_t base = cbase + (uint64_t)tid * kW6SB;
+  const uint64_t avail = p.avail ? p.avail : ~0ull;
+
+  // ---- A: classify, codes, masks ------------------------------------------------
+  uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+  if (base < n) {
+    v0 = WS_TEXT_LD(reinterpret_cast<const uint4*>(text + base));
+    v1 = WS_TEXT_LD(reinterpret_cast<const uint4*>(text + base) + 1);
+  }
+  const uint32_t m = alnum_mask16(v0) | (alnum_mask16(v1) << 16);
+  reinterpret_cast<uint4*>(sm.codes)[2 * tid] = alnum6_codes16(v0);
+  reinterpret_cast<uint4*>(sm.codes)[2 * tid + 1] = alnum6_codes16(v1);
+  if (tid < 4) {  // codes of the bytes after the chunk (words crossing its end)
+    const uint64_t a = cbase + kW6CB + 16 * tid;
+    const uint4 la = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4*>(sm.codes)[kW6CB / 16 + tid] = alnum6_codes16(la);
+  }
+  for (int i = tid; i < kW6Warps * 32; i += kW6Threads) (&sm.wcnt[0][0])[i] = 0;
+  if (tid == 0) sm.ends[kW6Threads] = 0;  // past the chunk: the rare path measures in global memory
+  if (lane == 0) sm.edge_first[wid] = m;
+  if (lane == 31) sm.edge_last[wid] = m;
+  uint32_t prev = __shfl_up_sync(0xffffffffu, m, 1) >> 31;
+  uint32_t next = __shfl_down_sync(0xffffffffu, m, 1) & 1u;
+  uint32_t gprev = 0, gnext = 0;  // the chunk's outer neighbours (global bytes)
+  if (tid == 0 && base > 0 && base - 1 < n) gprev = is_alnum_byte(text[base - 1]);
+  if (tid == kW6Threads - 1 && base + kW6SB < n) gnext = is_alnum_byte(text[base + kW6SB]);
+  __syncthreads();  // #1: codes, edge masks, zeroed counters
+  if (lane == 0) prev = wid == 0 ? gprev : sm.edge_last[wid - 1] >> 31;
+  if (lane == 31) next = wid == kW6Warps - 1 ? gnext : sm.edge_first[wid + 1] & 1u;
+  const uint32_t starts = m & ~((m << 1) | prev);
+  sm.ends[tid] = m & ~((m >> 1) | (next << 31));
+  const uint32_t c = __popc(starts);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  const uint32_t ww = __shfl_sync(0xffffffffu, incl, 31);  // words of the warp
+  {
+    uint32_t slot = incl - c;
+    for (uint32_t s = starts; s; s &= s - 1) sm.wl[wid][slot++] = (uint32_t)(lane * 32 + __ffs(s) - 1);
+  }
+  if (lane == 0) sm.wtot[wid] = ww;
+  __syncthreads();  // #2: every segment's end mask (words run across segments)
+
+  // ---- C: length, bin, rank in the warp's bin -----------------------------------
+  for (uint32_t j0 = 0; j0 < ww; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    if (j < ww) {
+      const uint32_t st = sm.wl[wid][j];
+      const uint32_t t = (uint32_t)wid * 32 + (st >> 5), i = st & 31;
+      // the word ends in its own segment or in the next one (branch-free);
+      // longer runs (and the chunk's last word) take the rare path
+      const uint32_t r = sm.ends[t] >> i, e1 = sm.ends[t + 1];
+      const uint32_t x = r ? r : e1;
+      uint32_t L = (uint32_t)__ffs(x) + (r ? 0u : 32u - i);
+      if (x == 0) L = w6_long_tail(sm, t + 1, 32 - i, text, cbase, avail, p.overflow);
+      if (L <= (uint32_t)kMaxPackedLen) {
+        const uint32_t bin = L - 1;
+        const uint32_t pos = atomicAdd(&sm.wcnt[wid][bin], 1u);
+        sm.wl[wid][j] = st | (bin << 10) | (pos << 15);
+      } else {  // long word: (start, len) straight into the long list (rare)
+        sm.wl[wid][j] = kW6Long;
+        if (p.keys) {
+          const uint32_t at = atomicAdd(p.fill + kLongBin, 1u);
+          p.longlist[at] = make_uint2((uint32_t)(cbase + (uint64_t)wid * kW6WB + st), L);
+        } else {
+          atomicAdd(p.fill + kLongBin, 1u);
+        }
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- D: warp bin-major order, each lane class starting at a multiple of 32 ------
+  // (a batch of 32 entries then holds one class: one packing path, one key width)
+  const uint32_t bc = sm.wcnt[wid][lane];
+  uint32_t binc = bc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, binc, d);
+    if (lane >= d) binc += t;
+  }
+  // lane classes of 6-bit keys: bins 0-4 | 5-9 | 10-20 | 21-31
+  const uint32_t e0 = __shfl_sync(0xffffffffu, binc, 4), e1c = __shfl_sync(0xffffffffu, binc, 9),
+                 e2 = __shfl_sync(0xffffffffu, binc, 20), e3 = __shfl_sync(0xffffffffu, binc, 31);
+  const uint32_t p1 = (e0 + 31) & ~31u, p2 = p1 + ((e1c - e0 + 31) & ~31u),
+                 p3 = p2 + ((e2 - e1c + 31) & ~31u), pend = p3 + ((e3 - e2 + 31) & ~31u);
+  const uint32_t cls = lane < 5 ? 0u : lane < 10 ? 1u : lane < 21 ? 2u : 3u;
+  const uint32_t cstart = cls == 0 ? 0u : cls == 1 ? e0 : cls == 2 ? e1c : e2;   // class's first word (unpadded)
+  const uint32_t cbase_p = cls == 0 ? 0u : cls == 1 ? p1 : cls == 2 ? p2 : p3;  // ... padded
+  const uint32_t wboff = cbase_p + (binc - bc - cstart);
+  sm.wboff[wid][lane] = wboff;
+  for (uint32_t k = lane; k < pend; k += 32) sm.ord[wid][k] = kW6Pad;
+  __syncwarp();
+  for (uint32_t j0 = 0; j0 < ww; j0 += 32) {
+    const uint32_t j = j0 + lane;
+    const uint32_t e = j < ww ? sm.wl[wid][j] : kW6Long;
+    const uint32_t bin = (e >> 10) & 31;
+    const uint32_t off = __shfl_sync(0xffffffffu, wboff, (int)bin);
+    if (!(e & kW6Long)) sm.ord[wid][off + (e >> 15)] = (uint16_t)(e & 0x7FFFu);
+  }
+  __syncthreads();  // #3: every warp's bin counts and offsets
+
+  // ---- CTA: reserve each bin's run, key address of every (warp, bin) sub-run -----------
+  if (tid < 32) {
+    const uint32_t b = tid;
+    uint32_t total = 0;
+#pragma unroll
+    for (int w = 0; w < kW6Warps; ++w) total += sm.wcnt[w][b];
+    uint32_t run = total ? atomicAdd(p.fill + b, total) : 0u;
+    const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc((int)b + 1, kEncAlnum6));
+    const uint64_t bb = p.bin_base[b];
+#pragma unroll
+    for (int w = 0; w < kW6Warps; ++w) {
+      sm.dst[w][b] = bb + ((uint64_t)run - sm.wboff[w][b]) * ks;  // modular: slot k at + k * ks
+      run += sm.wcnt[w][b];
+    }
+    uint32_t words = lane < kW6Warps ? sm.wtot[lane] : 0u;
+    words = __reduce_add_sync(0xffffffffu, words);
+    if (lane == 0 && words) atomicAdd(p.fill + kNumBins, words);
+  }
+  __syncthreads();  // #4
+
+  // ---- E: pack + store, one lane class per batch ------------------------------------
+  if (!p.keys) return;
+  uint8_t* keys = reinterpret_cast<uint8_t*>(p.keys);
+  const uint32_t cw = (uint32_t)wid * kW6WB;
+  for (uint32_t k = lane; k < p1; k += 32) {  // class 0: L <= 5, one uint32
+    const uint32_t e = sm.ord[wid][k];
+    if (e == kW6Pad) continue;
+    const uint32_t st = cw + (e & 1023u), bin = e >> 10;
+    uint64_t key[4];
+    pack6_fast(sm.codes, st, bin + 1, 0, key);
+    *reinterpret_cast<uint32_t*>(keys + sm.dst[wid][bin] + (uint64_t)k * 4) = (uint32_t)(key[0] >> 32);
+  }
+  for (uint32_t k = p1 + lane; k < p2; k += 32) {  // class 1: L 6-10, one uint64
+    const uint32_t e = sm.ord[wid][k];
+    if (e == kW6Pad) continue;
+    const uint32_t st = cw + (e & 1023u), bin = e >> 10;
+    uint64_t key[4];
+    pack6_fast(sm.codes, st, bin + 1, 1, key);
+    *reinterpret_cast<uint64_t*>(keys + sm.dst[wid][bin] + (uint64_t)k * 8) = key[0];
+  }
+  for (uint32_t k = p2 + lane; k < pend; k += 32) {  // classes 2-3: L 11-32, 2-3 uint64
+    const uint32_t e = sm.ord[wid][k];
+    if (e == kW6Pad) continue;
+    const uint32_t st = cw + (e & 1023u), bin = e >> 10, L = bin + 1;
+    const int lanes = lanes_for_len_enc((int)L, kEncAlnum6);
+    uint64_t key[4];
+    pack6_from_codes(sm.codes, st, L, lanes, key);
+    store_key(keys + sm.dst[wid][bin] + (uint64_t)k * key_bytes(lanes), lanes, key);
+  }
+}
+
 // kByReserve follow-up: one CTA per chunk moves the chunk's runs (one per
 // bin) from their reserved place (the bin's ingest region / the long list as
 // filled) to their corpus-order place (run_off = exclusive scan of run_cnt
@@ -977,7 +1193,16 @@ static size_t reserve_smem_bytes() {
   return (size_t)(kReserveSB * kIngestThreads + 64) + (size_t)kReserveSB * kIngestThreads / 2 * 4;
 }
 
+// WSORT_INGEST_V1=1: the segment-loop payload ingest (reserve_ingest_kernel)
+// instead of the word-parallel one (A/B and tests).
+bool ingest6_enabled() {
+  static const bool on = !(getenv("WSORT_INGEST_V1") && getenv("WSORT_INGEST_V1")[0] == '1');
+  return on;
+}
+
 void set_ingest_attributes() {
+  cudaFuncSetAttribute(ingest6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(W6Smem));
   cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncAlnum6>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve_smem_bytes());
   cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncRaw8>,
@@ -989,6 +1214,8 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
   if (!nchunks) return;
   if (p.fill && p.run_at)
     scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
+  else if (p.fill && p.enc == kEncAlnum6 && ingest6_enabled())
+    ingest6_kernel<<<nchunks, kW6Threads, sizeof(W6Smem), st>>>(text, n, p);
   else if (p.fill && p.enc == kEncAlnum6)
     reserve_ingest_kernel<kReserveSB, kEncAlnum6><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(
         text, n, p);
@@ -1000,7 +1227,7 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }
-uint32_t reserve_chunk_bytes() { return kReserveSB * kIngestThreads; }
+uint32_t reserve_chunk_bytes() { return ingest6_enabled() ? kW6CB : kReserveSB * kIngestThreads; }
 
 void launch_reorder_runs(const ReorderParams& r, cudaStream_t st) {
   if (r.nchunks) launch_pdl(reorder_runs_kernel, r.nchunks, kIngestThreads, 0, st, r);

@@ -1091,7 +1091,7 @@ void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st) {
 template <int LANES>
 static void launch_sample_t(const SampleLaunch& a, cudaStream_t st, cudaEvent_t* ev) {
   // every bucket's CTA zeroes its slot counters, sampled or not; the chain's
-  // kernels start while their predecessor drains (pdl_wait first). `ev`
+  // kernels launch as their predecessor exits (PDL; pdl_wait first). `ev`
   // (profiling): 10 events, a start / end pair per launch.
   auto mark = [&](int i) {  // end of launch i - 1 (ev[2i - 1]), start of launch i (ev[2i])
     if (!ev) return;

@@ -139,9 +139,11 @@ __device__ __forceinline__ uint32_t code6_at(const uint64_t* key) {
   }
 }
 
-// Programmatic dependent launch: a kernel launched with launch_pdl may start
-// while its predecessor in the stream drains; it waits here before touching
-// anything the predecessor wrote (a no-op for a normal launch).
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled as soon as every CTA of its predecessor in the stream has exited
+// (no kernel triggers griddepcontrol.launch_dependents early), so what it
+// overlaps is the launch latency, not the predecessor's work; it waits here
+// before touching anything the predecessor wrote (a no-op for a normal launch).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 #ifndef WS_PDL

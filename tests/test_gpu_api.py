@@ -21,7 +21,7 @@ from paper_1407_6603_b200.engine import (
     SchedulePolicy, SortConfig, SortStats, SortVariant, bubble_sort_bucket, sort_all_parallel,
     sort_all_sequential,
 )
-from paper_1407_6603_b200.ingest import load_text, preprocess_stats, tokenize
+from paper_1407_6603_b200.ingest import WORD_RE, load_text, preprocess_stats, tokenize
 from paper_1407_6603_b200.store import (
     LayoutKind, build_buckets, build_flat, build_store, emit_sorted,
 )
@@ -358,3 +358,31 @@ def test_verify_words_all_layouts():
 # test_bench.py (speedup / efficiency arithmetic, CSV / JSON / plot reports,
 # the timing matrix and the `bench` subcommand) is restated in
 # tests/test_harness.py against paper_1407_6603_b200/harness.py.
+
+
+@pytest.mark.parametrize("case", ["config1", "long_words", "chunked"])
+def test_preprocess_device_histogram(tmp_path, case, capsys):
+    # `wordsort preprocess` prints words / lmax / hist from the device's bucket
+    # counts (cli.py:171-181); they must equal the reference tokenizer's
+    from collections import Counter
+
+    from paper_1407_6603_b200 import synth
+    from paper_1407_6603_b200.ingest import preprocess_device
+
+    if case == "config1":
+        text = synth.generate(1)
+    elif case == "long_words":
+        text = b"x" * 40 + b" a bb " + b"Q" * 33 + b"!" + b"q" * 40 + b" " + b"z" * 200
+    else:  # > 16 MiB: chunked upload overlapped with the ingest
+        text = synth.generate(4, words=2_400_000, seed=3)
+    p = tmp_path / "in.txt"
+    p.write_bytes(text)
+    want = Counter(len(w) for w in WORD_RE.findall(text))
+    pre = preprocess_device(p)
+    assert pre.hist == dict(want) and pre.words == sum(want.values())
+    assert pre.lmax == max(want)
+    assert pre.timings.load_strip_seconds > 0 and pre.timings.bucket_build_seconds >= 0
+    status, out, _ = run_cli(capsys, "preprocess", p)
+    lines = out.splitlines()
+    assert status == 0 and f"words,{sum(want.values())}" in lines and f"lmax,{max(want)}" in lines
+    assert [ln for ln in lines if ln.startswith("hist,")] == [f"hist,{L},{want[L]}" for L in sorted(want)]

@@ -13,5 +13,6 @@ rm -rf "$ROOT/baseline/_ref"
 python -m pip install --no-index --no-build-isolation --no-deps --find-links /opt/wheelhouse \
     --target "$ROOT/baseline/_ref" "$TMP/pkg" > "$TMP/pip.log" 2>&1 || { cat "$TMP/pip.log"; exit 1; }
 cp -r "$SRC/tests" "$ROOT/baseline/_ref/ref_tests"
+mkdir -p "$ROOT/baseline/_ref/data" && cp -r "$SRC/data/." "$ROOT/baseline/_ref/data/"
 rm -rf "$TMP"
 echo "reference installed: $(ls "$ROOT/baseline/_ref")"
