@@ -503,13 +503,21 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
   const bool rts = rts_env && rts_env[0] == '1';
   static const char* nj_env = getenv("WSORT_NO_JOINT");
   const bool joint_ok = pay && lanes == 0 && !rts && !(nj_env && nj_env[0] == '1');
+  // digit width: the one-sweep passes take 10-bit digits on uint32 keys (the
+  // reduce-then-scan path and uint64 keys 8-bit)
+  const int db = rts ? 8 : radix_digit_bits(lanes);
   for (auto& s : segs) {
     s.final_buf = 0;
     if (!s.n) continue;
     const int bits = std::min(keybits, cbits * (int)h->buckets[s.stat_slot].len);
-    int passes = std::max(1, (bits + 7) / 8);
+    int passes = std::max(1, (bits + db - 1) / db);
     uint32_t jbits = 0;
-    if (joint_ok && bits <= 12) {  // <= 4096 distinct keys: counted, not sorted
+    if (h->enc == kEncAlnum6 && lanes == 0 && !rts) {
+      // 6-bit class-0 buckets: the rule radix_hist_early_kernel plans with (plan.cuh)
+      const RadixPlan rp = radix_plan_c0(h->buckets[s.stat_slot].len, (uint32_t)db, joint_ok, 12u);
+      passes = (int)rp.passes;
+      jbits = rp.jbits;
+    } else if (joint_ok && bits <= 12) {  // <= 4096 distinct keys: counted, not sorted
       jbits = (uint32_t)bits;
       passes = 0;
     }
@@ -526,7 +534,7 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
     // one-sweep: one histogram launch for the digit totals of every pass, then
     // one look-back launch per pass
     const size_t tot_words = (lanes == 0 ? std::max<size_t>(kRadixC0Segs, plan.size()) : plan.size()) *
-                             kRadixMaxPasses * 256;
+                             kRadixMaxPasses * kRadixTotStride;
     // the ingest already ran this histogram launch (same plan rules, same stream)
     const bool early = h->early_done && lanes == 0 && pay && joint_ok == h->early_joint &&
                        plan.size() <= (size_t)kRadixC0Segs;
@@ -552,7 +560,7 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
     DevBuf& sb = h->rstatus[lanes];
     const void* before = sb.p;
     const size_t cap0 = sb.cap;
-    WS_CUDA(sb.ensure((size_t)all_tiles * 256 * 8));
+    WS_CUDA(sb.ensure((size_t)all_tiles * ((size_t)1 << db) * 8));
     if (sb.p != before || sb.cap != cap0) WS_CUDA(cudaMemsetAsync(sb.p, 0, sb.cap, st));  // no stale epochs
     char name[32];
     snprintf(name, sizeof name, "radix_l%d", lanes);
@@ -574,7 +582,7 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
         r.n = pl.s->n;
         r.tile_begin = work;
         r.ntiles = pl.ntiles;
-        r.shift = pl.shift0 + 8 * std::max(p, 0);
+        r.shift = pl.shift0 + (uint32_t)db * std::max(p, 0);
         r.sid = (uint32_t)i;
         r.passes = (uint32_t)pl.passes;
         if (p < 0 && pl.jbits) {
@@ -960,7 +968,8 @@ bool early_hist_wanted() {
 }
 
 size_t radix_c0_zero_bytes() {  // totals + tickets + whole-key counters of class 0
-  return ((size_t)kRadixC0Segs * kRadixMaxPasses * 256 + kRadixMaxPasses + (2u << 6) + (2u << 12)) * 4;
+  return ((size_t)kRadixC0Segs * kRadixMaxPasses * kRadixTotStride + kRadixMaxPasses + (2u << 6) +
+          (2u << 12)) * 4;
 }
 
 int launch_early_hist(ws_handle* h, const uint64_t* region) {
@@ -979,7 +988,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   e.keys_cap = h->keys_cap.as<uint8_t>();
   for (int b = 0; b < 5; ++b) e.region[b] = region[b];
   e.totals = tb.as<uint32_t>();
-  e.joint = e.totals + (size_t)kRadixC0Segs * kRadixMaxPasses * 256 + kRadixMaxPasses;
+  e.joint = e.totals + (size_t)kRadixC0Segs * kRadixMaxPasses * kRadixTotStride + kRadixMaxPasses;
   e.joint_ok = !env_on("WSORT_NO_JOINT");
   {
     Phase ph(h, "radix_hist_l0", 0.0, 0, cst);  // bytes patched once the counts are known

@@ -19,9 +19,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "ws_common.cuh"
 #include "ws_kernels.h"
 #include "payload.cuh"
+#include "plan.cuh"
 
 namespace ws {
 namespace {
@@ -39,6 +42,24 @@ struct RadixCfg {
   static constexpr int E = sizeof(K) == 4 ? WS_RADIX_E4 : 8;  // keys per thread
   static constexpr int T = kRThreads * E;            // keys per tile
 };
+
+// One-sweep digit width: 10-bit digits for uint32 keys (a 30-bit 6-bit text
+// key of 5 characters takes 3 passes instead of 4, 18-24 bits take 2-3), 8
+// bits for uint64 keys. A thread owns DPT consecutive digits in the per-tile
+// digit phases; per-warp digit counters are 16-bit beyond 256 digits (a tile
+// holds < 2^16 keys).
+#ifndef WS_OS_DB4
+#define WS_OS_DB4 8  // 10 (3 passes of 30-bit keys instead of 4) measured slower: the 1024-digit look-back and scans cost more than a pass
+#endif
+template <class K>
+struct OsCfg {
+  static constexpr int DB = sizeof(K) == 4 ? WS_OS_DB4 : 8;
+  static constexpr int ND = 1 << DB;
+  static constexpr int DPT = ND / kRThreads;
+  using WC = typename std::conditional<(ND > 256), uint16_t, uint32_t>::type;
+};
+static_assert(OsCfg<uint32_t>::ND <= kRadixTotStride && OsCfg<uint32_t>::DPT >= 1, "digits");
+static_assert(RadixCfg<uint32_t>::T < (1 << 16), "16-bit digit counters");
 
 __device__ __forceinline__ const RadixSeg& rseg_at(const RadixLaunch& a, int i) {
   return a.segs ? a.segs[i] : a.inl[i];
@@ -119,21 +140,23 @@ struct RankSetter<E, E> {
   __device__ __forceinline__ static void set(Ranks<E>&, int, uint32_t) {}
 };
 
-template <class K, int E>
+template <class K, int E, int ND = kDigits, class WC = uint32_t>
 __device__ __forceinline__ void warp_rank(const K (&key)[E], uint32_t nvalid, uint32_t shift,
-                                          uint32_t* wcnt, Ranks<E>& rk) {
+                                          WC* wcnt, Ranks<E>& rk) {
   const int lane = threadIdx.x & 31;
   const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const bool ok = (uint32_t)(r * 32 + lane) < nvalid;
-    const uint32_t d = digit_of<K>(key[r], shift);
-    const uint32_t peers = match_digit8(d, ok);
+    const uint32_t d = (uint32_t)(key[r] >> shift) & (uint32_t)(ND - 1);
+    static_assert(ND == 256 || WS_MATCH_ANY, "ballot matching is 8-bit");
+    const uint32_t peers = WS_MATCH_ANY ? __match_any_sync(0xffffffffu, ok ? d : 0x10000u + lane)
+                                        : match_digit8(d, ok);
     uint32_t base = 0;
     if (ok) base = wcnt[d];
     RankSetter<0, E>::set(rk, r, base + __popc(peers & lt));
     __syncwarp();
-    if (ok && lane == 31 - __clz(peers)) wcnt[d] = base + __popc(peers);
+    if (ok && lane == 31 - __clz(peers)) wcnt[d] = (WC)(base + __popc(peers));
     __syncwarp();
   }
 }
@@ -317,6 +340,9 @@ constexpr uint64_t kStEpochMask = ~0x3FFFFFFFFull;
 #define WS_LOOK_W 4
 #endif
 constexpr int kLookW = WS_LOOK_W;  // predecessors loaded per look-back round
+#ifndef WS_LOOK_BACKOFF
+#define WS_LOOK_BACKOFF 0  // ns to sleep after a look-back round that found nothing new (0: spin)
+#endif
 #ifndef WS_OS_MINB
 #define WS_OS_MINB 3  // 80 registers, no spills (4: 64 with spills, measured slower)
 #endif
@@ -355,11 +381,13 @@ template <class K>
 __device__ __forceinline__ void hist_tile(const RadixSeg& sg, uint32_t t, uint32_t* sm,
                                           uint32_t* __restrict__ totals, uint32_t* __restrict__ joint) {
   using C = RadixCfg<K>;
-  constexpr int kP = (int)sizeof(K);  // at most one pass per key byte
-  uint32_t (*hist)[kDigits] = reinterpret_cast<uint32_t (*)[kDigits]>(sm);
+  using O = OsCfg<K>;
+  constexpr int ND = O::ND;
+  constexpr int kP = (8 * (int)sizeof(K) + O::DB - 1) / O::DB;  // passes of a full-width key
+  uint32_t (*hist)[ND] = reinterpret_cast<uint32_t (*)[ND]>(sm);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t jbits = sizeof(K) == 4 ? sg.jbits : 0u;
-  const int nzero = jbits ? (1 << jbits) : kP * kDigits;
+  const int nzero = jbits ? (1 << jbits) : kP * ND;
   for (int i = tid; i < nzero; i += kRThreads) sm[i] = 0;
   __syncthreads();
   const uint64_t first = (uint64_t)t * C::T + (uint64_t)wid * 32 * C::E;
@@ -383,16 +411,18 @@ __device__ __forceinline__ void hist_tile(const RadixSeg& sg, uint32_t t, uint32
 #pragma unroll
     for (int p = 0; p < kP; ++p) {
       if (p >= passes) break;
-      const uint32_t sh = sg.shift + 8 * p;
+      const uint32_t sh = sg.shift + O::DB * p;
 #pragma unroll
       for (int r = 0; r < C::E; ++r)
-        if ((uint32_t)(r * 32 + lane) < nvalid) atomicAdd(&hist[p][digit_of<K>(key[r], sh)], 1u);
+        if ((uint32_t)(r * 32 + lane) < nvalid)
+          atomicAdd(&hist[p][(uint32_t)(key[r] >> sh) & (uint32_t)(ND - 1)], 1u);
     }
     __syncthreads();
-    for (int p = 0; p < passes; ++p) {
-      const uint32_t c = hist[p][tid];
-      if (c) atomicAdd(totals + ((uint64_t)sg.sid * kRadixMaxPasses + p) * kDigits + tid, c);
-    }
+    for (int p = 0; p < passes; ++p)
+      for (int d = tid; d < ND; d += kRThreads) {
+        const uint32_t c = hist[p][d];
+        if (c) atomicAdd(totals + ((uint64_t)sg.sid * kRadixMaxPasses + p) * kRadixTotStride + d, c);
+      }
   }
   __syncthreads();  // sm is reused by the CTA's next tile
 }
@@ -401,9 +431,10 @@ template <class K>
 __global__ void __launch_bounds__(kRThreads)
 radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
   pdl_wait();
-  constexpr int kP = (int)sizeof(K);
-  constexpr int kSm = kP * kDigits > kJointMax ? kP * kDigits : kJointMax;
-  __shared__ uint32_t sm[kSm];  // hist[kP][256], or the joint counts of a jbits segment
+  using O = OsCfg<K>;
+  constexpr int kP = (8 * (int)sizeof(K) + O::DB - 1) / O::DB;
+  constexpr int kSm = kP * O::ND > kJointMax ? kP * O::ND : kJointMax;
+  __shared__ uint32_t sm[kSm];  // hist[kP][ND], or the joint counts of a jbits segment
   __shared__ int s_seg;
   const uint32_t tile = blockIdx.x;
   if (threadIdx.x < 32) {
@@ -428,21 +459,21 @@ __global__ void __launch_bounds__(kRThreads) radix_hist_early_kernel(const __gri
   for (int b = 0; b < 5; ++b) {
     const uint32_t n = e.fill[b];
     if (!n) continue;
-    const uint32_t bits = 6u * (uint32_t)(b + 1);
+    // plan.cuh: the host plans the same segments with the same rule
+    const RadixPlan pl = radix_plan_c0((uint32_t)b + 1, OsCfg<uint32_t>::DB, e.joint_ok != 0, 12u);
     RadixSeg r;
     memset(&r, 0, sizeof r);
     r.in = e.keys_cap + e.region[b];
     r.n = n;
     r.tile_begin = tiles;
     r.ntiles = (n + T - 1) / T;
-    r.shift = 32u - bits;
+    r.shift = pl.shift;
     r.sid = nseg;
-    r.passes = (bits + 7) / 8;
-    if (e.joint_ok && bits <= 12) {
-      r.jbits = bits;
+    r.passes = pl.passes;
+    if (pl.jbits) {
+      r.jbits = pl.jbits;
       r.joff = joff;
-      joff += 2u << bits;
-      r.passes = 0;
+      joff += 2u << pl.jbits;
     }
     tiles += r.ntiles;
     seg[nseg++] = r;
@@ -538,8 +569,12 @@ __global__ void __launch_bounds__(kRThreads, WS_OS_MINB)
 radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   pdl_wait();
   using C = RadixCfg<K>;
-  __shared__ uint32_t wcnt[kRWarps][kDigits];
-  __shared__ uint32_t s_gdelta[kDigits];  // global offset - tile-local start
+  using O = OsCfg<K>;
+  constexpr int ND = O::ND, DPT = O::DPT;
+  constexpr uint32_t DM = (uint32_t)ND - 1;
+  using WC = typename O::WC;
+  __shared__ __align__(16) WC wcnt[kRWarps][ND];
+  __shared__ uint32_t s_gdelta[ND];  // global offset - tile-local start, per digit
   __shared__ uint32_t s_wsum[2][kRWarps];
   __shared__ __align__(16) K stage[C::T];
   __shared__ int s_seg;
@@ -555,7 +590,10 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
       s_tile = tk;
     }
   }
-  for (int i = tid; i < kRWarps * kDigits; i += kRThreads) (&wcnt[0][0])[i] = 0;
+  {
+    uint32_t* w32 = reinterpret_cast<uint32_t*>(&wcnt[0][0]);
+    for (int i = tid; i < (int)(kRWarps * ND * sizeof(WC) / 4); i += kRThreads) w32[i] = 0;
+  }
   __syncthreads();
   const uint32_t tile = s_tile;
   WS_OS_STAMP(0);
@@ -565,8 +603,14 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   const uint64_t first = tfirst + (uint64_t)wid * 32 * C::E;
   const uint32_t nvalid = first < sg.n ? (uint32_t)umin64(sg.n - first, 32 * C::E) : 0u;
   const uint32_t ntile = (uint32_t)umin64(sg.n - tfirst, C::T);
-  // this pass's digit total (-> the digit's base in the segment), early
-  const uint32_t tot = a.totals[((uint64_t)sg.sid * kRadixMaxPasses + a.pass) * kDigits + tid];
+  const int d0 = tid * DPT;  // this thread's digits in the per-tile digit phases
+  // this pass's digit totals (-> the digits' bases in the segment), early
+  uint32_t tot[DPT];
+  {
+    const uint32_t* tp = a.totals + ((uint64_t)sg.sid * kRadixMaxPasses + a.pass) * kRadixTotStride + d0;
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) tot[k] = tp[k];
+  }
   const K* in = reinterpret_cast<const K*>(sg.in) + first;
   K key[C::E];
 #pragma unroll
@@ -575,23 +619,36 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     key[r] = j < nvalid ? __ldcs(in + j) : K(0);
   }
   Ranks<C::E> rk;
-  warp_rank<K, C::E>(key, nvalid, sg.shift, wcnt[wid], rk);
+  warp_rank<K, C::E, ND, WC>(key, nvalid, sg.shift, wcnt[wid], rk);
   __syncthreads();
   WS_OS_STAMP(1);
-  // per digit (thread = digit): exclusive over warps; the tile's count
-  uint32_t run = 0;
+  // per digit: exclusive over warps; the tile's count of the digit
+  uint32_t run[DPT];
 #pragma unroll
-  for (int w = 0; w < kRWarps; ++w) {
-    const uint32_t c = wcnt[w][tid];
-    wcnt[w][tid] = run;
-    run += c;
+  for (int k = 0; k < DPT; ++k) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) {
+      const uint32_t c = wcnt[w][d0 + k];
+      wcnt[w][d0 + k] = (WC)r;
+      r += c;
+    }
+    run[k] = r;
   }
-  uint64_t* status = a.status + (uint64_t)tile * kDigits + tid;
+  uint64_t* status = a.status + (uint64_t)tile * ND + d0;
   const uint64_t ep = (uint64_t)a.epoch << 34;
   const bool head = t == 0;  // the segment's first tile: its prefix is 0
-  st_status(status, ep | (head ? kStInc : kStAgg) | run);
-  // tile-local digit starts and the digits' bases in the segment (two scans)
-  uint32_t inc = run, inc2 = tot;
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) st_status(status + k, ep | (head ? kStInc : kStAgg) | run[k]);
+  // tile-local digit starts and the digits' bases in the segment (two scans
+  // over the ND digits: the thread's own DPT, then across threads)
+  uint32_t lsum = 0, lsum2 = 0;
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) {
+    lsum += run[k];
+    lsum2 += tot[k];
+  }
+  uint32_t inc = lsum, inc2 = lsum2;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
@@ -612,53 +669,94 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     wpre += w < wid ? s_wsum[0][w] : 0u;
     wpre2 += w < wid ? s_wsum[1][w] : 0u;
   }
-  const uint32_t doff = wpre + inc - run;
-  const uint32_t dbase = wpre2 + inc2 - tot;
+  uint32_t doff[DPT], dbase[DPT];
+  {
+    uint32_t x = wpre + inc - lsum, y = wpre2 + inc2 - lsum2;
 #pragma unroll
-  for (int w = 0; w < kRWarps; ++w) wcnt[w][tid] += doff;  // tile-local start of (warp, digit)
+    for (int k = 0; k < DPT; ++k) {
+      doff[k] = x;
+      dbase[k] = y;
+      x += run[k];
+      y += tot[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < DPT; ++k)
+#pragma unroll
+    for (int w = 0; w < kRWarps; ++w) wcnt[w][d0 + k] = (WC)(wcnt[w][d0 + k] + doff[k]);  // (warp, digit) start
   __syncthreads();
   // regroup the tile by digit in shared memory first (keys and ranks are
   // dead before the look-back's loads are in flight)
 #pragma unroll
   for (int r = 0; r < C::E; ++r) {
     const uint32_t j = r * 32 + lane;
-    if (j < nvalid) stage[wcnt[wid][digit_of<K>(key[r], sg.shift)] + rk.get(r)] = key[r];
+    if (j < nvalid) stage[wcnt[wid][(uint32_t)(key[r] >> sg.shift) & DM] + rk.get(r)] = key[r];
   }
-  // look-back over the segment's preceding tiles for this digit: a window of
-  // kLookW predecessors per load round, nearest first; the segment's first
-  // tile is always inclusive, so the walk stops there
+  // look-back over the segment's preceding tiles for this thread's digits: a
+  // window of kLookW predecessors per digit per load round (all loads of a
+  // round in flight together), nearest first; the segment's first tile is
+  // always inclusive, so every walk stops there
   WS_OS_STAMP(2);
-  uint32_t excl = 0;
+  uint32_t excl[DPT];
   uint32_t rounds = 0, stalls = 0;  // diagnostics (WSORT_OS_PROF)
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) excl[k] = 0;
   if (!head) {
-    uint32_t back = 1;  // distance of the nearest predecessor not yet consumed
+    uint32_t back[DPT];
+    bool done[DPT];
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) {
+      back[k] = 1;
+      done[k] = false;
+    }
     for (;;) {
       ++rounds;
-      uint64_t v[kLookW];
+      constexpr int LW = DPT > 1 ? (kLookW / DPT > 1 ? kLookW / DPT : 2) : kLookW;  // loads per digit
+      uint64_t v[DPT][LW];
 #pragma unroll
-      for (int w = 0; w < kLookW; ++w)
-        v[w] = back + w <= t ? ld_status(status - (uint64_t)(back + w) * kDigits) : (ep | kStInc);
-      uint32_t used = 0;
-      bool found = false;
+      for (int k = 0; k < DPT; ++k)
 #pragma unroll
-      for (int w = 0; w < kLookW; ++w) {
-        if (found || used < (uint32_t)w) continue;     // stopped earlier in this window
-        if ((v[w] & kStEpochMask) != ep) continue;     // not yet published in this launch
-        excl += (uint32_t)v[w];
-        found = (v[w] & kStInc) != 0;
-        used = w + 1;
+        for (int w = 0; w < LW; ++w)
+          v[k][w] = (!done[k] && back[k] + w <= t)
+                        ? ld_status(status + k - (uint64_t)(back[k] + w) * ND)
+                        : (ep | kStInc);
+      bool all = true;
+      uint32_t progress = 0;
+#pragma unroll
+      for (int k = 0; k < DPT; ++k) {
+        if (done[k]) continue;
+        uint32_t used = 0;
+        bool found = false;
+#pragma unroll
+        for (int w = 0; w < LW; ++w) {
+          if (found || used < (uint32_t)w) continue;         // stopped earlier in this window
+          if ((v[k][w] & kStEpochMask) != ep) continue;      // not yet published in this launch
+          excl[k] += (uint32_t)v[k][w];
+          found = (v[k][w] & kStInc) != 0;
+          used = w + 1;
+        }
+        done[k] = found;
+        all = all && found;
+        stalls += used < (uint32_t)LW;
+        back[k] += used;
+        progress += used;
       }
-      if (found) break;
-      stalls += used < (uint32_t)kLookW;
-      back += used;
+      if (all) break;
+#if WS_LOOK_BACKOFF
+      // nothing left to read: wait before polling again, so spinning warps
+      // do not take issue slots from the ranking warps of other tiles
+      if (progress == 0) __nanosleep(WS_LOOK_BACKOFF);
+#endif
     }
-    st_status(status, ep | kStInc | (excl + run));
+#pragma unroll
+    for (int k = 0; k < DPT; ++k) st_status(status + k, ep | kStInc | (excl[k] + run[k]));
   }
   if (a.prof && tid == 0) {
     a.prof[(uint64_t)tile * 8 + 5] = rounds;
     a.prof[(uint64_t)tile * 8 + 6] = stalls;
   }
-  s_gdelta[tid] = dbase + excl - doff;
+#pragma unroll
+  for (int k = 0; k < DPT; ++k) s_gdelta[d0 + k] = dbase[k] + excl[k] - doff[k];
   __syncthreads();
   WS_OS_STAMP(3);
   if (sg.pay) {  // the segment's last pass: payload records (characters + '\n') at rank * (L + 1)
@@ -666,7 +764,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     constexpr int kBits = 8 * (int)sizeof(K);
     for (uint32_t i = tid; i < ntile; i += kRThreads) {
       const K k = stage[i];
-      uint8_t* dst = sg.pay + (uint64_t)(s_gdelta[digit_of<K>(k, sg.shift)] + i) * (L + 1);
+      uint8_t* dst = sg.pay + (uint64_t)(s_gdelta[(uint32_t)(k >> sg.shift) & DM] + i) * (L + 1);
       if constexpr (sizeof(K) == 4) {
         // one-word keys: the record (<= 6 bytes) assembled little-endian in a
         // register and written with the fewest aligned stores (1/2/4 bytes)
@@ -720,7 +818,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   K* out = reinterpret_cast<K*>(sg.out);
   for (uint32_t i = tid; i < ntile; i += kRThreads) {
     const K k = stage[i];
-    out[s_gdelta[digit_of<K>(k, sg.shift)] + i] = k;
+    out[s_gdelta[(uint32_t)(k >> sg.shift) & DM] + i] = k;
   }
   if (a.prof) {
     __syncthreads();
@@ -763,6 +861,7 @@ void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st) {
 }
 
 int radix_tile_size(int lanes) { return lanes == 0 ? RadixCfg<uint32_t>::T : RadixCfg<uint64_t>::T; }
+int radix_digit_bits(int lanes) { return lanes == 0 ? OsCfg<uint32_t>::DB : OsCfg<uint64_t>::DB; }
 
 void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st) {
   if (!a.work_items) return;

@@ -145,7 +145,7 @@ struct RadixSeg {
   uint32_t n;
   uint32_t tile_begin;  // first tile (work item) of the segment
   uint32_t ntiles;
-  uint32_t shift;       // bit position of this pass's 8-bit digit (histogram: of pass 0)
+  uint32_t shift;       // bit position of this pass's digit (histogram: of pass 0)
   uint32_t sid;         // one-sweep: the segment's row in the totals table
   uint32_t passes;      // one-sweep histogram: passes of the segment
   uint8_t* pay;         // one-sweep, segment's last pass: write payload records here instead
@@ -154,14 +154,16 @@ struct RadixSeg {
   uint32_t joff;        //   keys of <= 12 bits) into joint[joff ..]; the segment then takes no pass
 };
 constexpr int kRadixMaxPasses = 8;  // one per key byte
+constexpr int kRadixTotStride = 1024;  // one-sweep totals: digits per (segment, pass) row
 struct RadixLaunch {
   const RadixSeg* segs;  // device table when nsegs > kInlineSegs, else nullptr
   int nsegs;
   uint32_t work_items;   // tiles of all segments
   uint32_t* counts;      // per segment [256][ntiles] tile histograms -> offsets
   uint32_t* totals;      // reduce-then-scan: [nsegs][256] digit totals of this pass (zeroed);
-                         // one-sweep: [sid][kRadixMaxPasses][256] (zeroed before the histogram)
-  uint64_t* status;      // one-sweep: [work_items][256] look-back words
+                         // one-sweep: [sid][kRadixMaxPasses][kRadixTotStride] (zeroed before
+                         // the histogram)
+  uint64_t* status;      // one-sweep: [work_items][2^digit bits] look-back words
   uint32_t* ticket;      // one-sweep: this launch's tile counter (zeroed)
   uint32_t epoch;        // one-sweep: unique per launch, < 2^30, != 0
   uint32_t pass;
@@ -171,6 +173,7 @@ struct RadixLaunch {
   RadixSeg inl[kInlineSegs];
 };
 int radix_tile_size(int lanes);
+int radix_digit_bits(int lanes);  // one-sweep digit width of a lane class (10: uint32 keys, 8: uint64)
 void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st);
 void launch_radix_hist(int lanes, const RadixLaunch& a, cudaStream_t st);
 // Class-0 histogram launch planned on the device (6-bit text keys, payload
@@ -179,7 +182,7 @@ struct EarlyHist {
   const uint32_t* fill;     // per-length word counts (bins 0..4 used)
   const uint8_t* keys_cap;  // the ingest's per-length key regions
   uint64_t region[5];       // byte offsets of lengths 1..5 in keys_cap
-  uint32_t* totals;         // [5][kRadixMaxPasses][256], zeroed
+  uint32_t* totals;         // [5][kRadixMaxPasses][kRadixTotStride], zeroed
   uint32_t* joint;          // whole-key counters, zeroed
   int joint_ok;             // count (not sort) keys of <= 12 bits
 };
