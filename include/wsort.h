@@ -186,6 +186,16 @@ int ws_profile(ws_handle* h, ws_phase* out, int32_t cap, int32_t* n);
 int ws_profile_reset(ws_handle* h);
 /* Kernel launches issued by this handle since creation. */
 int ws_launch_count(ws_handle* h, uint64_t* launches);
+
+/* Checked builds (compiled with WS_CHECKED=1; tools/checked_build.sh): every
+ * kernel bounds-checks its computed shared / global indices and records the
+ * first failing line per translation unit instead of faulting. Synchronizes
+ * the device, returns the number of failed checks since the last call (0 in a
+ * release build), the unit (0 ingest, 1 sort, 2 radix, 3 emit) and line of
+ * the first, and clears them. Not part of the reference's interface. */
+int ws_debug_checks(uint64_t* failures, int32_t* first_unit, int32_t* first_line);
+/* 1 when the library was built with WS_CHECKED=1. */
+int ws_checked_build(void);
 /* The handle's CUDA stream (cudaStream_t) for event timing by the caller. */
 int ws_stream(ws_handle* h, void** stream);
 

@@ -37,6 +37,7 @@ EXPORTS = (
     "ws_sort_text", "ws_sort_rows", "ws_sort_blocks", "ws_stats_closed_form",
     "ws_set_profiling", "ws_profile", "ws_profile_reset", "ws_launch_count", "ws_stream",
     "ws_host_alloc", "ws_host_free", "ws_sort_resident", "ws_output_device", "ws_sort_texts",
+    "ws_debug_checks", "ws_checked_build",
 )
 
 
@@ -95,6 +96,8 @@ def _declare(lib) -> None:
         "ws_host_free": (I, [V]),
         "ws_sort_resident": (I, [V, ctypes.c_uint64, c_u64p]),
         "ws_output_device": (I, [V, ctypes.POINTER(V), c_u64p]),
+        "ws_debug_checks": (I, [c_u64p, c_i32p, c_i32p]),
+        "ws_checked_build": (I, []),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -161,6 +164,25 @@ def device_bytes(address: int, size: int) -> bytes:
 
     t = torch.as_tensor(_DeviceSpan(address, size), device="cuda")
     return t.cpu().numpy().tobytes()
+
+
+CHECK_UNITS = ("ingest", "sort", "radix", "emit")
+
+
+def debug_checks() -> tuple[int, str]:
+    """(failed bounds checks since the last call, 'unit:line' of the first) of
+    a checked build (WS_CHECKED=1); (0, '') otherwise. Synchronizes the device."""
+    f = ctypes.c_uint64(0)
+    u = ctypes.c_int32(-1)
+    ln = ctypes.c_int32(0)
+    check(load_library().ws_debug_checks(ctypes.byref(f), ctypes.byref(u), ctypes.byref(ln)),
+          "ws_debug_checks")
+    where = f"{CHECK_UNITS[u.value]}.cu:{ln.value}" if f.value and u.value >= 0 else ""
+    return int(f.value), where
+
+
+def checked_build() -> bool:
+    return bool(load_library().ws_checked_build())
 
 
 def device_count() -> int:

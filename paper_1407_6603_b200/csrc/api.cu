@@ -2372,6 +2372,30 @@ int ws_profile_reset(ws_handle* h) {
   return WS_OK;
 }
 
+int ws_debug_checks(uint64_t* failures, int32_t* first_unit, int32_t* first_line) {
+  if (!failures) return fail(WS_ERR_ARG, "null argument");
+  if (WS_CHECKED && env_on("WSORT_CHECK_SELFTEST")) launch_check_selftest(nullptr);
+  WS_CUDA(cudaDeviceSynchronize());
+  int (*readers[])(unsigned int*, unsigned int*) = {check_reader_ingest, check_reader_sort,
+                                                   check_reader_radix, check_reader_emit};
+  *failures = 0;
+  if (first_unit) *first_unit = -1;
+  if (first_line) *first_line = 0;
+  for (int u = 0; u < 4; ++u) {
+    unsigned int f = 0, line = 0;
+    const int e = readers[u](&f, &line);
+    if (e) return fail_cuda((cudaError_t)e, "ws_debug_checks", __LINE__);
+    if (f && *failures == 0) {
+      if (first_unit) *first_unit = u;
+      if (first_line) *first_line = (int32_t)line;
+    }
+    *failures += f;
+  }
+  return WS_OK;
+}
+
+int ws_checked_build(void) { return WS_CHECKED; }
+
 int ws_launch_count(ws_handle* h, uint64_t* launches) {
   if (!h || !launches) return fail(WS_ERR_ARG, "null argument");
   *launches = h->launches;

@@ -52,6 +52,7 @@ emit_kernel(const __grid_constant__ EmitTable t, uint8_t* __restrict__ out, int 
   const EmitSeg sg = t.segs ? t.segs[s_seg] : t.inl[s_seg];
   const uint64_t w0 = (uint64_t)(blockIdx.x - sg.block_begin) * kEmitWords;
   const int cnt = (int)min((uint64_t)kEmitWords, (uint64_t)sg.n - w0);
+  WS_DCHECK(w0 < sg.n && (uint64_t)cnt * (sg.len + nl) + 16 <= (uint64_t)kEmitBuf);
   const int L = (int)sg.len;
   const int stride = L + nl;
   const uint64_t o0 = sg.out_off + w0 * stride;
@@ -266,5 +267,12 @@ void launch_len_keys(const uint2* words, uint64_t n, uint64_t* keys, cudaStream_
   uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
   len_keys_kernel<<<blocks, 256, 0, st>>>(words, n, keys);
 }
+
+// Checked builds: a kernel whose check always fails, so the detector itself is
+// tested (ws_debug_checks must report it).
+__global__ void check_selftest_kernel() { WS_DCHECK(threadIdx.x != 0); }
+void launch_check_selftest(cudaStream_t st) { check_selftest_kernel<<<1, 32, 0, st>>>(); }
+
+WS_DEFINE_CHECK_READER(check_reader_emit)
 
 }  // namespace ws

@@ -582,6 +582,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     while (s) {
       int i = __ffs(s) - 1;
       s &= s - 1;
+      WS_DCHECK(slot < (uint32_t)kMaxWordsPerWarp);
       wstart[wid][slot] = (uint16_t)(tid * 16 + i);
       wlen[wid][slot] = word_len(seg, i);
       ++slot;
@@ -655,6 +656,7 @@ scatter_kernel(const uint8_t* __restrict__ text, uint64_t n, const uint32_t* __r
     const uint32_t start = wstart[wid][j];
     const uint32_t bin = bin_of_len(L);
     if (bin != (uint32_t)kLongBin) {
+      WS_DCHECK(s_boff[bin] + wcnt[wid][bin] + wpos[wid][j] < s_boff[bin + 1]);
       ord[s_boff[bin] + wcnt[wid][bin] + wpos[wid][j]] = start | (L << 16);
     } else if (p.keys) {
       p.longlist[s_base[kLongBin] + wcnt[wid][kLongBin] + wpos[wid][j]] =
@@ -758,6 +760,8 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
     const uint32_t L = word_len_w<SB>(seg, i), bin = bin_of_len(L);
     const uint32_t at = atomicAdd(&s_cur[bin], 1u);
     const uint32_t start = (uint32_t)(tid * SB + i);
+    WS_DCHECK(bin == (uint32_t)kLongBin ? at < s_cnt[kLongBin] : at < s_boff[kMaxPackedLen]);
+    WS_DCHECK(L >= 1 && L < (1u << 16));
     if (bin != (uint32_t)kLongBin)
       ord[at] = start | (L << 16);
     else if (p.keys)
@@ -775,6 +779,10 @@ reserve_ingest_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParam
       const uint32_t e = ord[k];
       const uint32_t start = e & 0xFFFFu, L = e >> 16;
       const int lanes = lanes_for_len_enc(L, ENC);
+      // the key's slot in its length region stays inside the region's capacity
+      WS_DCHECK(L >= 1 && L <= (uint32_t)kMaxPackedLen && start < (uint32_t)kCB &&
+                k >= s_boff[L - 1] && k < s_boff[L] &&
+                s_base[L - 1] + (k - s_boff[L - 1]) <= (uint32_t)((n + 1) / (L + 1)));
       uint64_t key[4];
       if constexpr (codes)
         pack6_fast(chunk32, start, L, lanes, key);
@@ -1042,6 +1050,7 @@ reorder_runs_kernel(ReorderParams r) {
       if (s_pre[mid] <= k) lo = mid; else hi = mid - 1;
     }
     const uint32_t e = k - s_pre[lo], words = r.key_bytes[lo] >> 2;
+    WS_DCHECK(lo <= kLongBin && k >= s_pre[lo] && k < s_pre[lo + 1]);
     const uint32_t* src =
         reinterpret_cast<const uint32_t*>(r.src[lo]) + (uint64_t)(s_from[lo] + e) * words;
     uint32_t* dst = reinterpret_cast<uint32_t*>(r.dst[lo]) + (uint64_t)(s_to[lo] + e) * words;
@@ -1258,5 +1267,7 @@ void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t*
   uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
   pack_rows_kernel<<<blocks, 256, 0, st>>>(rows, n, width, keys);
 }
+
+WS_DEFINE_CHECK_READER(check_reader_ingest)
 
 }  // namespace ws

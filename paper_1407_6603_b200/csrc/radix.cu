@@ -551,6 +551,7 @@ joint_expand_kernel(const __grid_constant__ RadixLaunch a) {
   const uint32_t c1 = (uint32_t)((uint64_t)c * (part + 1) / kExpandParts);
   if (c1 <= c0) return;
   const uint32_t pre = cnt[(1u << sg.jbits) + v];  // copies of smaller values (joint_scan_kernel)
+  WS_DCHECK((uint64_t)pre + c1 <= sg.n);
   const int L = (int)sg.len;
   Key<0> k0;
   k0.w[0] = v << (32 - sg.jbits);
@@ -690,7 +691,10 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
 #pragma unroll
   for (int r = 0; r < C::E; ++r) {
     const uint32_t j = r * 32 + lane;
-    if (j < nvalid) stage[wcnt[wid][(uint32_t)(key[r] >> sg.shift) & DM] + rk.get(r)] = key[r];
+    if (j < nvalid) {
+      WS_DCHECK(wcnt[wid][(uint32_t)(key[r] >> sg.shift) & DM] + rk.get(r) < ntile);
+      stage[wcnt[wid][(uint32_t)(key[r] >> sg.shift) & DM] + rk.get(r)] = key[r];
+    }
   }
   // look-back over the segment's preceding tiles for this thread's digits: a
   // window of kLookW predecessors per digit per load round (all loads of a
@@ -764,6 +768,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
     constexpr int kBits = 8 * (int)sizeof(K);
     for (uint32_t i = tid; i < ntile; i += kRThreads) {
       const K k = stage[i];
+      WS_DCHECK(s_gdelta[(uint32_t)(k >> sg.shift) & DM] + i < sg.n);
       uint8_t* dst = sg.pay + (uint64_t)(s_gdelta[(uint32_t)(k >> sg.shift) & DM] + i) * (L + 1);
       if constexpr (sizeof(K) == 4) {
         // one-word keys: the record (<= 6 bytes) assembled little-endian in a
@@ -818,6 +823,7 @@ radix_onesweep_kernel(const __grid_constant__ RadixLaunch a) {
   K* out = reinterpret_cast<K*>(sg.out);
   for (uint32_t i = tid; i < ntile; i += kRThreads) {
     const K k = stage[i];
+    WS_DCHECK(s_gdelta[(uint32_t)(k >> sg.shift) & DM] + i < sg.n);
     out[s_gdelta[(uint32_t)(k >> sg.shift) & DM] + i] = k;
   }
   if (a.prof) {
@@ -876,5 +882,7 @@ void launch_radix_pass(int lanes, const RadixLaunch& a, cudaStream_t st) {
     radix_downsweep_kernel<uint64_t><<<a.work_items, kRThreads, 0, st>>>(a);
   }
 }
+
+WS_DEFINE_CHECK_READER(check_reader_radix)
 
 }  // namespace ws

@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(kTileThreads) tile_sort_kernel(const __grid_co
   const SegDesc sd = seg_at(a, find_segment(a, blockIdx.x));
   const uint64_t start = (uint64_t)(blockIdx.x - sd.tile_begin) * T;
   const int cnt = (int)min((uint64_t)T, (uint64_t)sd.n - start);
+  WS_DCHECK(start < sd.n && cnt > 0);
   const W* gin = (sd.in_ptr ? kv<LANES>(sd.in_ptr) : kv<LANES>(a.keys_in) + sd.key_off * NW) +
                  start * NW;
   const Window16 w = window16(gin, (uint32_t)cnt * KB);
@@ -496,6 +497,7 @@ __global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
   const int64_t a1 = (g.d1 == g.na + g.nb) ? g.na : (int64_t)a.splits[2 * item + 2];
   const int64_t b0 = g.d0 - a0, b1 = g.d1 - a1;
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
+  WS_DCHECK(la >= 0 && lb >= 0 && la + lb <= T && a1 <= g.na && b1 <= g.nb);
   const W* Ag = kv<LANES>(a.keys_in) + (sd.key_off + g.pair_base + a0) * NW;
   const W* Bg = kv<LANES>(a.keys_in) + (sd.key_off + g.pair_base + R + b0) * NW;
   const Window16 wa = window16(Ag, (uint32_t)la * KB);
@@ -827,7 +829,11 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
   W* out = kv<LANES>(a.keys_out);
 #pragma unroll
   for (int q = 0; q < kPartPer; ++q)
-    if (slot[q] != 0xFFFFFFFFu) stk<LANES>(out, (int)(s_base[slot[q]] + rank[q]), k[q]);
+    if (slot[q] != 0xFFFFFFFFu) {
+      WS_DCHECK(slot[q] < nslot && s_base[slot[q]] + rank[q] >= sg.key_off &&
+                s_base[slot[q]] + rank[q] < sg.key_off + sg.n);
+      stk<LANES>(out, (int)(s_base[slot[q]] + rank[q]), k[q]);
+    }
 }
 
 // Exclusive scan of each bucket's slot counts (one CTA per bucket), started
@@ -907,6 +913,7 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
   while (b + 1 < a.nsegs && sseg_at(a, b + 1).slot_base <= s) ++b;
   const SampleSeg& sg = sseg_at(a, b);
   W* base = kv<LANES>(a.keys_out) + (uint64_t)a.slot_off[s] * NW;
+  WS_DCHECK(a.slot_off[s] >= sg.key_off && a.slot_off[s] + cnt <= sg.key_off + sg.n);
   const int L = (int)sg.len;
   uint8_t* const out = (LANES <= 3 && sg.pay) ? sg.pay + (uint64_t)(a.slot_off[s] - sg.key_off) * (L + 1) : nullptr;
   if (cnt < 2) {
@@ -982,6 +989,7 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
         __syncthreads();
         const int64_t a1 = s_split;
         const int la = (int)(a1 - a0), lb = (int)((d1 - a1) - (d0 - a0));
+        WS_DCHECK(la >= 0 && lb >= 0 && la + lb <= TS && a1 <= (int64_t)na && d1 - a1 <= nb);
         const W* Ag = A + (uint64_t)a0 * NW;
         const W* Bg = B + (uint64_t)(d0 - a0) * NW;
         for (int j = threadIdx.x; j < la * NW; j += NT) sk[j] = Ag[j];
@@ -1140,5 +1148,7 @@ void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st) {
   const bool stats = a.idx_out != nullptr;
   WS_DISPATCH_LANES(launch_merge_t, lanes, stats, a, st);
 }
+
+WS_DEFINE_CHECK_READER(check_reader_sort)
 
 }  // namespace ws

@@ -139,6 +139,40 @@ __device__ __forceinline__ uint32_t code6_at(const uint64_t* key) {
   }
 }
 
+// Checked builds (make CHECKED=1 -> -DWS_CHECKED=1, tools/checked_build.sh):
+// WS_DCHECK(cond) records the first failing source line of this translation
+// unit in a device flag (no trap: the kernel keeps running and the context
+// stays usable), and ws_debug_checks() (include/wsort.h) reads and clears
+// the flags of every unit. The shipped build compiles the checks away.
+// (compute-sanitizer is closed on the GPU pool; these bounds checks on every
+// computed shared / global index are the memory-safety evidence instead.)
+#ifndef WS_CHECKED
+#define WS_CHECKED 0
+#endif
+namespace {
+__device__ unsigned int g_ws_check[2];  // [0] failures, [1] first failing line (per unit)
+}
+__device__ __forceinline__ void ws_check_fail(unsigned int line) {
+  if (atomicAdd(&g_ws_check[0], 1u) == 0) g_ws_check[1] = line;
+}
+#define WS_DCHECK(cond)                                   \
+  do {                                                    \
+    if (WS_CHECKED && !(cond)) ::ws::ws_check_fail(__LINE__); \
+  } while (0)
+// Host side: failures and first line of this unit's checks since the last call
+// (reads and clears the flag; defined once per unit by WS_DEFINE_CHECK_READER).
+#define WS_DEFINE_CHECK_READER(name)                                              \
+  int name(unsigned int* fails, unsigned int* line) {                            \
+    unsigned int v[2] = {0, 0};                                                   \
+    cudaError_t e = cudaMemcpyFromSymbol(v, g_ws_check, sizeof v);                \
+    if (e != cudaSuccess) return (int)e;                                          \
+    const unsigned int z[2] = {0, 0};                                             \
+    cudaMemcpyToSymbol(g_ws_check, z, sizeof z);                                  \
+    *fails = v[0];                                                                \
+    *line = v[1];                                                                 \
+    return 0;                                                                     \
+  }
+
 // Programmatic dependent launch: a kernel launched with launch_pdl may be
 // scheduled as soon as every CTA of its predecessor in the stream has exited
 // (no kernel triggers griddepcontrol.launch_dependents early), so what it

@@ -44,6 +44,13 @@ struct ReorderParams {
 };
 void launch_reorder_runs(const ReorderParams& r, cudaStream_t st);
 
+// checked builds: per translation unit, failures of WS_DCHECK since the last read
+int check_reader_ingest(unsigned int* fails, unsigned int* line);
+int check_reader_sort(unsigned int* fails, unsigned int* line);
+int check_reader_radix(unsigned int* fails, unsigned int* line);
+int check_reader_emit(unsigned int* fails, unsigned int* line);
+void launch_check_selftest(cudaStream_t st);  // one failing WS_DCHECK (detector self-test)
+
 // ingest.cu
 uint32_t chunk_count(uint64_t n);
 void launch_count(const uint8_t* text, uint64_t n, uint32_t* hist, uint32_t nchunks,

@@ -37,3 +37,19 @@ def config_text(rec: dict) -> bytes:
     if rec.get("prefix_words"):
         text = synth.prefix(text, rec["prefix_words"])
     return text
+
+
+@pytest.fixture(autouse=True)
+def _bounds_checks(request):
+    """With WSORT_CHECKED=1 (a library built by tools/checked_build.sh), every
+    GPU test also asserts that no kernel bounds check failed during it."""
+    yield
+    import os
+
+    if os.environ.get("WSORT_CHECKED") != "1" or request.node.get_closest_marker("gpu") is None:
+        return
+    from paper_1407_6603_b200 import _native
+
+    assert _native.checked_build(), "WSORT_CHECKED=1 but the library is not a checked build"
+    fails, where = _native.debug_checks()
+    assert fails == 0, f"{fails} device bounds checks failed, first at {where}"

@@ -482,3 +482,24 @@ def test_slot_merge_sort_route(smax):
     r = subprocess.run([sys.executable, "-c", _MERGE_ROUTE.format(root=str(root))], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+def test_checked_build_detector_fires():
+    # the bounds-check detector of a checked build (WSORT_CHECKED=1) reports a
+    # deliberately failing check; in a release build there are no checks
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    if os.environ.get("WSORT_CHECKED") != "1":
+        pytest.skip("release build: run under tools/checked_build.sh + WSORT_CHECKED=1")
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1407_6603_b200 import _native\n"
+            "print(_native.debug_checks())\n") % str(Path(__file__).resolve().parent.parent)
+    env = dict(os.environ, WSORT_CHECK_SELFTEST="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    fails, where = eval(r.stdout.strip().splitlines()[-1])
+    assert fails == 31 and where.startswith("emit.cu:"), (fails, where)
