@@ -1008,6 +1008,240 @@ ingest6_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
   }
 }
 
+// Payload-mode text ingest, 6-bit keys (the default; reserve_ingest_kernel is
+// the A/B arm). Measured per SASS region on config 4 (tools/ncu_sass_phases.py,
+// profiles/r02_ncu_ingest_*), reserve_ingest_kernel spends ~30 % of its
+// instructions on the front end (a third of that on the segmented suffix scan
+// that measures words running past a thread's segment), ~36 % on two divergent
+// per-thread word loops (count, then place) at ~55 % lane utilisation, and
+// ~32 % on packing keys from per-byte codes. This kernel:
+//   A  32 bytes per thread: byte classes, start / end masks; a word running
+//      past the thread's 32 bytes ends in the next thread's leading alnum run
+//      (one shuffle), or else is longer than 32 and takes the rare path (the
+//      long list); the 6-bit codes are compressed into one big-endian bit
+//      string per chunk in shared memory (6 words per thread)
+//   B  one divergent loop per thread over its words: length, bin, a shared
+//      reduction on the bin's counter, the word (start | bin) appended to the
+//      warp's list (slot = warp prefix of the thread's start count)
+//   D  per bin, one global atomic reserves the chunk's run; bin-major cursors
+//   P  full-lane pass over each warp's list: slot in the bin-major order from
+//      the bin's cursor (shared atomic), entry stored there
+//   E  per lane class (bins 0-4 | 5-9 | 10-20 | 21-31, contiguous in bin-major
+//      order), 256 words per step: the key is a funnel-shifted window of the
+//      bit string (2, 3, 5 or 7 shared loads), masked to L characters, stored
+//      to consecutive addresses.
+constexpr int kI7Threads = 256;
+constexpr int kI7Warps = kI7Threads / 32;
+constexpr int kI7SB = 32;                          // bytes per thread
+constexpr int kI7CB = kI7SB * kI7Threads;          // chunk bytes (== reserve_chunk_bytes())
+constexpr int kI7MaxWords = kI7SB * 32 / 2;        // words per warp at most
+constexpr uint32_t kI7Skip = 0xFFFFFFFFu;          // list entry of an L > 32 word
+constexpr int kI7Tail = 2;                         // 32-byte segments of codes past the chunk
+constexpr int kI7Bits = 6 * (kI7Threads + kI7Tail) + 8;  // bit-string words (+ read slack)
+
+struct I7Smem {
+  uint32_t bits[kI7Bits];                          // 6-bit codes as one big-endian bit string
+  uint32_t wl[kI7Warps][kI7MaxWords];              // chunk start | bin << 13 (word order)
+  uint16_t ord[kI7Warps * kI7MaxWords];            // bin-major order: index into wl
+  uint32_t cnt[kHistRows];
+  uint32_t cur[kNumBins];
+  uint32_t base[kHistRows];
+  uint32_t boff[kMaxPackedLen + 1];
+  unsigned long long dst[kMaxPackedLen];
+  uint32_t first[kI7Warps], last[kI7Warps];        // lane 0 (alnum mask, leading run) / lane 31 masks
+};
+
+// 32 text bytes (8 little-endian words) -> their 6-bit codes as 192 bits of a
+// big-endian bit string (first character in the top bits of w[0]).
+__device__ __forceinline__ void i7_bitstring(const uint4 (&v)[2], uint32_t (&w)[6]) {
+  uint32_t c[8];
+  const uint32_t x[8] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] = codes24(alnum6_codes4(x[k]));
+  w[0] = (c[0] << 8) | (c[1] >> 16);
+  w[1] = (c[1] << 16) | (c[2] >> 8);
+  w[2] = (c[2] << 24) | c[3];
+  w[3] = (c[4] << 8) | (c[5] >> 16);
+  w[4] = (c[5] << 16) | (c[6] >> 8);
+  w[5] = (c[6] << 24) | c[7];
+}
+
+// Bits [b, b + 32 * NW) of the string, NW words.
+template <int NW>
+__device__ __forceinline__ void i7_window(const uint32_t* __restrict__ bits, uint32_t b,
+                                          uint32_t (&o)[NW]) {
+  const uint32_t q = b >> 5, sh = b & 31u;
+  uint32_t prev = bits[q];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    const uint32_t nx = bits[q + k + 1];
+    o[k] = __funnelshift_l(nx, prev, sh);
+    prev = nx;
+  }
+}
+
+#ifndef WS_I7_MINB
+#define WS_I7_MINB 7  // 32 registers (A/B: 5 -> 160 us, 6 -> 149, 7-8 -> 143 on config 4)
+#endif
+__global__ void __launch_bounds__(kI7Threads, WS_I7_MINB)
+ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
+  extern __shared__ __align__(16) uint8_t i7_raw[];
+  I7Smem& sm = *reinterpret_cast<I7Smem*>(i7_raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t chunk = p.chunk0 + blockIdx.x;
+  const uint64_t cbase = chunk * kI7CB;
+  const uint64_t base = cbase + (uint64_t)tid * kI7SB;
+  const uint64_t avail = p.avail ? p.avail : ~0ull;
+  if (tid < kHistRows) sm.cnt[tid] = 0;
+
+  // ---- A ---------------------------------------------------------------------
+  uint4 v[2];
+  v[0] = v[1] = make_uint4(0, 0, 0, 0);
+  if (base < n) {  // padded text; streamed once (evict-first)
+    v[0] = WS_TEXT_LD(reinterpret_cast<const uint4*>(text + base));
+    v[1] = WS_TEXT_LD(reinterpret_cast<const uint4*>(text + base) + 1);
+  }
+  const uint32_t m = alnum_mask16(v[0]) | (alnum_mask16(v[1]) << 16);
+  const uint32_t lead = m == 0xFFFFFFFFu ? 32u : (uint32_t)__ffs(~m) - 1;  // leading alnum bytes
+  {
+    uint32_t w[6];
+    i7_bitstring(v, w);
+    uint2* d = reinterpret_cast<uint2*>(sm.bits + 6 * tid);
+    d[0] = make_uint2(w[0], w[1]);
+    d[1] = make_uint2(w[2], w[3]);
+    d[2] = make_uint2(w[4], w[5]);
+  }
+  if (tid < kI7Tail) {  // codes of the bytes after the chunk (words crossing its end)
+    const uint64_t a = cbase + kI7CB + (uint64_t)kI7SB * tid;
+    uint4 t[2];
+    t[0] = a < n ? *reinterpret_cast<const uint4*>(text + a) : make_uint4(0, 0, 0, 0);
+    t[1] = a + 16 < n ? *reinterpret_cast<const uint4*>(text + a + 16) : make_uint4(0, 0, 0, 0);
+    uint32_t w[6];
+    i7_bitstring(t, w);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) sm.bits[6 * (kI7Threads + tid) + k] = w[k];
+  } else if (tid < kI7Tail + 8) {
+    sm.bits[6 * (kI7Threads + kI7Tail) + tid - kI7Tail] = 0;
+  }
+  if (lane == 0) sm.first[wid] = lead;
+  if (lane == 31) sm.last[wid] = m >> 31;
+  uint32_t prev = __shfl_up_sync(0xffffffffu, m, 1) >> 31;
+  uint32_t nlead = __shfl_down_sync(0xffffffffu, lead, 1);  // next segment's leading alnum run
+  __syncthreads();  // #1: edge masks, counters
+  if (lane == 0)
+    prev = wid > 0 ? sm.last[wid - 1] : ((base > 0 && base - 1 < n) ? (uint32_t)is_alnum_byte(text[base - 1]) : 0u);
+  if (lane == 31) {
+    if (wid < kI7Warps - 1) {
+      nlead = sm.first[wid + 1];
+    } else {  // past the chunk: the next byte decides; a longer run is measured lazily
+      nlead = (base + kI7SB < n && is_alnum_byte(text[base + kI7SB])) ? 32u : 0u;
+    }
+  }
+  const uint32_t starts = m & ~((m << 1) | prev);
+  const uint32_t ends = m & ~((m >> 1) | ((nlead != 0) << 31));
+
+  // ---- B ---------------------------------------------------------------------
+  const uint32_t nst = (uint32_t)__popc(starts);
+  uint32_t incl = nst;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  const uint32_t ww = __shfl_sync(0xffffffffu, incl, 31);  // words of the warp
+  uint32_t* wl = sm.wl[wid] + (incl - nst);
+  for (uint32_t s = starts; s; s &= s - 1) {
+    const uint32_t i = (uint32_t)__ffs(s) - 1;
+    const uint32_t r = ends >> i;
+    uint32_t L = r ? (uint32_t)__ffs(r) : (32u - i) + nlead;
+    if (L > (uint32_t)kMaxPackedLen) {  // rare: measure in global memory, then the long list
+      if (!r && nlead == 32u)
+        L = (32u - i) + run_length_from(text, base + kI7SB, avail, p.overflow);
+      if (L > (uint32_t)kMaxPackedLen) {
+        const uint32_t at = atomicAdd(p.fill + kLongBin, 1u);
+        if (p.keys) p.longlist[at] = make_uint2((uint32_t)(base + i), L);
+        *wl++ = kI7Skip;
+        continue;
+      }
+    }
+    atomicAdd(&sm.cnt[L - 1], 1u);
+    *wl++ = ((uint32_t)tid * kI7SB + i) | ((L - 1) << 13);
+  }
+  if (lane == 0 && ww) atomicAdd(&sm.cnt[kNumBins], ww);
+  __syncthreads();  // #2: the chunk's bin counts
+
+  // ---- D ---------------------------------------------------------------------
+  if (tid < kMaxPackedLen && sm.cnt[tid]) sm.base[tid] = atomicAdd(p.fill + tid, sm.cnt[tid]);
+  if (tid == kNumBins && sm.cnt[kNumBins]) atomicAdd(p.fill + kNumBins, sm.cnt[kNumBins]);
+  if (wid == 1) {  // bin-major offsets (lane = bin) = the bins' cursors
+    const uint32_t c = sm.cnt[lane];
+    uint32_t inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += t;
+    }
+    sm.boff[lane] = inc - c;
+    sm.cur[lane] = inc - c;
+    if (lane == 31) sm.boff[kMaxPackedLen] = inc;
+  }
+  __syncthreads();  // #3
+  if (tid < kMaxPackedLen) {
+    const uint64_t ks = (uint64_t)key_bytes(lanes_for_len_enc(tid + 1, kEncAlnum6));
+    WS_DCHECK((uint64_t)sm.base[tid] + sm.cnt[tid] <= (n + 1) / (uint64_t)(tid + 2) || !sm.cnt[tid]);
+    sm.dst[tid] = p.bin_base[tid] + ((uint64_t)sm.base[tid] - sm.boff[tid]) * ks;  // modular
+  }
+
+  // ---- P ---------------------------------------------------------------------
+  for (uint32_t j = lane; j < ww; j += 32) {
+    const uint32_t e = sm.wl[wid][j];
+    if (e == kI7Skip) continue;
+    const uint32_t at = atomicAdd(&sm.cur[e >> 13], 1u);
+    WS_DCHECK(at < sm.boff[kMaxPackedLen]);
+    sm.ord[at] = (uint16_t)(wid * kI7MaxWords + j);
+  }
+  __syncthreads();  // #4: bin-major order, key addresses
+
+  // ---- E ---------------------------------------------------------------------
+  if (!p.keys) return;
+  uint8_t* keys = reinterpret_cast<uint8_t*>(p.keys);
+  const uint32_t e1 = sm.boff[5], e2 = sm.boff[10], e3 = sm.boff[21], e4 = sm.boff[kMaxPackedLen];
+  for (uint32_t k = tid; k < e1; k += kI7Threads) {  // class 0: L <= 5, the top 30 bits of a uint32
+    const uint32_t e = (&sm.wl[0][0])[sm.ord[k]], st = e & 8191u, bin = e >> 13;
+    uint32_t o[1];
+    i7_window<1>(sm.bits, 6 * st, o);
+    const uint32_t key = o[0] & (~0u << (26 - 6 * bin));
+    *reinterpret_cast<uint32_t*>(keys + sm.dst[bin] + (uint64_t)k * 4) = key;
+  }
+  for (uint32_t k = e1 + tid; k < e2; k += kI7Threads) {  // class 1: L 6-10, one uint64
+    const uint32_t e = (&sm.wl[0][0])[sm.ord[k]], st = e & 8191u, bin = e >> 13;
+    uint32_t o[2];
+    i7_window<2>(sm.bits, 6 * st, o);
+    const uint64_t key = (((uint64_t)o[0] << 32) | o[1]) & (~0ull << (58 - 6 * bin));
+    *reinterpret_cast<uint64_t*>(keys + sm.dst[bin] + (uint64_t)k * 8) = key;
+  }
+  for (uint32_t k = e2 + tid; k < e3; k += kI7Threads) {  // class 2: L 11-21, two uint64
+    const uint32_t e = (&sm.wl[0][0])[sm.ord[k]], st = e & 8191u, bin = e >> 13;
+    uint32_t o[4];
+    i7_window<4>(sm.bits, 6 * st, o);
+    const uint64_t k1 = (((uint64_t)o[2] << 32) | o[3]) & (~0ull << (122 - 6 * bin));
+    uint64_t* d = reinterpret_cast<uint64_t*>(keys + sm.dst[bin] + (uint64_t)k * 16);
+    d[0] = ((uint64_t)o[0] << 32) | o[1];
+    d[1] = k1;
+  }
+  for (uint32_t k = e3 + tid; k < e4; k += kI7Threads) {  // class 3: L 22-32, three uint64
+    const uint32_t e = (&sm.wl[0][0])[sm.ord[k]], st = e & 8191u, bin = e >> 13;
+    uint32_t o[6];
+    i7_window<6>(sm.bits, 6 * st, o);
+    const uint32_t bits = 6 * (bin + 1);  // 132..192
+    const uint64_t k2 = ((uint64_t)o[4] << 32) | o[5];
+    uint64_t* d = reinterpret_cast<uint64_t*>(keys + sm.dst[bin] + (uint64_t)k * 24);
+    d[0] = ((uint64_t)o[0] << 32) | o[1];
+    d[1] = ((uint64_t)o[2] << 32) | o[3];
+    d[2] = bits >= 192u ? k2 : k2 & (~0ull << (192u - bits));
+  }
+}
+
 // kByReserve follow-up: one CTA per chunk moves the chunk's runs (one per
 // bin) from their reserved place (the bin's ingest region / the long list as
 // filled) to their corpus-order place (run_off = exclusive scan of run_cnt
@@ -1210,10 +1444,23 @@ bool ingest6_enabled() {
   static const bool on = getenv("WSORT_INGEST6") && getenv("WSORT_INGEST6")[0] == '1';
   return on;
 }
+// WSORT_INGEST=reserve|6|7 picks the payload-mode 6-bit ingest (A/B arms).
+static int ingest_variant() {
+  static const int v = [] {
+    const char* e = getenv("WSORT_INGEST");
+    if (e && e[0] == 'r') return 1;
+    if (e && e[0] == '7') return 7;
+    if (ingest6_enabled() || (e && e[0] == '6')) return 6;
+    return 7;
+  }();
+  return v;
+}
 
 void set_ingest_attributes() {
   cudaFuncSetAttribute(ingest6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(W6Smem));
+  cudaFuncSetAttribute(ingest7_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(I7Smem));
   cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncAlnum6>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve_smem_bytes());
   cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncRaw8>,
@@ -1225,8 +1472,10 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
   if (!nchunks) return;
   if (p.fill && p.run_at)
     scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
-  else if (p.fill && p.enc == kEncAlnum6 && ingest6_enabled())
+  else if (p.fill && p.enc == kEncAlnum6 && ingest_variant() == 6)
     ingest6_kernel<<<nchunks, kW6Threads, sizeof(W6Smem), st>>>(text, n, p);
+  else if (p.fill && p.enc == kEncAlnum6 && ingest_variant() == 7)
+    ingest7_kernel<<<nchunks, kI7Threads, sizeof(I7Smem), st>>>(text, n, p);
   else if (p.fill && p.enc == kEncAlnum6)
     reserve_ingest_kernel<kReserveSB, kEncAlnum6><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(
         text, n, p);
@@ -1238,7 +1487,10 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }
-uint32_t reserve_chunk_bytes() { return ingest6_enabled() ? kW6CB : kReserveSB * kIngestThreads; }
+uint32_t reserve_chunk_bytes() {
+  static_assert(kI7CB == kW6CB, "payload-mode chunks");
+  return ingest_variant() == 1 ? kReserveSB * kIngestThreads : kI7CB;
+}
 
 void launch_reorder_runs(const ReorderParams& r, cudaStream_t st) {
   if (r.nchunks) launch_pdl(reorder_runs_kernel, r.nchunks, kIngestThreads, 0, st, r);

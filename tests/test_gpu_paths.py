@@ -47,6 +47,8 @@ print("ok")
     "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest
     "WSORT_SERIAL",           # every kernel on the main stream
     "WSORT_D2H_PER_CLASS",    # one emit + copy per lane class
+    "WSORT_INGEST=reserve",   # payload ingest by reserve_ingest_kernel (round-1 default)
+    "WSORT_INGEST=6",         # payload ingest by ingest6_kernel (word-parallel, measured slower)
     # A/B knobs used in the measurements (profiles/r01_ab_*.txt)
     "WSORT_CLASS_ORDER=3,2,1,0,4",
     "WSORT_CLASS_PRIO=0,-5,-5,-5,0",
