@@ -189,6 +189,10 @@ struct ws_handle {
   DevBuf rstatus[2];              // one-sweep look-back words
   bool payload_only = false;      // a fused sort wrote some buckets' payload without their keys
   bool early_req = false;         // the next ingest launches the class-0 histogram itself
+  bool tiny_req = false;          // the next ingest launches tiny_sort_kernel into `out` itself
+  bool tiny_launched = false;     // ... and did
+  bool tiny_done = false;         // ... and every bucket fitted: `out` holds the payload
+  DevBuf tiny_flag;
   bool early_done = false;        // ... and did (valid for the sort that follows)
   bool early_joint = false;       //     with whole-key counts for <= 12-bit keys
   bool split_early[kClasses + 1] = {false};  // ... and each multi-lane class's split launch
@@ -972,6 +976,29 @@ size_t radix_c0_zero_bytes() {  // totals + tickets + whole-key counters of clas
           (2u << 12)) * 4;
 }
 
+// Small corpora (tiny_sort_kernel): right behind the ingest on the main
+// stream, before the host reads the histogram; `out` holds n + 64 bytes.
+int launch_tiny(ws_handle* h, const uint64_t* region, uint64_t n) {
+  WS_CUDA(h->tiny_flag.ensure(64));
+  WS_CUDA(cudaMemsetAsync(h->tiny_flag.p, 0, 4, h->st));
+  TinyLaunch t;
+  memset(&t, 0, sizeof t);
+  t.fill = h->fill.as<uint32_t>();
+  t.keys_cap = h->keys_cap.as<uint8_t>();
+  for (int b = 0; b < kMaxPackedLen; ++b) t.region[b] = region[b];
+  t.out = h->out.as<uint8_t>();
+  t.out_cap = n + 64;
+  t.flag = h->tiny_flag.as<unsigned int>();
+  {
+    Phase ph(h, "tiny", 2.0 * (double)n, 1);
+    launch_tiny_sort(t, h->st);
+    ++h->launches;
+  }
+  WS_TRY(check_launch("tiny_sort"));
+  h->tiny_launched = true;
+  return WS_OK;
+}
+
 int launch_early_hist(ws_handle* h, const uint64_t* region) {
   cudaStream_t cst = h->serial ? h->st : h->cs[0];
   DevBuf& tb = h->rtotals[0];
@@ -1056,6 +1083,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
   } else if (n && !text) {
     return fail(WS_ERR_ARG, "null text");
   }
+  h->tiny_launched = h->tiny_done = false;
   h->ingested = h->sorted = h->have_stats = h->payload_only = false;
   h->have_tokens = false;
   h->unordered = false;
@@ -1199,7 +1227,8 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           gate_lk.unlock();
           if (getenv("WSORT_TRACE")) fprintf(stderr, "wsort-trace handle=%p h2d_landed=%.3f\n", (void*)h, trace_ms());
         }
-        if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        if (reserve && h->tiny_req && h->enc == kEncAlnum6) WS_TRY(launch_tiny(h, region, n));
+        else if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
         WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
                                 h->st));
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1224,10 +1253,14 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ++h->launches;
         }
         WS_TRY(check_launch("ingest_kernel"));
-        if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        if (reserve && h->tiny_req && h->enc == kEncAlnum6) WS_TRY(launch_tiny(h, region, n));
+        else if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
         tmark("early_enq");
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+        if (h->tiny_launched)
+          WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows + 1, h->tiny_flag.p, 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
+        h->tiny_done = h->tiny_launched && tot_host[kHistRows + 1] == 0 && tot_host[kLongBin] == 0;
         tmark("sync_ret");
       }
     } else {
@@ -2153,13 +2186,30 @@ namespace {
 // ws_sort_text body. `gate` (batch mode) serialises the host->device copy +
 // ingest of concurrent slots, so their PCIe transfers are staggered: one
 // corpus uploads while the previous ones sort and download.
+// Texts up to this size try tiny_sort_kernel first (WSORT_NO_TINY=1: never).
+constexpr uint64_t kTinyMaxText = 512 << 10;
+bool tiny_wanted(ws_handle* h, uint64_t n) {
+  static const bool off = env_on("WSORT_NO_TINY");
+  return !off && n > 0 && n <= kTinyMaxText && h->enc == kEncAlnum6;
+}
+
+// A tiny sort left the whole payload in `out`: the handle's state is that of a
+// fused sort (payload written, keys not sorted).
+void finish_tiny(ws_handle* h) {
+  h->sorted = true;
+  h->payload_only = true;
+}
+
 int sort_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, uint64_t cap,
                    uint64_t* written, std::mutex* gate) {
   static const bool trace = getenv("WSORT_TRACE") && getenv("WSORT_TRACE")[0] == '1';
   const double t_begin = trace ? trace_ms() : 0;
   h->early_req = early_hist_wanted();
+  h->enc = kEncAlnum6;
+  h->tiny_req = tiny_wanted(h, n);
+  if (h->tiny_req) WS_CUDA(h->out.ensure(n + 64));
   const int irc = ingest_text_impl(h, text, n, WS_INGEST_UNORDERED, gate);  // ends with a sync
-  h->early_req = false;
+  h->early_req = h->tiny_req = false;
   WS_TRY(irc);
   const double t_ingested = trace ? trace_ms() : 0;
   params_reset(h);  // the ingest synchronised: staging space is free again
@@ -2168,6 +2218,15 @@ int sort_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, 
   if (cap < size) return fail(WS_ERR_ARG, "output buffer too small");
   if (!size) return WS_OK;
   if (!out) return fail(WS_ERR_ARG, "null output buffer");
+  if (h->tiny_done) {  // the payload is on the device already
+    finish_tiny(h);
+    {
+      Phase ph(h, "d2h_out", (double)size, 1);
+      WS_CUDA(cudaMemcpyAsync(out, h->out.p, size, cudaMemcpyDeviceToHost, h->st));
+    }
+    WS_CUDA(cudaStreamSynchronize(h->st));
+    return WS_OK;
+  }
   WS_CUDA(h->out.ensure(size + 64));
   FusedEmit fe;
   fe.dout = h->out.as<uint8_t>();
@@ -2232,13 +2291,22 @@ int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   const double t_begin = trace ? trace_ms() : 0;
   tmark("begin");
   h->early_req = early_hist_wanted();
+  h->enc = kEncAlnum6;
+  h->tiny_req = tiny_wanted(h, n);
+  if (h->tiny_req) WS_CUDA(h->out.ensure(n + 64));
   const int irc = ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT | WS_INGEST_UNORDERED);
-  h->early_req = false;
+  h->early_req = h->tiny_req = false;
   WS_TRY(irc);
   const double t_ingested = trace ? trace_ms() : 0;
   tmark("ingest_ret");
   params_reset(h);
   const uint64_t size = emit_size(h, true);
+  if (h->tiny_done) {  // the payload is in `out` already
+    finish_tiny(h);
+    h->out_size = size;
+    if (written) *written = size;
+    return WS_OK;
+  }
   WS_CUDA(h->out.ensure(size + 64));
   FusedEmit fe;
   fe.dout = h->out.as<uint8_t>();

@@ -1011,6 +1011,79 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
   if (out) sub_emit<LANES>(base, cnt, L, out, pbuf);  // the merges' stores are visible to the CTA
 }
 
+// ---- small corpora: one CTA per bucket, straight after the ingest ------------------
+//
+// For a small text (ws_sort_text / ws_sort_resident / batches: payload mode)
+// the per-class chains cost more in launches and in the host's read-back of
+// the length histogram than in work. This launch goes in right behind the
+// ingest, before that read-back: CTA b takes the bucket of length b + 1 from
+// the ingest's fill counters, sorts it on chip with the tile network of a
+// 1024-thread CTA (OETS in registers + merge-path levels in shared memory, up
+// to 15360 one-word / 7168 multi-word keys) and writes its payload records at
+// the bucket's output offset (the prefix over shorter buckets of count * (L +
+// 1), also from the counters). A bucket beyond that, or any word longer than
+// 32, raises *flag and the call continues down the class chains (the keys are
+// only read here).
+constexpr int kTinyThreads = 1024;
+
+template <int LANES>
+constexpr size_t tiny_smem_lanes() {
+  return (size_t)kTinyThreads * TileCfg<LANES>::E * key_bytes(LANES) + 64 +
+         (size_t)kTinyThreads * (kMaxPackedLen + 1) + 64;
+}
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t kTinySmem =
+    cmax(cmax(tiny_smem_lanes<0>(), tiny_smem_lanes<1>()), cmax(tiny_smem_lanes<2>(), tiny_smem_lanes<3>()));
+
+template <int LANES>
+__device__ __forceinline__ void tiny_bucket(const KW<LANES>* __restrict__ in, uint32_t n, int L,
+                                            uint8_t* __restrict__ out, uint64_t* smem) {
+  constexpr int E = TileCfg<LANES>::E, NT = kTinyThreads, T = NT * E;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  using W = KW<LANES>;
+  W* sk = reinterpret_cast<W*>(smem);
+  uint8_t* pbuf = reinterpret_cast<uint8_t*>(smem) + (size_t)T * key_bytes(LANES) + 64;
+  for (uint32_t j = threadIdx.x; j < (uint32_t)(T * NW); j += NT) sk[j] = j < n * NW ? in[j] : ~W(0);
+  __syncthreads();
+  Key<LANES> r[E];
+  uint32_t ri[E];
+  uint64_t inv = 0;
+  tile_network<LANES, false, NT>(sk, nullptr, (int)n, 0u, r, ri, inv);
+  __syncthreads();
+  regs_to_smem<LANES, E, false>(sk, nullptr, threadIdx.x * E, r, ri);
+  __syncthreads();
+  emit_records_cta<LANES, NT>(sk, n, L, out, pbuf);
+}
+
+__global__ void __launch_bounds__(kTinyThreads, 1) tiny_sort_kernel(const __grid_constant__ TinyLaunch t) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int b = blockIdx.x;  // the bucket of length b + 1
+  const uint32_t n = t.fill[b];
+  const int L = b + 1, lanes = lanes_for_len_enc(L, kEncAlnum6);
+  const uint32_t cap = (uint32_t)kTinyThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E);
+  if (t.fill[kLongBin] != 0 || n > cap) {  // (every CTA checks the long words: all buckets may be empty)
+    if (threadIdx.x == 0) atomicOr(t.flag, 1u);
+    return;
+  }
+  if (n == 0) return;
+  uint64_t off = 0;
+  for (int q = 0; q < b; ++q) off += (uint64_t)t.fill[q] * (uint64_t)(q + 2);
+  WS_DCHECK(off + (uint64_t)n * (L + 1) <= t.out_cap);
+  const uint8_t* keys = t.keys_cap + t.region[b];
+  uint8_t* out = t.out + off;
+  switch (lanes) {
+    case 0: tiny_bucket<0>(reinterpret_cast<const KW<0>*>(keys), n, L, out, smem); break;
+    case 1: tiny_bucket<1>(reinterpret_cast<const KW<1>*>(keys), n, L, out, smem); break;
+    case 2: tiny_bucket<2>(reinterpret_cast<const KW<2>*>(keys), n, L, out, smem); break;
+    default: tiny_bucket<3>(reinterpret_cast<const KW<3>*>(keys), n, L, out, smem); break;
+  }
+}
+
+void launch_tiny_sort(const TinyLaunch& t, cudaStream_t st) {
+  launch_pdl(tiny_sort_kernel, kMaxPackedLen, kTinyThreads, kTinySmem, st, t);
+}
+
 // ---- host side ---------------------------------------------------------------------
 
 template <int LANES>
@@ -1059,6 +1132,7 @@ static void set_attrs_t() {
 // Opt every sort instantiation into > 48 KiB of dynamic shared memory on the
 // current device (called once per device by the handle).
 void set_sort_attributes() {
+  cudaFuncSetAttribute(tiny_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTinySmem);
   set_attrs_t<0, false>(); set_attrs_t<0, true>();
   set_attrs_t<1, false>(); set_attrs_t<1, true>();
   set_attrs_t<2, false>(); set_attrs_t<2, true>();

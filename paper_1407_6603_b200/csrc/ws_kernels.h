@@ -135,6 +135,18 @@ struct SplitEarly {
   uint32_t* hist;
 };
 void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st);
+// Small corpora: one CTA per length bucket sorts it on chip and writes its
+// payload records, straight after the payload-mode ingest (6-bit keys);
+// *flag is raised when a bucket does not fit a CTA or long words exist.
+struct TinyLaunch {
+  const uint32_t* fill;    // the ingest's per-bin counters (kHistRows)
+  const uint8_t* keys_cap;
+  uint64_t region[32];     // byte offsets of lengths 1..32 in keys_cap
+  uint8_t* out;            // payload destination (buckets ascending by length)
+  uint64_t out_cap;
+  unsigned int* flag;      // zeroed before the launch
+};
+void launch_tiny_sort(const TinyLaunch& t, cudaStream_t st);
 int sample_max_keys(int lanes);
 int part_tile_size();
 int subsort_tile_size(int lanes);  // keys one slot-sort CTA sorts in one network

@@ -503,3 +503,37 @@ def test_checked_build_detector_fires():
     assert r.returncode == 0, r.stderr[-2000:]
     fails, where = eval(r.stdout.strip().splitlines()[-1])
     assert fails == 31 and where.startswith("emit.cu:"), (fails, where)
+
+
+def _words_text(rng, lengths, alphabet=synth.ALNUM):
+    al = np.frombuffer(alphabet, dtype=np.uint8)
+    return b" ".join(bytes(rng.choice(al, size=int(L))) for L in lengths)
+
+
+@pytest.mark.parametrize("case", ["fits", "one_over_1lane", "one_over_2lane", "long_word", "all_lengths"])
+def test_tiny_path_and_its_fallbacks(case):
+    # texts <= 512 KiB first try tiny_sort_kernel (one CTA per bucket, right
+    # after the ingest); a bucket beyond a CTA (15360 one-word / 7168
+    # multi-word keys) or any word longer than 32 sends the call down the
+    # class chains. Each case checks the payload of both outcomes, the handle's
+    # state after it, and the batch API on the same texts.
+    rng = np.random.default_rng(hash(case) % 1000)
+    if case == "fits":
+        text = _words_text(rng, np.full(15360, 5)) + b" " + _words_text(rng, np.full(7168, 12))
+    elif case == "one_over_1lane":
+        text = _words_text(rng, np.full(15361, 4))
+    elif case == "one_over_2lane":
+        text = _words_text(rng, np.full(7169, 11))
+    elif case == "long_word":
+        text = _words_text(rng, rng.integers(1, 20, 3000)) + b" " + b"L" * 40
+    else:
+        text = _words_text(rng, rng.integers(1, 33, 20000))
+    assert len(text) <= 512 << 10
+    want, _ = oracle.sort_text(text, mode="fast")
+    assert sort_text(text) == want
+    h = _native.Handle(0)
+    texts = [np.frombuffer(t, dtype=np.uint8) for t in (text, text[: len(text) // 2])]
+    outs = [np.zeros(len(t) + 64, dtype=np.uint8) for t in texts]
+    sizes = h.sort_texts(texts, outs, inflight=2)
+    for t, o, n in zip(texts, outs, sizes):
+        assert o[:n].tobytes() == oracle.sort_text(t.tobytes(), mode="fast")[0]
