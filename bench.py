@@ -364,6 +364,7 @@ FAMILIES = {
     "partition": ("part_count_l1", "part_count_l2", "part_count_l3", "part_count_l4",
                   "part_scatter_l1", "part_scatter_l2", "part_scatter_l3", "part_scatter_l4"),
     "slot_sort": ("subsort_l1", "subsort_l2", "subsort_l3", "subsort_l4"),
+    "tiny_sort": ("tiny",),  # small corpora (<= 512 KiB): one CTA per bucket after the ingest
 }
 STATS_FAMILIES = {
     "stats_ingest": ("ingest", "reorder"),
