@@ -231,7 +231,10 @@ __device__ __forceinline__ void merge_path(const KW<LANES>* __restrict__ A, int 
     ia = ai < na ? IA[ai] : 0u;
     ib = bi < nb ? IB[bi] : 0u;
   }
-  // branch-free merge: take one side, advance it, reload only that side
+  // branch-free merge: take one side, advance it, reload only that side.
+  // A elements still pending when a b is taken: rem = a_rem_base - ai, kept
+  // as a 32-bit running count (E * rem < 2^32 for any bucket < 2^28 keys)
+  uint32_t rem = STATS ? (uint32_t)(a_rem_base - ai) : 0u, inv32 = 0;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const bool ta = (bi >= nb) || (ai < na && key_le<LANES>(ka, kb));
@@ -239,7 +242,8 @@ __device__ __forceinline__ void merge_path(const KW<LANES>* __restrict__ A, int 
     for (int l = 0; l < KeyTraits<LANES>::NW; ++l) r[k].w[l] = ta ? ka.w[l] : kb.w[l];
     if (STATS) {
       ri[k] = ta ? ia : ib;
-      inv += ta ? 0ull : (uint64_t)(a_rem_base - ai);
+      inv32 += ta ? 0u : rem;
+      rem -= ta ? 1u : 0u;
     }
     ai += ta ? 1 : 0;
     bi += ta ? 0 : 1;
@@ -258,6 +262,7 @@ __device__ __forceinline__ void merge_path(const KW<LANES>* __restrict__ A, int 
       ib = ta ? ib : ni;
     }
   }
+  if (STATS) inv += inv32;
 }
 
 // Registers (blocked, E per thread starting at element `base`) -> AoS smem.
@@ -439,12 +444,15 @@ struct PairGeom {
 __device__ __forceinline__ PairGeom pair_geom(const SegDesc& sd, uint32_t item, int64_t R, int T) {
   PairGeom g;
   g.n = sd.n;
-  const int64_t tpp = (2 * R + T - 1) / T;
-  const int64_t local = (int64_t)(item - sd.tile_begin);
-  g.pair_base = (local / tpp) * (2 * R);
+  // 32-bit division (work items and tiles per pair fit in 32 bits; a 64-bit
+  // divide is a long subroutine that every thread of every CTA would run)
+  const uint32_t tpp = (uint32_t)((2 * R + T - 1) / T);
+  const uint32_t local = item - sd.tile_begin;
+  const uint32_t pair = local / tpp;
+  g.pair_base = (int64_t)pair * (2 * R);
   g.na = min(R, g.n - g.pair_base);
   g.nb = g.n - g.pair_base > R ? min(R, g.n - g.pair_base - R) : 0;
-  g.d0 = (local % tpp) * T;
+  g.d0 = (int64_t)(local - pair * tpp) * T;
   g.empty = g.d0 >= g.na + g.nb;
   g.d1 = min(g.d0 + T, g.na + g.nb);
   return g;
@@ -475,8 +483,16 @@ __global__ void __launch_bounds__(256) merge_split_kernel(const __grid_constant_
   }
 }
 
+#ifndef WS_MERGE_STATS_MINB
+#define WS_MERGE_STATS_MINB 6  // stats mode, uint32 keys: 40 registers (8 CTAs/SM spilled 92-124 B)
+#endif
+#ifndef WS_MERGE_STATS_MINB1
+#define WS_MERGE_STATS_MINB1 4  // stats mode, multi-word keys
+#endif
 template <int LANES, bool STATS>
-__global__ void __launch_bounds__(kMergeThreads, MergeCfg<LANES>::MIN_BLOCKS)
+__global__ void __launch_bounds__(kMergeThreads, !STATS ? MergeCfg<LANES>::MIN_BLOCKS
+                                                        : (LANES == 0 ? WS_MERGE_STATS_MINB
+                                                                      : (LANES == 1 ? WS_MERGE_STATS_MINB1 : MergeCfg<LANES>::MIN_BLOCKS)))
     merge_kernel(const __grid_constant__ SortLaunch a) {
   pdl_wait();
   constexpr int E = MergeCfg<LANES>::E, T = MergeCfg<LANES>::T, NT = kMergeThreads;
