@@ -1151,6 +1151,10 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     static const char* lb_env = getenv("WSORT_LOOKBACK");
     const bool ordered_reserve = !reserve && !keep_tokens && !(lb_env && lb_env[0] == '1');
     const bool lookback = !reserve && !ordered_reserve;
+    // the ordered reserve ingest of text keys runs on 8 KiB chunks (ingest7_kernel<true>)
+    const uint64_t ocb = ordered_reserve && h->enc == kEncAlnum6 ? ordered_chunk_bytes() : ingest_chunk_bytes();
+    const uint32_t nchunks = ordered_reserve ? (uint32_t)((n + ocb - 1) / ocb) : chunk_count(n);
+    h->nchunks = nchunks;
     if (lookback) WS_CUDA(h->status.ensure((size_t)std::max<uint32_t>(nchunks, 1) * kLookbackRec * 4));
     if (ordered_reserve) {
       const size_t tb = (size_t)kHistRows * std::max<uint32_t>(nchunks, 1) * 4;
@@ -1190,7 +1194,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         WS_CUDA(h->overflow.ensure(256));
         WS_CUDA(cudaMemsetAsync(h->overflow.p, 0, 4, h->st));
         p.overflow = h->overflow.as<unsigned int>();
-        const uint64_t cb = reserve ? reserve_chunk_bytes() : ingest_chunk_bytes();
+        const uint64_t cb = reserve ? reserve_chunk_bytes() : ocb;
         // pieces of >= 8 MB let the ingest start before the whole text has
         // landed; in batch mode (gate) other corpora fill that gap, and one
         // copy keeps PCIe faster while the device->host direction is busy

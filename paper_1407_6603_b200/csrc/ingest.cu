@@ -1049,6 +1049,7 @@ struct I7Smem {
   uint32_t boff[kMaxPackedLen + 1];
   unsigned long long dst[kMaxPackedLen];
   uint32_t first[kI7Warps], last[kI7Warps];        // lane 0 (alnum mask, leading run) / lane 31 masks
+  uint32_t wcnt[kI7Warps][kHistRows];              // ORDERED: per-warp bin counts -> warp cursors
 };
 
 // 32 text bytes (8 little-endian words) -> their 6-bit codes as 192 bits of a
@@ -1083,6 +1084,13 @@ __device__ __forceinline__ void i7_window(const uint32_t* __restrict__ bits, uin
 #ifndef WS_I7_MINB
 #define WS_I7_MINB 7  // 32 registers (A/B: 5 -> 160 us, 6 -> 149, 7-8 -> 143 on config 4)
 #endif
+// ORDERED (stats mode, ScatterParams::run_at set): words keep corpus order
+// inside the chunk's run of every bin, counted per warp; the placement pass
+// ranks each warp's words by one MATCH.ANY per round against the warp's
+// cursors (warp order = corpus order), long words go to the long list at their
+// stable place, and each bin's run is recorded per chunk for
+// reorder_runs_kernel, which moves the runs into corpus order.
+template <bool ORDERED>
 __global__ void __launch_bounds__(kI7Threads, WS_I7_MINB)
 ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
   extern __shared__ __align__(16) uint8_t i7_raw[];
@@ -1093,6 +1101,8 @@ ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
   const uint64_t base = cbase + (uint64_t)tid * kI7SB;
   const uint64_t avail = p.avail ? p.avail : ~0ull;
   if (tid < kHistRows) sm.cnt[tid] = 0;
+  if (ORDERED)
+    for (int i = tid; i < kI7Warps * kHistRows; i += kI7Threads) (&sm.wcnt[0][0])[i] = 0;
 
   // ---- A ---------------------------------------------------------------------
   uint4 v[2];
@@ -1158,21 +1168,47 @@ ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
       if (!r && nlead == 32u)
         L = (32u - i) + run_length_from(text, base + kI7SB, avail, p.overflow);
       if (L > (uint32_t)kMaxPackedLen) {
-        const uint32_t at = atomicAdd(p.fill + kLongBin, 1u);
-        if (p.keys) p.longlist[at] = make_uint2((uint32_t)(base + i), L);
-        *wl++ = kI7Skip;
+        if (ORDERED) {  // placed (stably) by the placement pass; its length is measured again there
+          atomicAdd(&sm.wcnt[wid][kLongBin], 1u);
+          *wl++ = ((uint32_t)tid * kI7SB + i) | ((uint32_t)kLongBin << 13);
+        } else {
+          const uint32_t at = atomicAdd(p.fill + kLongBin, 1u);
+          if (p.keys) p.longlist[at] = make_uint2((uint32_t)(base + i), L);
+          *wl++ = kI7Skip;
+        }
         continue;
       }
     }
-    atomicAdd(&sm.cnt[L - 1], 1u);
+    atomicAdd(ORDERED ? &sm.wcnt[wid][L - 1] : &sm.cnt[L - 1], 1u);
     *wl++ = ((uint32_t)tid * kI7SB + i) | ((L - 1) << 13);
   }
-  if (lane == 0 && ww) atomicAdd(&sm.cnt[kNumBins], ww);
+  if (lane == 0 && ww) atomicAdd(ORDERED ? &sm.wcnt[wid][kNumBins] : &sm.cnt[kNumBins], ww);
   __syncthreads();  // #2: the chunk's bin counts
+  if (ORDERED && tid < kHistRows) {  // per bin: warp offsets inside the chunk's run, the chunk's count
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kI7Warps; ++w) {
+      const uint32_t c = sm.wcnt[w][tid];
+      sm.wcnt[w][tid] = run;
+      run += c;
+    }
+    sm.cnt[tid] = run;
+  }
+  if (ORDERED) __syncthreads();
 
   // ---- D ---------------------------------------------------------------------
-  if (tid < kMaxPackedLen && sm.cnt[tid]) sm.base[tid] = atomicAdd(p.fill + tid, sm.cnt[tid]);
-  if (tid == kNumBins && sm.cnt[kNumBins]) atomicAdd(p.fill + kNumBins, sm.cnt[kNumBins]);
+  if (ORDERED) {
+    if (tid < kHistRows) {  // reserve the runs, record them for the reorder
+      const uint32_t cnt = sm.cnt[tid];
+      const uint32_t at = cnt ? atomicAdd(p.fill + tid, cnt) : 0u;
+      sm.base[tid] = at;
+      p.run_at[(uint64_t)tid * p.nchunks_total + chunk] = at;
+      p.run_cnt[(uint64_t)tid * p.nchunks_total + chunk] = cnt;
+    }
+  } else {
+    if (tid < kMaxPackedLen && sm.cnt[tid]) sm.base[tid] = atomicAdd(p.fill + tid, sm.cnt[tid]);
+    if (tid == kNumBins && sm.cnt[kNumBins]) atomicAdd(p.fill + kNumBins, sm.cnt[kNumBins]);
+  }
   if (wid == 1) {  // bin-major offsets (lane = bin) = the bins' cursors
     const uint32_t c = sm.cnt[lane];
     uint32_t inc = c;
@@ -1193,12 +1229,38 @@ ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
   }
 
   // ---- P ---------------------------------------------------------------------
-  for (uint32_t j = lane; j < ww; j += 32) {
-    const uint32_t e = sm.wl[wid][j];
-    if (e == kI7Skip) continue;
-    const uint32_t at = atomicAdd(&sm.cur[e >> 13], 1u);
-    WS_DCHECK(at < sm.boff[kMaxPackedLen]);
-    sm.ord[at] = (uint16_t)(wid * kI7MaxWords + j);
+  if (ORDERED) {  // stable: rounds in word order, warp cursors (after every earlier warp's words)
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t* cur = sm.wcnt[wid];
+    for (uint32_t j0 = 0; j0 < ww; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t e = j < ww ? sm.wl[wid][j] : 0u;
+      const uint32_t bin = j < ww ? e >> 13 : 64u + (uint32_t)lane;  // no word: matches nobody
+      const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+      const uint32_t c0 = j < ww ? cur[bin] : 0u;
+      const uint32_t rank = c0 + (uint32_t)__popc(peers & lt);
+      __syncwarp();
+      if (j < ww && !(peers & lt)) cur[bin] = c0 + (uint32_t)__popc(peers);
+      if (j < ww) {
+        if (bin < (uint32_t)kMaxPackedLen) {
+          WS_DCHECK(sm.boff[bin] + rank < sm.boff[bin + 1]);
+          sm.ord[sm.boff[bin] + rank] = (uint16_t)(wid * kI7MaxWords + j);
+        } else if (p.keys) {  // long word (rare): its length again, its stable slot in the long list
+          const uint32_t st = e & 8191u;
+          const uint32_t L = run_length_from(text, cbase + st, avail, nullptr);
+          p.longlist[sm.base[kLongBin] + rank] = make_uint2((uint32_t)(cbase + st), L);
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    for (uint32_t j = lane; j < ww; j += 32) {
+      const uint32_t e = sm.wl[wid][j];
+      if (e == kI7Skip) continue;
+      const uint32_t at = atomicAdd(&sm.cur[e >> 13], 1u);
+      WS_DCHECK(at < sm.boff[kMaxPackedLen]);
+      sm.ord[at] = (uint16_t)(wid * kI7MaxWords + j);
+    }
   }
   __syncthreads();  // #4: bin-major order, key addresses
 
@@ -1459,7 +1521,9 @@ static int ingest_variant() {
 void set_ingest_attributes() {
   cudaFuncSetAttribute(ingest6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(W6Smem));
-  cudaFuncSetAttribute(ingest7_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(ingest7_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(I7Smem));
+  cudaFuncSetAttribute(ingest7_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(I7Smem));
   cudaFuncSetAttribute(reserve_ingest_kernel<kReserveSB, kEncAlnum6>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)reserve_smem_bytes());
@@ -1470,12 +1534,14 @@ void set_ingest_attributes() {
 void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st) {
   if (!nchunks) return;
-  if (p.fill && p.run_at)
+  if (p.fill && p.run_at && p.enc == kEncAlnum6 && ingest_variant() != 1)
+    ingest7_kernel<true><<<nchunks, kI7Threads, sizeof(I7Smem), st>>>(text, n, p);
+  else if (p.fill && p.run_at)
     scatter_kernel<kByReserve><<<nchunks, kIngestThreads, 0, st>>>(text, n, nullptr, nchunks, p);
   else if (p.fill && p.enc == kEncAlnum6 && ingest_variant() == 6)
     ingest6_kernel<<<nchunks, kW6Threads, sizeof(W6Smem), st>>>(text, n, p);
   else if (p.fill && p.enc == kEncAlnum6 && ingest_variant() == 7)
-    ingest7_kernel<<<nchunks, kI7Threads, sizeof(I7Smem), st>>>(text, n, p);
+    ingest7_kernel<false><<<nchunks, kI7Threads, sizeof(I7Smem), st>>>(text, n, p);
   else if (p.fill && p.enc == kEncAlnum6)
     reserve_ingest_kernel<kReserveSB, kEncAlnum6><<<nchunks, kIngestThreads, reserve_smem_bytes(), st>>>(
         text, n, p);
@@ -1487,6 +1553,9 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
 }
 
 uint32_t ingest_chunk_bytes() { return kChunk; }
+// Chunk of the ordered (stats-mode) text ingest: ingest7_kernel<true>'s 8 KiB,
+// or scatter_kernel<kByReserve>'s 4 KiB under WSORT_INGEST=reserve.
+uint32_t ordered_chunk_bytes() { return ingest_variant() == 1 ? (uint32_t)kChunk : (uint32_t)kI7CB; }
 uint32_t reserve_chunk_bytes() {
   static_assert(kI7CB == kW6CB, "payload-mode chunks");
   return ingest_variant() == 1 ? kReserveSB * kIngestThreads : kI7CB;

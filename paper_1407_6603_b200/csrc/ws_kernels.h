@@ -63,6 +63,7 @@ void launch_ingest_lookback(const uint8_t* text, uint64_t n, uint32_t nchunks,
                             const ScatterParams& p, cudaStream_t st);
 uint32_t ingest_chunk_bytes();
 uint32_t reserve_chunk_bytes();  // payload-mode (reserve_ingest_kernel) chunks
+uint32_t ordered_chunk_bytes();  // ordered (stats-mode) reserve ingest chunks (text)
 void set_ingest_attributes();    // once per device (dynamic shared memory opt-in)
 void launch_words_hist(const uint32_t* lens, uint64_t nwords, uint32_t wpw, uint32_t* whist,
                        uint32_t nwarps, cudaStream_t st);
