@@ -599,6 +599,21 @@ __device__ __forceinline__ const SampleSeg& sseg_at(const SampleLaunch& a, int i
 // (global, NW words each). The first-word search decides almost every key;
 // only a key whose first word equals a splitter's loads its remaining words
 // and searches the splitters sharing that word on them.
+// Multi-word keys with the full splitters in shared memory (the count pass):
+// one lower-bound search on full keys, then the equality test.
+template <int LANES>
+__device__ __forceinline__ uint32_t slot_of_full(const Key<LANES>* sps, uint32_t nsplit, const Key<LANES>& k) {
+  uint32_t lo = 0, len = nsplit;  // first splitter >= k
+  while (len > 0) {
+    const uint32_t half = len >> 1, mid = lo + half;
+    const bool less = key_lt<LANES>(sps[mid], k);
+    lo = less ? mid + 1 : lo;
+    len = less ? len - half - 1 : half;
+  }
+  const bool eq = lo < nsplit && !key_lt<LANES>(k, sps[lo]);
+  return 2 * lo + (eq ? 1u : 0u);
+}
+
 template <int LANES>
 __device__ __forceinline__ uint32_t slot_of(const uint64_t* sp, const uint64_t* __restrict__ spk,
                                             uint32_t nsplit, uint64_t p,
@@ -784,7 +799,10 @@ template <int LANES, bool COUNT>
 __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(const __grid_constant__ SampleLaunch a) {
   pdl_wait();
   using W = KW<LANES>;
-  __shared__ uint64_t s_split[kMaxSplit];
+  constexpr int NW = KeyTraits<LANES>::NW;
+  constexpr bool FULL = COUNT && NW >= 2;  // full splitters in smem, full keys loaded
+  __shared__ uint64_t s_split[FULL ? 1 : kMaxSplit];
+  __shared__ Key<(FULL ? LANES : 1)> s_spk[FULL ? kMaxSplit : 1];
   __shared__ uint32_t s_cnt[2 * kMaxSplit + 1];
   __shared__ uint32_t s_base[2 * kMaxSplit + 1];
   __shared__ int s_seg;
@@ -796,9 +814,14 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
   __syncthreads();
   const SampleSeg& sg = sseg_at(a, s_seg);
   const uint32_t nslot = 2 * sg.nsplit + 1;
-  if (COUNT)  // the scatter pass reads the slots the count pass found
+  if (COUNT && !FULL)  // the scatter pass reads the slots the count pass found
     for (uint32_t i = tid; i < sg.nsplit; i += kPartThreads)
-      s_split[i] = a.splitters[((uint64_t)sg.split_off + i) * KeyTraits<LANES>::NW];
+      s_split[i] = a.splitters[((uint64_t)sg.split_off + i) * NW];
+  if constexpr (FULL) {
+    uint64_t* d = reinterpret_cast<uint64_t*>(&s_spk[0]);
+    for (uint32_t i = tid; i < sg.nsplit * NW; i += kPartThreads)
+      d[i] = a.splitters[(uint64_t)sg.split_off * NW + i];
+  }
   for (uint32_t i = tid; i < nslot; i += kPartThreads) s_cnt[i] = 0;
   __syncthreads();
   const uint64_t first = (uint64_t)(blockIdx.x - sg.tile_begin) * kPartTile;
@@ -810,8 +833,11 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
   for (int q = 0; q < kPartPer; ++q) {  // every load in flight before the first search
     const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
     if (i < sg.n) {
-      if (COUNT) {
+      if (COUNT && !FULL) {
         k[q].w[0] = __ldg(in + i * KeyTraits<LANES>::NW);  // the 64-bit prefix is all it needs
+        slot[q] = 0;
+      } else if (COUNT) {
+        k[q] = gld<LANES>(in, (int64_t)i);
         slot[q] = 0;
       } else {
         k[q] = gld<LANES>(in, (int64_t)i);
@@ -824,8 +850,11 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
     const uint64_t i = first + (uint64_t)q * kPartThreads + tid;
     if (i < sg.n) {
       if (COUNT) {
-        slot[q] = slot_of<LANES>(s_split, a.splitters + (uint64_t)sg.split_off * KeyTraits<LANES>::NW,
-                                 sg.nsplit, (uint64_t)k[q].w[0], in, i);
+        if constexpr (FULL)
+          slot[q] = slot_of_full<(FULL ? LANES : 1)>(s_spk, sg.nsplit, k[q]);
+        else
+          slot[q] = slot_of<LANES>(s_split, a.splitters + (uint64_t)sg.split_off * KeyTraits<LANES>::NW,
+                                   sg.nsplit, (uint64_t)k[q].w[0], in, i);
         ids[q * kPartThreads + tid] = (uint16_t)slot[q];
       }
       rank[q] = atomicAdd(&s_cnt[slot[q]], 1u);
