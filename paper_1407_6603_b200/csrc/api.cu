@@ -192,7 +192,7 @@ struct ws_handle {
   bool tiny_req = false;          // the next ingest launches tiny_sort_kernel into `out` itself
   bool tiny_launched = false;     // ... and did
   bool tiny_done = false;         // ... and every bucket fitted: `out` holds the payload
-  DevBuf tiny_flag;
+  DevBuf tiny_flag, tiny_prof;
   bool early_done = false;        // ... and did (valid for the sort that follows)
   bool early_joint = false;       //     with whole-key counts for <= 12-bit keys
   bool split_early[kClasses + 1] = {false};  // ... and each multi-lane class's split launch
@@ -989,6 +989,12 @@ int launch_tiny(ws_handle* h, const uint64_t* region, uint64_t n) {
   t.out = h->out.as<uint8_t>();
   t.out_cap = n + 64;
   t.flag = h->tiny_flag.as<unsigned int>();
+  static const bool tprof = env_on("WSORT_TINY_PROF");
+  if (tprof) {  // diagnostics: per-bucket CTA times, printed after the ingest's sync
+    WS_CUDA(h->tiny_prof.ensure((64 + 16 * kMaxPackedLen) * 8));
+    WS_CUDA(cudaMemsetAsync(h->tiny_prof.p, 0, (64 + 16 * kMaxPackedLen) * 8, h->st));
+    t.prof = h->tiny_prof.as<unsigned long long>();
+  }
   {
     Phase ph(h, "tiny", 2.0 * (double)n, 1);
     launch_tiny_sort(t, h->st);
@@ -1265,6 +1271,24 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows + 1, h->tiny_flag.p, 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
         h->tiny_done = h->tiny_launched && tot_host[kHistRows + 1] == 0 && tot_host[kLongBin] == 0;
+        if (h->tiny_launched && env_on("WSORT_TINY_PROF")) {
+          unsigned long long tp[2 * kMaxPackedLen];
+          WS_CUDA(cudaMemcpy(tp, h->tiny_prof.p, sizeof tp, cudaMemcpyDeviceToHost));
+          unsigned long long t0 = ~0ull;
+          for (int b = 0; b < kMaxPackedLen; ++b) if (tp[2 * b]) t0 = std::min(t0, tp[2 * b]);
+          fprintf(stderr, "wsort-tiny");
+          for (int b = 0; b < kMaxPackedLen; ++b)
+            if (tp[2 * b]) fprintf(stderr, " L%d:%u[%.1f,%.1f]", b + 1, tot_host[b], (tp[2 * b] - t0) * 1e-3, (tp[2 * b + 1] - t0) * 1e-3);
+          fprintf(stderr, " us\n");
+          unsigned long long ph[16 * kMaxPackedLen];
+          WS_CUDA(cudaMemcpy(ph, h->tiny_prof.as<unsigned long long>() + 64, sizeof ph, cudaMemcpyDeviceToHost));
+          for (int b = 0; b < kMaxPackedLen; ++b) {
+            if (!tp[2 * b]) continue;
+            fprintf(stderr, "wsort-tiny-phases L%d:", b + 1);
+            for (int k = 2; k < 16; ++k) if (ph[16 * b + k]) fprintf(stderr, " %d:%.2f", k, (ph[16 * b + k] - tp[2 * b]) * 1e-3);
+            fprintf(stderr, "\n");
+          }
+        }
         tmark("sync_ret");
       }
     } else {

@@ -89,10 +89,22 @@ __device__ __forceinline__ void copy_span_out_t(const uint8_t* __restrict__ buf,
   for (uint64_t q = ae + threadIdx.x; q < g_end; q += NT) base[q] = buf[q - o0 + mis];
 }
 
+// Barrier over the CTA, or (NAMED) over its first NT threads only (named
+// barrier 1: the rest of the CTA has left).
+template <int NT, bool NAMED>
+__device__ __forceinline__ void nt_sync() {
+  if constexpr (NAMED) {
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  } else {
+    __syncthreads();
+  }
+}
+
 // Records of cnt sorted keys (NW words of W each, at `keys` in shared or
 // global memory) -> out, in rounds of NT keys staged in pbuf
-// (>= NT * (L + 1) + 32 bytes). Called by every thread of the CTA.
-template <int LANES, int NT>
+// (>= NT * (L + 1) + 32 bytes). Called by every thread of the CTA (NAMED:
+// by its first NT threads).
+template <int LANES, int NT, bool NAMED = false>
 __device__ void emit_records_cta(const typename KeyTraits<LANES>::W* keys, uint32_t cnt, int L,
                                  uint8_t* __restrict__ out, uint8_t* __restrict__ pbuf) {
   using W = typename KeyTraits<LANES>::W;
@@ -116,9 +128,9 @@ __device__ void emit_records_cta(const typename KeyTraits<LANES>::W* keys, uint3
       unpack6_swar<NL>(k, L, dst);
       dst[L] = '\n';
     }
-    __syncthreads();
+    nt_sync<NT, NAMED>();
     copy_span_out_t<NT>(pbuf, mis, ob, (uint64_t)n * R);
-    __syncthreads();
+    nt_sync<NT, NAMED>();
   }
 }
 

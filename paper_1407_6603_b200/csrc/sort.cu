@@ -303,7 +303,7 @@ __device__ __forceinline__ void smem_to_global(const KW<LANES>* sk, const uint32
 // sentinels behind them are already in place). Leaves the thread's E
 // outputs of the sorted tile (blocked) in r / ri; idx0 = idx of key 0.
 // NT = the CTA's threads (the tile holds NT * E keys).
-template <int LANES, bool STATS, int NT = kTileThreads>
+template <int LANES, bool STATS, int NT = kTileThreads, bool NAMED = false>
 __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cnt, uint32_t idx0,
                                              Key<LANES> (&r)[TileCfg<LANES>::E],
                                              uint32_t (&ri)[TileCfg<LANES>::E], uint64_t& inv) {
@@ -339,9 +339,9 @@ __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cn
   // Merge-path levels inside the tile.
 #pragma unroll 1
   for (int run = E; run < T && run < cnt; run <<= 1) {
-    __syncthreads();
+    nt_sync<NT, NAMED>();
     regs_to_smem<LANES, E, STATS>(sk, si, tid * E, r, ri);
-    __syncthreads();
+    nt_sync<NT, NAMED>();
     const int gt = (2 * run) / E;  // threads per merged pair
     const int a0 = (tid / gt) * 2 * run;
     if (a0 >= cnt) continue;  // a pair of sentinel runs: r already holds sentinels
@@ -1069,7 +1069,10 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
 // 1), also from the counters). A bucket beyond that, or any word longer than
 // 32, raises *flag and the call continues down the class chains (the keys are
 // only read here).
-constexpr int kTinyThreads = 1024;
+#ifndef WS_TINY_NT
+#define WS_TINY_NT 1024
+#endif
+constexpr int kTinyThreads = WS_TINY_NT;
 
 template <int LANES>
 constexpr size_t tiny_smem_lanes() {
@@ -1077,19 +1080,46 @@ constexpr size_t tiny_smem_lanes() {
          (size_t)kTinyThreads * (kMaxPackedLen + 1) + 64;
 }
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t kTinyRadixSmem = (size_t)2 * kTinyThreads * TileCfg<1>::E * 4 + (kTinyThreads / 32) * 256 * 4 + 32 * 4 +
+                                   (size_t)kTinyThreads * (kMaxPackedLen + 1) + 64;
 constexpr size_t kTinySmem =
-    cmax(cmax(tiny_smem_lanes<0>(), tiny_smem_lanes<1>()), cmax(tiny_smem_lanes<2>(), tiny_smem_lanes<3>()));
+    cmax(cmax(kTinyRadixSmem, tiny_smem_lanes<1>()), cmax(tiny_smem_lanes<2>(), tiny_smem_lanes<3>()));
+
+__device__ __forceinline__ void tiny_stamp(unsigned long long* st, int k) {
+  if (st && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    st[k] = t;
+  }
+}
+
+// The bucket's keys (16-byte aligned region start) into shared memory with one
+// bulk copy (up to 12 bytes past the bucket are read: still inside its region).
+__device__ __forceinline__ void tiny_load(void* dst, const void* src, uint32_t bytes) {
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t b16 = (bytes + 15) & ~15u;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, b16);
+    tma_load_1d(dst, src, b16, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+}
 
 template <int LANES>
 __device__ __forceinline__ void tiny_bucket(const KW<LANES>* __restrict__ in, uint32_t n, int L,
-                                            uint8_t* __restrict__ out, uint64_t* smem) {
+                                            uint8_t* __restrict__ out, uint64_t* smem,
+                                            unsigned long long* st = nullptr) {
   constexpr int E = TileCfg<LANES>::E, NT = kTinyThreads, T = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
   W* sk = reinterpret_cast<W*>(smem);
   uint8_t* pbuf = reinterpret_cast<uint8_t*>(smem) + (size_t)T * key_bytes(LANES) + 64;
-  for (uint32_t j = threadIdx.x; j < (uint32_t)(T * NW); j += NT) sk[j] = j < n * NW ? in[j] : ~W(0);
+  tiny_load(sk, in, n * (uint32_t)key_bytes(LANES));
+  for (uint32_t j = n * NW + threadIdx.x; j < (uint32_t)(T * NW); j += NT) sk[j] = ~W(0);
   __syncthreads();
+  tiny_stamp(st, 2);
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
@@ -1097,13 +1127,164 @@ __device__ __forceinline__ void tiny_bucket(const KW<LANES>* __restrict__ in, ui
   __syncthreads();
   regs_to_smem<LANES, E, false>(sk, nullptr, threadIdx.x * E, r, ri);
   __syncthreads();
+  tiny_stamp(st, 3);
   emit_records_cta<LANES, NT>(sk, n, L, out, pbuf);
+  tiny_stamp(st, 15);
+}
+
+// One-word (6-bit, L <= 5) buckets: stable LSD radix over the key's 6L bits
+// in shared memory, 8-bit digits (1-4 passes). Warp w ranks a contiguous
+// slice of the bucket in rounds of 32 keys (one MATCH.ANY per round against
+// its digit counters); a CTA-wide scan over (digit, warp) gives every key's
+// place. The comparison network of tiny_bucket took 40 us for config 0's 7.6k
+// three-character words.
+#ifndef WS_TINY_BALLOT
+#define WS_TINY_BALLOT 1  // digit peers by 8 ballots (fixed cost) instead of MATCH.ANY
+#endif
+__device__ __forceinline__ uint32_t tiny_peers8(uint32_t d, bool ok) {
+#if WS_TINY_BALLOT
+  uint32_t peers = __ballot_sync(0xffffffffu, ok);
+  if (!ok) peers = 0u;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bit = (d >> b) & 1u;
+    peers &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
+  }
+  return ok ? peers : (1u << (threadIdx.x & 31));
+#else
+  return __match_any_sync(0xffffffffu, ok ? d : 256u + (threadIdx.x & 31));
+#endif
+}
+
+// Records of sorted one-word 6-bit keys straight from registers: thread j
+// writes record j (<= 5 characters + '\n') with the fewest aligned stores.
+__device__ __forceinline__ void tiny_emit0(const uint32_t* keys, uint32_t n, int L, uint8_t* out) {
+  const uint32_t R = (uint32_t)L + 1;
+  for (uint32_t j = threadIdx.x; j < n; j += kTinyThreads) {
+    const uint32_t k = keys[j];
+    uint64_t rec = (uint64_t)'\n' << (8 * L);
+#pragma unroll
+    for (int c = 0; c < 5; ++c)
+      if (c < L) rec |= (uint64_t)alnum6_byte((k >> (26 - 6 * c)) & 63u) << (8 * c);
+    uint8_t* dst = out + (uint64_t)j * R;
+    uint32_t rem = R;
+    if (((uintptr_t)dst & 1) != 0) { *dst = (uint8_t)rec; rec >>= 8; ++dst; --rem; }
+    if (((uintptr_t)dst & 2) != 0 && rem >= 2) { *reinterpret_cast<uint16_t*>(dst) = (uint16_t)rec; rec >>= 16; dst += 2; rem -= 2; }
+    if (rem >= 4) { *reinterpret_cast<uint32_t*>(dst) = (uint32_t)rec; rec >>= 32; dst += 4; rem -= 4; }
+    if (rem >= 2) { *reinterpret_cast<uint16_t*>(dst) = (uint16_t)rec; rec >>= 16; dst += 2; rem -= 2; }
+    if (rem) *dst = (uint8_t)rec;
+  }
+}
+
+template <int NT>
+__device__ __forceinline__ uint32_t cta_excl_scan(uint32_t v, uint32_t* s_w /*[32]*/) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += u;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t x = lane < NT / 32 ? s_w[lane] : 0u;
+    uint32_t xi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, xi, d);
+      if (lane >= d) xi += u;
+    }
+    if (lane < NT / 32) s_w[lane] = xi - x;
+  }
+  __syncthreads();
+  return s_w[w] + inc - v;
+}
+
+
+__device__ void tiny_radix0(const uint32_t* __restrict__ in, uint32_t n, int L, uint8_t* __restrict__ out,
+                            uint64_t* smem, unsigned long long* st = nullptr) {
+  constexpr int NT = kTinyThreads, NWARP = NT / 32, R = (NT * TileCfg<1>::E + NT - 1) / NT;  // rounds
+  constexpr int TPD = NWARP / 8;  // threads per digit in the scan (8 warps' counters each)
+  static_assert(NWARP % 8 == 0 && NWARP * 256 == NT * 8, "scan layout: 8 counters per thread");
+  uint32_t* buf0 = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* buf1 = buf0 + NT * TileCfg<1>::E;
+  uint32_t* wc = buf1 + NT * TileCfg<1>::E;       // [NWARP][256]
+  uint32_t* s_w = wc + NWARP * 256;                 // [32]
+  uint8_t* pbuf = reinterpret_cast<uint8_t*>(s_w + 32);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t S = (n + NWARP - 1) / NWARP, s0 = min(n, w * S), s1 = min(n, s0 + S);
+  tiny_load(buf0, in, n * 4u);
+  tiny_stamp(st, 2);
+  const int bits = 6 * L, passes = (bits + 7) / 8;
+  uint32_t* a = buf0;
+  uint32_t* b = buf1;
+  for (int ps = 0; ps < passes; ++ps) {
+    const int shift = 32 - bits + 8 * ps;
+    for (int i = tid; i < NWARP * 256; i += NT) wc[i] = 0;
+    __syncthreads();
+    uint32_t rk[R], ky[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if ((uint32_t)(r * 32) >= S) break;  // uniform across the CTA
+      const uint32_t j = s0 + r * 32 + lane;
+      const bool ok = j < s1;
+      ky[r] = ok ? a[j] : 0u;
+      const uint32_t d = (ky[r] >> shift) & 255u;
+      const uint32_t peers = tiny_peers8(d, ok);
+      const uint32_t base = ok ? wc[w * 256 + d] : 0u;
+      rk[r] = base + __popc(peers & lt);
+      __syncwarp();
+      if (ok && !(peers & lt)) wc[w * 256 + d] = base + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    tiny_stamp(st, 3 + 3 * ps);
+    {  // exclusive offsets in (digit, warp) order: thread t = digit t / TPD, warps 8 (t % TPD) .. + 7
+      const int d = tid / TPD, q = tid % TPD;
+      uint32_t c[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c[k] = wc[(q * 8 + k) * 256 + d];
+        sum += c[k];
+      }
+      uint32_t run = cta_excl_scan<NT>(sum, s_w);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        wc[(q * 8 + k) * 256 + d] = run;
+        run += c[k];
+      }
+    }
+    __syncthreads();
+    tiny_stamp(st, 4 + 3 * ps);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if ((uint32_t)(r * 32) >= S) break;
+      const uint32_t j = s0 + r * 32 + lane;
+      if (j < s1) {
+        const uint32_t at = wc[w * 256 + ((ky[r] >> shift) & 255u)] + rk[r];
+        WS_DCHECK(at < n);
+        b[at] = ky[r];
+      }
+    }
+    __syncthreads();
+    tiny_stamp(st, 5 + 3 * ps);
+    uint32_t* t = a;
+    a = b;
+    b = t;
+  }
+  (void)pbuf;
+  tiny_emit0(a, n, L, out);
+  tiny_stamp(st, 15);
 }
 
 __global__ void __launch_bounds__(kTinyThreads, 1) tiny_sort_kernel(const __grid_constant__ TinyLaunch t) {
   pdl_wait();
   extern __shared__ __align__(16) uint64_t smem[];
   const int b = blockIdx.x;  // the bucket of length b + 1
+  unsigned long long t0 = 0;
+  if (t.prof && threadIdx.x == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
   const uint32_t n = t.fill[b];
   const int L = b + 1, lanes = lanes_for_len_enc(L, kEncAlnum6);
   const uint32_t cap = (uint32_t)kTinyThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E);
@@ -1118,10 +1299,16 @@ __global__ void __launch_bounds__(kTinyThreads, 1) tiny_sort_kernel(const __grid
   const uint8_t* keys = t.keys_cap + t.region[b];
   uint8_t* out = t.out + off;
   switch (lanes) {
-    case 0: tiny_bucket<0>(reinterpret_cast<const KW<0>*>(keys), n, L, out, smem); break;
-    case 1: tiny_bucket<1>(reinterpret_cast<const KW<1>*>(keys), n, L, out, smem); break;
-    case 2: tiny_bucket<2>(reinterpret_cast<const KW<2>*>(keys), n, L, out, smem); break;
-    default: tiny_bucket<3>(reinterpret_cast<const KW<3>*>(keys), n, L, out, smem); break;
+    case 0: tiny_radix0(reinterpret_cast<const uint32_t*>(keys), n, L, out, smem, t.prof ? t.prof + 64 + 16 * b : nullptr); break;
+    case 1: tiny_bucket<1>(reinterpret_cast<const KW<1>*>(keys), n, L, out, smem, t.prof ? t.prof + 64 + 16 * b : nullptr); break;
+    case 2: tiny_bucket<2>(reinterpret_cast<const KW<2>*>(keys), n, L, out, smem, t.prof ? t.prof + 64 + 16 * b : nullptr); break;
+    default: tiny_bucket<3>(reinterpret_cast<const KW<3>*>(keys), n, L, out, smem, t.prof ? t.prof + 64 + 16 * b : nullptr); break;
+  }
+  if (t.prof && threadIdx.x == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+    t.prof[2 * b] = t0;
+    t.prof[2 * b + 1] = t1;
   }
 }
 

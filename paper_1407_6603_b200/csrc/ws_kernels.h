@@ -146,6 +146,7 @@ struct TinyLaunch {
   uint8_t* out;            // payload destination (buckets ascending by length)
   uint64_t out_cap;
   unsigned int* flag;      // zeroed before the launch
+  unsigned long long* prof;  // diagnostics (WSORT_TINY_PROF): per CTA [start, end] globaltimer ns, or null
 };
 void launch_tiny_sort(const TinyLaunch& t, cudaStream_t st);
 int sample_max_keys(int lanes);
