@@ -430,8 +430,8 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
       launch_tile_sort(lanes, a, st);
       ++h->launches;
     } else {
-      launch_merge(lanes, a, st);  // partition + merge kernels
-      h->launches += 2;
+      launch_merge(lanes, a, st);  // merge kernel (+ a partition kernel when WS_MERGE_FUSED_SPLIT=0)
+      h->launches += merge_launches_per_level();
     }
     ph.end();
     WS_TRY(check_launch(name));

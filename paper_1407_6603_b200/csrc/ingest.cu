@@ -1081,6 +1081,9 @@ __device__ __forceinline__ void i7_window(const uint32_t* __restrict__ bits, uin
   }
 }
 
+#ifndef WS_I7_PAGG
+#define WS_I7_PAGG 0  // payload placement pass: 1 = warp-aggregated cursor atomics (MATCH.ANY)
+#endif
 #ifndef WS_I7_MINB
 #define WS_I7_MINB 7  // 32 registers (A/B: 5 -> 160 us, 6 -> 149, 7-8 -> 143 on config 4)
 #endif
@@ -1252,6 +1255,23 @@ ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
         }
       }
       __syncwarp();
+    }
+  } else if (WS_I7_PAGG) {  // warp-aggregated cursor atomics: one per distinct bin per round
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t j0 = 0; j0 < ww; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint32_t e = j < ww ? sm.wl[wid][j] : kI7Skip;
+      const uint32_t key = e == kI7Skip ? 64u + (uint32_t)lane : e >> 13;
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      uint32_t base = 0;
+      if (e != kI7Skip && lane == leader) base = atomicAdd(&sm.cur[key], (uint32_t)__popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (e != kI7Skip) {
+        const uint32_t at = base + (uint32_t)__popc(peers & lt);
+        WS_DCHECK(at < sm.boff[kMaxPackedLen]);
+        sm.ord[at] = (uint16_t)(wid * kI7MaxWords + j);
+      }
     }
   } else {
     for (uint32_t j = lane; j < ww; j += 32) {

@@ -483,6 +483,9 @@ __global__ void __launch_bounds__(256) merge_split_kernel(const __grid_constant_
   }
 }
 
+#ifndef WS_MERGE_FUSED_SPLIT
+#define WS_MERGE_FUSED_SPLIT 0  // 1: merge CTAs search their own splits, no partition launch (measured: same stats step)
+#endif
 #ifndef WS_MERGE_STATS_MINB
 #define WS_MERGE_STATS_MINB 6  // stats mode, uint32 keys: 40 registers (8 CTAs/SM spilled 92-124 B)
 #endif
@@ -506,11 +509,38 @@ __global__ void __launch_bounds__(kMergeThreads, !STATS ? MergeCfg<LANES>::MIN_B
   const int tid = threadIdx.x;
   const int64_t R = a.run;
   const uint32_t item = blockIdx.x;
+#if WS_MERGE_FUSED_SPLIT
+  // the CTA finds its own merge-path splits: warp 0 the A/B split of its first
+  // output, warp 1 that of its last + 1 (no partition launch, no dependent
+  // round trip between launches)
+  __shared__ int64_t s_split2[2];
+  const SegDesc sd = seg_at(a, find_segment(a, item));
+  const PairGeom g = pair_geom(sd, item, R, T);
+  if (g.empty) return;  // uniform across the CTA
+  {
+    const int w = tid >> 5;
+    if (w < 2) {
+      const int64_t d = w == 0 ? g.d0 : g.d1;
+      int64_t sp = 0;
+      if (w == 0 ? d > 0 : d < g.na + g.nb) {
+        const KW<LANES>* A = kv<LANES>(a.keys_in) + (sd.key_off + g.pair_base) * NW;
+        sp = merge_path_search_global<LANES>(A, g.na, A + R * NW, g.nb, d);
+      } else {
+        sp = w == 0 ? 0 : g.na;
+      }
+      if ((tid & 31) == 0) s_split2[w] = sp;
+    }
+    __syncthreads();
+  }
+  const int64_t a0 = s_split2[0];
+  const int64_t a1 = s_split2[1];
+#else
   const SegDesc sd = seg_at(a, (int)a.splits[2 * item + 1]);  // written by the partition pass
   const PairGeom g = pair_geom(sd, item, R, T);
   if (g.empty) return;  // uniform across the CTA
   const int64_t a0 = a.splits[2 * item];
   const int64_t a1 = (g.d1 == g.na + g.nb) ? g.na : (int64_t)a.splits[2 * item + 2];
+#endif
   const int64_t b0 = g.d0 - a0, b1 = g.d1 - a1;
   const int la = (int)(a1 - a0), lb = (int)(b1 - b0);
   WS_DCHECK(la >= 0 && lb >= 0 && la + lb <= T && a1 <= g.na && b1 <= g.nb);
@@ -1380,7 +1410,8 @@ static void launch_tile_t(const SortLaunch& a, cudaStream_t st) {
 
 template <int LANES, bool STATS>
 static void launch_merge_t(const SortLaunch& a, cudaStream_t st) {
-  launch_pdl(merge_split_kernel<LANES>, (a.work_items * 32 + 255) / 256, 256, 0, st, a);
+  if (!WS_MERGE_FUSED_SPLIT)
+    launch_pdl(merge_split_kernel<LANES>, (a.work_items * 32 + 255) / 256, 256, 0, st, a);
   launch_pdl(merge_kernel<LANES, STATS>, a.work_items, kMergeThreads,
              pass_smem_bytes<LANES, MergeCfg<LANES>::T, STATS>(), st, a);
 }
@@ -1448,6 +1479,8 @@ void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st, cudaE
     default: launch_sample_t<4>(a, st, ev); break;
   }
 }
+
+int merge_launches_per_level() { return WS_MERGE_FUSED_SPLIT ? 1 : 2; }
 
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st) {
   if (!a.work_items) return;

@@ -157,6 +157,7 @@ void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st, cudaE
 int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
 void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);
+int merge_launches_per_level();  // kernels launch_merge enqueues (1, or 2 with the partition pass)
 
 // radix.cu: payload-only LSD radix passes over one-word keys (classes 0, 1)
 struct RadixSeg {
