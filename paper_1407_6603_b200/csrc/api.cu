@@ -641,6 +641,8 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       if (p >= 0) {
         launch_radix_onesweep(lanes, a, st);
         if (p == 0) tmark("pass0_launched");
+        if (p == 1) tmark("pass1_launched");
+        if (p == 3) tmark("pass3_launched");
       } else if (!early) {
         launch_radix_hist(lanes, a, st);
       }
@@ -660,7 +662,9 @@ int radix_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint6
       }
     }
     if (njoint) {  // off the passes' chain: payload of the counted segments from their counts
+      tmark("joint_launch");
       launch_joint_expand(jlaunch, jblocks, njoint, st);
+      tmark("joint_launched");
       h->launches += 2;
       WS_TRY(check_launch("joint_expand"));
       if (on_done) {
@@ -1492,6 +1496,8 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       which.push_back(i);
     }
     if (segs.empty()) continue;
+    static const char* cls_mark[kClasses + 1] = {"cls0", "cls1", "cls2", "cls3", "cls4"};
+    tmark(cls_mark[c]);
     cudaStream_t cst = h->serial ? h->st : h->cs[c];
     cudaStream_t est = h->serial ? h->st : h->es[c];
     cudaStream_t dst = h->serial ? h->st : h->ds[c];

@@ -2,7 +2,7 @@
 # Checked build of the library (WS_CHECKED=1: device bounds checks on every
 # computed shared / global index, ws_debug_checks() reads them) into
 # build/checked/libwsort_b200.so. Run the GPU suite against it with
-#   WSORT_LIB=build/checked/libwsort_b200.so WSORT_CHECKED=1 python -m pytest tests -m gpu
+#   WSORT_LIB=$PWD/build/checked/libwsort_b200.so WSORT_CHECKED=1 python -m pytest tests -m gpu
 set -e
 cd "$(dirname "$0")/.."
 out=build/checked

@@ -16,9 +16,10 @@ t0, cases, fails = time.time(), 0, 0
 shared = _native.Handle(0)
 while time.time() - t0 < budget:
     words = []
+    small = rng.random() < 0.35  # <= 512 KiB texts also take the small-corpus kernel (tiny_sort_kernel)
     for _ in range(rng.integers(1, 14)):
         L = int(rng.integers(1, 60)); al = np.frombuffer(alphabets[rng.integers(0, len(alphabets))], dtype=np.uint8)
-        n = int(rng.integers(1, 30000 if L < 33 else 2000))
+        n = int(rng.integers(1, (3000 if small else 30000) if L < 33 else 2000))
         words += [bytes(r) for r in al[rng.integers(0, len(al), size=(n, L))]]
     rng.shuffle(words)
     text = seps[rng.integers(0, len(seps))].join(words)
