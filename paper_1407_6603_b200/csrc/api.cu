@@ -2081,7 +2081,8 @@ void ws_destroy(ws_handle* h) {
                     &h->rcounts[0], &h->rcounts[1], &h->rtotals[0], &h->rtotals[1], &h->rstatus[0], &h->rstatus[1],
                     &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
                     &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4],
-                    &h->ss_ids[1], &h->ss_ids[2], &h->ss_ids[3], &h->ss_ids[4]};
+                    &h->ss_ids[1], &h->ss_ids[2], &h->ss_ids[3], &h->ss_ids[4],
+                    &h->tiny_flag, &h->tiny_prof};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();
