@@ -1358,19 +1358,25 @@ reorder_runs_kernel(ReorderParams r) {
     }
   }
   __syncthreads();
-  const uint32_t total = s_pre[kNumBins];
-  for (uint32_t k = tid; k < total; k += kIngestThreads) {
-    int lo = 0, hi = kLongBin;  // last bin whose run starts at or before element k
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_pre[mid] <= k) lo = mid; else hi = mid - 1;
+  // one warp per run (runs b = w, w + 8, ...): a run is contiguous at both
+  // ends, so its 4-byte words are copied coalesced with no per-element search
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int b = wid; b <= kLongBin; b += kIngestThreads / 32) {
+    const uint32_t cnt = s_pre[b + 1] - s_pre[b];
+    if (!cnt) continue;
+    const uint32_t kw = r.key_bytes[b] >> 2;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(r.src[b]) + (uint64_t)s_from[b] * kw;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(r.dst[b]) + (uint64_t)s_to[b] * kw;
+    const uint32_t words = cnt * kw;
+    uint32_t q = lane;
+    for (; q + 96 < words; q += 128) {  // four independent loads in flight per lane
+      const uint32_t v0 = src[q], v1 = src[q + 32], v2 = src[q + 64], v3 = src[q + 96];
+      dst[q] = v0;
+      dst[q + 32] = v1;
+      dst[q + 64] = v2;
+      dst[q + 96] = v3;
     }
-    const uint32_t e = k - s_pre[lo], words = r.key_bytes[lo] >> 2;
-    WS_DCHECK(lo <= kLongBin && k >= s_pre[lo] && k < s_pre[lo + 1]);
-    const uint32_t* src =
-        reinterpret_cast<const uint32_t*>(r.src[lo]) + (uint64_t)(s_from[lo] + e) * words;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(r.dst[lo]) + (uint64_t)(s_to[lo] + e) * words;
-    for (uint32_t w = 0; w < words; ++w) dst[w] = src[w];
+    for (; q < words; q += 32) dst[q] = src[q];
   }
 }
 
