@@ -196,6 +196,8 @@ struct ws_handle {
   bool early_done = false;        // ... and did (valid for the sort that follows)
   bool early_joint = false;       //     with whole-key counts for <= 12-bit keys
   bool split_early[kClasses + 1] = {false};  // ... and each multi-lane class's split launch
+  bool count_early[kClasses + 1] = {false};  // ... and its count pass (device-planned)
+  DevBuf early_plan[kClasses + 1];            // the count pass's SampleLaunch, written by the split CTAs
   uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   DevBuf ss_ids[kClasses + 1];                            // per-key slot ids
@@ -805,7 +807,9 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   a.slot_ids = h->ss_ids[lanes].as<uint16_t>();
   // the ingest ran this class's split launch (same rules, same stream)
   a.split_done = h->split_early[lanes] ? 1 : 0;
+  a.count_done = a.split_done && h->count_early[lanes] ? 1 : 0;
   h->split_early[lanes] = false;
+  h->count_early[lanes] = false;
   double bytes = 0, nkeys = 0, pay_bytes = 0;
   for (const auto& s : segs) {
     bytes += 5.0 * s.n * key_bytes(lanes);
@@ -822,7 +826,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
       for (auto& e : ev) e = get_event(h);
     launch_sample_sort(lanes, a, st, h->prof ? ev : nullptr);
     tmark("ss_launched");
-    h->launches += 5;
+    h->launches += 5 - a.split_done - a.count_done;
     if (h->prof) {  // one record per kernel of the chain (kind 2: inside a phase)
       const double kb = key_bytes(lanes);
       const double split_b = a.split_done ? 0.0 : 8.0 * kb * std::min<double>(nkeys, 4096.0 * d.size());
@@ -838,7 +842,7 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
         r.a = ev[2 * i];
         r.b = ev[2 * i + 1];
         r.bytes = k[i].bytes;
-        r.launches = (i == 0 && a.split_done) ? 0 : 1;
+        r.launches = ((i == 0 && a.split_done) || (i == 1 && a.count_done)) ? 0 : 1;
         r.kind = 2;
         h->phases.push_back(r);
       }
@@ -1047,6 +1051,16 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     const int nb = lmax - lmin + 1;
     WS_CUDA(h->ss_split[c].ensure((size_t)nb * kMaxSplit * key_bytes(c) + 64));
     WS_CUDA(h->ss_slots[c].ensure((size_t)nb * (2 * kMaxSplit + 1) * 12 + 64));
+    // early count pass: slot ids for the most tiles the class's fitting buckets can have
+    static const bool count_ok = !env_on("WSORT_NO_EARLY_COUNT");
+    const uint64_t ptile = (uint64_t)part_tile_size();
+    uint64_t max_tiles = 0;
+    for (int L = lmin; L <= lmax; ++L)
+      max_tiles += (std::min<uint64_t>((h->n_text + 1) / (L + 1), sample_bucket_limit(c)) + ptile - 1) / ptile;
+    if (count_ok) {
+      WS_CUDA(h->ss_ids[c].ensure((size_t)max_tiles * ptile * 2 + 64));
+      WS_CUDA(h->early_plan[c].ensure(sizeof(SampleLaunch)));
+    }
     cudaStream_t sst = h->serial ? h->st : h->cs[c];
     if (sst != h->st) {
       cudaEvent_t ev = sync_event(h);
@@ -1067,6 +1081,11 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     se.cap = sample_bucket_limit(c);
     se.splitters = h->ss_split[c].as<uint64_t>();
     se.hist = h->ss_slots[c].as<uint32_t>();
+    if (count_ok) {
+      se.plan = h->early_plan[c].as<SampleLaunch>();
+      se.slot_ids = h->ss_ids[c].as<uint16_t>();
+      se.ptile = (uint32_t)ptile;
+    }
     {
       char nm[16];
       snprintf(nm, sizeof nm, "split_l%d", c);
@@ -1075,6 +1094,17 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
       ++h->launches;
     }
     h->split_early[c] = true;
+    if (count_ok) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, 2ull * sms));
+      char nm[20];
+      snprintf(nm, sizeof nm, "part_count_l%d", c);
+      Phase ph(h, nm, 0.0, 0, sst);
+      launch_partition_count_early(c, h->early_plan[c].as<SampleLaunch>(), grid, sst);
+      ++h->launches;
+      h->count_early[c] = true;
+    }
   }
   WS_TRY(check_launch("sample_split_early"));
   return WS_OK;
@@ -1252,6 +1282,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           p.overflow = nullptr;
           h->early_done = false;
           for (bool& f : h->split_early) f = false;
+          for (bool& f : h->count_early) f = false;
           WS_TRY(reset_chain());
         }
       }
@@ -1317,6 +1348,12 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           for (int L = 1; L <= kMaxPackedLen; ++L)  // sampled keys read
             if (lanes_for_len_enc(L, h->enc) == c && counts[L - 1])
               b += (double)key_bytes(c) * std::min<double>((double)counts[L - 1], 4096.0);
+        } else if (r.name.rfind("part_count_l", 0) == 0) {
+          const int c = r.name[12] - '0';
+          b = 0;
+          for (int L = 1; L <= kMaxPackedLen; ++L)  // keys read (first word for one-word keys), slot ids written
+            if (lanes_for_len_enc(L, h->enc) == c && counts[L - 1] <= sample_bucket_limit(c))
+              b += (double)counts[L - 1] * ((c == 1 ? 8.0 : (double)key_bytes(c)) + 2.0);
         }
         r.bytes = b;
       }

@@ -797,25 +797,45 @@ __global__ void __launch_bounds__(kSampleThreads) sample_split_early_kernel(cons
   extern __shared__ __align__(16) uint64_t dsm[];
   SampleSeg sg;
   memset(&sg, 0, sizeof sg);
-  uint32_t slots = 0, splits = 0;
-  bool mine = false;
+  uint32_t slots = 0, splits = 0, tiles = 0, key_off = 0, nfit = 0;
+  int idx = -1;
   for (int L = e.lmin; L <= e.lmax; ++L) {
     const uint32_t n = e.fill[L - 1];
+    const uint32_t koff = key_off;
+    key_off += n;  // class-relative element offset (plan_packed: every bucket of the class)
     if (!n || n > e.cap) continue;
     const SamplePlan pl = sample_plan(n, e.T, e.pmax, e.smax);
     if (L == e.lmin + (int)blockIdx.x) {
       sg.in = reinterpret_cast<const uint64_t*>(e.keys_cap + e.region[L - 1]);
+      sg.key_off = koff;
       sg.n = n;
       sg.nsplit = pl.nsplit;
       sg.m = pl.m;
       sg.split_off = splits;
       sg.slot_base = slots;
-      mine = true;
+      sg.tile_begin = tiles;
+      sg.len = (uint32_t)L;
+      idx = (int)nfit;
     }
     slots += 2 * pl.nsplit + 1;
     splits += pl.nsplit;
+    tiles += e.ptile ? (n + e.ptile - 1) / e.ptile : 0u;
+    ++nfit;
   }
-  if (mine) split_bucket<LANES>(sg, e.splitters, e.hist, reinterpret_cast<Key<LANES>*>(dsm));
+  if (e.plan && threadIdx.x == 0) {  // the early count pass's launch (sample_sort_segments' plan)
+    if (idx >= 0) e.plan->inl[idx] = sg;
+    if (blockIdx.x == 0) {
+      e.plan->segs = nullptr;
+      e.plan->nsegs = (int)nfit;
+      e.plan->nslots = slots;
+      e.plan->work_items = tiles;
+      e.plan->splitters = e.splitters;
+      e.plan->hist = e.hist;
+      e.plan->slot_ids = e.slot_ids;
+      e.plan->split_done = 1;
+    }
+  }
+  if (idx >= 0) split_bucket<LANES>(sg, e.splitters, e.hist, reinterpret_cast<Key<LANES>*>(dsm));
 }
 
 __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t tile) {
@@ -832,12 +852,10 @@ __device__ __forceinline__ int part_segment_of(const SampleLaunch& a, uint32_t t
 
 // Partition passes over one tile of a bucket. COUNT: per-slot counts into
 // a.hist. !COUNT: each key goes to cursor[slot] reservation + local rank.
+// One partition tile `item` (all threads of the CTA; the CTA's shared memory
+// is free again on return).
 template <int LANES, bool COUNT>
-#ifndef WS_PART_MINB
-#define WS_PART_MINB 1
-#endif
-__global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(const __grid_constant__ SampleLaunch a) {
-  pdl_wait();
+__device__ __forceinline__ void partition_tile(const SampleLaunch& a, uint32_t item) {
   using W = KW<LANES>;
   constexpr int NW = KeyTraits<LANES>::NW;
   constexpr bool FULL = COUNT && NW >= 2;  // full splitters in smem, full keys loaded
@@ -848,7 +866,7 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
   __shared__ int s_seg;
   const int tid = threadIdx.x;
   if (tid < 32) {
-    const int sgi = part_segment_of(a, blockIdx.x);
+    const int sgi = part_segment_of(a, item);
     if (tid == 0) s_seg = sgi;
   }
   __syncthreads();
@@ -864,9 +882,9 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
   }
   for (uint32_t i = tid; i < nslot; i += kPartThreads) s_cnt[i] = 0;
   __syncthreads();
-  const uint64_t first = (uint64_t)(blockIdx.x - sg.tile_begin) * kPartTile;
+  const uint64_t first = (uint64_t)(item - sg.tile_begin) * kPartTile;
   const W* in = kv<LANES>(sg.in);
-  uint16_t* ids = a.slot_ids + (uint64_t)blockIdx.x * kPartTile;
+  uint16_t* ids = a.slot_ids + (uint64_t)item * kPartTile;
   Key<LANES> k[kPartPer];
   uint32_t slot[kPartPer], rank[kPartPer];
 #pragma unroll
@@ -919,6 +937,29 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
                 s_base[slot[q]] + rank[q] < sg.key_off + sg.n);
       stk<LANES>(out, (int)(s_base[slot[q]] + rank[q]), k[q]);
     }
+}
+
+#ifndef WS_PART_MINB
+#define WS_PART_MINB 1
+#endif
+template <int LANES, bool COUNT>
+__global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(const __grid_constant__ SampleLaunch a) {
+  pdl_wait();
+  partition_tile<LANES, COUNT>(a, blockIdx.x);
+}
+
+// The count pass launched by the ingest right behind the class's split launch,
+// from the launch the split CTAs wrote (device-planned, same rules as the host
+// plan): a persistent grid over the class's partition tiles.
+template <int LANES>
+__global__ void __launch_bounds__(kPartThreads, 2) partition_count_early_kernel(const SampleLaunch* __restrict__ plan) {
+  pdl_wait();
+  const SampleLaunch& a = *plan;
+  const uint32_t items = a.work_items;
+  for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
+    partition_tile<LANES, true>(a, item);
+    __syncthreads();  // the tile's shared memory is reused by the next one
+  }
 }
 
 // Exclusive scan of each bucket's slot counts (one CTA per bucket), started
@@ -1461,7 +1502,7 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st, cudaEvent_t*
   if (!a.split_done)
     launch_pdl(sample_split_kernel<LANES>, a.nsegs, kSampleThreads, split_smem_bytes<LANES>(), st, a);
   mark(1);
-  launch_pdl(partition_kernel<LANES, true>, a.work_items, kPartThreads, 0, st, a);
+  if (!a.count_done) launch_pdl(partition_kernel<LANES, true>, a.work_items, kPartThreads, 0, st, a);
   mark(2);
   launch_pdl(slot_scan_kernel, a.nsegs, 1024, 0, st, a);
   mark(3);
@@ -1474,6 +1515,14 @@ static void launch_sample_t(const SampleLaunch& a, cudaStream_t st, cudaEvent_t*
 int sample_max_keys(int) { return kSampleSmem / 8; }
 int part_tile_size() { return kPartTile; }
 int subsort_tile_size(int lanes) { return kSubThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E); }
+
+void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st) {
+  switch (lanes) {
+    case 1: launch_pdl(partition_count_early_kernel<1>, grid, kPartThreads, 0, st, plan); break;
+    case 2: launch_pdl(partition_count_early_kernel<2>, grid, kPartThreads, 0, st, plan); break;
+    default: launch_pdl(partition_count_early_kernel<3>, grid, kPartThreads, 0, st, plan); break;
+  }
+}
 
 void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st) {
   const unsigned nb = (unsigned)(e.lmax - e.lmin + 1);

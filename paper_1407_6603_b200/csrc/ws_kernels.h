@@ -121,6 +121,7 @@ struct SampleLaunch {
   uint32_t* slot_off;     // per slot: class-relative element offset
   uint16_t* slot_ids;     // per key, in partition-tile order: its slot (count pass -> scatter pass)
   int split_done;         // the ingest already ran the split launch (sample_split_early_kernel)
+  int count_done;         // ... and the count pass (partition_count_early_kernel)
   SampleSeg inl[kInlineSegs];
 };
 // Split launch of one lane class planned on the device (6-bit text keys,
@@ -134,7 +135,16 @@ struct SplitEarly {
   uint64_t cap;            // larger buckets take the merge path
   uint64_t* splitters;     // the class's splitter and slot-counter buffers (max size)
   uint32_t* hist;
+  // early count pass (or null): the split CTAs write its launch (segment
+  // table of the buckets that fit, tiles, buffers) here, for
+  // partition_count_early_kernel right behind them
+  SampleLaunch* plan;
+  uint16_t* slot_ids;
+  uint32_t ptile;          // keys per partition tile
 };
+// The count pass of one multi-lane class, planned on the device (the split
+// launch's table): a persistent grid over the class's partition tiles.
+void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st);
 void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st);
 // Small corpora: one CTA per length bucket sorts it on chip and writes its
 // payload records, straight after the payload-mode ingest (6-bit keys);

@@ -42,6 +42,7 @@ print("ok")
     "WSORT_NO_JOINT",         # 1-2 character buckets by radix passes instead of whole-key counts
     "WSORT_NO_EARLY_HIST",    # class-0 histogram launched after the host plan, not by the ingest
     "WSORT_NO_EARLY_SPLIT",   # multi-lane split launches after the host plan, not by the ingest
+    "WSORT_NO_EARLY_COUNT",   # multi-lane count passes after the host plan (split still early)
     "WSORT_LOOKBACK",         # ordered ingest by the decoupled look-back
     "WSORT_TWO_PASS",         # count + scan + scatter ingest
     "WSORT_NO_CHUNKED_H2D",   # one host->device copy before the ingest
