@@ -369,7 +369,9 @@ FAMILIES = {
 STATS_FAMILIES = {
     "stats_ingest": ("ingest", "reorder"),
     "stats_tile_sort": ("tile_l0", "tile_l1", "tile_l2", "tile_l3", "tile_l4"),
-    "stats_merge": ("merge_l0", "merge_l1", "merge_l2", "merge_l3", "merge_l4"),
+    # merge kernels alone, and the merge-path partition launches of the same levels
+    "stats_merge": ("mergek_l0", "mergek_l1", "mergek_l2", "mergek_l3", "mergek_l4"),
+    "stats_merge_partition": ("msplit_l0", "msplit_l1", "msplit_l2", "msplit_l3", "msplit_l4"),
 }
 
 

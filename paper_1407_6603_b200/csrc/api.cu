@@ -432,8 +432,28 @@ int sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint64_t* k
       launch_tile_sort(lanes, a, st);
       ++h->launches;
     } else {
-      launch_merge(lanes, a, st);  // merge kernel (+ a partition kernel when WS_MERGE_FUSED_SPLIT=0)
+      // merge kernel (+ a partition kernel when WS_MERGE_FUSED_SPLIT=0); profiling:
+      // one record per kernel inside the level's phase (kind 2)
+      cudaEvent_t ev[3];
+      if (h->prof)
+        for (auto& e : ev) e = get_event(h);
+      launch_merge(lanes, a, st, h->prof ? ev : nullptr);
       h->launches += merge_launches_per_level();
+      if (h->prof) {
+        // (the partition kernel is a latency-bound merge-path search: no bytes claimed)
+        const struct { const char* nm; double bytes; int launches; } k[2] = {
+            {"msplit", 0.0, merge_launches_per_level() - 1}, {"mergek", bytes, 1}};
+        for (int i = 0; i < 2; ++i) {
+          PhaseRec r;
+          r.name = std::string(tag) + k[i].nm + "_l" + std::to_string(lanes);
+          r.a = ev[i];
+          r.b = ev[i + 1];
+          r.bytes = k[i].bytes;
+          r.launches = k[i].launches;
+          r.kind = 2;
+          h->phases.push_back(r);
+        }
+      }
     }
     ph.end();
     WS_TRY(check_launch(name));

@@ -1464,11 +1464,15 @@ static void launch_tile_t(const SortLaunch& a, cudaStream_t st) {
 }
 
 template <int LANES, bool STATS>
-static void launch_merge_t(const SortLaunch& a, cudaStream_t st) {
+static void launch_merge_t(const SortLaunch& a, cudaStream_t st, cudaEvent_t* ev) {
+  // ev (profiling, or null): before the partition kernel, between, after the merge
+  if (ev) cudaEventRecord(ev[0], st);
   if (!WS_MERGE_FUSED_SPLIT)
     launch_pdl(merge_split_kernel<LANES>, (a.work_items * 32 + 255) / 256, 256, 0, st, a);
+  if (ev) cudaEventRecord(ev[1], st);
   launch_pdl(merge_kernel<LANES, STATS>, a.work_items, kMergeThreads,
              pass_smem_bytes<LANES, MergeCfg<LANES>::T, STATS>(), st, a);
+  if (ev) cudaEventRecord(ev[2], st);
 }
 
 #define WS_DISPATCH_LANES(fn, lanes, stats, ...)                                    \
@@ -1545,10 +1549,10 @@ void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st, cudaE
 
 int merge_launches_per_level() { return WS_MERGE_FUSED_SPLIT ? 1 : 2; }
 
-void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st) {
+void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st, cudaEvent_t* ev) {
   if (!a.work_items) return;
   const bool stats = a.idx_out != nullptr;
-  WS_DISPATCH_LANES(launch_merge_t, lanes, stats, a, st);
+  WS_DISPATCH_LANES(launch_merge_t, lanes, stats, a, st, ev);
 }
 
 WS_DEFINE_CHECK_READER(check_reader_sort)

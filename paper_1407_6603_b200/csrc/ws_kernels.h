@@ -166,7 +166,8 @@ int subsort_tile_size(int lanes);  // keys one slot-sort CTA sorts in one networ
 void launch_sample_sort(int lanes, const SampleLaunch& a, cudaStream_t st, cudaEvent_t* ev = nullptr);
 int merge_tile_size(int lanes);
 void launch_tile_sort(int lanes, const SortLaunch& a, cudaStream_t st);
-void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st);
+// ev (profiling, or null): 3 events, before the partition kernel, between, after the merge
+void launch_merge(int lanes, const SortLaunch& a, cudaStream_t st, cudaEvent_t* ev = nullptr);
 int merge_launches_per_level();  // kernels launch_merge enqueues (1, or 2 with the partition pass)
 
 // radix.cu: payload-only LSD radix passes over one-word keys (classes 0, 1)
