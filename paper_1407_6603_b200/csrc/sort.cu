@@ -70,10 +70,13 @@ struct TileCfg {
   static constexpr int T = NT * E;
 };
 
+#ifndef WS_MERGE_EW
+#define WS_MERGE_EW 7  // outputs per thread in a merge pass of multi-word keys (odd; smaller tiles, more CTAs for the latency-bound smaller classes: stats step 1.583 -> 1.526 ms, 9: 1.531, 11: 1.59)
+#endif
 template <int LANES>
 struct MergeCfg {
   static constexpr int NT = kMergeThreads;
-  static constexpr int E = WS_MERGE_E;
+  static constexpr int E = LANES <= 0 ? WS_MERGE_E : WS_MERGE_EW;
   static constexpr int T = NT * E;
   static constexpr int MIN_BLOCKS = LANES <= 1 ? 2048 / NT : (LANES == 2 ? 1024 / NT : 512 / NT);
 };
