@@ -193,6 +193,7 @@ struct ws_handle {
   bool tiny_launched = false;     // ... and did
   bool tiny_done = false;         // ... and every bucket fitted: `out` holds the payload
   DevBuf tiny_flag, tiny_prof;
+  DevBuf first_sep;  // long_len_fix: first separator per 8 KiB chunk
   bool early_done = false;        // ... and did (valid for the sort that follows)
   bool early_joint = false;       //     with whole-key counts for <= 12-bit keys
   bool split_early[kClasses + 1] = {false};  // ... and each multi-lane class's split launch
@@ -1235,12 +1236,14 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     p.status = h->status.as<uint32_t>();
     p.totals = h->totals.as<uint32_t>();
     p.fill = lookback ? nullptr : h->fill.as<uint32_t>();
+    // fill[kHistRows]: long words whose length ingest7 leaves to long_len_fix
+    p.unknown = lookback ? nullptr : h->fill.as<unsigned int>() + kHistRows;
     p.run_at = ordered_reserve ? h->run_at.as<uint32_t>() : nullptr;
     p.run_cnt = ordered_reserve ? h->run_cnt.as<uint32_t>() : nullptr;
     const void* totals_src = lookback ? h->totals.p : h->fill.p;
     auto reset_chain = [&]() -> int {
       if (!lookback) {
-        WS_CUDA(cudaMemsetAsync(h->fill.p, 0, kHistRows * 4, h->st));
+        WS_CUDA(cudaMemsetAsync(h->fill.p, 0, (kHistRows + 1) * 4, h->st));
       } else {
         WS_CUDA(cudaMemsetAsync(h->status.p, 0, (size_t)nchunks * kLookbackRec * 4, h->st));
         WS_CUDA(cudaMemsetAsync(h->ticket.p, 0, 4, h->st));
@@ -1296,6 +1299,9 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
                                 h->st));
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
+        tot_host[kHistRows + 2] = 0;
+        if (p.unknown)
+          WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows + 2, p.unknown, 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
         redo = tot_host[kHistRows] != 0;  // a word spanned a whole piece: ingest again
         if (redo) {
@@ -1324,6 +1330,9 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
         if (h->tiny_launched)
           WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows + 1, h->tiny_flag.p, 4, cudaMemcpyDeviceToHost, h->st));
+        tot_host[kHistRows + 2] = 0;
+        if (p.unknown)
+          WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows + 2, p.unknown, 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaStreamSynchronize(h->st));
         h->tiny_done = h->tiny_launched && tot_host[kHistRows + 1] == 0 && tot_host[kLongBin] == 0;
         if (h->tiny_launched && env_on("WSORT_TINY_PROF")) {
@@ -1456,6 +1465,12 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
       ++h->launches;
     }
     WS_TRY(check_launch("scatter_kernel"));
+  }
+  if (single && tot_host[kHistRows + 2] && m) {  // long words the ingest left unmeasured
+    WS_CUDA(h->first_sep.ensure(long_fix_chunks(n) * 4 + 64));
+    launch_long_len_fix(dtext, n, h->longlist.as<uint2>(), m, h->first_sep.as<uint32_t>(), h->st);
+    h->launches += 2;
+    WS_TRY(check_launch("long_len_fix"));
   }
   WS_TRY(group_long_words(h, m));
   tmark("grouped");
@@ -2139,7 +2154,7 @@ void ws_destroy(ws_handle* h) {
                     &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
                     &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4],
                     &h->ss_ids[1], &h->ss_ids[2], &h->ss_ids[3], &h->ss_ids[4],
-                    &h->tiny_flag, &h->tiny_prof};
+                    &h->tiny_flag, &h->tiny_prof, &h->first_sep};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();

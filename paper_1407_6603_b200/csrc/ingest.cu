@@ -19,6 +19,7 @@
 // A word belongs to the chunk that holds its first byte; a word running past
 // its chunk is measured by scanning forward in global memory (the text is
 // zero padded, and zero is a separator).
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 
@@ -70,6 +71,32 @@ __device__ uint32_t run_length_from(const uint8_t* __restrict__ text, uint64_t p
     len += 16;
     pos += 16;
   }
+}
+
+// run_length_from for at most `limit` bytes: the length, or ~0u when the run
+// is longer (ingest7 leaves such words to long_len_fix_kernel, so one thread
+// never walks a multi-megabyte word).
+constexpr uint32_t kLongScan = 256;
+__device__ uint32_t bounded_run_length(const uint8_t* __restrict__ text, uint64_t pos, uint32_t limit,
+                                       uint64_t avail, unsigned int* overflow) {
+  uint32_t len = 0;
+  while ((pos & 15) != 0) {
+    if (!is_alnum_byte(text[pos])) return len;
+    ++len;
+    ++pos;
+  }
+  while (len < limit) {
+    if (pos + 16 > avail) {
+      if (overflow) atomicOr(overflow, 1u);
+      return len;
+    }
+    const uint4 v = *reinterpret_cast<const uint4*>(text + pos);
+    const uint32_t m = alnum_mask16(v);
+    if (m != 0xFFFFu) return len + __ffs(~m) - 1;
+    len += 16;
+    pos += 16;
+  }
+  return ~0u;
 }
 
 // Starts/ends of the thread's 16-byte segment plus word lengths.
@@ -1167,14 +1194,20 @@ ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
     const uint32_t i = (uint32_t)__ffs(s) - 1;
     const uint32_t r = ends >> i;
     uint32_t L = r ? (uint32_t)__ffs(r) : (32u - i) + nlead;
-    if (L > (uint32_t)kMaxPackedLen) {  // rare: measure in global memory, then the long list
-      if (!r && nlead == 32u)
-        L = (32u - i) + run_length_from(text, base + kI7SB, avail, p.overflow);
-      if (L > (uint32_t)kMaxPackedLen) {
-        if (ORDERED) {  // placed (stably) by the placement pass; its length is measured again there
+    if (L > (uint32_t)kMaxPackedLen) {  // rare
+      if (!r && nlead == 32u) {
+        // runs on past the next segment's first byte (the chunk's last thread
+        // only knows that byte) or through it: measured up to a bound; longer
+        // words get length 0 here and are measured after the ingest
+        const uint32_t more = bounded_run_length(text, base + kI7SB, kLongScan, avail, p.overflow);
+        L = more == ~0u ? 0u : (32u - i) + more;
+      }
+      if (L - 1u >= (uint32_t)kMaxPackedLen) {  // L == 0 or L > 32: the long list
+        if (ORDERED) {  // placed (stably) by the placement pass, which measures it again
           atomicAdd(&sm.wcnt[wid][kLongBin], 1u);
           *wl++ = ((uint32_t)tid * kI7SB + i) | ((uint32_t)kLongBin << 13);
         } else {
+          if (!L && p.unknown) atomicAdd(p.unknown, 1u);
           const uint32_t at = atomicAdd(p.fill + kLongBin, 1u);
           if (p.keys) p.longlist[at] = make_uint2((uint32_t)(base + i), L);
           *wl++ = kI7Skip;
@@ -1250,7 +1283,9 @@ ingest7_kernel(const uint8_t* __restrict__ text, uint64_t n, ScatterParams p) {
           sm.ord[sm.boff[bin] + rank] = (uint16_t)(wid * kI7MaxWords + j);
         } else if (p.keys) {  // long word (rare): its length again, its stable slot in the long list
           const uint32_t st = e & 8191u;
-          const uint32_t L = run_length_from(text, cbase + st, avail, nullptr);
+          const uint32_t L0 = bounded_run_length(text, cbase + st, kLongScan, avail, p.overflow);
+          const uint32_t L = L0 == ~0u ? 0u : L0;  // 0: measured after the ingest
+          if (!L && p.unknown) atomicAdd(p.unknown, 1u);
           p.longlist[sm.base[kLongBin] + rank] = make_uint2((uint32_t)(cbase + st), L);
         }
       }
@@ -1613,6 +1648,93 @@ void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t*
   if (!n) return;
   uint32_t blocks = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 16);
   pack_rows_kernel<<<blocks, 256, 0, st>>>(rows, n, width, keys);
+}
+
+// ---- long words the ingest left unmeasured ---------------------------------------
+constexpr uint32_t kFixChunk = 8192;
+
+// first_sep[c] = offset of the first non-alnum byte of 8 KiB chunk c (bytes
+// past the text count as separators), or ~0u when the chunk is all alnum.
+__global__ void __launch_bounds__(256) chunk_first_sep_kernel(const uint8_t* __restrict__ text, uint64_t n,
+                                                             uint32_t* __restrict__ first_sep) {
+  __shared__ uint32_t s_min;
+  if (threadIdx.x == 0) s_min = ~0u;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * kFixChunk + (uint64_t)threadIdx.x * 32;
+  uint32_t f = ~0u;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint64_t q = base + 16 * k;
+    if (q >= n) {
+      f = min(f, (uint32_t)(threadIdx.x * 32 + 16 * k));
+      break;
+    }
+    const uint32_t m = alnum_mask16(*reinterpret_cast<const uint4*>(text + q));  // padded text
+    if (m != 0xFFFFu) {
+      f = min(f, (uint32_t)(threadIdx.x * 32 + 16 * k) + (uint32_t)__ffs(~m) - 1);
+      break;
+    }
+  }
+  f = __reduce_min_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f != ~0u) atomicMin(&s_min, f);
+  __syncthreads();
+  if (threadIdx.x == 0) first_sep[blockIdx.x] = s_min;
+}
+
+// One warp per long-list entry of length 0: the word's end is the first
+// separator after its start + 33 - in the rest of its chunk (512-byte warp
+// steps), or else at first_sep of the first later chunk that has one (32
+// chunk entries per step).
+__global__ void __launch_bounds__(256) long_len_fix_kernel(const uint8_t* __restrict__ text, uint64_t n,
+                                                          uint2* __restrict__ longlist, uint64_t m,
+                                                          const uint32_t* __restrict__ first_sep) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t nchunks = (n + kFixChunk - 1) / kFixChunk;
+  for (uint64_t e = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < m;
+       e += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+    const uint2 w = longlist[e];
+    if (w.y != 0) continue;  // warp-uniform
+    const uint64_t start = w.x;
+    uint64_t end = ~0ull;
+    // the rest of the start's chunk, 16 bytes per lane per step
+    const uint64_t c0 = start / kFixChunk, cend = min(n, (c0 + 1) * kFixChunk);
+    for (uint64_t q0 = (start + 33) & ~15ull; q0 < cend && end == ~0ull; q0 += 512) {
+      const uint64_t q = q0 + 16 * (uint64_t)lane;
+      uint32_t hit = ~0u;
+      if (q < cend) {
+        uint32_t mk = alnum_mask16(*reinterpret_cast<const uint4*>(text + q));
+        // bytes before start + 33 are inside the word (known alnum)
+        if (q < start + 33) mk |= (1u << (uint32_t)(start + 33 - q)) - 1u;
+        if (mk != 0xFFFFu) hit = (uint32_t)(q - q0) + (uint32_t)__ffs(~mk) - 1;
+      }
+      hit = __reduce_min_sync(0xffffffffu, hit);
+      if (hit != ~0u) end = q0 + hit;
+    }
+    // later chunks: the first one with a separator
+    for (uint64_t c = c0 + 1; c < nchunks && end == ~0ull; c += 32) {
+      const uint64_t cc = c + lane;
+      const uint32_t f = cc < nchunks ? first_sep[cc] : ~0u;
+      const uint32_t has = __ballot_sync(0xffffffffu, f != ~0u);
+      if (has) {
+        const int src = __ffs(has) - 1;
+        const uint32_t fo = __shfl_sync(0xffffffffu, f, src);
+        end = (c + (uint64_t)src) * kFixChunk + fo;
+      }
+    }
+    if (end == ~0ull || end > n) end = n;
+    if (lane == 0) longlist[e].y = (uint32_t)(end - start);
+  }
+}
+
+uint64_t long_fix_chunks(uint64_t n) { return (n + kFixChunk - 1) / kFixChunk; }
+
+void launch_long_len_fix(const uint8_t* text, uint64_t n, uint2* longlist, uint64_t m,
+                         uint32_t* first_sep, cudaStream_t st) {
+  if (!m || !n) return;
+  const uint64_t nc = long_fix_chunks(n);
+  chunk_first_sep_kernel<<<(unsigned)nc, 256, 0, st>>>(text, n, first_sep);
+  const uint64_t blocks = std::min<uint64_t>((m * 32 + 255) / 256, 148 * 16);
+  long_len_fix_kernel<<<(unsigned)blocks, 256, 0, st>>>(text, n, longlist, m, first_sep);
 }
 
 WS_DEFINE_CHECK_READER(check_reader_ingest)

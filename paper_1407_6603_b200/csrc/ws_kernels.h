@@ -22,6 +22,8 @@ struct ScatterParams {
   uint32_t* totals;             // [kHistRows] per-bin totals, written by the last chunk
   uint64_t avail;               // bytes of text already on the device (0 = all)
   unsigned int* overflow;       // set when a word runs past `avail`
+  unsigned int* unknown;        // ingest7: long words whose length is measured after the ingest
+                                // (long-list entry (start, 0); long_len_fix), counted here
   // reserve mode (payload-only sorts): when set, each chunk reserves its run
   // of every bin with one atomicAdd on fill[row] instead of the look-back;
   // runs then land in completion order, so bucket order is not corpus order
@@ -72,6 +74,12 @@ void launch_words_scatter(const uint8_t* bytes, const uint64_t* starts, const ui
                           const ScatterParams& p, cudaStream_t st);
 void launch_pack_rows(const uint8_t* rows, uint64_t n, uint32_t width, uint64_t* keys,
                       cudaStream_t st);
+// Long words the ingest left unmeasured (length 0 in the long list): first
+// separator of every 8 KiB chunk (first_sep[nchunks], scratch), then one warp
+// per entry finds the word's end (the rest of its chunk, then the chunk table).
+void launch_long_len_fix(const uint8_t* text, uint64_t n, uint2* longlist, uint64_t m,
+                         uint32_t* first_sep, cudaStream_t st);
+uint64_t long_fix_chunks(uint64_t n);  // entries of first_sep for a text of n bytes
 
 // sort.cu
 // Segment tables of up to kInlineSegs entries travel in the kernel

@@ -71,6 +71,37 @@ def test_word_spanning_whole_chunks_payload_mode():
         assert sort_text(t) == want
 
 
+def test_long_words_around_the_scan_bound():
+    # the ingest measures a long word up to a bound (256 bytes past its
+    # thread's segment) and leaves longer ones to the post-ingest length fix;
+    # words around that bound, and short words that start in a chunk's last
+    # segment and end past it (which that segment cannot tell from long
+    # ones), at every alignment and next to chunk edges, in a text above the
+    # tiny-path limit
+    rng = np.random.default_rng(17)
+    fill = b" ".join(synth.random_words(7, 120_000, max_len=12, min_len=1))
+    parts = [fill[:300_000]]
+    for L in (20, 33, 200, 255, 256, 257, 280, 287, 288, 289, 300, 511, 1000, 5000, 70_000):
+        for off in (0, 1, 15, 16, 31):
+            parts.append(b" " * (1 + off) + bytes(rng.choice(list(b"abcXYZ"), size=L)))
+    for edge in (4096, 8192):  # ordered and payload chunk edges
+        for short in (3, 20, 40):
+            pos = sum(len(p) for p in parts)
+            gap = (-pos - short // 2) % edge
+            parts.append(b" " * max(gap, 1) + b"k" * short)
+    parts.append(b" " + fill[300_000:])
+    text = b"".join(parts)
+    assert len(text) > 600_000
+    want, _ = oracle.sort_text(text, mode="fast", max_len=80_000)
+    assert sort_text(text) == want
+    for shift in (1, 9):
+        assert sort_text(b" " * shift + text) == want
+    dc = DeviceCorpus()
+    dc.ingest(text)
+    dc.sort(want_stats=True)
+    assert dc.payload() == want
+
+
 @pytest.mark.parametrize("L", [1, 7, 8, 9, 16, 17, 24, 25, 32, 33, 40, 64, 65, 100, 1000])
 def test_single_length_buckets(L):
     words = synth.random_words(L, 300, max_len=L, min_len=L)
