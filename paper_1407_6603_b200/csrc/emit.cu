@@ -120,25 +120,47 @@ void launch_emit(int lanes, int enc, const EmitTable& t, uint32_t blocks, uint8_
 }
 
 // ---------------------------------------------------------------------------
-// Long words (L > 32): one warp per word, bytes copied from the text.
+// Long words (L > 32): one warp per 4 KiB piece of a word (a bucket's words
+// share one length, so piece -> (word, offset) is a division), bytes copied
+// from the text as destination-aligned 4-byte stores, each assembled from the
+// two aligned source words it straddles (funnel shift); ragged ends bytewise.
 // order[i] (optional) maps output position -> index into words[].
+constexpr uint32_t kEmitPiece = 4096;
+
 __global__ void emit_long_kernel(const uint8_t* __restrict__ text, const uint2* __restrict__ words,
                                  const uint32_t* __restrict__ order, uint64_t n, uint32_t len,
-                                 uint8_t* __restrict__ out, int nl) {
+                                 uint32_t ppw, uint8_t* __restrict__ out, int nl) {
   const uint64_t gw = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gw >= n) return;
-  const uint2 w = words[order ? order[gw] : gw];
-  uint8_t* dst = out + gw * (uint64_t)(len + nl);
-  for (uint32_t b = lane; b < len; b += 32) dst[b] = text[(uint64_t)w.x + b];
-  if (nl && lane == 0) dst[len] = '\n';
+  const uint32_t lane = threadIdx.x & 31;
+  if (gw >= n * ppw) return;
+  const uint64_t word = gw / ppw;
+  const uint32_t b0 = (uint32_t)(gw - word * ppw) * kEmitPiece;
+  const uint32_t b1 = min(len, b0 + kEmitPiece);
+  const uint2 w = words[order ? order[word] : word];
+  uint8_t* dst = out + word * (uint64_t)(len + nl);
+  const uint8_t* src = text + w.x;
+  const uint32_t head = min((uint32_t)(-(uintptr_t)(dst + b0) & 3), b1 - b0);
+  if (lane < head) dst[b0 + lane] = src[b0 + lane];
+  const uint32_t b = b0 + head, nw = (b1 - b) >> 2;
+  uint32_t* dw = reinterpret_cast<uint32_t*>(dst + b);
+  const uint32_t sh = (uint32_t)((uintptr_t)(src + b) & 3) * 8;
+  const uint32_t* sw = reinterpret_cast<const uint32_t*>((uintptr_t)(src + b) & ~(uintptr_t)3);
+  if (sh) {
+    for (uint32_t k = lane; k < nw; k += 32) dw[k] = __funnelshift_r(sw[k], sw[k + 1], sh);
+  } else {
+    for (uint32_t k = lane; k < nw; k += 32) dw[k] = sw[k];
+  }
+  const uint32_t t = b + 4 * nw;
+  if (lane < b1 - t) dst[t + lane] = src[t + lane];
+  if (nl && lane == 0 && b1 == len) dst[len] = '\n';
 }
 
 void launch_emit_long(const uint8_t* text, const uint2* words, const uint32_t* order, uint64_t n,
                       uint32_t len, uint8_t* out, int with_newline, cudaStream_t st) {
   if (!n) return;
-  uint64_t threads = n * 32;
-  emit_long_kernel<<<(uint32_t)((threads + 255) / 256), 256, 0, st>>>(text, words, order, n, len,
+  const uint32_t ppw = (len + kEmitPiece - 1) / kEmitPiece;
+  const uint64_t threads = n * ppw * 32;
+  emit_long_kernel<<<(uint32_t)((threads + 255) / 256), 256, 0, st>>>(text, words, order, n, len, ppw,
                                                                       out, with_newline);
 }
 

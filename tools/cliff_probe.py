@@ -1,5 +1,6 @@
 """Resident-step time on adversarial inputs (performance cliffs), payload
-checked against the oracle: python tools/cliff_probe.py [names...]"""
+checked against the oracle: python tools/cliff_probe.py [--phases] [names...]
+(--phases: also the per-phase device times of one profiled step)"""
 import json, statistics, sys, time
 sys.path.insert(0, '.')
 import numpy as np
@@ -40,11 +41,22 @@ def run(name, text):
         a.record(); h.sort_resident(len(text)); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
     got = device_bytes(*h.output_device())
+    phases = None
+    if PHASES:
+        h.profile(reset=True)
+        h.set_profiling(True)
+        h.sort_resident(len(text))
+        h.set_profiling(False)
+        phases = {}
+        for p in h.profile(reset=True):
+            phases[p["name"]] = round(phases.get(p["name"], 0) + p["ms"], 4)
     t0 = time.time()
     want, _ = oracle.sort_text(text, mode="fast", max_len=1 << 27)
     print(json.dumps({"case": name, "bytes": len(text), "ms": round(statistics.median(ts), 4),
-                      "parity": got == want, "oracle_s": round(time.time() - t0, 1)}), flush=True)
+                      "parity": got == want, "oracle_s": round(time.time() - t0, 1),
+                      **({"phases": phases} if phases else {})}), flush=True)
 
 
-for name in sys.argv[1:] or CASES:
+PHASES = "--phases" in sys.argv
+for name in [a for a in sys.argv[1:] if a != "--phases"] or CASES:
     run(name, CASES[name]())
