@@ -672,6 +672,12 @@ def main():
         bench_reference(args)
     else:
         bench_ours(args)
+    # The JSON line is out. Skip interpreter teardown: with the reference's
+    # numba thread pool and the CUDA context both alive, teardown crashed once
+    # (SIGSEGV after the line was printed) on a fresh box.
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(0)
 
 
 if __name__ == "__main__":

@@ -202,6 +202,7 @@ struct ws_handle {
   uint32_t radix_epoch = 0;
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   DevBuf ss_ids[kClasses + 1];                            // per-key slot ids
+  DevBuf ss_scratch;  // slot-sort merge scratch when the input keys sit in keys[0]
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
   uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
@@ -821,6 +822,17 @@ int sample_sort_segments(ws_handle* h, int lanes, std::vector<SegIn>& segs, uint
   a.nslots = slots;
   a.work_items = tiles;
   a.keys_out = out_class;
+  // slots beyond a tile merge through the class region of keys[0] when no
+  // bucket reads its input from there (the single-pass ingest leaves the keys
+  // in keys_cap), else through a buffer of their own
+  bool in_k0 = false;
+  for (const auto& s : segs) in_k0 |= s.in_ptr == class_keys(h, 0, lanes, s.key_off);
+  if (!in_k0) {
+    a.scratch = class_keys(h, 0, lanes, 0);
+  } else {
+    WS_CUDA(h->ss_scratch.ensure((size_t)h->class_elems[lanes] * key_bytes(lanes) + 64));
+    a.scratch = h->ss_scratch.as<uint64_t>();
+  }
   a.splitters = h->ss_split[lanes].as<uint64_t>();
   a.hist = h->ss_slots[lanes].as<uint32_t>();
   a.cursor = a.hist + slots;
@@ -1225,7 +1237,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
       WS_CUDA(h->longlist2.ensure(((n + 1) / (kMaxPackedLen + 2) + 1) * sizeof(uint2)));
     }
     WS_CUDA(h->ticket.ensure(256));
-    WS_CUDA(h->fill.ensure(kHistRows * 4));
+    WS_CUDA(h->fill.ensure((kHistRows + 1) * 4));  // + the unknown-length counter
     for (int b = 0; b < kMaxPackedLen; ++b) p.bin_base[b] = region[b];
     p.keys = h->keys_cap.as<uint64_t>();
     p.longlist = h->longlist.as<uint2>();
@@ -2154,7 +2166,7 @@ void ws_destroy(ws_handle* h) {
                     &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
                     &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4],
                     &h->ss_ids[1], &h->ss_ids[2], &h->ss_ids[3], &h->ss_ids[4],
-                    &h->tiny_flag, &h->tiny_prof, &h->first_sep};
+                    &h->tiny_flag, &h->tiny_prof, &h->first_sep, &h->ss_scratch};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();

@@ -1091,10 +1091,11 @@ __global__ void __launch_bounds__(kSubThreads, LANES <= 1 ? WS_SUB1_MINB : WS_SU
   // A slot beyond one tile (sampling variance, or a sample that misses the
   // bucket's spread): merge sort in O(cnt log cnt) by this CTA. Tiles of TS
   // keys are sorted on chip, then merge-path levels ping-pong between the
-  // slot and its scratch: the same range of the bucket's input keys, which no
-  // one reads after the scatter pass. The block pass writes to the side that
+  // slot and its scratch: the slot's range in a third buffer (a.scratch; not
+  // the input keys, which a later ws_sort of the same ingest reads again). The
+  // block pass writes to the side that
   // makes the last level land in the slot.
-  W* const scratch = const_cast<W*>(kv<LANES>(sg.in)) + (uint64_t)(a.slot_off[s] - sg.key_off) * NW;
+  W* const scratch = kv<LANES>(a.scratch) + (uint64_t)a.slot_off[s] * NW;
   const uint32_t blocks = (cnt + TS - 1) / TS;
   int levels = 0;
   while ((1u << levels) < blocks) ++levels;

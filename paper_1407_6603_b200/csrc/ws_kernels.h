@@ -123,6 +123,9 @@ struct SampleLaunch {
   uint32_t nslots;
   uint32_t work_items;    // partition tiles of all buckets
   uint64_t* keys_out;     // the class region of the output key buffer
+  uint64_t* scratch;      // class region of a buffer that is neither the input nor keys_out:
+                          // slot sorts beyond a tile merge through it (never the input keys,
+                          // which a later ws_sort of the same ingest reads again)
   uint64_t* splitters;    // 64-bit key prefixes
   uint32_t* hist;         // per slot: keys (zeroed before the launch)
   uint32_t* cursor;       // per slot: reservation cursor

@@ -397,6 +397,29 @@ def test_fused_payload_sort_then_emit_needs_sort():
     h.close()
 
 
+def test_slot_beyond_tile_keeps_input_for_a_second_sort():
+    # The sample's positions (i * n / m) all hold the smallest word, every other
+    # position a distinct larger word: all splitters are equal, so one slot
+    # holds ~n keys, far beyond a slot sort's tile, and takes the in-CTA merge
+    # sort. Its merge scratch must not be the input keys: a second ws_sort of
+    # the same ingest reads them again (found as a 1-in-60 failure of
+    # test_fused_payload_sort_then_emit_needs_sort on unordered ingests).
+    rng2 = np.random.default_rng(11)
+    n, m = 30_000, 256
+    sampled = {i * n // m for i in range(m)}
+    letters = np.frombuffer(b"abcdefghijklmnopqrstuvwxyz", np.uint8)
+    words = []
+    for i in range(n):
+        words.append(b"000000" if i in sampled else bytes(letters[rng2.integers(0, 26, size=6)]))
+    want = b"".join(w + b"\n" for w in sorted(words))
+    h = _native.Handle(0)
+    h.ingest_words(words)
+    for _ in range(3):
+        h.sort(False)
+        assert h.emit_lines().tobytes() == want
+    h.close()
+
+
 def test_fused_slot_records_repeats_singletons_and_alignment():
     # multi-lane buckets (6..32 characters) whose slot sorts write payload
     # records directly: one word repeated 1..90k times (pattern fill at every
