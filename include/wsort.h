@@ -186,6 +186,13 @@ int ws_profile(ws_handle* h, ws_phase* out, int32_t cap, int32_t* n);
 int ws_profile_reset(ws_handle* h);
 /* Kernel launches issued by this handle since creation. */
 int ws_launch_count(ws_handle* h, uint64_t* launches);
+/* Lane classes (bit c = class c: words of 1-5, 6-10, 11-21, 22-32 characters)
+ * whose payload the last fused sort (ws_sort_text / ws_sort_texts /
+ * ws_sort_resident) produced by counting distinct words instead of sorting
+ * every occurrence (texts that repeat their vocabulary; same bytes either way:
+ * the reference's printed payload, cli.py:97, depends only on which words a
+ * bucket holds and how often). 0 when every class was sorted. */
+int ws_counted_classes(ws_handle* h, int32_t* mask);
 
 /* Checked builds (compiled with WS_CHECKED=1; tools/checked_build.sh): every
  * kernel bounds-checks its computed shared / global indices and records the

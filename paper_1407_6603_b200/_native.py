@@ -37,7 +37,7 @@ EXPORTS = (
     "ws_sort_text", "ws_sort_rows", "ws_sort_blocks", "ws_stats_closed_form",
     "ws_set_profiling", "ws_profile", "ws_profile_reset", "ws_launch_count", "ws_stream",
     "ws_host_alloc", "ws_host_free", "ws_sort_resident", "ws_output_device", "ws_sort_texts",
-    "ws_debug_checks", "ws_checked_build",
+    "ws_debug_checks", "ws_checked_build", "ws_counted_classes",
 )
 
 
@@ -91,6 +91,7 @@ def _declare(lib) -> None:
         "ws_profile": (I, [V, ctypes.POINTER(WsPhase), ctypes.c_int32, c_i32p]),
         "ws_profile_reset": (I, [V]),
         "ws_launch_count": (I, [V, c_u64p]),
+        "ws_counted_classes": (I, [V, c_i32p]),
         "ws_stream": (I, [V, ctypes.POINTER(V)]),
         "ws_host_alloc": (I, [ctypes.c_uint64, ctypes.POINTER(V)]),
         "ws_host_free": (I, [V]),
@@ -389,6 +390,13 @@ class Handle:
         v = ctypes.c_uint64(0)
         check(self.lib.ws_launch_count(self.h, ctypes.byref(v)))
         return int(v.value)
+
+    def counted_classes(self) -> int:
+        """Bit c set: the last fused sort counted lane class c's distinct words
+        instead of sorting every occurrence (same payload bytes)."""
+        m = ctypes.c_int32(0)
+        check(self.lib.ws_counted_classes(self.h, ctypes.byref(m)))
+        return int(m.value)
 
     def stream(self) -> int:
         s = c_void_p()

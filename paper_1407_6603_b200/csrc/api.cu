@@ -137,6 +137,7 @@ struct Bucket {
   int final_buf = 0;         // packed: which key/idx buffer holds the sorted run
   int64_t inv = 0, kmax = 0; // stats (valid after ws_sort(h, 1))
   const uint64_t* in_ptr = nullptr;  // packed: the unsorted keys (ingest output)
+  uint32_t dd_n = 0;         // counted class (dedupe.cu): the bucket's distinct words
 };
 
 struct PhaseRec {
@@ -203,6 +204,17 @@ struct ws_handle {
   DevBuf ss_split[kClasses + 1], ss_slots[kClasses + 1];  // sample sort of classes 1..4
   DevBuf ss_ids[kClasses + 1];                            // per-key slot ids
   DevBuf ss_scratch;  // slot-sort merge scratch when the input keys sit in keys[0]
+  // distinct-word counting (dedupe.cu): control words + tables, distinct keys, run prefixes
+  DevBuf dd_pool, dd_keys, dd_aux, dd_ts, dd_plan;
+  cudaEvent_t ev_dd = nullptr, ev_chain = nullptr;  // aggregate launched / device-planned chain done
+  bool dd_chain = false;          // the chain behind the aggregate launch writes the counted classes' payload
+  cudaStream_t zs = nullptr;      // zeroes the table pool beside the ingest
+  cudaEvent_t ev_zero = nullptr;
+  bool dd_req = false;            // the next ingest counts distinct words right behind itself
+  bool dd_launched = false;       // ... and did
+  bool dd_ok[kClasses + 1] = {false};  // per lane class: every bucket stayed in budget
+  int dd_used = 0;                // classes the last fused sort took through the counts (bit mask)
+  DdLayout dd_lay;                // tables / distinct-key lists of the current buckets
   PinBuf pin_params, pin_small;
   size_t param_used = 0;
   uint64_t out_size = 0;  // payload bytes left in `out` by ws_sort_resident
@@ -320,6 +332,7 @@ int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev,
       if (h->ds[c]) WS_CUDA(cudaStreamSynchronize(h->ds[c]));
     }
     if (h->hs) WS_CUDA(cudaStreamSynchronize(h->hs));
+    if (h->zs) WS_CUDA(cudaStreamSynchronize(h->zs));
     size_t need = std::max<size_t>(2 * (off + bytes), 1 << 20);
     if (need > h->pin_params.cap) {
       h->pin_params.release();
@@ -1046,6 +1059,114 @@ int launch_tiny(ws_handle* h, const uint64_t* region, uint64_t n) {
   return WS_OK;
 }
 
+// Distinct-word counting (dedupe.cu) right behind the payload-mode ingest, on
+// the main stream: the ingest's sync then also covers its counters. WSORT_NO_DEDUPE=1
+// turns it off; WSORT_DEDUPE_MIN=bytes sets the smallest text that tries it.
+bool dedupe_wanted(uint64_t n) {
+  static const bool off = env_on("WSORT_NO_DEDUPE") || env_on("WSORT_D2H_PER_CLASS") ||
+                          env_on("WSORT_NO_FUSED_PAYLOAD");
+  static const uint64_t min_text = [] {
+    const char* e = getenv("WSORT_DEDUPE_MIN");
+    return e ? (uint64_t)strtoull(e, nullptr, 0) : (uint64_t)(1u << 20);
+  }();
+  return !off && n >= min_text;
+}
+
+size_t dd_pool_bytes(uint64_t n) { return (size_t)kDdCtlWords * 4 + dd_max_table_slots(n) * 8; }
+
+// Zero the control words and the table pool for a text of n bytes (upper
+// bound: the counts are not known yet) on the side stream.
+int dd_zero_pool(ws_handle* h, uint64_t n, cudaStream_t st) {
+  WS_CUDA(h->dd_pool.ensure(dd_pool_bytes(n) + 64));
+  WS_CUDA(h->dd_keys.ensure(dd_max_dk_bytes(n) + 64));
+  WS_CUDA(h->dd_ts.ensure(dd_max_dk_bytes(n) + 64));
+  // per-distinct-word arrays A and B + the run prefix's tile totals
+  WS_CUDA(h->dd_aux.ensure((2 * dd_max_distinct(n) + dd_max_distinct(n) / kDdTile + 4 * kDdLens +
+                            (n + 1) / 1024 + 2 * kDdLens) * 4 + 64));  // ... and the output tiles' first runs
+  WS_CUDA(h->dd_plan.ensure(sizeof(DdDevPlan)));
+  WS_CUDA(h->out.ensure(n + 1 + 64));  // the payload never exceeds the text by more than a byte
+  WS_CUDA(cudaMemsetAsync(h->dd_pool.p, 0, dd_pool_bytes(n), st));
+  return WS_OK;
+}
+
+int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
+  if (h->dd_launched) {  // a redone ingest: the pool holds the first attempt's entries
+    WS_TRY(dd_zero_pool(h, h->n_text, h->st));
+  } else {
+    WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_zero, 0));
+  }
+  DdAgg a;
+  memset(&a, 0, sizeof a);
+  a.fill = h->fill.as<uint32_t>();
+  a.keys_cap = h->keys_cap.as<uint8_t>();
+  for (int b = 0; b < 32; ++b) a.region[b] = region[b];
+  a.ctl = h->dd_pool.as<uint32_t>();
+  a.table = reinterpret_cast<uint2*>(h->dd_pool.as<uint32_t>() + kDdCtlWords);
+  a.dk = h->dd_keys.as<uint8_t>();
+  a.aux = h->dd_aux.as<uint32_t>();
+  a.plan = h->dd_plan.as<DdDevPlan>();
+  a.stile1 = (uint32_t)dd_sort_tile_size(1);
+  a.stilen = (uint32_t)dd_sort_tile_size(2);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  const uint64_t max_tiles = (h->n_text + 1) / 2 / 4096 + 32;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, 2ull * sms));
+  {
+    Phase ph(h, "dd_aggregate", 0.0, 0, h->st);  // bytes patched once the counts are known
+    launch_dd_aggregate(a, grid, h->st);
+    ++h->launches;
+  }
+  WS_TRY(check_launch("dd_aggregate"));
+  h->dd_launched = true;
+  // The rest of the counted classes' path, planned on the device (the
+  // aggregate launch's last CTA) and enqueued now on the side stream: distinct
+  // keys sorted (tiles, then a rank merge), run prefixes, payload records --
+  // while the host still waits for the ingest's counters.
+  h->dd_chain = false;
+  {
+    cudaStream_t xs = h->serial ? h->st : h->zs;  // (serialised profiles: everything on the main stream)
+    WS_CUDA(cudaEventRecord(h->ev_dd, h->st));
+    if (xs != h->st) WS_CUDA(cudaStreamWaitEvent(xs, h->ev_dd, 0));
+    DdChain c;
+    memset(&c, 0, sizeof c);
+    c.fill = a.fill;
+    c.ctl = a.ctl;
+    c.plan = h->dd_plan.as<DdDevPlan>();
+    c.keys_cap = a.keys_cap;
+    for (int b = 0; b < 32; ++b) c.region[b] = region[b];
+    c.table = a.table;
+    c.dk = a.dk;
+    c.ts = h->dd_ts.as<uint8_t>();
+    c.aux = a.aux;
+    c.out = h->out.as<uint8_t>();
+    const int cgrid = 4 * sms;
+    {
+      Phase ph(h, "dd_tiles", 0.0, 0, xs);  // bytes patched once the counts are known
+      launch_dd_tiles(c, cgrid, xs);
+      ++h->launches;
+    }
+    {
+      Phase ph(h, "dd_rank", 0.0, 0, xs);
+      launch_dd_rank(c, cgrid, xs);
+      ++h->launches;
+    }
+    {
+      Phase ph(h, "dd_prefix", 0.0, 0, xs);
+      launch_dd_prefix(c, cgrid, xs);
+      h->launches += 3;
+    }
+    {
+      Phase ph(h, "dd_expand", 0.0, 0, xs);
+      launch_dd_chain_expand(c, 8 * sms, xs);
+      ++h->launches;
+    }
+    WS_CUDA(cudaEventRecord(h->ev_chain, xs));
+    WS_TRY(check_launch("dd_chain"));
+    h->dd_chain = true;
+  }
+  return WS_OK;
+}
+
 int launch_early_hist(ws_handle* h, const uint64_t* region) {
   cudaStream_t cst = h->serial ? h->st : h->cs[0];
   DevBuf& tb = h->rtotals[0];
@@ -1064,6 +1185,8 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   e.totals = tb.as<uint32_t>();
   e.joint = e.totals + (size_t)kRadixC0Segs * kRadixMaxPasses * kRadixTotStride + kRadixMaxPasses;
   e.joint_ok = !env_on("WSORT_NO_JOINT");
+  const uint32_t* dd_skip = h->dd_launched ? h->dd_pool.as<uint32_t>() + kDdCtlSkip : nullptr;
+  e.skip = dd_skip;
   {
     Phase ph(h, "radix_hist_l0", 0.0, 0, cst);  // bytes patched once the counts are known
     launch_radix_hist_early(e, cst);
@@ -1114,6 +1237,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     se.cap = sample_bucket_limit(c);
     se.splitters = h->ss_split[c].as<uint64_t>();
     se.hist = h->ss_slots[c].as<uint32_t>();
+    se.skip = dd_skip ? dd_skip + c : nullptr;
     if (count_ok) {
       se.plan = h->early_plan[c].as<SampleLaunch>();
       se.slot_ids = h->ss_ids[c].as<uint16_t>();
@@ -1134,7 +1258,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
       char nm[20];
       snprintf(nm, sizeof nm, "part_count_l%d", c);
       Phase ph(h, nm, 0.0, 0, sst);
-      launch_partition_count_early(c, h->early_plan[c].as<SampleLaunch>(), grid, sst);
+      launch_partition_count_early(c, h->early_plan[c].as<SampleLaunch>(), grid, sst, se.skip);
       ++h->launches;
       h->count_early[c] = true;
     }
@@ -1142,6 +1266,8 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   WS_TRY(check_launch("sample_split_early"));
   return WS_OK;
 }
+
+constexpr int kDdHostOff = 64;  // dedupe control words in the pinned read-back area (uint32 index)
 
 int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flags,
                      std::mutex* gate = nullptr) {
@@ -1157,6 +1283,9 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     return fail(WS_ERR_ARG, "null text");
   }
   h->tiny_launched = h->tiny_done = false;
+  h->dd_launched = h->dd_chain = false;
+  h->dd_used = 0;
+  for (bool& f : h->dd_ok) f = false;
   h->ingested = h->sorted = h->have_stats = h->payload_only = false;
   h->have_tokens = false;
   h->unordered = false;
@@ -1224,6 +1353,13 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     static const char* lb_env = getenv("WSORT_LOOKBACK");
     const bool ordered_reserve = !reserve && !keep_tokens && !(lb_env && lb_env[0] == '1');
     const bool lookback = !reserve && !ordered_reserve;
+    // distinct-word counting behind the ingest: the table pool is zeroed on a
+    // side stream while the ingest runs
+    const bool dd_try = reserve && h->dd_req && h->enc == kEncAlnum6 && !h->tiny_req && n > 0;
+    if (dd_try) {
+      WS_TRY(dd_zero_pool(h, n, h->zs));
+      WS_CUDA(cudaEventRecord(h->ev_zero, h->zs));
+    }
     // the ordered reserve ingest of text keys runs on 8 KiB chunks (ingest7_kernel<true>)
     const uint64_t ocb = ordered_reserve && h->enc == kEncAlnum6 ? ordered_chunk_bytes() : ingest_chunk_bytes();
     const uint32_t nchunks = ordered_reserve ? (uint32_t)((n + ocb - 1) / ocb) : chunk_count(n);
@@ -1306,8 +1442,14 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           gate_lk.unlock();
           if (getenv("WSORT_TRACE")) fprintf(stderr, "wsort-trace handle=%p h2d_landed=%.3f\n", (void*)h, trace_ms());
         }
-        if (reserve && h->tiny_req && h->enc == kEncAlnum6) WS_TRY(launch_tiny(h, region, n));
-        else if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        if (reserve && h->tiny_req && h->enc == kEncAlnum6) {
+          WS_TRY(launch_tiny(h, region, n));
+        } else {
+          if (dd_try) WS_TRY(launch_dd_aggregate_early(h, region));
+          if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        }
+        if (h->dd_launched)
+          WS_CUDA(cudaMemcpyAsync(tot_host + kDdHostOff, h->dd_pool.p, kDdCtlWords * 4, cudaMemcpyDeviceToHost, h->st));
         WS_CUDA(cudaMemcpyAsync(tot_host + kHistRows, h->overflow.p, 4, cudaMemcpyDeviceToHost,
                                 h->st));
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1321,7 +1463,7 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           h->early_done = false;
           for (bool& f : h->split_early) f = false;
           for (bool& f : h->count_early) f = false;
-          WS_TRY(reset_chain());
+          WS_TRY(reset_chain());  // (a second dd_aggregate launch zeroes the pool itself)
         }
       }
       if (!chunked || redo) {
@@ -1336,8 +1478,14 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           ++h->launches;
         }
         WS_TRY(check_launch("ingest_kernel"));
-        if (reserve && h->tiny_req && h->enc == kEncAlnum6) WS_TRY(launch_tiny(h, region, n));
-        else if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        if (reserve && h->tiny_req && h->enc == kEncAlnum6) {
+          WS_TRY(launch_tiny(h, region, n));
+        } else {
+          if (dd_try) WS_TRY(launch_dd_aggregate_early(h, region));
+          if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+        }
+        if (h->dd_launched)
+          WS_CUDA(cudaMemcpyAsync(tot_host + kDdHostOff, h->dd_pool.p, kDdCtlWords * 4, cudaMemcpyDeviceToHost, h->st));
         tmark("early_enq");
         WS_CUDA(cudaMemcpyAsync(tot_host, totals_src, kHistRows * 4, cudaMemcpyDeviceToHost, h->st));
         if (h->tiny_launched)
@@ -1376,6 +1524,41 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     tmark("synced");
     WS_TRY(plan_packed(h, counts));  // compact layout of the sort buffers
     tmark("planned");
+    if (h->dd_launched) {
+      // classes whose buckets all stayed in budget sort their distinct words only
+      const uint32_t* ctl = tot_host + kDdHostOff;
+      uint32_t n32[kDdLens];
+      for (int b = 0; b < kDdLens; ++b) n32[b] = (uint32_t)counts[b];
+      dd_host_layout(n32, h->dd_lay);
+      for (int c = 0; c < 4; ++c) h->dd_ok[c] = ctl[kDdCtlSkip + c] != 0;
+      for (auto& bk : h->buckets) {
+        if (bk.is_long || !h->dd_ok[bk.lanes]) continue;
+        bk.dd_n = ctl[kDdCtlCount + bk.len - 1];
+        if (bk.dd_n == 0 || bk.dd_n > h->dd_lay.dcap[bk.len - 1] || bk.dd_n > bk.count)
+          return fail(WS_ERR_STATE, "distinct-word count out of range");
+      }
+      if (h->dd_ok[0]) h->early_done = false;  // the class's early launches did nothing
+      for (int c = 1; c < 4; ++c)
+        if (h->dd_ok[c]) h->split_early[c] = h->count_early[c] = false;
+      if (h->prof) {
+        double kb = 0;
+        for (auto& bk : h->buckets)
+          if (!bk.is_long) kb += (double)bk.count * key_bytes(bk.lanes);
+        double dkb = 0, pay = 0;  // counted classes: distinct keys, payload records
+        for (auto& bk : h->buckets)
+          if (!bk.is_long && h->dd_ok[bk.lanes]) {
+            dkb += (double)bk.dd_n * (key_bytes(bk.lanes) + 4.0);
+            pay += (double)bk.count * (bk.len + 1);
+          }
+        for (auto& r : h->phases) {
+          if (r.bytes != 0.0) continue;
+          if (r.name == "dd_aggregate") r.bytes = kb;
+          else if (r.name == "dd_tiles" || r.name == "dd_rank") r.bytes = 2.0 * dkb;  // keys + occurrences in and out
+          else if (r.name == "dd_prefix") r.bytes = dkb;
+          else if (r.name == "dd_expand") r.bytes = pay + dkb;
+        }
+      }
+    }
     if (h->prof && h->early_phase_first) {  // bytes of the device-planned early launches
       for (size_t i = h->early_phase_first - 1; i < h->phases.size(); ++i) {
         PhaseRec& r = h->phases[i];
@@ -1533,6 +1716,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   if (stats && h->unordered)
     return fail(WS_ERR_STATE, "stats need corpus order: ingest without WS_INGEST_UNORDERED");
   if (fe) h->sorted = true;  // bucket final buffers are fixed at planning time
+  h->dd_used = 0;
   h->payload_only = false;
   const int nb = (int)h->buckets.size();
   if (stats) {
@@ -1548,6 +1732,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   long long* km = stats ? h->stat_k.as<long long>() : nullptr;
   // packed buckets: one schedule per lane class, each class on its own stream
   // (the classes are independent; small classes fill the big one's bubbles)
+  if (h->dd_chain) WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_chain, 0));  // the call ends after the chain
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
   // class 0 (radix: a chain of small passes, the longest) is submitted first
   // on a high-priority stream; the multi-lane classes fill around it
@@ -1572,6 +1757,8 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     }
     std::vector<SegIn> segs;
     std::vector<int> which;
+    // a counted class: its words were counted behind the ingest and every bucket stayed in budget
+    const bool dd_cls = !stats && fe && !fe->per_class && c < 4 && h->dd_ok[c] && h->unordered && h->dd_chain;
     for (int i = 0; i < nb; ++i) {
       const Bucket& b = h->buckets[i];
       if (b.is_long || b.lanes != c) continue;
@@ -1580,6 +1767,28 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       which.push_back(i);
     }
     if (segs.empty()) continue;
+    if (dd_cls) h->dd_used |= 1 << c;
+    if (dd_cls) {
+      // the device-planned chain behind the ingest writes this class's payload
+      h->payload_only = true;
+      if (fe->host) {
+        cudaStream_t dst = h->ds[c];
+        uint64_t lo = UINT64_MAX, hi = 0;
+        for (int i : which) {
+          lo = std::min(lo, fe->off[i]);
+          hi = std::max(hi, fe->off[i + 1]);
+        }
+        WS_CUDA(cudaStreamWaitEvent(dst, h->ev_chain, 0));
+        {
+          Phase ph(h, "d2h_out", (double)(hi - lo), 1, dst);
+          WS_CUDA(cudaMemcpyAsync(fe->host + lo, fe->dout + lo, hi - lo, cudaMemcpyDeviceToHost, dst));
+        }
+        cudaEvent_t e2 = sync_event(h);
+        WS_CUDA(cudaEventRecord(e2, dst));
+        WS_CUDA(cudaStreamWaitEvent(h->st, e2, 0));
+      }
+      continue;
+    }
     static const char* cls_mark[kClasses + 1] = {"cls0", "cls1", "cls2", "cls3", "cls4"};
     tmark(cls_mark[c]);
     cudaStream_t cst = h->serial ? h->st : h->cs[c];
@@ -1640,10 +1849,11 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
     if (!stats && c == 0 && !(no_radix && no_radix[0] == '1')) {
       // the last pass of each bucket writes its payload records directly
       static const char* no_fuse = getenv("WSORT_NO_FUSED_PAYLOAD");
-      const bool fuse = on_done && !(no_fuse && no_fuse[0] == '1');
+      const bool fuse = on_done && !(no_fuse && no_fuse[0] == '1') && !dd_cls;
       WS_TRY(radix_sort_segments(h, c, segs, k0, k1, cst, on_done, fuse ? fe->dout : nullptr,
                                  fuse ? &fe->off : nullptr));
       for (const SegIn& sg : segs) h->payload_only |= sg.emitted;
+      h->payload_only |= dd_cls;
     } else if (!stats && c >= 1 && !(no_sample && no_sample[0] == '1')) {
       // buckets beyond what the splitter budget keeps at slot size go through
       // the merge path (same stream; both leave per-bucket final buffers)
@@ -1657,7 +1867,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       static const char* no_fuse_s = getenv("WSORT_NO_FUSED_PAYLOAD");
       static const char* no_fuse_slots = getenv("WSORT_NO_FUSED_SLOTS");
       static const char* fuse_mask = getenv("WSORT_FUSED_SLOT_CLASSES");  // experiment: bit c = class c
-      const bool fuse_s = on_done && !(no_fuse_s && no_fuse_s[0] == '1') &&
+      const bool fuse_s = on_done && !dd_cls && !(no_fuse_s && no_fuse_s[0] == '1') &&
                           !(no_fuse_slots && no_fuse_slots[0] == '1') &&
                           (!fuse_mask || ((strtol(fuse_mask, nullptr, 0) >> c) & 1));
       if (!fit.empty())
@@ -1670,6 +1880,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       for (size_t j = 0; j < segs.size(); ++j)
         segs[j].final_buf = segs[j].n <= cap ? fit[fi++].final_buf : big[bi++].final_buf;
       for (const SegIn& sg : fit) h->payload_only |= sg.emitted;
+      h->payload_only |= dd_cls;
       (void)fit_w; (void)big_w;
     } else {
       WS_TRY(sort_segments(h, c, segs, k0, k1, h->idx[0].as<uint32_t>(),
@@ -1763,6 +1974,7 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   }
   WS_TRY(check_launch("sort"));
   h->early_done = false;  // early launches serve only the sort right after their ingest
+  for (bool& f : h->dd_ok) f = false;  // ... and so do the distinct-word counts
   for (bool& f : h->split_early) f = false;
   h->sorted = true;
   h->have_stats = stats;
@@ -2131,6 +2343,10 @@ int ws_create(ws_handle** out, int32_t device) {
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&h->ds[c], cudaStreamNonBlocking, prio_hi);
   }
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->zs, cudaStreamNonBlocking, prio_lo);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_zero, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dd, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_chain, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   for (int c = 0; c <= kClasses && e == cudaSuccess; ++c)
     e = cudaEventCreateWithFlags(&h->ev_join[c], cudaEventDisableTiming);
@@ -2149,6 +2365,7 @@ void ws_destroy(ws_handle* h) {
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->hs) cudaStreamSynchronize(h->hs);
+  if (h->zs) cudaStreamSynchronize(h->zs);
   for (int c = 0; c <= kClasses; ++c) {
     if (h->cs[c]) cudaStreamSynchronize(h->cs[c]);
     if (h->es[c]) cudaStreamSynchronize(h->es[c]);
@@ -2166,7 +2383,8 @@ void ws_destroy(ws_handle* h) {
                     &h->ss_split[1], &h->ss_split[2], &h->ss_split[3], &h->ss_split[4],
                     &h->ss_slots[1], &h->ss_slots[2], &h->ss_slots[3], &h->ss_slots[4],
                     &h->ss_ids[1], &h->ss_ids[2], &h->ss_ids[3], &h->ss_ids[4],
-                    &h->tiny_flag, &h->tiny_prof, &h->first_sep, &h->ss_scratch};
+                    &h->tiny_flag, &h->tiny_prof, &h->first_sep, &h->ss_scratch,
+                    &h->dd_pool, &h->dd_keys, &h->dd_aux, &h->dd_ts, &h->dd_plan};
   for (DevBuf* b : bufs) b->release();
   h->pin_params.release();
   h->pin_small.release();
@@ -2183,6 +2401,10 @@ void ws_destroy(ws_handle* h) {
     if (h->ev_join[c]) cudaEventDestroy(h->ev_join[c]);
   }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_zero) cudaEventDestroy(h->ev_zero);
+  if (h->ev_dd) cudaEventDestroy(h->ev_dd);
+  if (h->ev_chain) cudaEventDestroy(h->ev_chain);
+  if (h->zs) cudaStreamDestroy(h->zs);
   if (h->hs) cudaStreamDestroy(h->hs);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
@@ -2326,9 +2548,10 @@ int sort_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, uint8_t* out, 
   h->early_req = early_hist_wanted();
   h->enc = kEncAlnum6;
   h->tiny_req = tiny_wanted(h, n);
+  h->dd_req = dedupe_wanted(n);
   if (h->tiny_req) WS_CUDA(h->out.ensure(n + 64));
   const int irc = ingest_text_impl(h, text, n, WS_INGEST_UNORDERED, gate);  // ends with a sync
-  h->early_req = h->tiny_req = false;
+  h->early_req = h->tiny_req = h->dd_req = false;
   WS_TRY(irc);
   const double t_ingested = trace ? trace_ms() : 0;
   params_reset(h);  // the ingest synchronised: staging space is free again
@@ -2412,9 +2635,10 @@ int ws_sort_resident(ws_handle* h, uint64_t n, uint64_t* written) {
   h->early_req = early_hist_wanted();
   h->enc = kEncAlnum6;
   h->tiny_req = tiny_wanted(h, n);
+  h->dd_req = dedupe_wanted(n);
   if (h->tiny_req) WS_CUDA(h->out.ensure(n + 64));
   const int irc = ingest_text_impl(h, nullptr, n, WS_INGEST_RESIDENT | WS_INGEST_UNORDERED);
-  h->early_req = h->tiny_req = false;
+  h->early_req = h->tiny_req = h->dd_req = false;
   WS_TRY(irc);
   const double t_ingested = trace ? trace_ms() : 0;
   tmark("ingest_ret");
@@ -2564,11 +2788,12 @@ int ws_debug_checks(uint64_t* failures, int32_t* first_unit, int32_t* first_line
   if (WS_CHECKED && env_on("WSORT_CHECK_SELFTEST")) launch_check_selftest(nullptr);
   WS_CUDA(cudaDeviceSynchronize());
   int (*readers[])(unsigned int*, unsigned int*) = {check_reader_ingest, check_reader_sort,
-                                                   check_reader_radix, check_reader_emit};
+                                                   check_reader_radix, check_reader_emit,
+                                                   check_reader_dedupe};
   *failures = 0;
   if (first_unit) *first_unit = -1;
   if (first_line) *first_line = 0;
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < 5; ++u) {
     unsigned int f = 0, line = 0;
     const int e = readers[u](&f, &line);
     if (e) return fail_cuda((cudaError_t)e, "ws_debug_checks", __LINE__);
@@ -2587,6 +2812,12 @@ int ws_launch_count(ws_handle* h, uint64_t* launches) {
   if (!h || !launches) return fail(WS_ERR_ARG, "null argument");
   *launches = h->launches;
   for (ws_handle* p : h->peers) *launches += p->launches;  // ws_sort_texts slots
+  return WS_OK;
+}
+
+int ws_counted_classes(ws_handle* h, int32_t* mask) {
+  if (!h || !mask) return fail(WS_ERR_ARG, "null argument");
+  *mask = h->dd_used;
   return WS_OK;
 }
 

@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __gr
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_early_kernel(const __grid_constant__ SplitEarly e) {
   extern __shared__ __align__(16) uint64_t dsm[];
+  if (e.skip && *e.skip) return;  // the class's words were counted instead (dedupe.cu)
   SampleSeg sg;
   memset(&sg, 0, sizeof sg);
   uint32_t slots = 0, splits = 0, tiles = 0, key_off = 0, nfit = 0;
@@ -955,8 +956,9 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
 // from the launch the split CTAs wrote (device-planned, same rules as the host
 // plan): a persistent grid over the class's partition tiles.
 template <int LANES>
-__global__ void __launch_bounds__(kPartThreads, 2) partition_count_early_kernel(const SampleLaunch* __restrict__ plan) {
+__global__ void __launch_bounds__(kPartThreads, 2) partition_count_early_kernel(const SampleLaunch* __restrict__ plan, const uint32_t* __restrict__ skip) {
   pdl_wait();
+  if (skip && *skip) return;  // no split launch wrote `plan` for this call (dedupe.cu)
   const SampleLaunch& a = *plan;
   const uint32_t items = a.work_items;
   for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
@@ -1407,6 +1409,73 @@ void launch_tiny_sort(const TinyLaunch& t, cudaStream_t st) {
 
 // ---- host side ---------------------------------------------------------------------
 
+// ---- distinct-word counting: tile sort of the distinct keys (dedupe.cu's chain) ----
+
+constexpr int kDdSortThreads = kTileThreads;
+template <int LANES>
+constexpr size_t dd_sort_smem() { return pass_smem_bytes<LANES, TileCfg<LANES>::T, true>(); }
+constexpr size_t kDdSortSmem = cmax(cmax(dd_sort_smem<0>(), dd_sort_smem<1>()), cmax(dd_sort_smem<2>(), dd_sort_smem<3>()));
+
+// One tile of a counted bucket's distinct keys (as the aggregate launch
+// appended them) sorted on chip by the tile network; each key's occurrences
+// are fetched from its table slot and follow it (array B).
+template <int LANES>
+__device__ void dd_sort_tile(const DdDevPlan& p, const DdChain& c, int b, uint32_t tile, uint8_t* sbytes) {
+  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kDdSortThreads;
+  constexpr int NW = KeyTraits<LANES>::NW;
+  using W = KW<LANES>;
+  W* sk = reinterpret_cast<W*>(sbytes);
+  uint32_t* si = reinterpret_cast<uint32_t*>(sbytes + keys_smem_bytes<LANES, T, true>());
+  const int tid = threadIdx.x;
+  const uint32_t start = tile * T;
+  const int cnt = (int)min((uint32_t)T, p.D[b] - start);
+  const W* gin = reinterpret_cast<const W*>(c.dk + p.dk_off[b]) + (uint64_t)start * NW;
+  for (int j = tid; j < T * NW; j += NT) sk[j] = j < cnt * NW ? gin[j] : ~W(0);
+  __syncthreads();
+  Key<LANES> r[E];
+  uint32_t ri[E];
+  uint64_t inv = 0;
+  tile_network<LANES, true, NT>(sk, si, cnt, 0u, r, ri, inv);
+  W* gout = reinterpret_cast<W*>(c.ts + p.dk_off[b]) + (uint64_t)start * NW;
+  const uint32_t* dslot = c.aux + p.aux_off[b] + start;
+  uint32_t* ocnt = c.aux + p.aux_total + p.aux_off[b] + start;
+  const uint2* tab = c.table + p.tab_off[b];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int pos = tid * E + k;
+    if (pos >= cnt) break;
+    WS_DCHECK(ri[k] < (uint32_t)cnt);
+#pragma unroll
+    for (int l = 0; l < NW; ++l) gout[(uint64_t)pos * NW + l] = r[k].w[l];
+    ocnt[pos] = tab[dslot[ri[k]]].y;
+  }
+  __syncthreads();  // the tile's shared memory is reused by the CTA's next tile
+}
+
+__global__ void __launch_bounds__(kDdSortThreads) dd_tile_sort_kernel(const __grid_constant__ DdChain c) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint64_t smem[];
+  uint8_t* sbytes = reinterpret_cast<uint8_t*>(smem);
+  const DdDevPlan& p = *c.plan;
+  const uint32_t total = p.st_begin[32];
+  for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
+    const int b = __popc(__ballot_sync(0xffffffffu, p.st_begin[1 + (threadIdx.x & 31)] <= g));
+    const uint32_t tile = g - p.st_begin[b];
+    switch (lanes_for_len_enc(b + 1, kEncAlnum6)) {
+      case 0: dd_sort_tile<0>(p, c, b, tile, sbytes); break;
+      case 1: dd_sort_tile<1>(p, c, b, tile, sbytes); break;
+      case 2: dd_sort_tile<2>(p, c, b, tile, sbytes); break;
+      default: dd_sort_tile<3>(p, c, b, tile, sbytes); break;
+    }
+  }
+}
+
+int dd_sort_tile_size(int lanes) { return lanes <= 1 ? TileCfg<1>::T : TileCfg<2>::T; }
+
+void launch_dd_tiles(const DdChain& c, int grid, cudaStream_t st) {
+  launch_pdl(dd_tile_sort_kernel, grid, kDdSortThreads, kDdSortSmem, st, c);
+}
+
 template <int LANES>
 static constexpr size_t subsort_smem_bytes() {
   return keys_smem_bytes<LANES, kSubThreads * TileCfg<LANES>::E, false>() * (WS_SUB_DB ? 2 : 1) + kSubPayBuf;
@@ -1453,6 +1522,7 @@ static void set_attrs_t() {
 // Opt every sort instantiation into > 48 KiB of dynamic shared memory on the
 // current device (called once per device by the handle).
 void set_sort_attributes() {
+  cudaFuncSetAttribute(dd_tile_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDdSortSmem);
   cudaFuncSetAttribute(tiny_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTinySmem);
   set_attrs_t<0, false>(); set_attrs_t<0, true>();
   set_attrs_t<1, false>(); set_attrs_t<1, true>();
@@ -1524,11 +1594,12 @@ int sample_max_keys(int) { return kSampleSmem / 8; }
 int part_tile_size() { return kPartTile; }
 int subsort_tile_size(int lanes) { return kSubThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E); }
 
-void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st) {
+void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st,
+                                  const uint32_t* skip) {
   switch (lanes) {
-    case 1: launch_pdl(partition_count_early_kernel<1>, grid, kPartThreads, 0, st, plan); break;
-    case 2: launch_pdl(partition_count_early_kernel<2>, grid, kPartThreads, 0, st, plan); break;
-    default: launch_pdl(partition_count_early_kernel<3>, grid, kPartThreads, 0, st, plan); break;
+    case 1: launch_pdl(partition_count_early_kernel<1>, grid, kPartThreads, 0, st, plan, skip); break;
+    case 2: launch_pdl(partition_count_early_kernel<2>, grid, kPartThreads, 0, st, plan, skip); break;
+    default: launch_pdl(partition_count_early_kernel<3>, grid, kPartThreads, 0, st, plan, skip); break;
   }
 }
 

@@ -152,10 +152,12 @@ struct SplitEarly {
   SampleLaunch* plan;
   uint16_t* slot_ids;
   uint32_t ptile;          // keys per partition tile
+  const uint32_t* skip;    // or null: nonzero = the class's words were counted (dedupe.cu), do nothing
 };
 // The count pass of one multi-lane class, planned on the device (the split
 // launch's table): a persistent grid over the class's partition tiles.
-void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st);
+void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st,
+                                  const uint32_t* skip = nullptr);
 void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st);
 // Small corpora: one CTA per length bucket sorts it on chip and writes its
 // payload records, straight after the payload-mode ingest (6-bit keys);
@@ -229,6 +231,7 @@ struct EarlyHist {
   uint32_t* totals;         // [5][kRadixMaxPasses][kRadixTotStride], zeroed
   uint32_t* joint;          // whole-key counters, zeroed
   int joint_ok;             // count (not sort) keys of <= 12 bits
+  const uint32_t* skip;     // or null: nonzero = the class's words were counted (dedupe.cu), do nothing
 };
 constexpr int kRadixC0Segs = 5;  // class-0 buckets at most (the totals table is sized for them)
 void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st);
@@ -237,6 +240,71 @@ void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st);
 // blocks = sum of 2^jbits over the launch's jbits segments (njsegs of them).
 void launch_joint_expand(const RadixLaunch& a, uint32_t blocks, uint32_t njsegs, cudaStream_t st);
 void launch_radix_onesweep(int lanes, const RadixLaunch& a, cudaStream_t st);
+
+// dedupe.cu: distinct-word counting (payload mode, 6-bit text keys)
+struct DdLayout;
+void dd_host_layout(const uint32_t* n, DdLayout& o);  // plan.cuh's layout with the 6-bit key sizes
+// control words at the head of the table pool (zeroed with it)
+constexpr int kDdCtlCount = 0;   // [32] distinct words per length
+constexpr int kDdCtlOvf = 32;    // [32] the bucket ran out of its table budget
+constexpr int kDdCtlDone = 64;   // CTAs of the aggregate launch that have finished
+constexpr int kDdCtlSkip = 68;   // [4] per lane class: every bucket stayed in budget
+constexpr int kDdCtlWords = 128;
+struct DdAgg {
+  const uint32_t* fill;     // the ingest's per-length word counts
+  const uint8_t* keys_cap;  // ... and per-length key regions
+  uint64_t region[32];
+  uint2* table;             // table pool (after the control words)
+  uint8_t* dk;              // distinct-key pool
+  uint32_t* ctl;
+  uint32_t* aux;            // per-distinct-word array A: the word's table slot
+  struct DdDevPlan* plan;   // or null: the last CTA writes the chain's plan
+  uint32_t stile1, stilen;  // keys per sorted tile (one-word / wider keys: dd_sort_tile_size)
+};
+void launch_dd_aggregate(const DdAgg& a, int grid, cudaStream_t st);
+constexpr int kDdTile = 256;    // distinct words per block of the run prefix
+// records per output tile by word length (~16 KB of records)
+__host__ __device__ constexpr uint32_t dd_xtile_of_len(int L) { return L <= 7 ? 2048u : (L <= 15 ? 1024u : 512u); }
+constexpr int kDdXTileMax = 2048;
+int check_reader_dedupe(unsigned int* fails, unsigned int* line);
+// The counted classes' whole chain after the aggregate launch, planned on the
+// device (no host round trip): the aggregate launch's last CTA writes
+// DdDevPlan from the ingest's counters and its control words; the kernels behind it
+// (tile sort of the distinct keys, rank merge of the tiles, run prefixes,
+// expand) run grid-stride over the plan's work items.
+struct DdDevPlan {
+  uint32_t n[32], D[32];     // words / distinct words (D = 0: bucket empty or its class is sorted, not counted)
+  uint32_t slots[32];
+  uint32_t stile[32];        // keys per sorted tile of the bucket's class
+  uint64_t tab_off[32], dk_off[32];
+  uint64_t pay_off[32];      // the bucket's payload records in the output
+  uint32_t aux_off[32];      // per-distinct-word arrays A (aux) and B (aux + aux_total)
+  uint32_t tsum_off[32];     // tile totals of the run prefix
+  uint32_t xs_off[32];       // per output tile: the run holding its first record
+  uint32_t xtile[32];        // records per output tile (by record size)
+  uint32_t aux_total;
+  uint32_t st_begin[33];     // work-item prefixes: sorted tiles,
+  uint32_t rk_begin[33];     //   blocks of kDdTile distinct words,
+  uint32_t x_begin[33];      //   output tiles of xtile records
+};
+struct DdChain {
+  const uint32_t* fill;
+  const uint32_t* ctl;
+  DdDevPlan* plan;
+  const uint8_t* keys_cap;
+  uint64_t region[32];
+  uint2* table;
+  uint8_t* dk;               // distinct keys as appended -> finally sorted
+  uint8_t* ts;               // tile-sorted distinct keys
+  uint32_t* aux;
+  uint8_t* out;              // payload
+};
+int dd_sort_tile_size(int lanes);
+// sort.cu: tile sort; dedupe.cu: rank merge, run prefixes (3 kernels), expand
+void launch_dd_tiles(const DdChain& c, int grid, cudaStream_t st);
+void launch_dd_rank(const DdChain& c, int grid, cudaStream_t st);
+void launch_dd_prefix(const DdChain& c, int grid, cudaStream_t st);
+void launch_dd_chain_expand(const DdChain& c, int grid, cudaStream_t st);
 
 // emit.cu
 struct EmitSeg {

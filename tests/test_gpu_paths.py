@@ -57,7 +57,27 @@ print("ok")
     "CUDA_DEVICE_MAX_CONNECTIONS=32",
 ])
 def test_diagnostic_paths_agree(knob):
+    """The sort paths themselves: distinct-word counting off (a text that
+    repeats its vocabulary would otherwise never reach them in payload mode)."""
     words = 2_600_000 if knob == "WSORT_NO_CHUNKED_H2D" else 300_000  # > 16 MiB for the H2D knob
+    name, _, value = knob.partition("=")
+    env = dict(os.environ, **{name: value or "1"}, WSORT_NO_DEDUPE="1")
+    r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=str(ROOT), words=words)],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("knob", [
+    "WSORT_NO_DEDUPE",        # every class sorted (no distinct-word counting)
+    "WSORT_DEDUPE_MIN=0",     # counting from the smallest text that skips the small-corpus kernel
+    "WSORT_NO_RADIX", "WSORT_NO_SAMPLE", "WSORT_NO_EARLY_HIST", "WSORT_NO_EARLY_SPLIT",
+    "WSORT_NO_EARLY_COUNT", "WSORT_NO_CHUNKED_H2D", "WSORT_SERIAL", "WSORT_NO_JOINT",
+    "WSORT_INGEST=reserve",
+])
+def test_diagnostic_paths_agree_with_counting(knob):
+    """The same knobs with distinct-word counting on (the default): the
+    distinct keys go through the knob's sort path."""
+    words = 2_600_000 if knob == "WSORT_NO_CHUNKED_H2D" else 300_000
     name, _, value = knob.partition("=")
     env = dict(os.environ, **{name: value or "1"})
     r = subprocess.run([sys.executable, "-c", SCRIPT.format(root=str(ROOT), words=words)],
