@@ -1109,13 +1109,30 @@ int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
   a.stilen = (uint32_t)dd_sort_tile_size(2);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  // two launches side by side: the uint32 keys (lengths 1-5) on the main
+  // stream, the wider keys on the side stream
   const uint64_t max_tiles = (h->n_text + 1) / 2 / 4096 + 32;
-  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, 2ull * sms));
-  {
-    Phase ph(h, "dd_aggregate", 0.0, 0, h->st);  // bytes patched once the counts are known
-    launch_dd_aggregate(a, grid, h->st);
+  int grid[2];
+  a.total_ctas = 0;
+  for (int g = 0; g < 2; ++g) {
+    grid[g] = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, (uint64_t)dd_aggregate_ctas_per_sm(g) * sms));
+    a.total_ctas += (uint32_t)grid[g];
+  }
+  cudaStream_t side[2] = {h->st, h->serial ? h->st : h->zs};
+  WS_CUDA(cudaEventRecord(h->ev_dd, h->st));  // the ingest's keys and counters (and the zeroed pool)
+  static const char* nm[2] = {"dd_aggregate", "dd_aggregate_hi"};
+  for (int g = 1; g >= 0; --g) {
+    if (side[g] != h->st) WS_CUDA(cudaStreamWaitEvent(side[g], h->ev_dd, 0));
+    Phase ph(h, nm[g], 0.0, 0, side[g]);  // bytes patched once the counts are known
+    launch_dd_aggregate(a, g, grid[g], side[g]);
     ++h->launches;
   }
+  for (int g = 1; g < 2; ++g)  // the main stream (and the host's read-back) waits for both
+    if (side[g] != h->st) {
+      cudaEvent_t e = sync_event(h);
+      WS_CUDA(cudaEventRecord(e, side[g]));
+      WS_CUDA(cudaStreamWaitEvent(h->st, e, 0));
+    }
   WS_TRY(check_launch("dd_aggregate"));
   h->dd_launched = true;
   // The rest of the counted classes' path, planned on the device (the
@@ -1157,7 +1174,7 @@ int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
     }
     {
       Phase ph(h, "dd_expand", 0.0, 0, xs);
-      launch_dd_chain_expand(c, 8 * sms, xs);
+      launch_dd_chain_expand(c, dd_expand_ctas_per_sm() * sms, xs);
       ++h->launches;
     }
     WS_CUDA(cudaEventRecord(h->ev_chain, xs));
@@ -1541,9 +1558,12 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
       for (int c = 1; c < 4; ++c)
         if (h->dd_ok[c]) h->split_early[c] = h->count_early[c] = false;
       if (h->prof) {
-        double kb = 0;
+        double kb = 0, kb0 = 0;
         for (auto& bk : h->buckets)
-          if (!bk.is_long) kb += (double)bk.count * key_bytes(bk.lanes);
+          if (!bk.is_long) {
+            kb += (double)bk.count * key_bytes(bk.lanes);
+            if (bk.lanes == 0) kb0 += (double)bk.count * 4.0;
+          }
         double dkb = 0, pay = 0;  // counted classes: distinct keys, payload records
         for (auto& bk : h->buckets)
           if (!bk.is_long && h->dd_ok[bk.lanes]) {
@@ -1552,7 +1572,8 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
           }
         for (auto& r : h->phases) {
           if (r.bytes != 0.0) continue;
-          if (r.name == "dd_aggregate") r.bytes = kb;
+          if (r.name == "dd_aggregate") r.bytes = kb0;
+          else if (r.name == "dd_aggregate_hi") r.bytes = kb - kb0;
           else if (r.name == "dd_tiles" || r.name == "dd_rank") r.bytes = 2.0 * dkb;  // keys + occurrences in and out
           else if (r.name == "dd_prefix") r.bytes = dkb;
           else if (r.name == "dd_expand") r.bytes = pay + dkb;

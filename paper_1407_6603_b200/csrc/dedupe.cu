@@ -38,7 +38,8 @@ namespace {
 
 constexpr int kAggThreads = 512;
 constexpr int kAggTile = 4096;    // keys per tile
-constexpr int kAggSlots = 8192;   // shared-memory table slots (load <= 1/2)
+constexpr int kAggSlotBits = 13;
+constexpr int kAggSlots = 1 << kAggSlotBits;  // shared-memory table slots (load <= 1/2)
 constexpr uint32_t kRepBits = 13; // slot = occurrences << 13 | (key index in tile + 1)
 constexpr uint32_t kRepMask = (1u << kRepBits) - 1;
 constexpr uint32_t kMaxProbes = 4096;  // a longer probe sequence means the table is (nearly) full
@@ -83,24 +84,29 @@ __device__ __forceinline__ uint32_t hmix(uint32_t h, uint32_t v) {
   return (h << 13) | (h >> 19);
 }
 
+// Hash whose HIGH bits are the good ones (the shared-memory slot is its top
+// bits, the bucket-table slot a multiply-high): one-word keys by one odd
+// multiply (Fibonacci hashing; the keys differ in their high bits, the low
+// ones pad short words with zeros), wider keys word by word.
 template <int LANES>
 __device__ __forceinline__ uint32_t dd_hash(const Key<LANES>& k) {
-  uint32_t h = 0x9E3779B9u;
+  if constexpr (LANES == 0) {
+    uint32_t h = (uint32_t)k.w[0] * 0x9E3779B1u;
+    return h ^ (h >> 15) * 0x85EBCA6Bu;
+  } else {
+    uint32_t h = 0x9E3779B9u;
 #pragma unroll
-  for (int q = 0; q < KeyTraits<LANES>::NW; ++q) {
-    if constexpr (LANES == 0) {
-      h = hmix(h, k.w[q]);
-    } else {
+    for (int q = 0; q < KeyTraits<LANES>::NW; ++q) {
       h = hmix(h, (uint32_t)(k.w[q] >> 32));
       h = hmix(h, (uint32_t)k.w[q]);
     }
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
   }
-  h ^= h >> 16;
-  h *= 0x85EBCA6Bu;
-  h ^= h >> 13;
-  h *= 0xC2B2AE35u;
-  h ^= h >> 16;
-  return h;
 }
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -187,7 +193,7 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     for (int e = 0; e < G; ++e) {
       const uint32_t idx = tid + (e0 + e) * kAggThreads;
       if (idx >= cnt) continue;
-      uint32_t s = dd_hash<LANES>(k[e]) & (kAggSlots - 1);
+      uint32_t s = dd_hash<LANES>(k[e]) >> (32 - kAggSlotBits);
       for (;;) {
         uint32_t v = *reinterpret_cast<volatile uint32_t*>(&tab[s]);
         if (v == 0) {
@@ -344,7 +350,17 @@ __device__ void dd_write_plan(const DdAgg& a, const DdLayout& lay, const uint32_
   }
 }
 
-__global__ void __launch_bounds__(kAggThreads, 2) dd_aggregate_kernel(const __grid_constant__ DdAgg a) {
+#ifndef WS_DD_LO_MINB
+#define WS_DD_LO_MINB 3  // CTAs per SM of the one-word-key launch (register cap 65536 / (512 * MINB))
+#endif
+// One launch per key width group, side by side: GRP 0 = the uint32 keys
+// (lengths 1-5: most words, few registers, more CTAs per SM to hide the
+// flush's L2 round trips), 1 = the wider keys. (A third launch for the
+// one-lane keys measured no faster: the SMs are full either way.)
+// The last CTA of all launches finishes the control words.
+__host__ __device__ constexpr int dd_group_of_class(int cls) { return cls == 0 ? 0 : 1; }
+template <int GRP>
+__global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_aggregate_kernel(const __grid_constant__ DdAgg a) {
   __shared__ AggSmem sm;
   __shared__ DdLayout lay;
   __shared__ uint32_t s_n[kDdLens], s_tb[kDdLens + 1];
@@ -357,7 +373,7 @@ __global__ void __launch_bounds__(kAggThreads, 2) dd_aggregate_kernel(const __gr
     uint32_t run = 0;
     for (int b = 0; b < kDdLens; ++b) {
       s_tb[b] = run;
-      run += (s_n[b] + kAggTile - 1) / kAggTile;
+      if (dd_group_of_class(dd_class_of_len(b + 1)) == GRP) run += (s_n[b] + kAggTile - 1) / kAggTile;
     }
     s_tb[kDdLens] = run;
   }
@@ -376,11 +392,14 @@ __global__ void __launch_bounds__(kAggThreads, 2) dd_aggregate_kernel(const __gr
     const uint32_t base = (g - s_tb[b]) * kAggTile;
     void* dk = a.dk + lay.dk_off[b];
     uint32_t* dslot = a.aux + lay.aux_off[b];
-    switch (dd_class_of_len(b + 1)) {
-      case 0: agg_tile<0>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
-      case 1: agg_tile<1>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
-      case 2: agg_tile<2>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
-      default: agg_tile<3>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
+    if constexpr (GRP == 0) {
+      agg_tile<0>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b);
+    } else {
+      switch (dd_class_of_len(b + 1)) {
+        case 1: agg_tile<1>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
+        case 2: agg_tile<2>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
+        default: agg_tile<3>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
+      }
     }
   }
   // The last CTA to finish decides, per lane class, whether every bucket
@@ -388,7 +407,7 @@ __global__ void __launch_bounds__(kAggThreads, 2) dd_aggregate_kernel(const __gr
   // work then), and writes the plan of the chain behind this launch.
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.ctl + kDdCtlDone, 1u) == gridDim.x - 1;
+  if (tid == 0) s_last = atomicAdd(a.ctl + kDdCtlDone, 1u) == a.total_ctas - 1;
   __syncthreads();
   if (!s_last || tid >= 32) return;
   __threadfence();
@@ -406,9 +425,11 @@ __global__ void __launch_bounds__(kAggThreads, 2) dd_aggregate_kernel(const __gr
   if (a.plan) dd_write_plan(a, lay, s_n);
 }
 
-void launch_dd_aggregate(const DdAgg& a, int grid, cudaStream_t st) {
-  dd_aggregate_kernel<<<grid, kAggThreads, 0, st>>>(a);
+void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st) {
+  if (grp == 0) dd_aggregate_kernel<0><<<grid, kAggThreads, 0, st>>>(a);
+  else dd_aggregate_kernel<1><<<grid, kAggThreads, 0, st>>>(a);
 }
+int dd_aggregate_ctas_per_sm(int grp) { return grp == 0 ? WS_DD_LO_MINB : 2; }
 
 // ----------------------------------------------------------------------------
 // after the distinct keys are sorted: run prefixes and payload records
@@ -476,15 +497,17 @@ __device__ void expand_tile(const DdSeg& sg, uint32_t r0, uint32_t TR, uint32_t 
       if (sm.ro[mid] <= r) lo = mid; else hi = mid;
     }
     uint32_t nxt = sm.ro[lo + 1];
-    uint64_t k[NL];
+    uint32_t rec[kRecWords];  // the current run's record, decoded once
     auto fetch = [&](uint32_t i) {
       const W* kp = ks + (uint64_t)i * NW;
+      uint64_t k[NL];
       if constexpr (LANES == 0) {
         k[0] = (uint64_t)__ldg(kp) << 32;
       } else {
 #pragma unroll
         for (int l = 0; l < NL; ++l) k[l] = __ldg(kp + l);
       }
+      decode6_words<NL>(k, L, rec);
     };
     fetch(lo);
     uint8_t* dst = sm.pbuf + mis + (size_t)(tid * PER) * R;
@@ -495,8 +518,7 @@ __device__ void expand_tile(const DdSeg& sg, uint32_t r0, uint32_t TR, uint32_t 
         nxt = sm.ro[lo + 1];
         fetch(lo);
       }
-      unpack6_swar<NL>(k, L, dst);
-      dst[L] = '\n';
+      store_record(dst, rec, R);
     }
   }
   __syncthreads();
@@ -665,13 +687,25 @@ __global__ void __launch_bounds__(kDdTile) dd_xstart_kernel(const __grid_constan
   }
 }
 
-__global__ void __launch_bounds__(kXThreads) dd_expand_dev_kernel(const __grid_constant__ DdChain c) {
+constexpr int kXCtasPerSm = 6;
+__global__ void __launch_bounds__(kXThreads, kXCtasPerSm) dd_expand_dev_kernel(const __grid_constant__ DdChain c) {
   pdl_wait();
   __shared__ XSmem sm;
   const DdDevPlan& p = *c.plan;
   const uint32_t total = p.x_begin[32];
-  for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
-    const int b = bucket_of(p.x_begin, g);
+  uint32_t g = blockIdx.x;
+  if (g >= total) return;
+  int b = bucket_of(p.x_begin, g);
+  uint32_t j0 = c.aux[p.xs_off[b] + (g - p.x_begin[b])];
+  for (;;) {
+    // the next tile's bucket and first run are fetched before this tile's work
+    const uint32_t gn = g + gridDim.x;
+    int bn = 0;
+    uint32_t j0n = 0;
+    if (gn < total) {
+      bn = bucket_of(p.x_begin, gn);
+      j0n = c.aux[p.xs_off[bn] + (gn - p.x_begin[bn])];
+    }
     DdSeg sg;
     sg.keys_sorted = c.dk + p.dk_off[b];
     sg.D = p.D[b];
@@ -680,8 +714,8 @@ __global__ void __launch_bounds__(kXThreads) dd_expand_dev_kernel(const __grid_c
     sg.loc = c.aux + p.aux_off[b];
     sg.tsum = c.aux + p.tsum_off[b];
     sg.pay = c.out + p.pay_off[b];
-    const uint32_t t = g - p.x_begin[b], TR = p.xtile[b];
-    const uint32_t r0 = t * TR, j0 = c.aux[p.xs_off[b] + t];
+    const uint32_t TR = p.xtile[b];
+    const uint32_t r0 = (g - p.x_begin[b]) * TR;
     WS_DCHECK(j0 < sg.D);
     switch (dd_cls(b)) {
       case 0: expand_tile<0>(sg, r0, TR, j0, sm); break;
@@ -689,8 +723,14 @@ __global__ void __launch_bounds__(kXThreads) dd_expand_dev_kernel(const __grid_c
       case 2: expand_tile<2>(sg, r0, TR, j0, sm); break;
       default: expand_tile<3>(sg, r0, TR, j0, sm); break;
     }
+    if (gn >= total) break;
+    g = gn;
+    b = bn;
+    j0 = j0n;
   }
 }
+
+int dd_expand_ctas_per_sm() { return kXCtasPerSm; }
 
 void launch_dd_rank(const DdChain& c, int grid, cudaStream_t st) {
   launch_pdl(dd_rank_kernel, grid, kDdTile, 0, st, c);

@@ -71,6 +71,46 @@ __device__ __forceinline__ void unpack6_swar(const uint64_t (&k)[NL], int L, uin
   unpack6_group<NL, 0>(k, L, dst);
 }
 
+
+// The record of a key (L characters + '\n') as little-endian ASCII words:
+// byte i of the record is byte i % 4 of a[i / 4]. Decoded once per run of
+// equal words; store_record then writes it as often as the word occurs.
+constexpr int kRecWords = (kMaxPackedLen + 1 + 3) / 4;
+template <int NL, int G>
+__device__ __forceinline__ void decode6_words_g(const uint64_t (&k)[NL], int L, uint32_t (&a)[kRecWords]) {
+  if constexpr (G < kRecWords) {
+    if constexpr (4 * G < (NL * 64) / 6) {
+      a[G] = 4 * G < L ? ascii4_of_codes(code_bits24<NL, 24 * G>(k)) : 0u;
+    } else {
+      a[G] = 0u;
+    }
+    if (L / 4 == G) {  // the newline right after the last character
+      const int sh = 8 * (L & 3);
+      a[G] = (a[G] & ~(0xFFu << sh)) | (0x0Au << sh);
+    }
+    decode6_words_g<NL, G + 1>(k, L, a);
+  }
+}
+template <int NL>
+__device__ __forceinline__ void decode6_words(const uint64_t (&k)[NL], int L, uint32_t (&a)[kRecWords]) {
+  decode6_words_g<NL, 0>(k, L, a);
+}
+template <int G>
+__device__ __forceinline__ void store_record_g(uint8_t* dst, const uint32_t (&a)[kRecWords], int R) {
+  if constexpr (G < kRecWords) {
+    if (4 * G >= R) return;
+    const uint32_t w = a[G];
+    dst[4 * G] = (uint8_t)w;
+    if (4 * G + 1 < R) dst[4 * G + 1] = (uint8_t)(w >> 8);
+    if (4 * G + 2 < R) dst[4 * G + 2] = (uint8_t)(w >> 16);
+    if (4 * G + 3 < R) dst[4 * G + 3] = (uint8_t)(w >> 24);
+    store_record_g<G + 1>(dst, a, R);
+  }
+}
+__device__ __forceinline__ void store_record(uint8_t* dst, const uint32_t (&a)[kRecWords], int R) {
+  store_record_g<0>(dst, a, R);
+}
+
 // buf[mis, mis + total) -> out[0, total), where mis = out & 15: aligned
 // 16-byte stores for the body, byte stores for the ragged head and tail.
 template <int NT>

@@ -259,9 +259,12 @@ struct DdAgg {
   uint32_t* ctl;
   uint32_t* aux;            // per-distinct-word array A: the word's table slot
   struct DdDevPlan* plan;   // or null: the last CTA writes the chain's plan
+  uint32_t total_ctas;      // CTAs of all aggregate launches
   uint32_t stile1, stilen;  // keys per sorted tile (one-word / wider keys: dd_sort_tile_size)
 };
-void launch_dd_aggregate(const DdAgg& a, int grid, cudaStream_t st);
+// two launches side by side (grp 0: lengths 1-5, 1: the wider keys); a.total_ctas = both grids
+void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st);
+int dd_aggregate_ctas_per_sm(int grp);
 constexpr int kDdTile = 256;    // distinct words per block of the run prefix
 // records per output tile by word length (~16 KB of records)
 __host__ __device__ constexpr uint32_t dd_xtile_of_len(int L) { return L <= 7 ? 2048u : (L <= 15 ? 1024u : 512u); }
@@ -305,6 +308,7 @@ void launch_dd_tiles(const DdChain& c, int grid, cudaStream_t st);
 void launch_dd_rank(const DdChain& c, int grid, cudaStream_t st);
 void launch_dd_prefix(const DdChain& c, int grid, cudaStream_t st);
 void launch_dd_chain_expand(const DdChain& c, int grid, cudaStream_t st);
+int dd_expand_ctas_per_sm();  // the expand's grid: this many CTAs per SM, each looping over output tiles
 
 // emit.cu
 struct EmitSeg {
