@@ -208,6 +208,7 @@ struct ws_handle {
   DevBuf dd_pool, dd_keys, dd_aux, dd_ts, dd_plan;
   cudaEvent_t ev_dd = nullptr, ev_chain = nullptr;  // aggregate launched / device-planned chain done
   bool dd_chain = false;          // the chain behind the aggregate launch writes the counted classes' payload
+  bool dd_two_chains = false;     // ... as two chains side by side (class 0 / classes 1-3)
   cudaStream_t zs = nullptr;      // zeroes the table pool beside the ingest
   cudaEvent_t ev_zero = nullptr;
   bool dd_req = false;            // the next ingest counts distinct words right behind itself
@@ -1157,25 +1158,42 @@ int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
     c.aux = a.aux;
     c.out = h->out.as<uint8_t>();
     const int cgrid = 4 * sms;
-    {
-      Phase ph(h, "dd_tiles", 0.0, 0, xs);  // bytes patched once the counts are known
-      launch_dd_tiles(c, cgrid, xs);
-      ++h->launches;
-    }
-    {
-      Phase ph(h, "dd_rank", 0.0, 0, xs);
-      launch_dd_rank(c, cgrid, xs);
-      ++h->launches;
-    }
-    {
-      Phase ph(h, "dd_prefix", 0.0, 0, xs);
-      launch_dd_prefix(c, cgrid, xs);
-      h->launches += 3;
-    }
-    {
-      Phase ph(h, "dd_expand", 0.0, 0, xs);
-      launch_dd_chain_expand(c, dd_expand_ctas_per_sm() * sms, xs);
-      ++h->launches;
+    // WSORT_DD_TWO_CHAINS=1 (experiment, measured no faster): class 0 (the
+    // bucket with the most distinct words: the longest sort) and the other
+    // classes (most payload bytes) as two chains side by side.
+    static const bool two_chains = env_on("WSORT_DD_TWO_CHAINS");
+    const int nchain = (h->serial || !two_chains) ? 1 : 2;
+    h->dd_two_chains = nchain == 2;
+    cudaStream_t cst[2] = {xs, h->es[0]};
+    for (int k = 0; k < nchain; ++k) {
+      c.cls_mask = nchain == 1 ? 0xFu : (k == 0 ? 0x1u : 0xEu);
+      cudaStream_t s2 = cst[k];
+      if (s2 != xs && s2 != h->st) WS_CUDA(cudaStreamWaitEvent(s2, h->ev_dd, 0));
+      {
+        Phase ph(h, k ? "dd_tiles_hi" : "dd_tiles", 0.0, 0, s2);  // bytes patched once the counts are known
+        launch_dd_tiles(c, cgrid, s2);
+        ++h->launches;
+      }
+      {
+        Phase ph(h, k ? "dd_rank_hi" : "dd_rank", 0.0, 0, s2);
+        launch_dd_rank(c, cgrid, s2);
+        ++h->launches;
+      }
+      {
+        Phase ph(h, k ? "dd_prefix_hi" : "dd_prefix", 0.0, 0, s2);
+        launch_dd_prefix(c, cgrid, s2);
+        h->launches += 3;
+      }
+      {
+        Phase ph(h, k ? "dd_expand_hi" : "dd_expand", 0.0, 0, s2);
+        launch_dd_chain_expand(c, dd_expand_ctas_per_sm() * sms, s2);
+        ++h->launches;
+      }
+      if (s2 != xs) {  // the first chain's stream carries the end of both
+        cudaEvent_t e = sync_event(h);
+        WS_CUDA(cudaEventRecord(e, s2));
+        WS_CUDA(cudaStreamWaitEvent(xs, e, 0));
+      }
     }
     WS_CUDA(cudaEventRecord(h->ev_chain, xs));
     WS_TRY(check_launch("dd_chain"));
@@ -1564,19 +1582,29 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
             kb += (double)bk.count * key_bytes(bk.lanes);
             if (bk.lanes == 0) kb0 += (double)bk.count * 4.0;
           }
-        double dkb = 0, pay = 0;  // counted classes: distinct keys, payload records
+        double dkb = 0, pay = 0, dkb0 = 0, pay0 = 0;  // counted classes: distinct keys, payload records (0: class 0)
         for (auto& bk : h->buckets)
           if (!bk.is_long && h->dd_ok[bk.lanes]) {
             dkb += (double)bk.dd_n * (key_bytes(bk.lanes) + 4.0);
             pay += (double)bk.count * (bk.len + 1);
+            if (bk.lanes == 0) {
+              dkb0 += (double)bk.dd_n * 8.0;
+              pay0 += (double)bk.count * (bk.len + 1);
+            }
           }
         for (auto& r : h->phases) {
           if (r.bytes != 0.0) continue;
           if (r.name == "dd_aggregate") r.bytes = kb0;
           else if (r.name == "dd_aggregate_hi") r.bytes = kb - kb0;
-          else if (r.name == "dd_tiles" || r.name == "dd_rank") r.bytes = 2.0 * dkb;  // keys + occurrences in and out
-          else if (r.name == "dd_prefix") r.bytes = dkb;
-          else if (r.name == "dd_expand") r.bytes = pay + dkb;
+          else {  // chain kernels: "_hi" = the chain of classes 1-3 when two chains run
+            const bool hi = r.name.size() > 3 && r.name.compare(r.name.size() - 3, 3, "_hi") == 0;
+            const std::string base = hi ? r.name.substr(0, r.name.size() - 3) : r.name;
+            const bool two = h->dd_two_chains;
+            const double dk1 = !two ? dkb : (hi ? dkb - dkb0 : dkb0), py = !two ? pay : (hi ? pay - pay0 : pay0);
+            if (base == "dd_tiles" || base == "dd_rank") r.bytes = std::max(1.0, 2.0 * dk1);  // keys + occurrences in and out
+            else if (base == "dd_prefix") r.bytes = std::max(1.0, dk1);
+            else if (base == "dd_expand") r.bytes = std::max(1.0, py + dk1);
+          }
         }
       }
     }

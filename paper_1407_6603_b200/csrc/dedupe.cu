@@ -538,6 +538,8 @@ __device__ __forceinline__ int bucket_of(const uint32_t* begin, uint32_t g) {
 }
 
 __device__ __forceinline__ int dd_cls(int b) { return dd_class_of_len(b + 1); }
+// The launch handles bucket b (DdChain::cls_mask: one chain per group of lane classes).
+__device__ __forceinline__ bool in_mask(const DdChain& c, int b) { return (c.cls_mask >> dd_cls(b)) & 1u; }
 
 // Final rank of tile-sorted distinct word j of a bucket: its position in its
 // own tile plus the smaller words of every other tile (the words are distinct:
@@ -589,6 +591,7 @@ __global__ void __launch_bounds__(kDdTile) dd_rank_kernel(const __grid_constant_
   const uint32_t total = p.rk_begin[32];
   for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
     const int b = bucket_of(p.rk_begin, g);
+    if (!in_mask(c, b)) continue;
     const uint32_t j = (g - p.rk_begin[b]) * kDdTile + threadIdx.x;
     if (j >= p.D[b]) continue;
     switch (dd_cls(b)) {
@@ -610,6 +613,7 @@ __global__ void __launch_bounds__(kDdTile) dd_prefix_kernel(const __grid_constan
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
     const int b = bucket_of(p.rk_begin, g);
+    if (!in_mask(c, b)) continue;
     const uint32_t blk = g - p.rk_begin[b];
     const uint32_t j = blk * kDdTile + threadIdx.x;
     uint32_t* cnt = c.aux + p.aux_off[b];
@@ -638,7 +642,7 @@ __global__ void __launch_bounds__(1024) dd_tsum_kernel(const __grid_constant__ D
   const DdDevPlan& p = *c.plan;
   const int b = blockIdx.x;
   const uint32_t D = p.D[b];
-  if (!D) return;
+  if (!D || !in_mask(c, b)) return;
   uint32_t* tsum = c.aux + p.tsum_off[b];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t nt = (D + kDdTile - 1) / kDdTile;
@@ -674,6 +678,7 @@ __global__ void __launch_bounds__(kDdTile) dd_xstart_kernel(const __grid_constan
   const uint32_t total = p.rk_begin[32];
   for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
     const int b = bucket_of(p.rk_begin, g);
+    if (!in_mask(c, b)) continue;
     const uint32_t j = (g - p.rk_begin[b]) * kDdTile + threadIdx.x;
     const uint32_t D = p.D[b];
     if (j >= D) continue;
@@ -706,22 +711,24 @@ __global__ void __launch_bounds__(kXThreads, kXCtasPerSm) dd_expand_dev_kernel(c
       bn = bucket_of(p.x_begin, gn);
       j0n = c.aux[p.xs_off[bn] + (gn - p.x_begin[bn])];
     }
-    DdSeg sg;
-    sg.keys_sorted = c.dk + p.dk_off[b];
-    sg.D = p.D[b];
-    sg.n = p.n[b];
-    sg.len = (uint32_t)b + 1;
-    sg.loc = c.aux + p.aux_off[b];
-    sg.tsum = c.aux + p.tsum_off[b];
-    sg.pay = c.out + p.pay_off[b];
-    const uint32_t TR = p.xtile[b];
-    const uint32_t r0 = (g - p.x_begin[b]) * TR;
-    WS_DCHECK(j0 < sg.D);
-    switch (dd_cls(b)) {
-      case 0: expand_tile<0>(sg, r0, TR, j0, sm); break;
-      case 1: expand_tile<1>(sg, r0, TR, j0, sm); break;
-      case 2: expand_tile<2>(sg, r0, TR, j0, sm); break;
-      default: expand_tile<3>(sg, r0, TR, j0, sm); break;
+    if (in_mask(c, b)) {
+      DdSeg sg;
+      sg.keys_sorted = c.dk + p.dk_off[b];
+      sg.D = p.D[b];
+      sg.n = p.n[b];
+      sg.len = (uint32_t)b + 1;
+      sg.loc = c.aux + p.aux_off[b];
+      sg.tsum = c.aux + p.tsum_off[b];
+      sg.pay = c.out + p.pay_off[b];
+      const uint32_t TR = p.xtile[b];
+      const uint32_t r0 = (g - p.x_begin[b]) * TR;
+      WS_DCHECK(j0 < sg.D);
+      switch (dd_cls(b)) {
+        case 0: expand_tile<0>(sg, r0, TR, j0, sm); break;
+        case 1: expand_tile<1>(sg, r0, TR, j0, sm); break;
+        case 2: expand_tile<2>(sg, r0, TR, j0, sm); break;
+        default: expand_tile<3>(sg, r0, TR, j0, sm); break;
+      }
     }
     if (gn >= total) break;
     g = gn;

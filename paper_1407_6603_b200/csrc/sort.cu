@@ -1460,6 +1460,7 @@ __global__ void __launch_bounds__(kDdSortThreads) dd_tile_sort_kernel(const __gr
   const uint32_t total = p.st_begin[32];
   for (uint32_t g = blockIdx.x; g < total; g += gridDim.x) {
     const int b = __popc(__ballot_sync(0xffffffffu, p.st_begin[1 + (threadIdx.x & 31)] <= g));
+    if (!((c.cls_mask >> lanes_for_len_enc(b + 1, kEncAlnum6)) & 1u)) continue;  // another chain's bucket
     const uint32_t tile = g - p.st_begin[b];
     switch (lanes_for_len_enc(b + 1, kEncAlnum6)) {
       case 0: dd_sort_tile<0>(p, c, b, tile, sbytes); break;

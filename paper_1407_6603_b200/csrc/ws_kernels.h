@@ -301,6 +301,7 @@ struct DdChain {
   uint8_t* ts;               // tile-sorted distinct keys
   uint32_t* aux;
   uint8_t* out;              // payload
+  uint32_t cls_mask;         // lane classes this chain handles (bit c)
 };
 int dd_sort_tile_size(int lanes);
 // sort.cu: tile sort; dedupe.cu: rank merge, run prefixes (3 kernels), expand
