@@ -209,7 +209,8 @@ struct ws_handle {
   cudaEvent_t ev_dd = nullptr, ev_chain = nullptr;  // aggregate launched / device-planned chain done
   bool dd_chain = false;          // the chain behind the aggregate launch writes the counted classes' payload
   bool dd_two_chains = false;     // ... as two chains side by side (class 0 / classes 1-3)
-  cudaStream_t zs = nullptr;      // zeroes the table pool beside the ingest
+  cudaStream_t zs = nullptr;      // zeroes the table pool beside the ingest; the wider keys' counting
+  cudaStream_t xs = nullptr;      // class 0's chain behind its counting launch
   cudaEvent_t ev_zero = nullptr;
   bool dd_req = false;            // the next ingest counts distinct words right behind itself
   bool dd_launched = false;       // ... and did
@@ -334,6 +335,7 @@ int params_upload(ws_handle* h, const std::vector<T>& v, const T** dev,
     }
     if (h->hs) WS_CUDA(cudaStreamSynchronize(h->hs));
     if (h->zs) WS_CUDA(cudaStreamSynchronize(h->zs));
+    if (h->xs) WS_CUDA(cudaStreamSynchronize(h->xs));
     size_t need = std::max<size_t>(2 * (off + bytes), 1 << 20);
     if (need > h->pin_params.cap) {
       h->pin_params.release();
@@ -1084,7 +1086,7 @@ int dd_zero_pool(ws_handle* h, uint64_t n, cudaStream_t st) {
   // per-distinct-word arrays A and B + the run prefix's tile totals
   WS_CUDA(h->dd_aux.ensure((2 * dd_max_distinct(n) + dd_max_distinct(n) / kDdTile + 4 * kDdLens +
                             (n + 1) / 1024 + 2 * kDdLens) * 4 + 64));  // ... and the output tiles' first runs
-  WS_CUDA(h->dd_plan.ensure(sizeof(DdDevPlan)));
+  WS_CUDA(h->dd_plan.ensure(2 * sizeof(DdDevPlan)));
   WS_CUDA(h->out.ensure(n + 1 + 64));  // the payload never exceeds the text by more than a byte
   WS_CUDA(cudaMemsetAsync(h->dd_pool.p, 0, dd_pool_bytes(n), st));
   return WS_OK;
@@ -1110,90 +1112,89 @@ int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
   a.stilen = (uint32_t)dd_sort_tile_size(2);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  // two launches side by side: the uint32 keys (lengths 1-5) on the main
-  // stream, the wider keys on the side stream
+  // Two launches side by side -- the uint32 keys (lengths 1-5) on the main
+  // stream, the wider keys on the side stream -- and behind each the rest of
+  // its classes' path as a chain planned on the device (the launch's last
+  // CTA) and enqueued now: distinct keys sorted (tiles, then a rank merge),
+  // run prefixes, payload records, while the host still waits for the
+  // ingest's counters. Class 0's chain starts as soon as its own launch ends.
   const uint64_t max_tiles = (h->n_text + 1) / 2 / 4096 + 32;
   int grid[2];
-  a.total_ctas = 0;
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < 2; ++g)
     grid[g] = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, (uint64_t)dd_aggregate_ctas_per_sm(g) * sms));
-    a.total_ctas += (uint32_t)grid[g];
-  }
-  cudaStream_t side[2] = {h->st, h->serial ? h->st : h->zs};
+  // streams: [0] class 0's launch on the main stream (the host's read-back
+  // follows it), its chain on a side stream; [1] the wider keys' launch and
+  // chain on the stream that zeroed the pool
+  cudaStream_t agg_st[2] = {h->st, h->serial ? h->st : h->zs};
+  cudaStream_t chain_st[2] = {h->serial ? h->st : h->xs, h->serial ? h->st : h->zs};
   WS_CUDA(cudaEventRecord(h->ev_dd, h->st));  // the ingest's keys and counters (and the zeroed pool)
-  static const char* nm[2] = {"dd_aggregate", "dd_aggregate_hi"};
+  DdChain c;
+  memset(&c, 0, sizeof c);
+  c.fill = a.fill;
+  c.ctl = a.ctl;
+  c.keys_cap = a.keys_cap;
+  for (int b = 0; b < 32; ++b) c.region[b] = region[b];
+  c.table = a.table;
+  c.dk = a.dk;
+  c.ts = h->dd_ts.as<uint8_t>();
+  c.aux = a.aux;
+  c.out = h->out.as<uint8_t>();
+  const int cgrid = 4 * sms;
+  cudaEvent_t ev_hi = nullptr;
+  static const char* nm[2][5] = {{"dd_aggregate", "dd_tiles", "dd_rank", "dd_prefix", "dd_expand"},
+                                 {"dd_aggregate_hi", "dd_tiles_hi", "dd_rank_hi", "dd_prefix_hi", "dd_expand_hi"}};
   for (int g = 1; g >= 0; --g) {
-    if (side[g] != h->st) WS_CUDA(cudaStreamWaitEvent(side[g], h->ev_dd, 0));
-    Phase ph(h, nm[g], 0.0, 0, side[g]);  // bytes patched once the counts are known
-    launch_dd_aggregate(a, g, grid[g], side[g]);
-    ++h->launches;
-  }
-  for (int g = 1; g < 2; ++g)  // the main stream (and the host's read-back) waits for both
-    if (side[g] != h->st) {
-      cudaEvent_t e = sync_event(h);
-      WS_CUDA(cudaEventRecord(e, side[g]));
-      WS_CUDA(cudaStreamWaitEvent(h->st, e, 0));
+    if (agg_st[g] != h->st) WS_CUDA(cudaStreamWaitEvent(agg_st[g], h->ev_dd, 0));
+    {
+      Phase ph(h, nm[g][0], 0.0, 0, agg_st[g]);  // bytes patched once the counts are known
+      launch_dd_aggregate(a, g, grid[g], agg_st[g]);
+      ++h->launches;
     }
+    if (g == 1 && agg_st[1] != h->st) {  // the launch's end, before its chain joins the stream
+      ev_hi = sync_event(h);
+      WS_CUDA(cudaEventRecord(ev_hi, agg_st[1]));
+    }
+    cudaStream_t s2 = chain_st[g];
+    if (s2 != agg_st[g]) {
+      cudaEvent_t e = sync_event(h);
+      WS_CUDA(cudaEventRecord(e, agg_st[g]));
+      WS_CUDA(cudaStreamWaitEvent(s2, e, 0));
+    }
+    c.plan = h->dd_plan.as<DdDevPlan>() + g;
+    c.cls_mask = g == 0 ? 0x1u : 0xEu;
+    {
+      Phase ph(h, nm[g][1], 0.0, 0, s2);
+      launch_dd_tiles(c, cgrid, s2);
+      ++h->launches;
+    }
+    {
+      Phase ph(h, nm[g][2], 0.0, 0, s2);
+      launch_dd_rank(c, cgrid, s2);
+      ++h->launches;
+    }
+    {
+      Phase ph(h, nm[g][3], 0.0, 0, s2);
+      launch_dd_prefix(c, cgrid, s2);
+      h->launches += 3;
+    }
+    {
+      Phase ph(h, nm[g][4], 0.0, 0, s2);
+      launch_dd_chain_expand(c, dd_expand_ctas_per_sm() * sms, s2);
+      ++h->launches;
+    }
+  }
   WS_TRY(check_launch("dd_aggregate"));
   h->dd_launched = true;
-  // The rest of the counted classes' path, planned on the device (the
-  // aggregate launch's last CTA) and enqueued now on the side stream: distinct
-  // keys sorted (tiles, then a rank merge), run prefixes, payload records --
-  // while the host still waits for the ingest's counters.
-  h->dd_chain = false;
+  h->dd_two_chains = true;
   {
-    cudaStream_t xs = h->serial ? h->st : h->zs;  // (serialised profiles: everything on the main stream)
-    WS_CUDA(cudaEventRecord(h->ev_dd, h->st));
-    if (xs != h->st) WS_CUDA(cudaStreamWaitEvent(xs, h->ev_dd, 0));
-    DdChain c;
-    memset(&c, 0, sizeof c);
-    c.fill = a.fill;
-    c.ctl = a.ctl;
-    c.plan = h->dd_plan.as<DdDevPlan>();
-    c.keys_cap = a.keys_cap;
-    for (int b = 0; b < 32; ++b) c.region[b] = region[b];
-    c.table = a.table;
-    c.dk = a.dk;
-    c.ts = h->dd_ts.as<uint8_t>();
-    c.aux = a.aux;
-    c.out = h->out.as<uint8_t>();
-    const int cgrid = 4 * sms;
-    // WSORT_DD_TWO_CHAINS=1 (experiment, measured no faster): class 0 (the
-    // bucket with the most distinct words: the longest sort) and the other
-    // classes (most payload bytes) as two chains side by side.
-    static const bool two_chains = env_on("WSORT_DD_TWO_CHAINS");
-    const int nchain = (h->serial || !two_chains) ? 1 : 2;
-    h->dd_two_chains = nchain == 2;
-    cudaStream_t cst[2] = {xs, h->es[0]};
-    for (int k = 0; k < nchain; ++k) {
-      c.cls_mask = nchain == 1 ? 0xFu : (k == 0 ? 0x1u : 0xEu);
-      cudaStream_t s2 = cst[k];
-      if (s2 != xs && s2 != h->st) WS_CUDA(cudaStreamWaitEvent(s2, h->ev_dd, 0));
-      {
-        Phase ph(h, k ? "dd_tiles_hi" : "dd_tiles", 0.0, 0, s2);  // bytes patched once the counts are known
-        launch_dd_tiles(c, cgrid, s2);
-        ++h->launches;
-      }
-      {
-        Phase ph(h, k ? "dd_rank_hi" : "dd_rank", 0.0, 0, s2);
-        launch_dd_rank(c, cgrid, s2);
-        ++h->launches;
-      }
-      {
-        Phase ph(h, k ? "dd_prefix_hi" : "dd_prefix", 0.0, 0, s2);
-        launch_dd_prefix(c, cgrid, s2);
-        h->launches += 3;
-      }
-      {
-        Phase ph(h, k ? "dd_expand_hi" : "dd_expand", 0.0, 0, s2);
-        launch_dd_chain_expand(c, dd_expand_ctas_per_sm() * sms, s2);
-        ++h->launches;
-      }
-      if (s2 != xs) {  // the first chain's stream carries the end of both
-        cudaEvent_t e = sync_event(h);
-        WS_CUDA(cudaEventRecord(e, s2));
-        WS_CUDA(cudaStreamWaitEvent(xs, e, 0));
-      }
+    // the main stream (the host's read-back of the control words) waits for
+    // the wider keys' launch as well -- not for the chains
+    if (ev_hi) WS_CUDA(cudaStreamWaitEvent(h->st, ev_hi, 0));
+    cudaStream_t xs = chain_st[1];
+    if (chain_st[0] != xs) {  // the side stream carries the end of both chains
+      cudaEvent_t e = sync_event(h);
+      WS_CUDA(cudaEventRecord(e, chain_st[0]));
+      WS_CUDA(cudaStreamWaitEvent(xs, e, 0));
     }
     WS_CUDA(cudaEventRecord(h->ev_chain, xs));
     WS_TRY(check_launch("dd_chain"));
@@ -2393,6 +2394,7 @@ int ws_create(ws_handle** out, int32_t device) {
       e = cudaStreamCreateWithPriority(&h->ds[c], cudaStreamNonBlocking, prio_hi);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->zs, cudaStreamNonBlocking, prio_lo);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->xs, cudaStreamNonBlocking, prio_lo);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_zero, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dd, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_chain, cudaEventDisableTiming);
@@ -2415,6 +2417,7 @@ void ws_destroy(ws_handle* h) {
   if (h->st) cudaStreamSynchronize(h->st);
   if (h->hs) cudaStreamSynchronize(h->hs);
   if (h->zs) cudaStreamSynchronize(h->zs);
+  if (h->xs) cudaStreamSynchronize(h->xs);
   for (int c = 0; c <= kClasses; ++c) {
     if (h->cs[c]) cudaStreamSynchronize(h->cs[c]);
     if (h->es[c]) cudaStreamSynchronize(h->es[c]);
@@ -2454,6 +2457,7 @@ void ws_destroy(ws_handle* h) {
   if (h->ev_dd) cudaEventDestroy(h->ev_dd);
   if (h->ev_chain) cudaEventDestroy(h->ev_chain);
   if (h->zs) cudaStreamDestroy(h->zs);
+  if (h->xs) cudaStreamDestroy(h->xs);
   if (h->hs) cudaStreamDestroy(h->hs);
   if (h->st) cudaStreamDestroy(h->st);
   delete h;

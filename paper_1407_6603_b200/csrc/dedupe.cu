@@ -288,6 +288,8 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
 }
 
 __host__ __device__ inline int dd_class_of_len(int L) { return lanes_for_len_enc(L, kEncAlnum6); }
+// Counting launch (and chain) of a lane class: 0 = the uint32 keys, 1 = the wider keys.
+__host__ __device__ constexpr int dd_group_of_class(int cls) { return cls == 0 ? 0 : 1; }
 
 struct KbOfLen {
   __host__ __device__ uint32_t operator()(int L) const { return (uint32_t)key_bytes(dd_class_of_len(L)); }
@@ -299,12 +301,12 @@ void dd_host_layout(const uint32_t* n, DdLayout& o) { dd_layout(n, KbOfLen{}, o)
 
 // The chain's plan (DdDevPlan) from the per-length counts, the layout and the
 // aggregate launch's control words; one warp, lane b = length b + 1.
-__device__ void dd_write_plan(const DdAgg& a, const DdLayout& lay, const uint32_t* s_n) {
+__device__ void dd_write_plan(const DdAgg& a, int grp, const DdLayout& lay, const uint32_t* s_n) {
   const int b = threadIdx.x & 31;
-  DdDevPlan& p = *a.plan;
+  DdDevPlan& p = a.plan[grp];  // one plan per launch: its own buckets only
   const int cls = dd_class_of_len(b + 1);
   const uint32_t n = s_n[b];
-  const bool ok = n && a.ctl[kDdCtlSkip + cls] != 0;
+  const bool ok = n && dd_group_of_class(cls) == grp && a.ctl[kDdCtlSkip + cls] != 0;
   const uint32_t D = ok ? ld_relaxed(a.ctl + kDdCtlCount + b) : 0u;
   const uint32_t T = cls <= 1 ? a.stile1 : a.stilen;
   const uint32_t XT = dd_xtile_of_len(b + 1);
@@ -357,8 +359,7 @@ __device__ void dd_write_plan(const DdAgg& a, const DdLayout& lay, const uint32_
 // (lengths 1-5: most words, few registers, more CTAs per SM to hide the
 // flush's L2 round trips), 1 = the wider keys. (A third launch for the
 // one-lane keys measured no faster: the SMs are full either way.)
-// The last CTA of all launches finishes the control words.
-__host__ __device__ constexpr int dd_group_of_class(int cls) { return cls == 0 ? 0 : 1; }
+// Each launch's last CTA finishes its classes' control words and its chain's plan.
 template <int GRP>
 __global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_aggregate_kernel(const __grid_constant__ DdAgg a) {
   __shared__ AggSmem sm;
@@ -402,16 +403,16 @@ __global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_
       }
     }
   }
-  // The last CTA to finish decides, per lane class, whether every bucket
-  // stayed in budget (the early launches of the class's sort path skip their
-  // work then), and writes the plan of the chain behind this launch.
+  // The launch's last CTA to finish decides, for its lane classes, whether
+  // every bucket stayed in budget (the early launches of the class's sort
+  // path skip their work then), and writes the plan of the chain behind it.
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.ctl + kDdCtlDone, 1u) == a.total_ctas - 1;
+  if (tid == 0) s_last = atomicAdd(a.ctl + kDdCtlDone + GRP, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last || tid >= 32) return;
   __threadfence();
-  if (tid < 4) {
+  if (tid < 4 && dd_group_of_class(tid) == GRP) {
     bool ok = true, any = false;
     for (int b = 0; b < kDdLens; ++b) {
       if (dd_class_of_len(b + 1) != tid || !s_n[b]) continue;
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_
   }
   __syncwarp();
   __threadfence();
-  if (a.plan) dd_write_plan(a, lay, s_n);
+  if (a.plan) dd_write_plan(a, GRP, lay, s_n);
 }
 
 void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st) {

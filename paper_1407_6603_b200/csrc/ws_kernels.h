@@ -247,7 +247,7 @@ void dd_host_layout(const uint32_t* n, DdLayout& o);  // plan.cuh's layout with 
 // control words at the head of the table pool (zeroed with it)
 constexpr int kDdCtlCount = 0;   // [32] distinct words per length
 constexpr int kDdCtlOvf = 32;    // [32] the bucket ran out of its table budget
-constexpr int kDdCtlDone = 64;   // CTAs of the aggregate launch that have finished
+constexpr int kDdCtlDone = 64;   // [2] CTAs of each aggregate launch that have finished
 constexpr int kDdCtlSkip = 68;   // [4] per lane class: every bucket stayed in budget
 constexpr int kDdCtlWords = 128;
 struct DdAgg {
@@ -258,11 +258,10 @@ struct DdAgg {
   uint8_t* dk;              // distinct-key pool
   uint32_t* ctl;
   uint32_t* aux;            // per-distinct-word array A: the word's table slot
-  struct DdDevPlan* plan;   // or null: the last CTA writes the chain's plan
-  uint32_t total_ctas;      // CTAs of all aggregate launches
+  struct DdDevPlan* plan;   // or null: [2], each launch's last CTA writes its chain's plan
   uint32_t stile1, stilen;  // keys per sorted tile (one-word / wider keys: dd_sort_tile_size)
 };
-// two launches side by side (grp 0: lengths 1-5, 1: the wider keys); a.total_ctas = both grids
+// two launches side by side (grp 0: lengths 1-5, 1: the wider keys)
 void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st);
 int dd_aggregate_ctas_per_sm(int grp);
 constexpr int kDdTile = 256;    // distinct words per block of the run prefix

@@ -70,7 +70,6 @@ def test_diagnostic_paths_agree(knob):
 @pytest.mark.parametrize("knob", [
     "WSORT_NO_DEDUPE",        # every class sorted (no distinct-word counting)
     "WSORT_DEDUPE_MIN=0",     # counting from the smallest text that skips the small-corpus kernel
-    "WSORT_DD_TWO_CHAINS",    # the counted classes' chain as two (class 0 / classes 1-3) side by side
     "WSORT_NO_RADIX", "WSORT_NO_SAMPLE", "WSORT_NO_EARLY_HIST", "WSORT_NO_EARLY_SPLIT",
     "WSORT_NO_EARLY_COUNT", "WSORT_NO_CHUNKED_H2D", "WSORT_SERIAL", "WSORT_NO_JOINT",
     "WSORT_INGEST=reserve",
