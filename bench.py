@@ -21,8 +21,10 @@ One JSON line on rank 0:
              algorithmic bytes per launch / its CUDA-event duration (events
              around every launch in K profiled steps run after the timed
              ones), against MEASURED_PEAKS.json; roofline_rows lists every
-             family (ingest, one-sweep radix, radix histogram, sample split,
-             partition, slot sort; stats mode: ingest, tile sort, merge).
+             family (ingest; counting path: aggregate, distinct sort, run
+             prefix, expand; sort paths: one-sweep radix, radix histogram,
+             sample split, partition, slot sort; stats mode: ingest, tile
+             sort, merge).
   cpu_baseline  the unmodified reference (baseline/_ref, numba _bubble_rows on
              a worker pool; tools/vendor_reference.sh) on the host cores, on a
              bounded prefix of the same text, with the oracle's C port of the
@@ -365,6 +367,12 @@ FAMILIES = {
                   "part_scatter_l1", "part_scatter_l2", "part_scatter_l3", "part_scatter_l4"),
     "slot_sort": ("subsort_l1", "subsort_l2", "subsort_l3", "subsort_l4"),
     "tiny_sort": ("tiny",),  # small corpora (<= 512 KiB): one CTA per bucket after the ingest
+    # distinct-word counting (texts that repeat their vocabulary): every key read once
+    # and counted; distinct keys sorted (tiles + rank merge); run prefixes; payload records
+    "count_aggregate": ("dd_aggregate", "dd_aggregate_hi"),
+    "count_sort_distinct": ("dd_tiles", "dd_tiles_hi", "dd_rank", "dd_rank_hi"),
+    "count_run_prefix": ("dd_prefix", "dd_prefix_hi"),
+    "count_expand": ("dd_expand", "dd_expand_hi"),
 }
 STATS_FAMILIES = {
     "stats_ingest": ("ingest", "reorder"),
@@ -468,6 +476,7 @@ def bench_ours(args) -> None:
             torch.cuda.synchronize(dev)
             dev_ms.append(a.elapsed_time(b))
         launches = h.launch_count() - launches0
+        counted = h.counted_classes()
         # the timed path's own output, byte-compared after the loop
         resident_ok = None
         if want is not None:
@@ -618,7 +627,10 @@ def bench_ours(args) -> None:
             "config": {"workload": wl, "words": words,
                        "text_bytes": n, "payload_bytes": written, "buckets": len(lengths),
                        "l2_flush": "256 MiB memset on the timed stream between steps",
-                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       # lane classes (bit c: words of 1-5 / 6-10 / 11-21 / 22-32 characters) whose
+                       # payload came from counting distinct words, not from sorting every occurrence
+                       "counted_classes": counted},
             "e2e": {"value": batch_value, "unit": UNIT, "h2d_bytes_per_step": n,
                     "d2h_bytes_per_step": batch_sizes[0] if batch_sizes else 0,
                     "ms_per_step": t_batch, "gpu_launches": batch_launches,

@@ -322,25 +322,30 @@ __device__ void dd_write_plan(const DdAgg& a, int grp, const DdLayout& lay, cons
   uint64_t pay = (uint64_t)n * (uint32_t)(b + 2);  // records of L + 1 bytes (every bucket: the payload holds them all)
   uint32_t tq = lay.dcap[b] / kDdTile + 2;         // tile totals
   uint32_t st = (D + T - 1) / T, rk = (D + kDdTile - 1) / kDdTile, x = ok ? (n + XT - 1) / XT : 0u;
+  // (array offsets run over every bucket, whichever launch it belongs to: the
+  // two chains share the arrays; work items only over this plan's buckets)
+  uint32_t xa = (n + XT - 1) / XT;
   const uint64_t pay0 = pay;
-  const uint32_t tq0 = tq, st0 = st, rk0 = rk, x0 = x;
+  const uint32_t tq0 = tq, st0 = st, rk0 = rk, x0 = x, xa0 = xa;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint64_t u0 = __shfl_up_sync(0xffffffffu, pay, o);
     const uint32_t u1 = __shfl_up_sync(0xffffffffu, tq, o), u2 = __shfl_up_sync(0xffffffffu, st, o);
     const uint32_t u3 = __shfl_up_sync(0xffffffffu, rk, o), u4 = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t u5 = __shfl_up_sync(0xffffffffu, xa, o);
     if (b >= o) {
       pay += u0;
       tq += u1;
       st += u2;
       rk += u3;
       x += u4;
+      xa += u5;
     }
   }
   const uint32_t tq_all = __shfl_sync(0xffffffffu, tq, 31);
   p.pay_off[b] = pay - pay0;
   p.tsum_off[b] = 2u * lay.aux_total + (tq - tq0);
-  p.xs_off[b] = 2u * lay.aux_total + tq_all + (x - x0);
+  p.xs_off[b] = 2u * lay.aux_total + tq_all + (xa - xa0);
   p.st_begin[b] = st - st0;
   p.rk_begin[b] = rk - rk0;
   p.x_begin[b] = x - x0;
