@@ -7,21 +7,27 @@
 // device counts them, sorts the distinct keys only and writes every word as
 // often as it occurred -- the same bytes as sorting all occurrences:
 //
-//   dd_aggregate_kernel  (right behind the ingest, planned on the device from
-//       its per-length counters) reads every packed key once: a tile of 4096
-//       keys is counted in a shared-memory table (slot = representative key
-//       index + occurrences), then each distinct key of the tile goes into
-//       the bucket's table in HBM/L2 (CAS on the representative index, atomic
-//       add of the tile's count). The first insertion of a key also appends
-//       it to the bucket's distinct-key list. A bucket whose distinct words
-//       exceed its table's budget (plan.cuh: n/16) raises its overflow flag;
-//       its class then keeps the sort paths (radix / sample sort).
-//   [the existing class chains sort the distinct-key lists, keys only]
-//   dd_lookup_kernel     sorted distinct keys -> occurrences (table probe),
-//       exclusive prefix inside tiles of 256 + tile totals
-//   dd_scan_kernel       exclusive prefix of the tile totals
-//   dd_expand_kernel     one CTA per 1024 output records: finds the runs that
-//       cover them and writes `word + '\n'` records with aligned 16-byte
+//   dd_aggregate_kernel<GRP>  (right behind the ingest, planned on the device
+//       from its per-length counters; one launch for the uint32 keys, one for
+//       the wider keys, side by side) reads every packed key once: a tile of
+//       4096 keys is counted in a shared-memory table (slot = occurrences +
+//       the index of one occurrence in the tile), the occupied slots are
+//       compacted, and each distinct key of the tile goes into the bucket's
+//       table in HBM/L2 (CAS on an empty slot, atomic add of the tile's
+//       count). Words seen for the first time are appended to the bucket's
+//       distinct-key list, one reservation per tile. A bucket whose distinct
+//       words exceed its table's budget (plan.cuh: n/8) raises its overflow
+//       flag; its class then keeps the sort paths (radix / sample sort). Each
+//       launch's last CTA writes its classes' OK flags and the plan
+//       (DdDevPlan) of the chain enqueued behind it -- no host round trip.
+//   dd_tile_sort_kernel (sort.cu)  tiles of the distinct keys sorted on chip,
+//       each key's occurrences fetched from its table slot
+//   dd_rank_kernel    every key's final rank = its tile position + the smaller
+//       keys of the bucket's other tiles (binary searches; no ties)
+//   dd_prefix_kernel, dd_tsum_kernel  occurrences -> run starts (two levels)
+//   dd_xstart_kernel  per output tile: the run holding its first record
+//   dd_expand_dev_kernel  grid-stride over output tiles of ~16 KB: `word + '\n'`
+//       records staged in shared memory and written with aligned 16-byte
 //       stores (a run covering the whole tile is a pattern fill).
 //
 // Stats mode (SortStats needs corpus order) never takes this path.
