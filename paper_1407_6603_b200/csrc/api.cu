@@ -207,6 +207,9 @@ struct ws_handle {
   // distinct-word counting (dedupe.cu): control words + tables, distinct keys, run prefixes
   DevBuf dd_pool, dd_keys, dd_aux, dd_ts, dd_plan;
   cudaEvent_t ev_dd = nullptr, ev_chain = nullptr;  // aggregate launched / device-planned chain done
+  cudaEvent_t ev_probe = nullptr;  // the counting path's probe done (the sort paths' early launches wait for it)
+  cudaEvent_t ev_lo = nullptr, ev_hi = nullptr;  // the two counting launches done
+  DdAgg dd_agg;                   // the counting launches' parameters (stage 0 -> stage 1)
   bool dd_chain = false;          // the chain behind the aggregate launch writes the counted classes' payload
   bool dd_two_chains = false;     // ... as two chains side by side (class 0 / classes 1-3)
   cudaStream_t zs = nullptr;      // zeroes the table pool beside the ingest; the wider keys' counting
@@ -1064,13 +1067,16 @@ int launch_tiny(ws_handle* h, const uint64_t* region, uint64_t n) {
 
 // Distinct-word counting (dedupe.cu) right behind the payload-mode ingest, on
 // the main stream: the ingest's sync then also covers its counters. WSORT_NO_DEDUPE=1
-// turns it off; WSORT_DEDUPE_MIN=bytes sets the smallest text that tries it.
+// turns it off; WSORT_DEDUPE_MIN=bytes sets the smallest text that tries it
+// (default 32 MiB: smaller texts are bound by launch latencies and the host's
+// enqueue, where the counting path's dozen extra launches cost more than its
+// counting saves -- configs 1-3 measured 0.15-0.26 ms with it against 0.14-0.20).
 bool dedupe_wanted(uint64_t n) {
   static const bool off = env_on("WSORT_NO_DEDUPE") || env_on("WSORT_D2H_PER_CLASS") ||
                           env_on("WSORT_NO_FUSED_PAYLOAD");
   static const uint64_t min_text = [] {
     const char* e = getenv("WSORT_DEDUPE_MIN");
-    return e ? (uint64_t)strtoull(e, nullptr, 0) : (uint64_t)(1u << 20);
+    return e ? (uint64_t)strtoull(e, nullptr, 0) : (uint64_t)(32u << 20);
   }();
   return !off && n >= min_text;
 }
@@ -1092,42 +1098,75 @@ int dd_zero_pool(ws_handle* h, uint64_t n, cudaStream_t st) {
   return WS_OK;
 }
 
-int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
-  if (h->dd_launched) {  // a redone ingest: the pool holds the first attempt's entries
-    WS_TRY(dd_zero_pool(h, h->n_text, h->st));
-  } else {
-    WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_zero, 0));
-  }
-  DdAgg a;
-  memset(&a, 0, sizeof a);
-  a.fill = h->fill.as<uint32_t>();
-  a.keys_cap = h->keys_cap.as<uint8_t>();
-  for (int b = 0; b < 32; ++b) a.region[b] = region[b];
-  a.ctl = h->dd_pool.as<uint32_t>();
-  a.table = reinterpret_cast<uint2*>(h->dd_pool.as<uint32_t>() + kDdCtlWords);
-  a.dk = h->dd_keys.as<uint8_t>();
-  a.aux = h->dd_aux.as<uint32_t>();
-  a.plan = h->dd_plan.as<DdDevPlan>();
-  a.stile1 = (uint32_t)dd_sort_tile_size(1);
-  a.stilen = (uint32_t)dd_sort_tile_size(2);
+// Stage 0 (right behind the ingest): the probe and the two counting launches.
+// Stage 1 (after the sort paths' early launches have been enqueued, so those
+// are not held back by the host's enqueue of a dozen more launches): the
+// chains behind the counting launches.
+int launch_dd_counting(ws_handle* h, const uint64_t* region, int stage) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-  // Two launches side by side -- the uint32 keys (lengths 1-5) on the main
-  // stream, the wider keys on the side stream -- and behind each the rest of
-  // its classes' path as a chain planned on the device (the launch's last
-  // CTA) and enqueued now: distinct keys sorted (tiles, then a rank merge),
-  // run prefixes, payload records, while the host still waits for the
-  // ingest's counters. Class 0's chain starts as soon as its own launch ends.
-  const uint64_t max_tiles = (h->n_text + 1) / 2 / 4096 + 32;
-  int grid[2];
-  for (int g = 0; g < 2; ++g)
-    grid[g] = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, (uint64_t)dd_aggregate_ctas_per_sm(g) * sms));
   // streams: [0] class 0's launch on the main stream (the host's read-back
   // follows it), its chain on a side stream; [1] the wider keys' launch and
   // chain on the stream that zeroed the pool
   cudaStream_t agg_st[2] = {h->st, h->serial ? h->st : h->zs};
   cudaStream_t chain_st[2] = {h->serial ? h->st : h->xs, h->serial ? h->st : h->zs};
-  WS_CUDA(cudaEventRecord(h->ev_dd, h->st));  // the ingest's keys and counters (and the zeroed pool)
+  static const char* nm[2][5] = {{"dd_aggregate", "dd_tiles", "dd_rank", "dd_prefix", "dd_expand"},
+                                 {"dd_aggregate_hi", "dd_tiles_hi", "dd_rank_hi", "dd_prefix_hi", "dd_expand_hi"}};
+  DdAgg& a = h->dd_agg;
+  if (stage == 0) {
+    if (h->dd_launched) {  // a redone ingest: the pool holds the first attempt's entries
+      WS_TRY(dd_zero_pool(h, h->n_text, h->st));
+    } else {
+      WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_zero, 0));
+    }
+    memset(&a, 0, sizeof a);
+    a.fill = h->fill.as<uint32_t>();
+    a.keys_cap = h->keys_cap.as<uint8_t>();
+    for (int b = 0; b < 32; ++b) a.region[b] = region[b];
+    a.ctl = h->dd_pool.as<uint32_t>();
+    a.table = reinterpret_cast<uint2*>(h->dd_pool.as<uint32_t>() + kDdCtlWords);
+    a.dk = h->dd_keys.as<uint8_t>();
+    a.aux = h->dd_aux.as<uint32_t>();
+    a.plan = h->dd_plan.as<DdDevPlan>();
+    a.stile1 = (uint32_t)dd_sort_tile_size(1);
+    a.stilen = (uint32_t)dd_sort_tile_size(2);
+    // First the probe: one CTA per length judges the bucket's first keys, so a
+    // text of mostly different words gives its classes up within microseconds
+    // and the sort paths' early launches (which wait for the probe only) start.
+    {
+      Phase ph(h, "dd_probe", 0.0, 0, h->st);
+      launch_dd_probe(a, h->st);
+      ++h->launches;
+    }
+    WS_CUDA(cudaEventRecord(h->ev_probe, h->st));
+    // Two launches side by side -- the uint32 keys (lengths 1-5) on the main
+    // stream, the wider keys on the side stream. Each launch's last CTA plans
+    // the chain that stage 1 enqueues behind it.
+    const uint64_t max_tiles = (h->n_text + 1) / 2 / 4096 + 32;
+    WS_CUDA(cudaEventRecord(h->ev_dd, h->st));  // the ingest's keys and counters (and the zeroed pool)
+    for (int g = 1; g >= 0; --g) {
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(max_tiles, (uint64_t)dd_aggregate_ctas_per_sm(g) * sms));
+      if (agg_st[g] != h->st) WS_CUDA(cudaStreamWaitEvent(agg_st[g], h->ev_dd, 0));
+      Phase ph(h, nm[g][0], 0.0, 0, agg_st[g]);  // bytes patched once the counts are known
+      launch_dd_aggregate(a, g, grid, agg_st[g]);
+      ++h->launches;
+    }
+    WS_CUDA(cudaEventRecord(h->ev_lo, h->st));  // class 0's launch: its chain starts behind it
+    if (agg_st[1] != h->st) {
+      // the main stream (the host's read-back of the control words) waits for
+      // the wider keys' launch as well -- not for the chains
+      WS_CUDA(cudaEventRecord(h->ev_hi, agg_st[1]));
+      WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_hi, 0));
+    }
+    WS_TRY(check_launch("dd_aggregate"));
+    h->dd_launched = true;
+    h->dd_chain = false;
+    return WS_OK;
+  }
+  // stage 1: behind each counting launch the rest of its classes' path,
+  // planned on the device and enqueued now -- distinct keys sorted (tiles, then
+  // a rank merge), run prefixes, payload records -- while the host still waits
+  // for the ingest's counters. Class 0's chain starts when its own launch ends.
   DdChain c;
   memset(&c, 0, sizeof c);
   c.fill = a.fill;
@@ -1140,26 +1179,9 @@ int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
   c.aux = a.aux;
   c.out = h->out.as<uint8_t>();
   const int cgrid = 4 * sms;
-  cudaEvent_t ev_hi = nullptr;
-  static const char* nm[2][5] = {{"dd_aggregate", "dd_tiles", "dd_rank", "dd_prefix", "dd_expand"},
-                                 {"dd_aggregate_hi", "dd_tiles_hi", "dd_rank_hi", "dd_prefix_hi", "dd_expand_hi"}};
   for (int g = 1; g >= 0; --g) {
-    if (agg_st[g] != h->st) WS_CUDA(cudaStreamWaitEvent(agg_st[g], h->ev_dd, 0));
-    {
-      Phase ph(h, nm[g][0], 0.0, 0, agg_st[g]);  // bytes patched once the counts are known
-      launch_dd_aggregate(a, g, grid[g], agg_st[g]);
-      ++h->launches;
-    }
-    if (g == 1 && agg_st[1] != h->st) {  // the launch's end, before its chain joins the stream
-      ev_hi = sync_event(h);
-      WS_CUDA(cudaEventRecord(ev_hi, agg_st[1]));
-    }
     cudaStream_t s2 = chain_st[g];
-    if (s2 != agg_st[g]) {
-      cudaEvent_t e = sync_event(h);
-      WS_CUDA(cudaEventRecord(e, agg_st[g]));
-      WS_CUDA(cudaStreamWaitEvent(s2, e, 0));
-    }
+    if (g == 0 && s2 != h->st) WS_CUDA(cudaStreamWaitEvent(s2, h->ev_lo, 0));
     c.plan = h->dd_plan.as<DdDevPlan>() + g;
     c.cls_mask = g == 0 ? 0x1u : 0xEu;
     {
@@ -1183,23 +1205,16 @@ int launch_dd_aggregate_early(ws_handle* h, const uint64_t* region) {
       ++h->launches;
     }
   }
-  WS_TRY(check_launch("dd_aggregate"));
-  h->dd_launched = true;
   h->dd_two_chains = true;
-  {
-    // the main stream (the host's read-back of the control words) waits for
-    // the wider keys' launch as well -- not for the chains
-    if (ev_hi) WS_CUDA(cudaStreamWaitEvent(h->st, ev_hi, 0));
-    cudaStream_t xs = chain_st[1];
-    if (chain_st[0] != xs) {  // the side stream carries the end of both chains
-      cudaEvent_t e = sync_event(h);
-      WS_CUDA(cudaEventRecord(e, chain_st[0]));
-      WS_CUDA(cudaStreamWaitEvent(xs, e, 0));
-    }
-    WS_CUDA(cudaEventRecord(h->ev_chain, xs));
-    WS_TRY(check_launch("dd_chain"));
-    h->dd_chain = true;
+  cudaStream_t xs = chain_st[1];
+  if (chain_st[0] != xs) {  // the side stream carries the end of both chains
+    cudaEvent_t e = sync_event(h);
+    WS_CUDA(cudaEventRecord(e, chain_st[0]));
+    WS_CUDA(cudaStreamWaitEvent(xs, e, 0));
   }
+  WS_CUDA(cudaEventRecord(h->ev_chain, xs));
+  WS_TRY(check_launch("dd_chain"));
+  h->dd_chain = true;
   return WS_OK;
 }
 
@@ -1208,8 +1223,10 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   DevBuf& tb = h->rtotals[0];
   WS_CUDA(tb.ensure(radix_c0_zero_bytes() + 64));
   if (cst != h->st) {
-    cudaEvent_t ev = sync_event(h);
-    WS_CUDA(cudaEventRecord(ev, h->st));
+    // behind the ingest -- or, with the counting path launched, behind its
+    // probe (not behind the counting launches that follow it on the main stream)
+    cudaEvent_t ev = h->dd_launched ? h->ev_probe : sync_event(h);
+    if (!h->dd_launched) WS_CUDA(cudaEventRecord(ev, h->st));
     WS_CUDA(cudaStreamWaitEvent(cst, ev, 0));
   }
   WS_CUDA(cudaMemsetAsync(tb.p, 0, radix_c0_zero_bytes(), cst));
@@ -1221,8 +1238,9 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
   e.totals = tb.as<uint32_t>();
   e.joint = e.totals + (size_t)kRadixC0Segs * kRadixMaxPasses * kRadixTotStride + kRadixMaxPasses;
   e.joint_ok = !env_on("WSORT_NO_JOINT");
-  const uint32_t* dd_skip = h->dd_launched ? h->dd_pool.as<uint32_t>() + kDdCtlSkip : nullptr;
-  e.skip = dd_skip;
+  // with the counting path launched, a class's early launches run only if its probe gave the class up
+  const uint32_t* dd_go = h->dd_launched ? h->dd_pool.as<uint32_t>() + kDdCtlProbe : nullptr;
+  e.go = dd_go;
   {
     Phase ph(h, "radix_hist_l0", 0.0, 0, cst);  // bytes patched once the counts are known
     launch_radix_hist_early(e, cst);
@@ -1255,8 +1273,8 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     }
     cudaStream_t sst = h->serial ? h->st : h->cs[c];
     if (sst != h->st) {
-      cudaEvent_t ev = sync_event(h);
-      WS_CUDA(cudaEventRecord(ev, h->st));
+      cudaEvent_t ev = h->dd_launched ? h->ev_probe : sync_event(h);
+      if (!h->dd_launched) WS_CUDA(cudaEventRecord(ev, h->st));
       WS_CUDA(cudaStreamWaitEvent(sst, ev, 0));
     }
     SplitEarly se;
@@ -1273,7 +1291,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
     se.cap = sample_bucket_limit(c);
     se.splitters = h->ss_split[c].as<uint64_t>();
     se.hist = h->ss_slots[c].as<uint32_t>();
-    se.skip = dd_skip ? dd_skip + c : nullptr;
+    se.go = dd_go ? dd_go + c : nullptr;
     if (count_ok) {
       se.plan = h->early_plan[c].as<SampleLaunch>();
       se.slot_ids = h->ss_ids[c].as<uint16_t>();
@@ -1294,7 +1312,7 @@ int launch_early_hist(ws_handle* h, const uint64_t* region) {
       char nm[20];
       snprintf(nm, sizeof nm, "part_count_l%d", c);
       Phase ph(h, nm, 0.0, 0, sst);
-      launch_partition_count_early(c, h->early_plan[c].as<SampleLaunch>(), grid, sst, se.skip);
+      launch_partition_count_early(c, h->early_plan[c].as<SampleLaunch>(), grid, sst, se.go);
       ++h->launches;
       h->count_early[c] = true;
     }
@@ -1481,8 +1499,9 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         if (reserve && h->tiny_req && h->enc == kEncAlnum6) {
           WS_TRY(launch_tiny(h, region, n));
         } else {
-          if (dd_try) WS_TRY(launch_dd_aggregate_early(h, region));
+          if (dd_try) WS_TRY(launch_dd_counting(h, region, 0));
           if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+          if (dd_try) WS_TRY(launch_dd_counting(h, region, 1));
         }
         if (h->dd_launched)
           WS_CUDA(cudaMemcpyAsync(tot_host + kDdHostOff, h->dd_pool.p, kDdCtlWords * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1517,8 +1536,9 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         if (reserve && h->tiny_req && h->enc == kEncAlnum6) {
           WS_TRY(launch_tiny(h, region, n));
         } else {
-          if (dd_try) WS_TRY(launch_dd_aggregate_early(h, region));
+          if (dd_try) WS_TRY(launch_dd_counting(h, region, 0));
           if (reserve && h->early_req && h->enc == kEncAlnum6) WS_TRY(launch_early_hist(h, region));
+          if (dd_try) WS_TRY(launch_dd_counting(h, region, 1));
         }
         if (h->dd_launched)
           WS_CUDA(cudaMemcpyAsync(tot_host + kDdHostOff, h->dd_pool.p, kDdCtlWords * 4, cudaMemcpyDeviceToHost, h->st));
@@ -1573,9 +1593,11 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
         if (bk.dd_n == 0 || bk.dd_n > h->dd_lay.dcap[bk.len - 1] || bk.dd_n > bk.count)
           return fail(WS_ERR_STATE, "distinct-word count out of range");
       }
-      if (h->dd_ok[0]) h->early_done = false;  // the class's early launches did nothing
+      // a class's early launches ran only if the probe gave the class up
+      // (a class that ran out of budget later sorts without them)
+      if (!ctl[kDdCtlProbe + 0]) h->early_done = false;
       for (int c = 1; c < 4; ++c)
-        if (h->dd_ok[c]) h->split_early[c] = h->count_early[c] = false;
+        if (!ctl[kDdCtlProbe + c]) h->split_early[c] = h->count_early[c] = false;
       if (h->prof) {
         double kb = 0, kb0 = 0;
         for (auto& bk : h->buckets)
@@ -1630,6 +1652,16 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
               b += (double)counts[L - 1] * ((c == 1 ? 8.0 : (double)key_bytes(c)) + 2.0);
         }
         r.bytes = b;
+        // a counted class's early launches returned at once (device flag): their
+        // records keep the launch but not the sort path's name or bytes
+        int ec = -1;
+        if (r.name == "radix_hist_l0") ec = 0;
+        else if (r.name.rfind("split_l", 0) == 0) ec = r.name[7] - '0';
+        else if (r.name.rfind("part_count_l", 0) == 0) ec = r.name[12] - '0';
+        if (ec >= 0 && ec < 4 && h->dd_launched && !tot_host[kDdHostOff + kDdCtlProbe + ec]) {
+          r.name = "gated_" + r.name;
+          r.bytes = 0;
+        }
       }
       h->early_phase_first = 0;
     }
@@ -2397,6 +2429,9 @@ int ws_create(ws_handle** out, int32_t device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->xs, cudaStreamNonBlocking, prio_lo);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_zero, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dd, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_probe, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_lo, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_hi, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_chain, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
   for (int c = 0; c <= kClasses && e == cudaSuccess; ++c)
@@ -2455,6 +2490,9 @@ void ws_destroy(ws_handle* h) {
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_zero) cudaEventDestroy(h->ev_zero);
   if (h->ev_dd) cudaEventDestroy(h->ev_dd);
+  if (h->ev_probe) cudaEventDestroy(h->ev_probe);
+  if (h->ev_lo) cudaEventDestroy(h->ev_lo);
+  if (h->ev_hi) cudaEventDestroy(h->ev_hi);
   if (h->ev_chain) cudaEventDestroy(h->ev_chain);
   if (h->zs) cudaStreamDestroy(h->zs);
   if (h->xs) cudaStreamDestroy(h->xs);

@@ -44,11 +44,12 @@ namespace {
 
 constexpr int kAggThreads = 512;
 constexpr int kAggTile = 4096;    // keys per tile
+constexpr int kProbeKeys = 1024;  // keys of a bucket's first tile the probe counts
 constexpr int kAggSlotBits = 13;
 constexpr int kAggSlots = 1 << kAggSlotBits;  // shared-memory table slots (load <= 1/2)
 constexpr uint32_t kRepBits = 13; // slot = occurrences << 13 | (key index in tile + 1)
 constexpr uint32_t kRepMask = (1u << kRepBits) - 1;
-constexpr uint32_t kMaxProbes = 4096;  // a longer probe sequence means the table is (nearly) full
+constexpr uint32_t kMaxProbes = 64;  // tables stay at most half full: a longer probe sequence means the bucket is out of budget
 static_assert(kAggTile < (1 << kRepBits), "tile index must fit the slot's low bits");
 
 template <int LANES>
@@ -158,7 +159,7 @@ __device__ __forceinline__ int dd_insert(const DdTab& t, const Key<LANES>& k, ui
     }
     if (++s == t.slots) s = 0;
     // a long probe sequence: the table is filling up because the bucket ran out of budget
-    if ((probe & 15u) == 15u && ld_relaxed(ovf)) return -1;
+    if ((probe & 7u) == 7u && ld_relaxed(ovf)) return -1;
   }
   return -1;
 }
@@ -175,17 +176,21 @@ struct AggSmem {
   uint32_t nnew, dbase;
 };
 
-// One tile of a bucket: count in shared memory, then flush to the bucket's table.
-template <int LANES>
+// One tile of a bucket: count in shared memory, then flush to the bucket's
+// table. PROBE (dd_probe_kernel): only count the tile and judge it -- a full
+// tile of mostly different words gives the bucket's lane class up (*probe).
+template <int LANES, bool PROBE = false>
 __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm, void* dk,
-                         uint32_t* dslot, uint32_t dcap, uint32_t* dcount, uint32_t* ovf) {
+                         uint32_t* dslot, uint32_t dcap, uint32_t* dcount, uint32_t* ovf,
+                         uint32_t* covf, uint32_t* probe = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t* tab = sm.tab;
   for (int i = tid; i < kAggSlots; i += kAggThreads) tab[i] = 0;
   if (tid == 0) sm.nnew = 0;
   __syncthreads();
-  const uint32_t cnt = min((uint32_t)kAggTile, n - base);
-  constexpr int E = kAggTile / kAggThreads;
+  // (the probe judges a bucket by its first kProbeKeys keys)
+  const uint32_t cnt = min((uint32_t)(PROBE ? kProbeKeys : kAggTile), n - base);
+  constexpr int E = (PROBE ? kProbeKeys : kAggTile) / kAggThreads;
   constexpr int G = LANES <= 1 ? E : (LANES == 2 ? 4 : 2);  // keys in flight per thread
 #pragma unroll 1
   for (int e0 = 0; e0 < E; e0 += G) {
@@ -243,6 +248,19 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     at += __popc(bal);
   }
   __syncthreads();
+  // A full tile of mostly different words: the bucket does not repeat its
+  // vocabulary, counting it would cost more than sorting it. Give the bucket
+  // (and with it its lane class) up now, before its table fills.
+  if (cnt == (uint32_t)(PROBE ? kProbeKeys : kAggTile) && nd * 4u > cnt * 3u) {
+    if (tid == 0) {
+      atomicExch(ovf, 1u);
+      atomicExch(covf, 1u);
+      if (PROBE) atomicExch(probe, 1u);
+    }
+    __syncthreads();
+    return;
+  }
+  if constexpr (PROBE) return;
   bool fail = false;
   for (uint32_t q = tid; q < nd; q += kAggThreads) {
     const uint32_t v = tab[sm.list[q]];
@@ -272,7 +290,10 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
       }
     }
   }
-  if (fail) atomicExch(ovf, 1u);
+  if (fail) {
+    atomicExch(ovf, 1u);
+    atomicExch(covf, 1u);
+  }
   __syncthreads();
   const uint32_t nn = min(sm.nnew, (uint32_t)kAggNewCap);
   if (nn) {
@@ -280,7 +301,10 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     __syncthreads();
     const uint32_t db = sm.dbase;
     if (db + nn > dcap) {
-      if (tid == 0) atomicExch(ovf, 1u);
+      if (tid == 0) {
+        atomicExch(ovf, 1u);
+        atomicExch(covf, 1u);
+      }
     } else {
       for (uint32_t i = tid; i < nn; i += kAggThreads) {
         const uint32_t v = tab[sm.list[sm.new_q[i]]];
@@ -395,8 +419,10 @@ __global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_
   const uint32_t tiles = s_tb[kDdLens];
   for (uint32_t g = blockIdx.x; g < tiles; g += gridDim.x) {
     const int b = __popc(__ballot_sync(0xffffffffu, s_tb[1 + (tid & 31)] <= g));
-    // the bucket is out of budget already (one answer for the whole CTA: agg_tile has barriers)
-    if (__syncthreads_or(tid == 0 ? (int)ld_relaxed(ovf + b) : 0)) continue;
+    // the bucket, or another bucket of its lane class, is out of budget already: the class
+    // will be sorted (one answer for the whole CTA: agg_tile has barriers)
+    uint32_t* covf = a.ctl + kDdCtlClsOvf + dd_class_of_len(b + 1);
+    if (__syncthreads_or(tid == 0 ? (int)(ld_relaxed(ovf + b) | ld_relaxed(covf)) : 0)) continue;
     DdTab t;
     t.keys = a.keys_cap + a.region[b];
     t.tab = a.table + lay.tab_off[b];
@@ -405,12 +431,12 @@ __global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_
     void* dk = a.dk + lay.dk_off[b];
     uint32_t* dslot = a.aux + lay.aux_off[b];
     if constexpr (GRP == 0) {
-      agg_tile<0>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b);
+      agg_tile<0>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b, covf);
     } else {
       switch (dd_class_of_len(b + 1)) {
-        case 1: agg_tile<1>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
-        case 2: agg_tile<2>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
-        default: agg_tile<3>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b); break;
+        case 1: agg_tile<1>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b, covf); break;
+        case 2: agg_tile<2>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b, covf); break;
+        default: agg_tile<3>(t, s_n[b], base, sm, dk, dslot, lay.dcap[b], dcount + b, ovf + b, covf); break;
       }
     }
   }
@@ -435,6 +461,35 @@ __global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_
   __syncwarp();
   __threadfence();
   if (a.plan) dd_write_plan(a, GRP, lay, s_n);
+}
+
+// One CTA per length: the bucket's first tile counted and judged (a few
+// microseconds), so that a text of mostly different words (configs 2, 3) gives
+// its lane classes up before the counting launches run, and the sort paths'
+// early launches -- which wait for this kernel only -- start at once.
+__global__ void __launch_bounds__(kAggThreads) dd_probe_kernel(const __grid_constant__ DdAgg a) {
+  __shared__ AggSmem sm;
+  const int b = blockIdx.x;
+  const uint32_t n = a.fill[b];
+  if (n < (uint32_t)kAggTile) return;
+  DdTab t;
+  t.keys = a.keys_cap + a.region[b];
+  t.tab = nullptr;
+  t.slots = 0;
+  const int cls = dd_class_of_len(b + 1);
+  uint32_t* ovf = a.ctl + kDdCtlOvf + b;
+  uint32_t* covf = a.ctl + kDdCtlClsOvf + cls;
+  uint32_t* probe = a.ctl + kDdCtlProbe + cls;
+  switch (cls) {
+    case 0: agg_tile<0, true>(t, n, 0, sm, nullptr, nullptr, 0, nullptr, ovf, covf, probe); break;
+    case 1: agg_tile<1, true>(t, n, 0, sm, nullptr, nullptr, 0, nullptr, ovf, covf, probe); break;
+    case 2: agg_tile<2, true>(t, n, 0, sm, nullptr, nullptr, 0, nullptr, ovf, covf, probe); break;
+    default: agg_tile<3, true>(t, n, 0, sm, nullptr, nullptr, 0, nullptr, ovf, covf, probe); break;
+  }
+}
+
+void launch_dd_probe(const DdAgg& a, cudaStream_t st) {
+  dd_probe_kernel<<<kDdLens, kAggThreads, 0, st>>>(a);
 }
 
 void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st) {

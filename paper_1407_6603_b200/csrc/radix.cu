@@ -453,7 +453,7 @@ radix_hist_kernel(const __grid_constant__ RadixLaunch a) {
 // ascending length; whole-key counts for <= 12-bit keys when allowed).
 __global__ void __launch_bounds__(kRThreads) radix_hist_early_kernel(const __grid_constant__ EarlyHist e) {
   __shared__ uint32_t sm[kJointMax];
-  if (e.skip && *e.skip) return;  // class 0's words were counted instead (dedupe.cu)
+  if (e.go && !*e.go) return;  // class 0's words are being counted instead (dedupe.cu)
   constexpr uint32_t T = RadixCfg<uint32_t>::T;
   RadixSeg seg[5];
   uint32_t nseg = 0, tiles = 0, joff = 0;

@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(kSampleThreads) sample_split_kernel(const __gr
 template <int LANES>
 __global__ void __launch_bounds__(kSampleThreads) sample_split_early_kernel(const __grid_constant__ SplitEarly e) {
   extern __shared__ __align__(16) uint64_t dsm[];
-  if (e.skip && *e.skip) return;  // the class's words were counted instead (dedupe.cu)
+  if (e.go && !*e.go) return;  // the class's words are being counted instead (dedupe.cu)
   SampleSeg sg;
   memset(&sg, 0, sizeof sg);
   uint32_t slots = 0, splits = 0, tiles = 0, key_off = 0, nfit = 0;
@@ -956,9 +956,9 @@ __global__ void __launch_bounds__(kPartThreads, WS_PART_MINB) partition_kernel(c
 // from the launch the split CTAs wrote (device-planned, same rules as the host
 // plan): a persistent grid over the class's partition tiles.
 template <int LANES>
-__global__ void __launch_bounds__(kPartThreads, 2) partition_count_early_kernel(const SampleLaunch* __restrict__ plan, const uint32_t* __restrict__ skip) {
+__global__ void __launch_bounds__(kPartThreads, 2) partition_count_early_kernel(const SampleLaunch* __restrict__ plan, const uint32_t* __restrict__ go) {
   pdl_wait();
-  if (skip && *skip) return;  // no split launch wrote `plan` for this call (dedupe.cu)
+  if (go && !*go) return;  // no split launch wrote `plan` for this call (dedupe.cu)
   const SampleLaunch& a = *plan;
   const uint32_t items = a.work_items;
   for (uint32_t item = blockIdx.x; item < items; item += gridDim.x) {
@@ -1596,11 +1596,11 @@ int part_tile_size() { return kPartTile; }
 int subsort_tile_size(int lanes) { return kSubThreads * (lanes <= 1 ? TileCfg<1>::E : TileCfg<2>::E); }
 
 void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st,
-                                  const uint32_t* skip) {
+                                  const uint32_t* go) {
   switch (lanes) {
-    case 1: launch_pdl(partition_count_early_kernel<1>, grid, kPartThreads, 0, st, plan, skip); break;
-    case 2: launch_pdl(partition_count_early_kernel<2>, grid, kPartThreads, 0, st, plan, skip); break;
-    default: launch_pdl(partition_count_early_kernel<3>, grid, kPartThreads, 0, st, plan, skip); break;
+    case 1: launch_pdl(partition_count_early_kernel<1>, grid, kPartThreads, 0, st, plan, go); break;
+    case 2: launch_pdl(partition_count_early_kernel<2>, grid, kPartThreads, 0, st, plan, go); break;
+    default: launch_pdl(partition_count_early_kernel<3>, grid, kPartThreads, 0, st, plan, go); break;
   }
 }
 

@@ -152,12 +152,12 @@ struct SplitEarly {
   SampleLaunch* plan;
   uint16_t* slot_ids;
   uint32_t ptile;          // keys per partition tile
-  const uint32_t* skip;    // or null: nonzero = the class's words were counted (dedupe.cu), do nothing
+  const uint32_t* go;      // or null: run only if nonzero (dedupe.cu's probe gave the class up; else its words are counted)
 };
 // The count pass of one multi-lane class, planned on the device (the split
 // launch's table): a persistent grid over the class's partition tiles.
 void launch_partition_count_early(int lanes, const SampleLaunch* plan, int grid, cudaStream_t st,
-                                  const uint32_t* skip = nullptr);
+                                  const uint32_t* go = nullptr);
 void launch_sample_split_early(int lanes, const SplitEarly& e, cudaStream_t st);
 // Small corpora: one CTA per length bucket sorts it on chip and writes its
 // payload records, straight after the payload-mode ingest (6-bit keys);
@@ -231,7 +231,7 @@ struct EarlyHist {
   uint32_t* totals;         // [5][kRadixMaxPasses][kRadixTotStride], zeroed
   uint32_t* joint;          // whole-key counters, zeroed
   int joint_ok;             // count (not sort) keys of <= 12 bits
-  const uint32_t* skip;     // or null: nonzero = the class's words were counted (dedupe.cu), do nothing
+  const uint32_t* go;       // or null: run only if nonzero (dedupe.cu's probe gave class 0 up; else its words are counted)
 };
 constexpr int kRadixC0Segs = 5;  // class-0 buckets at most (the totals table is sized for them)
 void launch_radix_hist_early(const EarlyHist& e, cudaStream_t st);
@@ -249,6 +249,8 @@ constexpr int kDdCtlCount = 0;   // [32] distinct words per length
 constexpr int kDdCtlOvf = 32;    // [32] the bucket ran out of its table budget
 constexpr int kDdCtlDone = 64;   // [2] CTAs of each aggregate launch that have finished
 constexpr int kDdCtlSkip = 68;   // [4] per lane class: every bucket stayed in budget
+constexpr int kDdCtlClsOvf = 72; // [4] per lane class: a bucket ran out of budget (the class's other tiles stop)
+constexpr int kDdCtlProbe = 76;  // [4] per lane class: dd_probe_kernel gave the class up (its sort path's early launches run)
 constexpr int kDdCtlWords = 128;
 struct DdAgg {
   const uint32_t* fill;     // the ingest's per-length word counts
@@ -261,6 +263,8 @@ struct DdAgg {
   struct DdDevPlan* plan;   // or null: [2], each launch's last CTA writes its chain's plan
   uint32_t stile1, stilen;  // keys per sorted tile (one-word / wider keys: dd_sort_tile_size)
 };
+// first tile of every bucket judged (mostly different words: the class is given up)
+void launch_dd_probe(const DdAgg& a, cudaStream_t st);
 // two launches side by side (grp 0: lengths 1-5, 1: the wider keys)
 void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st);
 int dd_aggregate_ctas_per_sm(int grp);

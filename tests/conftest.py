@@ -4,8 +4,16 @@ from pathlib import Path
 
 import pytest
 
+import os
+
 ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = ROOT / "tests" / "golden"
+# The library counts distinct words (csrc/dedupe.cu) only for texts of 32 MiB
+# and more by default; the suite lowers that to 1 MiB (read once per process,
+# before the first library call) so that its mid-size fixtures -- and every
+# knob subprocess, which inherits the environment -- go through the counting
+# path as well. Tests of the sort paths themselves set WSORT_NO_DEDUPE=1.
+os.environ.setdefault("WSORT_DEDUPE_MIN", str(1 << 20))
 if str(ROOT) not in sys.path:
     sys.path.insert(0, str(ROOT))
 
