@@ -1411,6 +1411,14 @@ int ingest_text_impl(ws_handle* h, const uint8_t* text, uint64_t n, int32_t flag
     // side stream while the ingest runs
     const bool dd_try = reserve && h->dd_req && h->enc == kEncAlnum6 && !h->tiny_req && n > 0;
     if (dd_try) {
+      // the counting path's two side streams exist only on handles that count
+      // (a handle for small texts keeps the stream set its class chains were tuned with)
+      if (!h->zs) {
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+        WS_CUDA(cudaStreamCreateWithPriority(&h->zs, cudaStreamNonBlocking, prio_lo));
+        WS_CUDA(cudaStreamCreateWithPriority(&h->xs, cudaStreamNonBlocking, prio_lo));
+      }
       WS_TRY(dd_zero_pool(h, n, h->zs));
       WS_CUDA(cudaEventRecord(h->ev_zero, h->zs));
     }
@@ -2425,8 +2433,6 @@ int ws_create(ws_handle** out, int32_t device) {
     if (e == cudaSuccess)
       e = cudaStreamCreateWithPriority(&h->ds[c], cudaStreamNonBlocking, prio_hi);
   }
-  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->zs, cudaStreamNonBlocking, prio_lo);
-  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&h->xs, cudaStreamNonBlocking, prio_lo);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_zero, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dd, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_probe, cudaEventDisableTiming);
