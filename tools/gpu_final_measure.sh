@@ -1,8 +1,8 @@
 #!/bin/bash
-# Round-end measurement set: bench (config 4) + configs 0-3, reference arm,
-# launch list of the bench command, ncu --set full of the main kernels
-# (counting path on config 4; sort paths with WSORT_NO_DEDUPE=1; stats mode;
-# small corpus).
+# Round-end measurement set: bench (config 4) + configs 0-3, the sort paths
+# alone (WSORT_NO_DEDUPE=1), reference arm, timeline, launch list of the bench
+# command. (ncu --set full captures: tools/gpu_dd_ncu.sh; their reports are
+# large, keep gpurun_out/ under 64 MiB or nothing is copied back.)
 TAG=${1:-x}
 mkdir -p gpurun_out
 timeout 900 python bench.py > gpurun_out/fm_${TAG}_bench.json 2> gpurun_out/fm_${TAG}_bench.err; echo "bench rc=$?"
@@ -14,9 +14,3 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/f
 timeout 300 python tools/dd_check.py 4 > gpurun_out/fm_${TAG}_timeline_config4.txt 2>/dev/null; head -1 gpurun_out/fm_${TAG}_timeline_config4.txt
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/fm_${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo "launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ingest7|dd_" -s 0 -c 16 \
-   -o gpurun_out/fm_${TAG}_counting python tools/run_resident.py 4 1 > gpurun_out/fm_${TAG}_ncu_counting.log 2>&1; echo "ncu counting rc=$?"
-WSORT_NO_DEDUPE=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"radix_onesweep|subsort|partition_kernel" -s 0 -c 10 \
-   -o gpurun_out/fm_${TAG}_payload python tools/run_resident.py 4 1 > gpurun_out/fm_${TAG}_ncu_payload.log 2>&1; echo "ncu sort paths rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"merge_kernel|tile_sort|ingest7_kernel<1>|reorder" -c 10 \
-   -o gpurun_out/fm_${TAG}_stats python tools/run_stats.py 1 > gpurun_out/fm_${TAG}_ncu_stats.log 2>&1; echo "ncu stats rc=$?"
