@@ -96,6 +96,21 @@ def test_one_bucket_over_budget_sends_its_class_to_the_sort():
     assert not mask & 1, mask
 
 
+def test_late_overflow_after_a_passing_probe():
+    """The probe sees a bucket's first keys only: a text that starts with one
+    repeated word and then turns into distinct words passes it, the counting
+    launch gives the class up later, and the class is sorted without the early
+    launches (which ran for nobody)."""
+    uniq6 = synth.random_words(31, 150_000, max_len=6, min_len=6)
+    uniq3 = synth.random_words(37, 5000, max_len=3, min_len=3)
+    text = b" ".join([b"Repeat"] * 20_000 + [b"the"] * 20_000 + list(uniq6) + list(uniq3) + [b"tail"] * 9000)
+    assert len(text) >= 1 << 20
+    got, mask = counted_payload(text)
+    assert got == want_of(text)
+    assert not mask & 2, mask  # class 1 (the 6-character bucket) ran out of budget
+    assert mask & 1, mask      # class 0 repeats enough
+
+
 def test_long_words_and_heavy_runs():
     """One word filling whole output tiles, runs of one, and words beyond 32
     characters (never counted) side by side."""
