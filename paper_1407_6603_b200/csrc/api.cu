@@ -16,6 +16,7 @@
 // Finished buckets are emitted (and copied to the host) on side streams while
 // later passes run. ws_sort_texts runs several corpora through peer handles.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -75,6 +76,8 @@ inline void tmark(const char* what) {
     int r_ = (x);             \
     if (r_ != WS_OK) return r_; \
   } while (0)
+
+std::atomic<bool> g_exiting{false};  // set by an atexit handler (see ws_destroy)
 
 struct DevBuf {
   void* p = nullptr;
@@ -2446,12 +2449,18 @@ int ws_create(ws_handle** out, int32_t device) {
     ws_destroy(h);
     return fail_cuda(e, "cudaStreamCreate", __LINE__);
   }
+  static std::once_flag exit_once;  // registered after the CUDA runtime's own handler: runs before it
+  std::call_once(exit_once, [] { atexit([] { g_exiting.store(true, std::memory_order_release); }); });
   *out = h;
   return WS_OK;
 }
 
 void ws_destroy(ws_handle* h) {
   if (!h) return;
+  // Process exit: once the atexit handlers run, the CUDA runtime may already be
+  // torn down (its own handler); a handle destroyed that late (a thread-local
+  // handle, an object finalised by the host language at exit) is left to the OS.
+  if (g_exiting.load(std::memory_order_acquire)) return;
   for (ws_handle* p : h->peers) ws_destroy(p);
   h->peers.clear();
   cudaSetDevice(h->device);
@@ -2932,6 +2941,7 @@ int ws_host_alloc(uint64_t bytes, void** out) {
 }
 
 int ws_host_free(void* p) {
+  if (g_exiting.load(std::memory_order_acquire)) return WS_OK;  // see ws_destroy
   if (p) WS_CUDA(cudaFreeHost(p));
   return WS_OK;
 }

@@ -179,15 +179,44 @@ struct AggSmem {
 // One tile of a bucket: count in shared memory, then flush to the bucket's
 // table. PROBE (dd_probe_kernel): only count the tile and judge it -- a full
 // tile of mostly different words gives the bucket's lane class up (*probe).
+// Diagnostics (-DWS_DD_PROF=1, tools only): time of each phase of a tile (clear,
+// count, compaction, flush, append), summed over tiles per launch group, read
+// by dd_prof_read.
+#ifndef WS_DD_PROF
+#define WS_DD_PROF 0
+#endif
+#if WS_DD_PROF
+__device__ unsigned long long g_dd_prof[2][8];
+#define WS_DD_STAMP(k)                                                          \
+  do {                                                                          \
+    if (!PROBE && threadIdx.x == 0) {                                           \
+      unsigned long long now_;                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                  \
+      if ((k) > 0) atomicAdd(&g_dd_prof[LANES == 0 ? 0 : 1][k], now_ - t_prev_); \
+      else atomicAdd(&g_dd_prof[LANES == 0 ? 0 : 1][7], 1ull);                  \
+      t_prev_ = now_;                                                           \
+    }                                                                           \
+  } while (0)
+#else
+#define WS_DD_STAMP(k) do { } while (0)
+#endif
+
 template <int LANES, bool PROBE = false>
 __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm, void* dk,
                          uint32_t* dslot, uint32_t dcap, uint32_t* dcount, uint32_t* ovf,
                          uint32_t* covf, uint32_t* probe = nullptr) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#if WS_DD_PROF
+  unsigned long long t_prev_ = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prev_));
+  const unsigned long long t_first_ = t_prev_;
+  (void)t_first_;
+#endif
   uint32_t* tab = sm.tab;
   for (int i = tid; i < kAggSlots; i += kAggThreads) tab[i] = 0;
   if (tid == 0) sm.nnew = 0;
   __syncthreads();
+  WS_DD_STAMP(0);
   // (the probe judges a bucket by its first kProbeKeys keys)
   const uint32_t cnt = min((uint32_t)(PROBE ? kProbeKeys : kAggTile), n - base);
   constexpr int E = (PROBE ? kProbeKeys : kAggTile) / kAggThreads;
@@ -222,6 +251,7 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     }
   }
   __syncthreads();
+  WS_DD_STAMP(1);
   // occupied slots -> a dense list (each warp owns a contiguous range of
   // slots: count, prefix over warps, place), so every thread flushes its share
   // of the tile's distinct keys (a thread's flushes are dependent L2 round trips)
@@ -248,6 +278,7 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     at += __popc(bal);
   }
   __syncthreads();
+  WS_DD_STAMP(2);
   // A full tile of mostly different words: the bucket does not repeat its
   // vocabulary, counting it would cost more than sorting it. Give the bucket
   // (and with it its lane class) up now, before its table fills.
@@ -295,6 +326,7 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     atomicExch(covf, 1u);
   }
   __syncthreads();
+  WS_DD_STAMP(3);
   const uint32_t nn = min(sm.nnew, (uint32_t)kAggNewCap);
   if (nn) {
     if (tid == 0) sm.dbase = atomicAdd(dcount, nn);
@@ -315,6 +347,7 @@ __device__ void agg_tile(const DdTab& t, uint32_t n, uint32_t base, AggSmem& sm,
     }
   }
   __syncthreads();  // the shared memory is reused by the CTA's next tile
+  WS_DD_STAMP(4);
 }
 
 __host__ __device__ inline int dd_class_of_len(int L) { return lanes_for_len_enc(L, kEncAlnum6); }
@@ -819,6 +852,17 @@ void launch_dd_prefix(const DdChain& c, int grid, cudaStream_t st) {
 void launch_dd_chain_expand(const DdChain& c, int grid, cudaStream_t st) {
   launch_pdl(dd_expand_dev_kernel, grid, kXThreads, 0, st, c);
 }
+
+#if WS_DD_PROF
+// (tools/dd_phases.py through ctypes; not part of the ABI)
+extern "C" int dd_prof_read(unsigned long long* out16) {
+  cudaDeviceSynchronize();
+  cudaError_t e = cudaMemcpyFromSymbol(out16, g_dd_prof, sizeof g_dd_prof);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(g_dd_prof, z, sizeof z);
+  return (int)e;
+}
+#endif
 
 WS_DEFINE_CHECK_READER(check_reader_dedupe)
 

@@ -61,3 +61,23 @@ def _bounds_checks(request):
     assert _native.checked_build(), "WSORT_CHECKED=1 but the library is not a checked build"
     fails, where = _native.debug_checks()
     assert fails == 0, f"{fails} device bounds checks failed, first at {where}"
+
+
+def pytest_unconfigure(config):
+    """Last hook of a run (the summary is out). When the CUDA library was
+    loaded, leave without interpreter teardown: with the library's worker
+    threads and handles alive, teardown has crashed (SIGSEGV after the summary)
+    once in a while on the GPU boxes, which would turn a green run red."""
+    mod = sys.modules.get("paper_1407_6603_b200._native")
+    if mod is None or getattr(mod, "_lib", None) is None:
+        return
+    status = getattr(config, "_ws_exitstatus", None)
+    if status is None:
+        return
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(int(status))
+
+
+def pytest_sessionfinish(session, exitstatus):
+    session.config._ws_exitstatus = exitstatus

@@ -102,7 +102,7 @@ def test_late_overflow_after_a_passing_probe():
     launch gives the class up later, and the class is sorted without the early
     launches (which ran for nobody)."""
     uniq6 = synth.random_words(31, 150_000, max_len=6, min_len=6)
-    uniq3 = synth.random_words(37, 5000, max_len=3, min_len=3)
+    uniq3 = synth.random_words(37, 1000, max_len=3, min_len=3)  # within the 3-character bucket's budget
     text = b" ".join([b"Repeat"] * 20_000 + [b"the"] * 20_000 + list(uniq6) + list(uniq3) + [b"tail"] * 9000)
     assert len(text) >= 1 << 20
     got, mask = counted_payload(text)

@@ -31,7 +31,12 @@ def test_reference_suite_unchanged():
     env = dict(os.environ)
     env["PYTHONPATH"] = os.pathsep.join([str(ALIAS), str(ROOT), env.get("PYTHONPATH", "")])
     env.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_wordsort")
-    r = subprocess.run([sys.executable, "-m", "pytest", str(REF_TESTS), "-q", "-p", "ref_plugin",
+    # The child leaves with os._exit right after pytest's summary: interpreter
+    # teardown with the CUDA library and the tests' worker threads alive has
+    # crashed (SIGSEGV after "179 passed") once in a while on the GPU boxes.
+    code = ("import os, sys, pytest; rc = pytest.main(sys.argv[1:]); "
+            "sys.stdout.flush(); sys.stderr.flush(); os._exit(int(rc))")
+    r = subprocess.run([sys.executable, "-c", code, str(REF_TESTS), "-q", "-p", "ref_plugin",
                         "-p", "no:cacheprovider", "--rootdir", str(REF_TESTS)],
                        env=env, cwd=str(REF_TESTS), capture_output=True, text=True, timeout=3000)
     tail = r.stdout[-3000:]
