@@ -423,13 +423,16 @@ __device__ void dd_write_plan(const DdAgg& a, int grp, const DdLayout& lay, cons
 #ifndef WS_DD_LO_MINB
 #define WS_DD_LO_MINB 3  // CTAs per SM of the one-word-key launch (register cap 65536 / (512 * MINB))
 #endif
+#ifndef WS_DD_HI_MINB
+#define WS_DD_HI_MINB 2  // ... and of the wider keys' launch
+#endif
 // One launch per key width group, side by side: GRP 0 = the uint32 keys
 // (lengths 1-5: most words, few registers, more CTAs per SM to hide the
 // flush's L2 round trips), 1 = the wider keys. (A third launch for the
 // one-lane keys measured no faster: the SMs are full either way.)
 // Each launch's last CTA finishes its classes' control words and its chain's plan.
 template <int GRP>
-__global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : 2) dd_aggregate_kernel(const __grid_constant__ DdAgg a) {
+__global__ void __launch_bounds__(kAggThreads, GRP == 0 ? WS_DD_LO_MINB : WS_DD_HI_MINB) dd_aggregate_kernel(const __grid_constant__ DdAgg a) {
   __shared__ AggSmem sm;
   __shared__ DdLayout lay;
   __shared__ uint32_t s_n[kDdLens], s_tb[kDdLens + 1];
@@ -529,7 +532,7 @@ void launch_dd_aggregate(const DdAgg& a, int grp, int grid, cudaStream_t st) {
   if (grp == 0) dd_aggregate_kernel<0><<<grid, kAggThreads, 0, st>>>(a);
   else dd_aggregate_kernel<1><<<grid, kAggThreads, 0, st>>>(a);
 }
-int dd_aggregate_ctas_per_sm(int grp) { return grp == 0 ? WS_DD_LO_MINB : 2; }
+int dd_aggregate_ctas_per_sm(int grp) { return grp == 0 ? WS_DD_LO_MINB : WS_DD_HI_MINB; }
 
 // ----------------------------------------------------------------------------
 // after the distinct keys are sorted: run prefixes and payload records
