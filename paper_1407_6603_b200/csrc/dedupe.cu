@@ -49,7 +49,7 @@ constexpr int kAggSlotBits = 13;
 constexpr int kAggSlots = 1 << kAggSlotBits;  // shared-memory table slots (load <= 1/2)
 constexpr uint32_t kRepBits = 13; // slot = occurrences << 13 | (key index in tile + 1)
 constexpr uint32_t kRepMask = (1u << kRepBits) - 1;
-constexpr uint32_t kMaxProbes = 64;  // tables stay at most half full: a longer probe sequence means the bucket is out of budget
+constexpr uint32_t kMaxProbes = 128;  // tables stay at most half full (longest expected probe sequence ~5 ln n there): longer means out of budget
 static_assert(kAggTile < (1 << kRepBits), "tile index must fit the slot's low bits");
 
 template <int LANES>
