@@ -115,3 +115,18 @@ def test_replica_harness_gloo_world2(tmp_path):
     res = json.loads(outs[0][0].strip().splitlines()[-1])
     assert res["t_job"] == 11.0 and res["words"] == 4000.0
     assert res["lens"][0] != res["lens"][1]  # distinct replica corpora
+
+
+def test_counting_layout_fits_its_allocation_bounds(tmp_path):
+    """csrc/plan.cuh: for any split of a text into words of 1..32 characters the
+    counting path's tables, distinct-key lists and per-distinct-word arrays
+    (dd_layout) fit what the host allocates and zeroes before the counts are
+    known (dd_max_*); the same header is compiled into the kernels."""
+    import subprocess
+
+    root = Path(__file__).resolve().parent.parent
+    exe = tmp_path / "dd_plan_bounds"
+    subprocess.run(["g++", "-O2", "-std=c++17", f"-I{root / 'paper_1407_6603_b200' / 'csrc'}",
+                    str(root / "tests" / "cpp" / "dd_plan_bounds.cpp"), "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
