@@ -1071,15 +1071,16 @@ int launch_tiny(ws_handle* h, const uint64_t* region, uint64_t n) {
 // Distinct-word counting (dedupe.cu) right behind the payload-mode ingest, on
 // the main stream: the ingest's sync then also covers its counters. WSORT_NO_DEDUPE=1
 // turns it off; WSORT_DEDUPE_MIN=bytes sets the smallest text that tries it
-// (default 32 MiB: smaller texts are bound by launch latencies and the host's
+// (default 48 MiB: smaller texts are bound by launch latencies and the host's
 // enqueue, where the counting path's dozen extra launches cost more than its
-// counting saves -- configs 1-3 measured 0.15-0.26 ms with it against 0.14-0.20).
+// counting saves -- config-4-like texts of 31 MB: 0.280 vs 0.259 ms, of 63 MB:
+// 0.374 vs 0.414 ms, tools/dd_threshold.py; configs 1-3: 0.15-0.26 vs 0.14-0.20 ms).
 bool dedupe_wanted(uint64_t n) {
   static const bool off = env_on("WSORT_NO_DEDUPE") || env_on("WSORT_D2H_PER_CLASS") ||
                           env_on("WSORT_NO_FUSED_PAYLOAD");
   static const uint64_t min_text = [] {
     const char* e = getenv("WSORT_DEDUPE_MIN");
-    return e ? (uint64_t)strtoull(e, nullptr, 0) : (uint64_t)(32u << 20);
+    return e ? (uint64_t)strtoull(e, nullptr, 0) : (uint64_t)(48u << 20);
   }();
   return !off && n >= min_text;
 }

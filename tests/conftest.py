@@ -8,7 +8,7 @@ import os
 
 ROOT = Path(__file__).resolve().parent.parent
 GOLDEN = ROOT / "tests" / "golden"
-# The library counts distinct words (csrc/dedupe.cu) only for texts of 32 MiB
+# The library counts distinct words (csrc/dedupe.cu) only for texts of 48 MiB
 # and more by default; the suite lowers that to 1 MiB (read once per process,
 # before the first library call) so that its mid-size fixtures -- and every
 # knob subprocess, which inherits the environment -- go through the counting
