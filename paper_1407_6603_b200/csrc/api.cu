@@ -1826,7 +1826,6 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
   long long* km = stats ? h->stat_k.as<long long>() : nullptr;
   // packed buckets: one schedule per lane class, each class on its own stream
   // (the classes are independent; small classes fill the big one's bubbles)
-  if (h->dd_chain) WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_chain, 0));  // the call ends after the chain
   WS_CUDA(cudaEventRecord(h->ev_fork, h->st));
   // class 0 (radix: a chain of small passes, the longest) is submitted first
   // on a high-priority stream; the multi-lane classes fill around it
@@ -2066,6 +2065,9 @@ int sort_impl(ws_handle* h, bool stats, FusedEmit* fe = nullptr) {
       h->buckets[i].kmax = hk[i];
     }
   }
+  // the call ends after the counted classes' chains (joined last: classes that
+  // are sorted fork from the main stream above and run beside them)
+  if (h->dd_chain) WS_CUDA(cudaStreamWaitEvent(h->st, h->ev_chain, 0));
   WS_TRY(check_launch("sort"));
   h->early_done = false;  // early launches serve only the sort right after their ingest
   for (bool& f : h->dd_ok) f = false;  // ... and so do the distinct-word counts
