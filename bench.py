@@ -369,7 +369,9 @@ FAMILIES = {
     "tiny_sort": ("tiny",),  # small corpora (<= 512 KiB): one CTA per bucket after the ingest
     # distinct-word counting (texts that repeat their vocabulary): every key read once
     # and counted; distinct keys sorted (tiles + rank merge); run prefixes; payload records
-    "count_aggregate": ("dd_aggregate", "dd_aggregate_hi"),
+    # (two kernels, as in the ncu launch list: the uint32-key launch and the wider keys' launch)
+    "count_aggregate": ("dd_aggregate",),
+    "count_aggregate_wide": ("dd_aggregate_hi",),
     "count_sort_distinct": ("dd_tiles", "dd_tiles_hi", "dd_rank", "dd_rank_hi"),
     "count_run_prefix": ("dd_prefix", "dd_prefix_hi"),
     "count_expand": ("dd_expand", "dd_expand_hi"),
