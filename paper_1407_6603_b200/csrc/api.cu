@@ -1132,8 +1132,8 @@ int launch_dd_counting(ws_handle* h, const uint64_t* region, int stage) {
     a.dk = h->dd_keys.as<uint8_t>();
     a.aux = h->dd_aux.as<uint32_t>();
     a.plan = h->dd_plan.as<DdDevPlan>();
-    a.stile1 = (uint32_t)dd_sort_tile_size(1);
-    a.stilen = (uint32_t)dd_sort_tile_size(2);
+    a.stile1 = (uint32_t)dd_sort_tile_size(0);
+    a.stilen = (uint32_t)dd_sort_tile_size(1);
     // First the probe: one CTA per length judges the bucket's first keys, so a
     // text of mostly different words gives its classes up within microseconds
     // and the sort paths' early launches (which wait for the probe only) start.

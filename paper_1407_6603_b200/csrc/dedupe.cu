@@ -371,7 +371,7 @@ __device__ void dd_write_plan(const DdAgg& a, int grp, const DdLayout& lay, cons
   const uint32_t n = s_n[b];
   const bool ok = n && dd_group_of_class(cls) == grp && a.ctl[kDdCtlSkip + cls] != 0;
   const uint32_t D = ok ? ld_relaxed(a.ctl + kDdCtlCount + b) : 0u;
-  const uint32_t T = cls <= 1 ? a.stile1 : a.stilen;
+  const uint32_t T = cls == 0 ? a.stile1 : a.stilen;
   const uint32_t XT = dd_xtile_of_len(b + 1);
   p.n[b] = ok ? n : 0u;
   p.D[b] = D;

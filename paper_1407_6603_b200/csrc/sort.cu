@@ -309,12 +309,13 @@ __device__ __forceinline__ void smem_to_global(const KW<LANES>* sk, const uint32
 // sk2 (keys only, optional): a second key buffer; the merge levels then
 // alternate buffers and need one barrier per level instead of two (a level
 // writes the buffer no thread can still be reading).
-template <int LANES, bool STATS, int NT = kTileThreads, bool NAMED = false>
+// EO (or 0): keys per thread, overriding the lane class's tile width.
+template <int LANES, bool STATS, int NT = kTileThreads, bool NAMED = false, int EO = 0>
 __device__ __forceinline__ void tile_network(KW<LANES>* sk, uint32_t* si, int cnt, uint32_t idx0,
-                                             Key<LANES> (&r)[TileCfg<LANES>::E],
-                                             uint32_t (&ri)[TileCfg<LANES>::E], uint64_t& inv,
+                                             Key<LANES> (&r)[EO ? EO : TileCfg<LANES>::E],
+                                             uint32_t (&ri)[EO ? EO : TileCfg<LANES>::E], uint64_t& inv,
                                              KW<LANES>* sk2 = nullptr) {
-  constexpr int E = TileCfg<LANES>::E, T = NT * E;
+  constexpr int E = EO ? EO : TileCfg<LANES>::E, T = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   const int tid = (int)threadIdx.x;
 #pragma unroll
@@ -1413,15 +1414,24 @@ void launch_tiny_sort(const TinyLaunch& t, cudaStream_t st) {
 
 constexpr int kDdSortThreads = kTileThreads;
 template <int LANES>
-constexpr size_t dd_sort_smem() { return pass_smem_bytes<LANES, TileCfg<LANES>::T, true>(); }
+constexpr size_t dd_sort_smem() { return pass_smem_bytes<LANES, kTileThreads * (LANES == 1 ? TileCfg<2>::E : TileCfg<LANES>::E), true>(); }
 constexpr size_t kDdSortSmem = cmax(cmax(dd_sort_smem<0>(), dd_sort_smem<1>()), cmax(dd_sort_smem<2>(), dd_sort_smem<3>()));
 
 // One tile of a counted bucket's distinct keys (as the aggregate launch
 // appended them) sorted on chip by the tile network; each key's occurrences
 // are fetched from its table slot and follow it (array B).
+// Keys per thread of the distinct keys' tiles: the one-lane keys' buckets hold a
+// few thousand distinct words each, so they take the narrow tile (half the
+// on-chip sort's latency, 2-3 tiles to rank-merge); the uint32 keys' one large
+// bucket keeps the wide tile (fewer tiles for its rank merge).
+template <int LANES>
+struct DdTileE {
+  static constexpr int E = LANES == 1 ? TileCfg<2>::E : TileCfg<LANES>::E;
+};
+
 template <int LANES>
 __device__ void dd_sort_tile(const DdDevPlan& p, const DdChain& c, int b, uint32_t tile, uint8_t* sbytes) {
-  constexpr int E = TileCfg<LANES>::E, T = TileCfg<LANES>::T, NT = kDdSortThreads;
+  constexpr int E = DdTileE<LANES>::E, NT = kDdSortThreads, T = NT * E;
   constexpr int NW = KeyTraits<LANES>::NW;
   using W = KW<LANES>;
   W* sk = reinterpret_cast<W*>(sbytes);
@@ -1435,7 +1445,7 @@ __device__ void dd_sort_tile(const DdDevPlan& p, const DdChain& c, int b, uint32
   Key<LANES> r[E];
   uint32_t ri[E];
   uint64_t inv = 0;
-  tile_network<LANES, true, NT>(sk, si, cnt, 0u, r, ri, inv);
+  tile_network<LANES, true, NT, false, E>(sk, si, cnt, 0u, r, ri, inv);
   W* gout = reinterpret_cast<W*>(c.ts + p.dk_off[b]) + (uint64_t)start * NW;
   const uint32_t* dslot = c.aux + p.aux_off[b] + start;
   uint32_t* ocnt = c.aux + p.aux_total + p.aux_off[b] + start;
@@ -1471,7 +1481,7 @@ __global__ void __launch_bounds__(kDdSortThreads) dd_tile_sort_kernel(const __gr
   }
 }
 
-int dd_sort_tile_size(int lanes) { return lanes <= 1 ? TileCfg<1>::T : TileCfg<2>::T; }
+int dd_sort_tile_size(int lanes) { return lanes == 0 ? TileCfg<0>::T : TileCfg<2>::T; }
 
 void launch_dd_tiles(const DdChain& c, int grid, cudaStream_t st) {
   launch_pdl(dd_tile_sort_kernel, grid, kDdSortThreads, kDdSortSmem, st, c);

@@ -261,7 +261,7 @@ struct DdAgg {
   uint32_t* ctl;
   uint32_t* aux;            // per-distinct-word array A: the word's table slot
   struct DdDevPlan* plan;   // or null: [2], each launch's last CTA writes its chain's plan
-  uint32_t stile1, stilen;  // keys per sorted tile (one-word / wider keys: dd_sort_tile_size)
+  uint32_t stile1, stilen;  // keys per sorted tile (uint32 keys / keys of 1-3 lanes: dd_sort_tile_size)
 };
 // first tile of every bucket judged (mostly different words: the class is given up)
 void launch_dd_probe(const DdAgg& a, cudaStream_t st);
